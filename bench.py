@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""ZipPIR online-answer throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N \
+        --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+Workload (BASELINE.json configs[1]): 1 GiB DB per GPU, d0 = 32768 records x
+32768 output rows (u8, uniform, seeded), LWE n = 1024, q = 2^32, 2048-bit
+Paillier modulus; one query per step: b = DB qu mod 2^32, the compression
+t_g = (sum_j 2^(32j)(b + H ck_o)) mod m for all d1' = 521 groups. With N
+GPUs the DB is N GiB, row-sharded (group aligned, 1 GiB per GPU: weak
+scaling) and the per-shard t is gathered over NCCL.
+
+value   = DB bytes (all ranks) / device time per answer, inputs resident in
+          HBM; the DB (1 GiB) exceeds L2 (126 MB), so no flush is needed.
+e2e     = same metric through protocol.respond() with host inputs
+          (numpy qu0, Python-int ck_o) and a host ResponseMessage.
+roofline: the GEMV kernel, algorithmic bytes d0*d1 + 4 d0 + 4 d1 per launch
+          over its CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline: the reference's own algorithm (oracle/ref_port.py: float64
+          BLAS GEMV + 240-prime RNS) on a bounded row sample, rank 0, N=1.
+"""
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D0 = 32768
+D1 = 32768
+N_LWE = 1024
+BITS = 2048
+CAP = 63
+CPU_SAMPLE_ROWS = 32 * CAP  # 2016 DB rows = 32 groups
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=50)
+    return ap.parse_args()
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# -- seeded inputs (no oracle on the product path) ---------------------------
+
+def _is_prime(x):
+    for p in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37):
+        if x % p == 0:
+            return x == p
+    d, s = x - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41):
+        y = pow(a, d, x)
+        if y in (1, x - 1):
+            continue
+        for _ in range(s - 1):
+            y = y * y % x
+            if y == x - 1:
+                break
+        else:
+            return False
+    return True
+
+
+def paillier_modulus(bits, seed):
+    """m = p q with two seeded bits/2-bit primes (same recipe as paillier.py:69-86)."""
+    import math
+    rng = random.Random(seed)
+    half = bits // 2
+    while True:
+        ps = []
+        for _ in range(2):
+            x = rng.randrange(1 << (half - 1), 1 << half) | 1
+            while not _is_prime(x):
+                x += 2
+            ps.append(x)
+        p, q = ps
+        m = p * q
+        if p != q and m.bit_length() == bits and math.gcd(m, (p - 1) * (q - 1)) == 1:
+            return m
+
+
+def db_slice(rank, rows):
+    return np.frombuffer(np.random.default_rng(7 + rank).bytes(D0 * rows),
+                         dtype=np.uint8).reshape(D0, rows)
+
+
+# -- clocks --------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def _traffic():
+    p = os.path.join(ROOT, "profiles", "gemv_traffic.json")
+    try:
+        return json.load(open(p)).get("bytes_per_launch")
+    except Exception:
+        return None
+
+
+# -- CPU baseline (reference algorithm port; rank 0 only) --------------------
+
+def cpu_baseline(m, repeats=7):
+    from oracle import ref_port
+    rows = CPU_SAMPLE_ROWS
+    db = db_slice(0, D1)[:, :rows].copy()
+    from paper_2603_09190_b200.prg import Stream, DOM_PUBLIC_MATRIX
+    A = Stream(b"\x00" * 16, DOM_PUBLIC_MATRIX).words32(D0 * N_LWE).reshape(D0, N_LWE)
+    st = ref_port.PortState(db, A, CAP)
+    rng = np.random.default_rng(11)
+    qu = rng.integers(0, 1 << 32, D0, dtype=np.uint64)
+    r = random.Random(12)
+    ck_o = [r.randrange(m) for _ in range(N_LWE)]
+    times = []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        st.respond_t(qu, ck_o, m)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return {"value": D0 * rows / best / 1e9, "unit": "GB/s", "cores": os.cpu_count(),
+            "kind": "port",
+            "sample": f"{rows} of {D1} DB rows ({rows // CAP} groups) x d0={D0}, n={N_LWE}, "
+                      f"{BITS}-bit m; reference algorithm (centered float64 BLAS GEMV + "
+                      f"240x27-bit RNS matvec + Garner), best of {repeats}, "
+                      f"median {statistics.median(times) * 1e3:.1f} ms",
+            "best_s": best}
+
+
+def run_reference(args):
+    rank, world, _ = _dist_env()
+    if rank != 0:
+        return
+    m = paillier_modulus(BITS, 2048)
+    from oracle import ref_port
+    rows = CPU_SAMPLE_ROWS
+    db = db_slice(0, D1)[:, :rows].copy()
+    from paper_2603_09190_b200.prg import Stream, DOM_PUBLIC_MATRIX
+    A = Stream(b"\x00" * 16, DOM_PUBLIC_MATRIX).words32(D0 * N_LWE).reshape(D0, N_LWE)
+    st = ref_port.PortState(db, A, CAP)
+    rng = np.random.default_rng(11)
+    qu = rng.integers(0, 1 << 32, D0, dtype=np.uint64)
+    r = random.Random(12)
+    ck_o = [r.randrange(m) for _ in range(N_LWE)]
+    steps = max(1, min(args.steps, 50))
+    for _ in range(min(args.warmup, 3)):
+        st.respond_t(qu, ck_o, m)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st.respond_t(qu, ck_o, m)
+    dt = (time.perf_counter() - t0) / steps
+    v = D0 * rows / dt / 1e9
+    sample = (f"{rows} of {D1} DB rows ({rows // CAP} groups) x d0={D0} per step; reference "
+              "algorithm port (oracle/ref_port.py: float64 BLAS GEMV + 240-prime RNS)")
+    print(json.dumps({
+        "impl": "reference", "metric": "online server throughput (DB GB/s per query)",
+        "value": v, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 3),
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8xu32 / 2048-bit", "data": "synthetic",
+        "config": {"workload": "1 GiB DB (32768 x 32768 u8), n=1024, q=2^32, 2048-bit Paillier, "
+                               "single query (sampled rows)", "d0": D0, "d1": D1},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# -- B200 path -----------------------------------------------------------------
+
+def run_b200(args):
+    import torch
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import _lib, build as zb
+    from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
+    from paper_2603_09190_b200.shard import ShardedServer, shard_bounds
+    zb.build()
+    _lib.load()
+
+    d1_total = D1 * world
+    params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, d1_total, BITS)
+    bounds = shard_bounds(d1_total, params.capacity, world)
+    lo, hi, g_lo, g_hi = bounds[rank]
+    t0 = time.perf_counter()
+    db = db_slice(rank, hi - lo)
+    srv = ShardedServer(params, db, rank, world, group)
+    st = srv.state
+    setup_s = time.perf_counter() - t0
+    m = paillier_modulus(BITS, 2048)
+    kctx = key_ctx(m, dev)
+    pk = z.PaillierPublicKey(m, m.bit_length())
+    reg = z.ClientRegistration(pk, b"\x05" * 16, z.client_id_of(pk))
+    stream = torch.cuda.current_stream(dev)
+
+    # per-client hint (offline): one device multi-exponentiation, all groups
+    torch.cuda.synchronize()
+    th = time.perf_counter()
+    reg.hints[0] = z.hint(st, reg, 0)
+    torch.cuda.synchronize()
+    hint_s = time.perf_counter() - th
+
+    rng = np.random.default_rng(100 + rank)
+    qu = rng.integers(0, 1 << 32, D0, dtype=np.uint64)
+    r = random.Random(200)
+    ck_o = [r.randrange(m) for _ in range(N_LWE)]
+    lay = st.layout
+    q32 = np.zeros(lay.ld, dtype=np.uint32)
+    q32[:D0] = qu.astype(np.uint32)
+    qu_dev = torch.from_numpy(q32.view(np.int32)).to(dev).reshape(1, lay.ld)
+    cko_dev = torch.from_numpy(ints_to_limbs(ck_o, kctx.lm).view(np.int32)).to(dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    for _ in range(max(args.warmup, 3)):
+        srv.answer(qu_dev, cko_dev, kctx, kctx.lm, stream)
+    clocks = ClockSampler(local)
+    clocks.start()
+    # burn-in so the sampled clocks reflect steady load (not part of timing)
+    tb = time.perf_counter()
+    while time.perf_counter() - tb < 1.5:
+        for _ in range(50):
+            srv.answer(qu_dev, cko_dev, kctx, kctx.lm, stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_events = [[ev(), ev(), ev()] for _ in range(args.steps)]
+    e_start, e_end = ev(), ev()
+    e_start.record(stream)
+    for i in range(args.steps):
+        srv.answer(qu_dev, cko_dev, kctx, kctx.lm, stream, step_events[i])
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e_start.elapsed_time(e_end) / args.steps
+    gemv_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in step_events)
+    comp_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in step_events)
+    if world > 1:
+        t = torch.tensor([ms, gemv_ms, comp_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, gemv_ms, comp_ms = t.tolist()
+
+    # e2e through the public API (host buffers, H2D/D2H inside)
+    qmsg = z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck_o, qu)
+    for _ in range(3):
+        z.respond(st, reg, qmsg)
+    e2e_times = []
+    for _ in range(args.e2e_steps):
+        if world > 1:
+            dist.barrier()
+        t1 = time.perf_counter()
+        resp = z.respond(st, reg, qmsg)
+        if world > 1:
+            tl = torch.from_numpy(ints_to_limbs(resp.t, kctx.lm).view(np.int32)).to(dev)
+            from paper_2603_09190_b200.shard import gather_groups
+            full = gather_groups(tl, bounds, rank)
+            full.cpu()
+        e2e_times.append(time.perf_counter() - t1)
+    e2e_s = statistics.mean(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+
+    db_bytes_total = D0 * d1_total
+    db_bytes_rank = D0 * (hi - lo)
+    value = db_bytes_total / (ms / 1e3) / 1e9
+    gemv_bytes = D0 * (hi - lo) + 4 * D0 + 4 * (hi - lo)
+    peak, peak_src = _peaks()
+    achieved = gemv_bytes / (gemv_ms / 1e3) / 1e9
+    answer_bytes = gemv_bytes + 4 * N_LWE * (hi - lo) + 256 * N_LWE + 256 * (g_hi - g_lo)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(m)
+    if rank == 0:
+        h2d = 4 * D0 + 4 * kctx.lm * N_LWE
+        d2h = 4 * kctx.lm * params.d1_prime
+        out = {
+            "metric": "online server throughput (DB GB/s per query)",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8xu32 mod 2^32 / 2048-bit Montgomery",
+            "data": "synthetic (seeded uniform u8 DB, uniform qu0 / ck_o, seeded Paillier modulus)",
+            "config": {"workload": "BASELINE configs[1]: 1 GiB DB per GPU (32768 x 32768 u8), "
+                                   "n=1024, q=2^32, 2048-bit Paillier, single query, SEPARATE",
+                       "d0": D0, "d1": d1_total, "groups": params.d1_prime,
+                       "parallelism": f"db-row shards x{world}",
+                       "l2": "no flush: DB (1 GiB/GPU) > L2 (126 MB)"},
+            "gpu_launches": 4 * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "gemv_dp4a_kernel (+qplanes)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic(),
+                         "peak_source": peak_src,
+                         "bytes_per_launch": gemv_bytes},
+            "answer_roofline": {"bytes": answer_bytes, "ms": ms,
+                                "achieved_gbs": answer_bytes / (ms / 1e3) / 1e9,
+                                "frac": answer_bytes / (ms / 1e3) / 1e9 / peak,
+                                "gemv_ms": gemv_ms, "compress_ms": comp_ms},
+            "e2e": {"value": db_bytes_total / e2e_s / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond()"},
+            "clocks": clk,
+            "setup_s": setup_s, "hint_s_per_client": hint_s,
+            "per_gpu_db_bytes": db_bytes_rank,
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = _args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,97 @@
+/* C ABI of the B200-native ZipPIR server hot path (libzpir_b200.so).
+ *
+ * Plain pointers and sizes only: every buffer argument is DEVICE memory on
+ * the current CUDA device, every `stream` is a cudaStream_t passed as void*
+ * (NULL = legacy default stream). Limbs are little-endian uint32 words.
+ * Every entry point returns 0 on success or a nonzero status
+ * (1 = bad input -> Python ValueError, 2 = CUDA failure, 3 = unsupported
+ * width); zpir_last_error() returns the calling thread's last message.
+ * Nothing throws across this boundary; all entry points are re-entrant
+ * (no global mutable state besides the thread-local error string), so the
+ * reference's connection threads and hint-worker thread may call them
+ * concurrently on their own streams (server.py:215-228, :72-84).
+ *
+ * The reference (Python, /root/reference/pkg/src/zippir) has no FFI of its
+ * own; each function below names the reference code it replaces, and the
+ * ctypes binding a maintainer would add is in INTEGRATION.md
+ * (paper_2603_09190_b200/_lib.py is that binding).
+ */
+#ifndef ZIPPIR_B200_H
+#define ZIPPIR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZPIR_ABI_VERSION 1
+
+int zpir_abi_version(void);
+const char* zpir_last_error(void);
+
+/* Database layout: dbt[c*ld + i] = db[i*ld_src + c] for i < d0, c < d1,
+ * zero padding up to rows x ld (rows % 128 == 0, ld % 64 == 0).
+ * Replaces the centered float64 copy _dbt_c built in
+ * ServerGlobalState.__init__ (protocol.py:190-193). */
+int zpir_transpose_db(const uint8_t* db, int64_t d0, int64_t d1, int64_t ld_src,
+                      uint8_t* dbt, int64_t rows, int64_t ld, void* stream);
+
+/* Global hint H[c,k] = qmask & -(sum_i dbt[c,i] * A[i,k]), A is (ld x lda)
+ * row-major u32 with zero rows >= d0 and zero columns >= n, H is (rows x n).
+ * Replaces ServerGlobalState._global_hint_fast / _global_hint_slow
+ * (protocol.py:195-217). */
+int zpir_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* A,
+                     int64_t lda, int64_t n, uint32_t* H, uint32_t qmask, void* stream);
+
+/* Online GEMV b = qmask & (dbt * qu) for nvec query vectors qu[v*ld + i]
+ * (zero-padded to ld), b[v*rows + c]. workspace: zpir_gemv_workspace_bytes.
+ * Replaces ServerGlobalState.db_matvec (protocol.py:242-257). */
+int64_t zpir_gemv_workspace_bytes(int64_t ld, int64_t nvec);
+int zpir_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* qu, int64_t nvec,
+              uint32_t* b, uint32_t qmask, void* workspace, void* stream);
+
+/* Answer compression, row stage: z[c, 0..lm+2) = (b[c] & qmask) +
+ * sum_k H[c,k] * cko[k, 0..lm) exactly (rows % 32 == 0, lm % 32 == 0).
+ * Replaces rns.rns_matmul_mod's residue products (rns.py:163-188). */
+int zpir_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint32_t* b,
+                     uint32_t qmask, const uint32_t* cko, int lm, uint32_t* z, void* stream);
+
+/* Answer compression, group stage: t[g] = (sum_j 2^(32j) z[g*cap+j]) mod m,
+ * m given as lm limbs with np = -m^-1 mod 2^32 and rpow[s] = R^(s+1) mod m
+ * (R = 2^(32 lm)) for s < nchunks. t rows have stride t_ld (zero-extended).
+ * Replaces Garner reconstruction + scaled_b + the final add (rns.py:94-127,
+ * protocol.py:259-269, :349-350) for gamma = q = 2^32. */
+int zpir_answer_groups(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
+                       const uint32_t* m, uint32_t np, const uint32_t* rpow, int nchunks,
+                       uint32_t* t, int64_t t_ld, void* stream);
+
+/* COMBINED response K[g] = (1 + t[g] m) k[g] mod m^2; m^2 as l2 limbs with
+ * np2, r2 = R^2 mod m^2, mr = m R mod m^2 (R = 2^(32 l2)); t zero-extended
+ * to l2 limbs. Replaces the trivial_encrypt + add loop of respond()
+ * (protocol.py:354-358; paillier.py:104-106, :120-123). */
+int zpir_combine(const uint32_t* t, const uint32_t* k, int64_t groups, int l2,
+                 const uint32_t* m2, uint32_t np2, const uint32_t* r2, const uint32_t* mr,
+                 uint32_t* out, void* stream);
+
+/* out[i] = a[i] * b[i] mod N (canonical), limbs % 32 == 0, r2 = R^2 mod N.
+ * Batched paillier.add (paillier.py:120-123). */
+int zpir_mulmod(const uint32_t* a, const uint32_t* b, int64_t count, int limbs, const uint32_t* N,
+                uint32_t np, const uint32_t* r2, uint32_t* out, void* stream);
+
+/* Multi-exponentiation out[g] = prod_k bases[k]^{e(g,k)} mod N for rows g,
+ * bases (n x limbs, canonical < N), exponent limb j of (g,k) at
+ * exps[g*row_stride + k*base_stride + j*limb_stride], j < elimbs.
+ * Replaces paillier.multiexp / paillier_matmul (paillier.py:134-203), as
+ * called by protocol.hint (protocol.py:291-296). */
+int64_t zpir_multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs);
+int zpir_multiexp(const uint32_t* bases, int64_t n, const uint32_t* exps, int64_t rows,
+                  int64_t row_stride, int64_t base_stride, int64_t limb_stride, int elimbs,
+                  int limbs, const uint32_t* N, uint32_t np, const uint32_t* r2, uint32_t* out,
+                  void* workspace, int64_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ZIPPIR_B200_H */

@@ -1,0 +1,277 @@
+// Online answer, compression half: t_g = (bs_g + hv_g) mod m, and COMBINED.
+//
+// Reference: respond() (protocol.py:333-365) computes hv = H_scaled * ck_o
+// mod m through a 240-prime RNS engine (rns.py:163-188) over H_rns (240 x d1'
+// x n float64, ~1 GB at 1 GiB) and adds bs = scaled_b(b) (protocol.py:259-269).
+// For gamma = q = 2^32 the batch-scaled hint is the little-endian
+// concatenation of H's 32-bit words (protocol.py:223-230), so
+//   t_g = ( sum_j 2^(32 j) * (b_c + y_c) ) mod m,   c = g*cap + j,
+//   y_c = sum_k H[c,k] * ck_o[k]        (exact, < n 2^32 m)
+// (SURVEY 8c(ii)); the device reads H (4 bytes/entry, 128 MB at 1 GiB)
+// instead of H_rns.
+//
+//   answer_rows   z_c = b_c + y_c as (Lm + 2) 32-bit limbs, Lm = limbs of m.
+//   answer_groups X_g = sum_j 2^(32j) z_{g*cap+j}; t_g = X_g mod m via
+//                 t = sum_s mont(X_s, R^(s+1) mod m) over Lm-limb chunks X_s.
+//   combine       K_g = (1 + t_g m) * k_g mod m^2 (paillier.py:104-123).
+#include "bignum.cuh"
+
+namespace zpir {
+
+// z[c, 0..Lm+2) = (b[c] & qmask) + sum_k H[c,k] * cko[k, 0..Lm)
+// 128 threads, tile = 32 rows x 64 limbs, each thread 4 rows x 4 limbs with
+// 96-bit accumulators; row-wise carry propagation in shared memory.
+__global__ void __launch_bounds__(128)
+answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __restrict__ b,
+                   uint32_t qmask, const uint32_t* __restrict__ cko, int lm,
+                   uint32_t* __restrict__ z) {
+  __shared__ __align__(16) uint32_t sH[16][32];
+  __shared__ __align__(16) uint32_t sC[16][64];
+  __shared__ uint32_t sS[32][64][3];
+  const int t = threadIdx.x, tr = t >> 4, tc = t & 15;
+  const int64_t row0 = (int64_t)blockIdx.x * 32;
+  const int wz = lm + 2;
+  // row-carry state, owned by threads 0..31 (one row each)
+  unsigned __int128 carry = 0;
+  if (t < 32) carry = (unsigned __int128)(b[row0 + t] & qmask);
+
+  for (int ch = 0; ch < lm; ch += 64) {
+    uint32_t lo[4][4], mi[4][4], hi[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) lo[r][c] = mi[r][c] = hi[r][c] = 0;
+    for (int64_t k0 = 0; k0 < n; k0 += 16) {
+      {
+        const int row = t >> 2, kq = (t & 3) * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t k = k0 + kq + i;
+          sH[kq + i][row] = (k < n) ? H[(row0 + row) * n + k] : 0u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int idx = t + i * 128, kk = idx >> 6, l = idx & 63;
+        const int64_t k = k0 + kk;
+        sC[kk][l] = (k < n && ch + l < lm) ? cko[k * lm + ch + l] : 0u;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int kk = 0; kk < 16; ++kk) {
+        const uint4 hv = *reinterpret_cast<const uint4*>(&sH[kk][tr * 4]);
+        const uint32_t h[4] = {hv.x, hv.y, hv.z, hv.w};
+        uint32_t c[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c[j] = sC[kk][tc + 16 * j];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            asm("mad.lo.cc.u32 %0, %3, %4, %0;\n\t"
+                "madc.hi.cc.u32 %1, %3, %4, %1;\n\t"
+                "addc.u32 %2, %2, 0;"
+                : "+r"(lo[r][j]), "+r"(mi[r][j]), "+r"(hi[r][j])
+                : "r"(h[r]), "r"(c[j]));
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        sS[tr * 4 + r][tc + 16 * j][0] = lo[r][j];
+        sS[tr * 4 + r][tc + 16 * j][1] = mi[r][j];
+        sS[tr * 4 + r][tc + 16 * j][2] = hi[r][j];
+      }
+    __syncthreads();
+    if (t < 32) {
+      uint32_t* zr = z + (row0 + t) * wz;
+      const int lim = min(64, lm - ch);
+      for (int l = 0; l < lim; ++l) {
+        const unsigned __int128 s = (unsigned __int128)sS[t][l][0] |
+                                    ((unsigned __int128)sS[t][l][1] << 32) |
+                                    ((unsigned __int128)sS[t][l][2] << 64);
+        const unsigned __int128 v = s + carry;
+        zr[ch + l] = (uint32_t)v;
+        carry = v >> 32;
+      }
+    }
+    __syncthreads();
+  }
+  if (t < 32) {
+    uint32_t* zr = z + (row0 + t) * wz;
+    zr[lm] = (uint32_t)carry;
+    zr[lm + 1] = (uint32_t)(carry >> 32);
+  }
+}
+
+// One warp per group. Shared memory per warp: nchunks*Lm u64 position sums
+// (reused as the X limbs). t is written with row stride t_ld (>= Lm),
+// zero-extended.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+answer_groups_kernel(const uint32_t* __restrict__ z, int64_t d1, int cap, int64_t groups,
+                     const uint32_t* __restrict__ mod, uint32_t np,
+                     const uint32_t* __restrict__ rpow, int nchunks, uint32_t* __restrict__ t,
+                     int64_t t_ld) {
+  constexpr int LM = 32 * LPL;
+  extern __shared__ unsigned long long smem_u64[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (g >= groups) return;
+  const int nx = nchunks * LM;
+  unsigned long long* S = smem_u64 + (size_t)wid * nx;
+  const int wz = LM + 2;
+  const int64_t c0 = g * cap;
+  const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
+  for (int P = lane; P < nx; P += 32) {
+    unsigned long long s = 0;
+    const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
+    for (int j = jlo; j <= jhi; ++j) s += z[(c0 + j) * wz + (P - j)];
+    S[P] = s;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    uint32_t* X = reinterpret_cast<uint32_t*>(S);  // in-place: X[P] written after S[P] read
+    unsigned long long c = 0;
+    for (int P = 0; P < nx; ++P) {
+      const unsigned long long s = S[P];
+      const unsigned __int128 v = (unsigned __int128)s + c;
+      X[P] = (uint32_t)v;
+      c = (unsigned long long)(v >> 32);
+    }
+  }
+  __syncwarp();
+  const uint32_t* X = reinterpret_cast<const uint32_t*>(S);
+  uint32_t n_[LPL], res[LPL], x[LPL], rp[LPL];
+  big_load<LPL>(n_, mod, lane);
+  big_set_small<LPL>(res, 0, lane);
+  for (int s = 0; s < nchunks; ++s) {
+#pragma unroll
+    for (int i = 0; i < LPL; ++i) x[i] = X[s * LM + lane * LPL + i];
+    big_load<LPL>(rp, rpow + (size_t)s * LM, lane);
+    mont_mul<LPL>(x, x, rp, n_, np, lane);
+    const uint32_t cy = big_add<LPL>(res, x, lane);
+    big_cond_sub<LPL>(res, cy, n_, lane);
+  }
+  uint32_t* out = t + g * t_ld;
+  big_store<LPL>(out, res, lane);
+  for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
+}
+
+// K_g = (1 + t_g m) k_g mod m^2, one warp per group, with m^2 context
+// (n2, np2), r2 = R^2 mod m^2, mr = m R mod m^2.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+combine_kernel(const uint32_t* __restrict__ t, const uint32_t* __restrict__ k, int64_t groups,
+               const uint32_t* __restrict__ n2, uint32_t np2, const uint32_t* __restrict__ r2,
+               const uint32_t* __restrict__ mr, uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= groups) return;
+  uint32_t n_[LPL], a[LPL], b[LPL], one[LPL];
+  big_load<LPL>(n_, n2, lane);
+  big_load<LPL>(a, t + g * L, lane);
+  big_load<LPL>(b, mr, lane);
+  mont_mul<LPL>(a, a, b, n_, np2, lane);  // t m  (< m^2, exact)
+  big_set_small<LPL>(one, 1, lane);
+  big_add<LPL>(a, one, lane);             // 1 + t m  (< m^2, no carry out)
+  big_load<LPL>(b, k + g * L, lane);
+  mont_mul<LPL>(a, a, b, n_, np2, lane);  // (1 + t m) k R^-1
+  big_load<LPL>(b, r2, lane);
+  mont_mul<LPL>(a, a, b, n_, np2, lane);  // (1 + t m) k
+  big_store<LPL>(out + g * L, a, lane);
+}
+
+// out[i] = a[i] * b[i] mod N (canonical), one warp per product: two Montgomery
+// products, the second against R^2 mod N. Backs paillier.add-style batches.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+mulmod_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, int64_t count,
+              const uint32_t* __restrict__ n, uint32_t np, const uint32_t* __restrict__ r2,
+              uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= count) return;
+  uint32_t n_[LPL], x[LPL], y[LPL];
+  big_load<LPL>(n_, n, lane);
+  big_load<LPL>(x, a + i * L, lane);
+  big_load<LPL>(y, b + i * L, lane);
+  mont_mul<LPL>(x, x, y, n_, np, lane);
+  big_load<LPL>(y, r2, lane);
+  mont_mul<LPL>(x, x, y, n_, np, lane);
+  big_store<LPL>(out + i * L, x, lane);
+}
+
+int answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint32_t* b,
+                       uint32_t qmask, const uint32_t* cko, int lm, uint32_t* z, cudaStream_t st) {
+  if (rows % 32 || n <= 0 || lm <= 0 || lm % 32) {
+    set_error("answer_rows: bad shapes (rows=%lld n=%lld lm=%d)", (long long)rows, (long long)n, lm);
+    return kErrInput;
+  }
+  answer_rows_kernel<<<(unsigned)(rows / 32), 128, 0, st>>>(H, n, b, qmask, cko, lm, z);
+  return check_launch("answer_rows");
+}
+
+#define ZPIR_LPL_DISPATCH(LPLV, ...)                                   \
+  switch (LPLV) {                                                      \
+    case 1: { constexpr int LPL = 1; __VA_ARGS__; } break;            \
+    case 2: { constexpr int LPL = 2; __VA_ARGS__; } break;            \
+    case 3: { constexpr int LPL = 3; __VA_ARGS__; } break;            \
+    case 4: { constexpr int LPL = 4; __VA_ARGS__; } break;            \
+    case 6: { constexpr int LPL = 6; __VA_ARGS__; } break;            \
+    case 8: { constexpr int LPL = 8; __VA_ARGS__; } break;            \
+    default:                                                           \
+      set_error("unsupported limb width %d (limbs per lane)", LPLV); \
+      return kErrUnsupported;                                          \
+  }
+
+int answer_groups_launch(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
+                         const uint32_t* mod, uint32_t np, const uint32_t* rpow, int nchunks,
+                         uint32_t* t, int64_t t_ld, cudaStream_t st) {
+  if (lm % 32 || nchunks * lm < cap + lm + 2 || t_ld < lm || cap <= 0) {
+    set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
+    return kErrInput;
+  }
+  const size_t smem = (size_t)4 * nchunks * lm * sizeof(unsigned long long);
+  const unsigned grid = (unsigned)ceil_div(groups, 4);
+  ZPIR_LPL_DISPATCH(lm / 32, {
+    cudaFuncSetAttribute(answer_groups_kernel<LPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    answer_groups_kernel<LPL><<<grid, 128, smem, st>>>(z, d1, cap, groups, mod, np, rpow, nchunks,
+                                                       t, t_ld);
+  });
+  return check_launch("answer_groups");
+}
+
+int combine_launch(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* n2,
+                   uint32_t np2, const uint32_t* r2, const uint32_t* mr, uint32_t* out,
+                   cudaStream_t st) {
+  if (l2 % 32) {
+    set_error("combine: limb count %d not a multiple of 32", l2);
+    return kErrInput;
+  }
+  const unsigned grid = (unsigned)ceil_div(groups, 4);
+  ZPIR_LPL_DISPATCH(l2 / 32, {
+    combine_kernel<LPL><<<grid, 128, 0, st>>>(t, k, groups, n2, np2, r2, mr, out);
+  });
+  return check_launch("combine");
+}
+
+int mulmod_launch(const uint32_t* a, const uint32_t* b, int64_t count, int limbs, const uint32_t* n,
+                  uint32_t np, const uint32_t* r2, uint32_t* out, cudaStream_t st) {
+  if (limbs % 32) {
+    set_error("mulmod: limb count %d not a multiple of 32", limbs);
+    return kErrInput;
+  }
+  const unsigned grid = (unsigned)ceil_div(count, 4);
+  ZPIR_LPL_DISPATCH(limbs / 32, {
+    mulmod_kernel<LPL><<<grid, 128, 0, st>>>(a, b, count, n, np, r2, out);
+  });
+  return check_launch("mulmod");
+}
+
+}  // namespace zpir

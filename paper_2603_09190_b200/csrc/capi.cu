@@ -1,0 +1,114 @@
+// extern "C" boundary (include/zippir_b200.h): status codes + thread-local
+// error string; no exceptions cross this boundary.
+#include <cstdarg>
+#include <cstdio>
+
+#include "../../include/zippir_b200.h"
+#include "zpir_common.cuh"
+
+namespace zpir {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int transpose_db_launch(const uint8_t*, int64_t, int64_t, int64_t, uint8_t*, int64_t, int64_t,
+                        cudaStream_t);
+int hint_gemm_launch(const uint8_t*, int64_t, int64_t, const uint32_t*, int64_t, int64_t,
+                     uint32_t*, uint32_t, cudaStream_t);
+int gemv_launch(const uint8_t*, int64_t, int64_t, const uint32_t*, int64_t, uint32_t*, uint32_t,
+                uint32_t*, cudaStream_t);
+int answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint32_t*, uint32_t,
+                       const uint32_t*, int, uint32_t*, cudaStream_t);
+int answer_groups_launch(const uint32_t*, int64_t, int, int64_t, int, const uint32_t*, uint32_t,
+                         const uint32_t*, int, uint32_t*, int64_t, cudaStream_t);
+int combine_launch(const uint32_t*, const uint32_t*, int64_t, int, const uint32_t*, uint32_t,
+                   const uint32_t*, const uint32_t*, uint32_t*, cudaStream_t);
+int mulmod_launch(const uint32_t*, const uint32_t*, int64_t, int, const uint32_t*, uint32_t,
+                  const uint32_t*, uint32_t*, cudaStream_t);
+int64_t multiexp_workspace_bytes(int64_t, int64_t, int, int);
+int multiexp_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t, int64_t, int64_t,
+                    int, int, const uint32_t*, uint32_t, const uint32_t*, uint32_t*, void*,
+                    int64_t, cudaStream_t);
+
+}  // namespace zpir
+
+using namespace zpir;
+
+#define ZPIR_GUARD(expr)                              \
+  do {                                                \
+    try {                                             \
+      return (expr);                                  \
+    } catch (...) {                                   \
+      set_error("unexpected C++ exception");          \
+      return kErrCuda;                                \
+    }                                                 \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" {
+
+int zpir_abi_version(void) { return ZPIR_ABI_VERSION; }
+
+const char* zpir_last_error(void) { return g_err; }
+
+int zpir_transpose_db(const uint8_t* db, int64_t d0, int64_t d1, int64_t ld_src, uint8_t* dbt,
+                      int64_t rows, int64_t ld, void* stream) {
+  ZPIR_GUARD(transpose_db_launch(db, d0, d1, ld_src, dbt, rows, ld, S(stream)));
+}
+
+int zpir_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* A, int64_t lda,
+                     int64_t n, uint32_t* H, uint32_t qmask, void* stream) {
+  ZPIR_GUARD(hint_gemm_launch(dbt, rows, ld, A, lda, n, H, qmask, S(stream)));
+}
+
+int64_t zpir_gemv_workspace_bytes(int64_t ld, int64_t nvec) { return ld * nvec * 4; }
+
+int zpir_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* qu, int64_t nvec,
+              uint32_t* b, uint32_t qmask, void* workspace, void* stream) {
+  ZPIR_GUARD(gemv_launch(dbt, rows, ld, qu, nvec, b, qmask, static_cast<uint32_t*>(workspace),
+                         S(stream)));
+}
+
+int zpir_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint32_t* b, uint32_t qmask,
+                     const uint32_t* cko, int lm, uint32_t* z, void* stream) {
+  ZPIR_GUARD(answer_rows_launch(H, rows, n, b, qmask, cko, lm, z, S(stream)));
+}
+
+int zpir_answer_groups(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
+                       const uint32_t* m, uint32_t np, const uint32_t* rpow, int nchunks,
+                       uint32_t* t, int64_t t_ld, void* stream) {
+  ZPIR_GUARD(
+      answer_groups_launch(z, d1, cap, groups, lm, m, np, rpow, nchunks, t, t_ld, S(stream)));
+}
+
+int zpir_combine(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* m2,
+                 uint32_t np2, const uint32_t* r2, const uint32_t* mr, uint32_t* out,
+                 void* stream) {
+  ZPIR_GUARD(combine_launch(t, k, groups, l2, m2, np2, r2, mr, out, S(stream)));
+}
+
+int zpir_mulmod(const uint32_t* a, const uint32_t* b, int64_t count, int limbs, const uint32_t* N,
+                uint32_t np, const uint32_t* r2, uint32_t* out, void* stream) {
+  ZPIR_GUARD(mulmod_launch(a, b, count, limbs, N, np, r2, out, S(stream)));
+}
+
+int64_t zpir_multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs) {
+  return multiexp_workspace_bytes(n, rows, elimbs, limbs);
+}
+
+int zpir_multiexp(const uint32_t* bases, int64_t n, const uint32_t* exps, int64_t rows,
+                  int64_t row_stride, int64_t base_stride, int64_t limb_stride, int elimbs,
+                  int limbs, const uint32_t* N, uint32_t np, const uint32_t* r2, uint32_t* out,
+                  void* workspace, int64_t ws_bytes, void* stream) {
+  ZPIR_GUARD(multiexp_launch(bases, n, exps, rows, row_stride, base_stride, limb_stride, elimbs,
+                             limbs, N, np, r2, out, workspace, ws_bytes, S(stream)));
+}
+
+}  // extern "C"

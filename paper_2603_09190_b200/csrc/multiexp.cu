@@ -1,0 +1,225 @@
+// Per-client compressed hint: k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2.
+//
+// Reference: hint() (protocol.py:291-296) -> paillier_matmul (paillier.py:
+// 196-203) -> multiexp (paillier.py:134-193): w=6 windows, buckets 1..63,
+// running-sum combine, one row at a time in gmpy2 (361,620 4096-bit group
+// multiplications per entry at BASELINE parameters).
+//
+// B200 design (exact, same group element, canonical output < m^2):
+//   to_mont       bases -> Montgomery form (one warp per base).
+//   window        one warp per (row g, window w): counting-sort the 6-bit
+//                 digits of the n exponents into buckets in shared memory,
+//                 then for d = 63..1 form bucket_d = prod of its bases,
+//                 running *= bucket_d, total *= running, all in registers
+//                 (the running product never leaves the warp); write the
+//                 window total W[g][w].
+//   combine       one warp per row: acc = acc^(2^6) * W[g][w] from the top
+//                 window down, then out of Montgomery form.
+// Exponents are read in place through a strided-limb view: limb j of
+// exponent (g, k) is E[g*rs + k*bs + j*ls]. For the hint that view is H
+// itself (rs = cap*n, bs = 1, ls = n), since with gamma = 2^32 the limbs of
+// H_scaled[g][k] are H[g*cap + j][k] (protocol.py:223-230); no H_scaled is
+// ever materialised.
+#include <algorithm>
+
+#include "bignum.cuh"
+
+namespace zpir {
+
+constexpr int kWin = 6;
+constexpr int kBuckets = 1 << kWin;
+
+__device__ __forceinline__ uint32_t exp_digit(const uint32_t* __restrict__ E, int64_t off,
+                                              int64_t ls, int elimbs, int bitpos) {
+  const int j = bitpos >> 5, sh = bitpos & 31;
+  if (j >= elimbs) return 0u;
+  uint32_t v = E[off + j * ls] >> sh;
+  if (sh > 32 - kWin && j + 1 < elimbs) v |= E[off + (j + 1) * ls] << (32 - sh);
+  return v & (kBuckets - 1);
+}
+
+template <int LPL>
+__global__ void __launch_bounds__(128)
+to_mont_kernel(const uint32_t* __restrict__ x, int64_t count, const uint32_t* __restrict__ n,
+               uint32_t np, const uint32_t* __restrict__ r2, uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= count) return;
+  uint32_t n_[LPL], a[LPL], b[LPL];
+  big_load<LPL>(n_, n, lane);
+  big_load<LPL>(a, x + i * L, lane);
+  big_load<LPL>(b, r2, lane);
+  mont_mul<LPL>(a, a, b, n_, np, lane);
+  big_store<LPL>(out + i * L, a, lane);
+}
+
+// Shared memory per warp: cnt[64] + off[64] (u32) + list[n] (u32).
+template <int LPL>
+__global__ void __launch_bounds__(128)
+window_kernel(const uint32_t* __restrict__ bases, int64_t n, const uint32_t* __restrict__ E,
+              int64_t rows, int64_t rs, int64_t bs, int64_t ls, int elimbs, int nwin,
+              const uint32_t* __restrict__ N, uint32_t np, uint32_t* __restrict__ W,
+              uint8_t* __restrict__ flags) {
+  constexpr int L = 32 * LPL;
+  extern __shared__ uint32_t smem_u32[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  uint32_t* cnt = smem_u32 + (size_t)wid * (2 * kBuckets + n);
+  uint32_t* off = cnt + kBuckets;
+  uint32_t* list = off + kBuckets;
+  uint32_t n_[LPL];
+  big_load<LPL>(n_, N, lane);
+  const int64_t tasks = rows * nwin;
+  for (int64_t task = (int64_t)blockIdx.x * wpb + wid; task < tasks;
+       task += (int64_t)gridDim.x * wpb) {
+    const int64_t g = task / nwin;
+    const int win = (int)(task - g * nwin);
+    const int bitpos = win * kWin;
+    cnt[lane] = 0;
+    cnt[lane + 32] = 0;
+    __syncwarp();
+    for (int64_t k = lane; k < n; k += 32) {
+      const uint32_t d = exp_digit(E, g * rs + k * bs, ls, elimbs, bitpos);
+      if (d) atomicAdd(&cnt[d], 1u);
+    }
+    __syncwarp();
+    // exclusive scan of cnt[0..63]: lane holds entries 2*lane, 2*lane+1
+    const uint32_t c0 = cnt[2 * lane], c1 = cnt[2 * lane + 1];
+    uint32_t incl = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(ZPIR_FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const uint32_t excl = incl - c0 - c1;
+    off[2 * lane] = excl;
+    off[2 * lane + 1] = excl + c0;
+    __syncwarp();
+    for (int64_t k = lane; k < n; k += 32) {
+      const uint32_t d = exp_digit(E, g * rs + k * bs, ls, elimbs, bitpos);
+      if (d) list[atomicAdd(&off[d], 1u)] = (uint32_t)k;
+    }
+    __syncwarp();
+    // off[d] is now the end of bucket d
+    bool has_run = false, has_tot = false;
+    uint32_t run[LPL], tot[LPL], bkt[LPL], x[LPL];
+    for (int d = kBuckets - 1; d >= 1; --d) {
+      const uint32_t c = cnt[d];
+      if (c) {
+        const uint32_t e = off[d], s = e - c;
+        big_load<LPL>(bkt, bases + (size_t)list[s] * L, lane);
+        for (uint32_t i = s + 1; i < e; ++i) {
+          big_load<LPL>(x, bases + (size_t)list[i] * L, lane);
+          mont_mul<LPL>(bkt, bkt, x, n_, np, lane);
+        }
+        if (has_run) mont_mul<LPL>(run, run, bkt, n_, np, lane);
+        else big_copy<LPL>(run, bkt);
+        has_run = true;
+      }
+      if (has_run) {
+        if (has_tot) mont_mul<LPL>(tot, tot, run, n_, np, lane);
+        else big_copy<LPL>(tot, run);
+        has_tot = true;
+      }
+    }
+    if (has_tot) big_store<LPL>(W + (size_t)task * L, tot, lane);
+    if (lane == 0) flags[task] = has_tot ? 1 : 0;
+    __syncwarp();
+  }
+}
+
+template <int LPL>
+__global__ void __launch_bounds__(128)
+combine_windows_kernel(const uint32_t* __restrict__ W, const uint8_t* __restrict__ flags,
+                       int64_t rows, int nwin, const uint32_t* __restrict__ N, uint32_t np,
+                       uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= rows) return;
+  uint32_t n_[LPL], acc[LPL], x[LPL];
+  big_load<LPL>(n_, N, lane);
+  bool has = false;
+  for (int w = nwin - 1; w >= 0; --w) {
+    if (has)
+      for (int s = 0; s < kWin; ++s) mont_mul<LPL>(acc, acc, acc, n_, np, lane);
+    const int64_t task = g * nwin + w;
+    if (flags[task]) {
+      big_load<LPL>(x, W + (size_t)task * L, lane);
+      if (has) mont_mul<LPL>(acc, acc, x, n_, np, lane);
+      else big_copy<LPL>(acc, x);
+      has = true;
+    }
+  }
+  if (has) {
+    big_set_small<LPL>(x, 1, lane);
+    mont_mul<LPL>(acc, acc, x, n_, np, lane);  // leave Montgomery form
+  } else {
+    big_set_small<LPL>(acc, 1, lane);          // all exponents zero -> 1 (paillier.py:145-146)
+  }
+  big_store<LPL>(out + g * L, acc, lane);
+}
+
+int64_t multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs) {
+  const int64_t nwin = ceil_div((int64_t)32 * elimbs, kWin);
+  const int64_t a = ((n * limbs * 4 + 255) / 256) * 256;
+  const int64_t w = ((rows * nwin * limbs * 4 + 255) / 256) * 256;
+  const int64_t f = ((rows * nwin + 255) / 256) * 256;
+  return a + w + f;
+}
+
+#define ZPIR_LPL_DISPATCH2(LPLV, ...)                                  \
+  switch (LPLV) {                                                      \
+    case 1: { constexpr int LPL = 1; __VA_ARGS__; } break;            \
+    case 2: { constexpr int LPL = 2; __VA_ARGS__; } break;            \
+    case 3: { constexpr int LPL = 3; __VA_ARGS__; } break;            \
+    case 4: { constexpr int LPL = 4; __VA_ARGS__; } break;            \
+    case 6: { constexpr int LPL = 6; __VA_ARGS__; } break;            \
+    case 8: { constexpr int LPL = 8; __VA_ARGS__; } break;            \
+    default:                                                           \
+      set_error("unsupported limb width %d (limbs per lane)", LPLV); \
+      return kErrUnsupported;                                          \
+  }
+
+int multiexp_launch(const uint32_t* bases, int64_t n, const uint32_t* E, int64_t rows, int64_t rs,
+                    int64_t bs, int64_t ls, int elimbs, int limbs, const uint32_t* N, uint32_t np,
+                    const uint32_t* r2, uint32_t* out, void* ws, int64_t ws_bytes,
+                    cudaStream_t st) {
+  if (limbs % 32 || n <= 0 || rows <= 0 || elimbs <= 0) {
+    set_error("multiexp: bad shapes (n=%lld rows=%lld elimbs=%d limbs=%d)", (long long)n,
+              (long long)rows, elimbs, limbs);
+    return kErrInput;
+  }
+  if (ws_bytes < multiexp_workspace_bytes(n, rows, elimbs, limbs)) {
+    set_error("multiexp: workspace too small");
+    return kErrInput;
+  }
+  const int nwin = (int)ceil_div((int64_t)32 * elimbs, kWin);
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  uint32_t* bm = reinterpret_cast<uint32_t*>(p);
+  p += ((n * limbs * 4 + 255) / 256) * 256;
+  uint32_t* W = reinterpret_cast<uint32_t*>(p);
+  p += ((rows * nwin * limbs * 4 + 255) / 256) * 256;
+  uint8_t* flags = p;
+  const size_t smem = (size_t)4 * (2 * kBuckets + n) * sizeof(uint32_t);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ZPIR_LPL_DISPATCH2(limbs / 32, {
+    to_mont_kernel<LPL><<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(bases, n, N, np, r2, bm);
+    if (int e = check_launch("multiexp to_mont")) return e;
+    cudaFuncSetAttribute(window_kernel<LPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const int64_t tasks = rows * nwin;
+    const int64_t grid = std::min<int64_t>(ceil_div(tasks, 4), (int64_t)sms * 32);
+    window_kernel<LPL><<<(unsigned)grid, 128, smem, st>>>(bm, n, E, rows, rs, bs, ls, elimbs,
+                                                          nwin, N, np, W, flags);
+    if (int e = check_launch("multiexp window")) return e;
+    combine_windows_kernel<LPL><<<(unsigned)ceil_div(rows, 4), 128, 0, st>>>(W, flags, rows, nwin,
+                                                                             N, np, out);
+  });
+  return check_launch("multiexp combine");
+}
+
+}  // namespace zpir

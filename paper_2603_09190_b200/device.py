@@ -1,0 +1,113 @@
+"""Device selection, pinned staging and thin wrappers over the C ABI.
+
+Every function here takes/returns torch tensors on a CUDA device and calls
+one extern "C" entry point on the caller's current stream. torch is used for
+device memory, streams and events only.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_09190_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    _lib.load()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device(device)
+
+
+def u32_tensor(arr, device) -> torch.Tensor:
+    """Host uint32 array -> device int32 tensor holding the same bits."""
+    a = np.ascontiguousarray(arr, dtype=np.uint32)
+    return torch.from_numpy(a.view(np.int32)).to(device, non_blocking=False)
+
+
+def to_host_u32(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _s(stream):
+    return _lib.stream_handle(stream)
+
+
+def transpose_db(db_dev, d0, d1, rows, ld, stream=None):
+    out = torch.empty((rows, ld), dtype=torch.uint8, device=db_dev.device)
+    _lib.call("zpir_transpose_db", _lib.ptr(db_dev), d0, d1, d1, _lib.ptr(out), rows, ld, _s(stream))
+    return out
+
+
+def global_hint(dbt, A_dev, n, qmask, stream=None):
+    rows, ld = dbt.shape
+    H = torch.empty((rows, n), dtype=torch.int32, device=dbt.device)
+    _lib.call("zpir_global_hint", _lib.ptr(dbt), rows, ld, _lib.ptr(A_dev), A_dev.shape[1], n,
+              _lib.ptr(H), qmask, _s(stream))
+    return H
+
+
+def gemv(dbt, qu_dev, qmask, out=None, ws=None, stream=None):
+    """b = DB * qu mod 2^32 for qu of shape (nvec, ld) (int32 bits)."""
+    rows, ld = dbt.shape
+    nvec = qu_dev.shape[0]
+    if out is None:
+        out = torch.empty((nvec, rows), dtype=torch.int32, device=dbt.device)
+    if ws is None:
+        ws = torch.empty(int(_lib.lib().zpir_gemv_workspace_bytes(ld, nvec)) // 4,
+                         dtype=torch.int32, device=dbt.device)
+    _lib.call("zpir_gemv", _lib.ptr(dbt), rows, ld, _lib.ptr(qu_dev), nvec, _lib.ptr(out), qmask,
+              _lib.ptr(ws), _s(stream))
+    return out
+
+
+def answer_rows(H, b, qmask, cko, lm, out=None, stream=None):
+    rows, n = H.shape
+    if out is None:
+        out = torch.empty((rows, lm + 2), dtype=torch.int32, device=H.device)
+    _lib.call("zpir_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(b), qmask, _lib.ptr(cko), lm,
+              _lib.ptr(out), _s(stream))
+    return out
+
+
+def answer_groups(z, d1, cap, groups, kctx, t_ld, out=None, stream=None):
+    lm = kctx.lm
+    nchunks = -(-(cap + lm + 2) // lm)
+    rpow = kctx.d_rpow(nchunks)
+    if out is None:
+        out = torch.empty((groups, t_ld), dtype=torch.int32, device=z.device)
+    _lib.call("zpir_answer_groups", _lib.ptr(z), d1, cap, groups, lm, _lib.ptr(kctx.d_m),
+              kctx.cm.np, _lib.ptr(rpow), nchunks, _lib.ptr(out), t_ld, _s(stream))
+    return out
+
+
+def combine(t, k, kctx, out=None, stream=None):
+    groups = t.shape[0]
+    if out is None:
+        out = torch.empty((groups, kctx.l2), dtype=torch.int32, device=t.device)
+    _lib.call("zpir_combine", _lib.ptr(t), _lib.ptr(k), groups, kctx.l2, _lib.ptr(kctx.d_m2),
+              kctx.c2.np, _lib.ptr(kctx.d_r2sq), _lib.ptr(kctx.d_mr), _lib.ptr(out), _s(stream))
+    return out
+
+
+def mulmod(a, b, limbs, d_n, np_, d_r2, stream=None):
+    count = a.shape[0]
+    out = torch.empty_like(a)
+    _lib.call("zpir_mulmod", _lib.ptr(a), _lib.ptr(b), count, limbs, _lib.ptr(d_n), np_,
+              _lib.ptr(d_r2), _lib.ptr(out), _s(stream))
+    return out
+
+
+def multiexp(bases, E, rows, rs, bs, ls, elimbs, kctx, stream=None):
+    """rows x (prod_k bases[k]^e(g,k) mod m^2); bases (n, l2) canonical."""
+    n = bases.shape[0]
+    l2 = kctx.l2
+    ws_bytes = int(_lib.lib().zpir_multiexp_workspace_bytes(n, rows, elimbs, l2))
+    ws = torch.empty(ws_bytes // 4 + 64, dtype=torch.int32, device=bases.device)
+    out = torch.empty((rows, l2), dtype=torch.int32, device=bases.device)
+    _lib.call("zpir_multiexp", _lib.ptr(bases), n, _lib.ptr(E), rows, rs, bs, ls, elimbs, l2,
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_r2sq), _lib.ptr(out),
+              _lib.ptr(ws), ws_bytes, _s(stream))
+    return out

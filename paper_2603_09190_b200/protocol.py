@@ -1,0 +1,308 @@
+"""ZipPIR server protocol on the B200 path: drop-in for the reference's
+ServerGlobalState / hint / respond (protocol.py:159-365).
+
+Same names, argument meaning, return types and exceptions as the reference:
+  ServerGlobalState(params, db, basis=None, db_version=0)  ValueError on
+      shape / symbol range (protocol.py:166-169)
+  hint(state, reg, query_index) -> ClientHint              (protocol.py:291-296)
+  respond(state, reg, qmsg, mode=None, timings=None)       ValueError on
+      dimensions / mode, KeyError on a missing or stale hint (:337-341),
+      timings keys db_matvec / hint_matvec / total (:361-364), COMBINED
+      bumps exactly d1' adds and 0 modexp (counters)
+Objects from the reference package (ProtocolParams, ClientRegistration,
+QueryMessage, ...) are accepted too: only their attributes are read.
+
+Device state per database (built once, swapped whole on update):
+  dbt  u8  (rows, ld)  DB = db^T, rows = d1 padded to whole groups and 128,
+                       ld = d0 padded to 64  (1 GiB at BASELINE config 2)
+  H    u32 (rows, n)   global hint -DB A mod q (128 MiB at config 2)
+  A    u32 (ld, lda)   public matrix, kept for incremental row updates
+There is no CPU fallback: without the CUDA library or a GPU every entry point
+raises.
+"""
+
+from dataclasses import dataclass, field
+import hashlib
+import threading
+import time
+
+import numpy as np
+import torch
+
+from . import counters, device
+from .bigint import ints_to_limbs, key_ctx, limbs_to_ints
+from .paillier import PaillierCiphertext, PaillierPublicKey, sample_ciphertext  # noqa: F401
+from .params import Layout, LweParams, ProtocolParams  # noqa: F401
+from .prg import Stream, DOM_PUBLIC_MATRIX
+
+SEPARATE = "separate"
+COMBINED = "combined"
+
+
+@dataclass
+class HintRequest:
+    pk: PaillierPublicKey
+    seed: bytes
+
+
+@dataclass
+class QueryMessage:
+    client_id: bytes
+    query_index: int
+    mode: str
+    ck_o: list       # n integers in [0, m)
+    qu0: np.ndarray  # d0 integers in [0, q)
+
+
+@dataclass
+class ClientHint:
+    query_index: int
+    db_version: int
+    entries: list    # d1' PaillierCiphertexts
+    # device copy of the entries (groups x l2 u32 limbs), kept for COMBINED
+    dev: object = field(default=None, repr=False, compare=False)
+
+
+@dataclass
+class ResponseMessage:
+    mode: str
+    query_index: int
+    t: list
+    k: list
+
+
+@dataclass
+class ClientRegistration:
+    pk: PaillierPublicKey
+    seed: bytes
+    client_id: bytes
+    hints: dict = field(default_factory=dict)
+    consumed: set = field(default_factory=set)
+
+
+def client_id_of(pk) -> bytes:
+    return hashlib.sha256(pk.serialize()).digest()
+
+
+class _Staging(threading.local):
+    """Per-thread pinned host buffers for the per-query H2D / D2H copies."""
+
+    def __init__(self):
+        self.bufs = {}
+
+    def get(self, key, nbytes):
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8).pin_memory()
+            self.bufs[key] = buf
+        return buf[:nbytes]
+
+
+_staging = _Staging()
+
+
+def _h2d(arr: np.ndarray, dev, key, stream) -> torch.Tensor:
+    """Host array -> device tensor (same bytes, int32 view for u32 data)."""
+    raw = np.ascontiguousarray(arr)
+    pinned = _staging.get(key, raw.nbytes)
+    pinned.numpy()[:] = raw.view(np.uint8).reshape(-1)
+    out = torch.empty(raw.nbytes, dtype=torch.uint8, device=dev)
+    with torch.cuda.stream(stream):
+        out.copy_(pinned, non_blocking=True)
+    return out
+
+
+def _d2h_u32(t: torch.Tensor, key, stream) -> np.ndarray:
+    nbytes = t.numel() * 4
+    pinned = _staging.get(key, nbytes)
+    with torch.cuda.stream(stream):
+        pinned.copy_(t.reshape(-1).view(torch.uint8), non_blocking=True)
+    stream.synchronize()
+    return pinned.numpy().view(np.uint32).reshape(t.shape).copy()
+
+
+class ServerGlobalState:
+    """Database-derived state, immutable between update_database calls."""
+
+    def __init__(self, params, db, basis=None, db_version: int = 0, device_=None):
+        lwe = params.lwe
+        db = np.asarray(db)
+        if db.shape != (params.d0, params.d1):
+            raise ValueError("database shape mismatch")
+        if int(db.max(initial=0)) >= lwe.p:
+            raise ValueError("database symbol out of range")
+        self.params = params
+        self.db = db
+        self.db_version = db_version
+        self.basis = basis  # accepted for API compatibility; no RNS on this path
+        lay = self.layout = Layout(params)
+        dev = self.device = device.require_cuda(device_)
+        stream = torch.cuda.current_stream(dev)
+        n, d0, d1 = lay.n, lay.d0, lay.d1
+        A32 = Stream(params.a_seed, DOM_PUBLIC_MATRIX).words32(d0 * n).reshape(d0, n)
+        self._A32 = A32
+        self._A64 = None
+        A_pad = np.zeros((lay.ld, lay.lda), dtype=np.uint32)
+        A_pad[:d0, :n] = A32
+        t0 = time.perf_counter()
+        self.A_dev = device.u32_tensor(A_pad, dev)
+        db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+        self.dbt = device.transpose_db(db_dev, d0, d1, lay.rows, lay.ld, stream)
+        del db_dev
+        self.H_dev = device.global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
+        stream.synchronize()
+        self.hint_time = time.perf_counter() - t0
+        self._H_host = None
+        self._H_scaled = None
+        self._lock = threading.Lock()
+
+    # -- reference-compatible views (materialised lazily on the host) ------
+
+    @property
+    def A(self) -> np.ndarray:
+        if self._A64 is None:
+            self._A64 = self._A32.astype(np.uint64)
+        return self._A64
+
+    @property
+    def H(self) -> np.ndarray:
+        with self._lock:
+            if self._H_host is None:
+                h = device.to_host_u32(self.H_dev[: self.layout.d1])
+                self._H_host = h.astype(np.uint64)
+            return self._H_host
+
+    @property
+    def H_scaled(self) -> list:
+        """d1' rows of packed big integers (protocol.py:219-238), host view."""
+        with self._lock:
+            if self._H_scaled is None:
+                lay = self.layout
+                h = device.to_host_u32(self.H_dev[: lay.groups * lay.cap])
+                rows = []
+                for g in range(lay.groups):
+                    blk = np.ascontiguousarray(h[g * lay.cap:(g + 1) * lay.cap].astype("<u4").T)
+                    rows.append([int.from_bytes(blk[i].tobytes(), "little") for i in range(lay.n)])
+                self._H_scaled = rows
+            return self._H_scaled
+
+    # -- online path -------------------------------------------------------
+
+    def _stage_query(self, qu, stream):
+        lay = self.layout
+        qu = np.asarray(qu)
+        if qu.shape != (lay.d0,):
+            raise ValueError("query dimensions do not match the parameters")
+        q32 = np.zeros(lay.ld, dtype=np.uint32)
+        q32[: lay.d0] = qu.astype(np.uint64) & np.uint64(0xFFFFFFFF)
+        return _h2d(q32, self.device, "qu", stream).view(torch.int32).reshape(1, lay.ld)
+
+    def db_matvec(self, qu) -> np.ndarray:
+        """b = db^T qu mod q (protocol.py:242-257), uint64 (d1,)."""
+        stream = torch.cuda.current_stream(self.device)
+        qd = self._stage_query(qu, stream)
+        b = device.gemv(self.dbt, qd, self.layout.qmask, stream=stream)
+        return _d2h_u32(b[0, : self.layout.d1], "b", stream).astype(np.uint64)
+
+    def scaled_b(self, b) -> list:
+        """Group b into d1' packed integers (protocol.py:259-269), host view."""
+        lay = self.layout
+        arr = np.asarray(b, dtype=np.uint64).astype("<u4")
+        return [int.from_bytes(arr[g * lay.cap:(g + 1) * lay.cap].tobytes(), "little")
+                for g in range(lay.groups)]
+
+    def answer_device(self, qu_dev, cko_dev, kctx, t_ld, stream, events=None):
+        """t (groups x t_ld u32 limbs) for one staged query; all on device."""
+        lay = self.layout
+        if events:
+            events[0].record(stream)
+        b = device.gemv(self.dbt, qu_dev, lay.qmask, stream=stream)
+        if events:
+            events[1].record(stream)
+        z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, kctx.lm, stream=stream)
+        t = device.answer_groups(z, lay.d1, lay.cap, lay.groups, kctx, t_ld, stream=stream)
+        if events:
+            events[2].record(stream)
+        return t
+
+
+def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
+    """The seeded compression-key ciphertexts for one query index (protocol.py:285-288)."""
+    return [sample_ciphertext(pk, seed, (query_index << 32) | i) for i in range(n)]
+
+
+def hint(state: ServerGlobalState, reg, query_index: int, stream=None) -> ClientHint:
+    """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups in one
+    device multi-exponentiation; exponents read in place from H."""
+    lay = state.layout
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    kctx = key_ctx(reg.pk.m, dev)
+    ck_r = [c.c for c in derive_ck_r(reg.pk, reg.seed, query_index, lay.n)]
+    bases = _h2d(ints_to_limbs(ck_r, kctx.l2), dev, "bases", stream).view(torch.int32)
+    bases = bases.reshape(lay.n, kctx.l2)
+    out = device.multiexp(bases, state.H_dev, lay.groups, lay.cap * lay.n, 1, lay.n, lay.cap,
+                          kctx, stream)
+    entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
+    counters.bump("group_mult", lay.groups * lay.n)
+    return ClientHint(query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
+                      dev=out)
+
+
+def _stored_device(stored, kctx, dev, stream):
+    d = getattr(stored, "dev", None)
+    if d is not None and d.device == dev and d.shape[1] == kctx.l2:
+        return d
+    vals = [(c.c if hasattr(c, "c") else int(c)) % kctx.m2 for c in stored.entries]
+    d = _h2d(ints_to_limbs(vals, kctx.l2), dev, "k", stream).view(torch.int32)
+    return d.reshape(len(vals), kctx.l2)
+
+
+def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
+            stream=None) -> ResponseMessage:
+    lay = state.layout
+    mode = mode or qmsg.mode
+    if len(qmsg.ck_o) != lay.n or len(qmsg.qu0) != lay.d0:
+        raise ValueError("query dimensions do not match the parameters")
+    stored = reg.hints.get(qmsg.query_index)
+    if stored is None or stored.db_version != state.db_version:
+        raise KeyError("no hint for this query index and database version")
+    if mode not in (SEPARATE, COMBINED):
+        raise ValueError("unknown response mode")
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    kctx = key_ctx(reg.pk.m, dev)
+    t_total = time.perf_counter()
+    events = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timings is not None else None
+    qu_dev = state._stage_query(qmsg.qu0, stream)
+    cko = _h2d(ints_to_limbs(qmsg.ck_o, kctx.lm), dev, "cko", stream).view(torch.int32)
+    cko = cko.reshape(lay.n, kctx.lm)
+    if mode == SEPARATE:
+        t_dev = state.answer_device(qu_dev, cko, kctx, kctx.lm, stream, events)
+        t = limbs_to_ints(_d2h_u32(t_dev, "t", stream))
+        out = ResponseMessage(SEPARATE, qmsg.query_index, t, stored.entries)
+    else:
+        t_dev = state.answer_device(qu_dev, cko, kctx, kctx.l2, stream, events)
+        k_dev = _stored_device(stored, kctx, dev, stream)
+        K = device.combine(t_dev, k_dev, kctx, stream=stream)
+        vals = limbs_to_ints(_d2h_u32(K, "K", stream))
+        counters.bump("add", lay.groups)
+        counters.bump("group_mult", lay.groups)
+        out = ResponseMessage(COMBINED, qmsg.query_index, [], [PaillierCiphertext(v) for v in vals])
+    if timings is not None:
+        stream.synchronize()
+        timings["db_matvec"] = events[0].elapsed_time(events[1]) / 1e3
+        timings["hint_matvec"] = events[1].elapsed_time(events[2]) / 1e3
+        timings["total"] = time.perf_counter() - t_total
+    return out
+
+
+def client_storage_hint_transfer(reg, query_index: int) -> ClientHint:
+    """Hand the stored hint to the client; single use (protocol.py:399-408)."""
+    if query_index in reg.consumed:
+        raise ValueError("hint already consumed")
+    h = reg.hints.get(query_index)
+    if h is None:
+        raise KeyError("no hint for this query index")
+    reg.consumed.add(query_index)
+    return h
