@@ -90,6 +90,36 @@ int zpir_multiexp(const uint32_t* bases, int64_t n, const uint32_t* exps, int64_
                   int limbs, const uint32_t* N, uint32_t np, const uint32_t* r2, uint32_t* out,
                   void* workspace, int64_t ws_bytes, void* stream);
 
+/* ---- tcgen05 (UMMA kind::i8) engine -------------------------------------
+ * Query byte planes: planes[(4v+l)*ld + i] = byte l of qu[v*ld + i], rows
+ * 4*nvec .. prow-1 zeroed (prow = 16 for nvec <= 4, 256 for nvec <= 64). */
+int zpir_query_planes(const uint32_t* qu, int64_t ld, int64_t nvec, uint8_t* planes, int64_t prow,
+                      void* stream);
+
+/* b[v*rows + r] = (dbt * qu_v)[r] mod 2^32 on the tensor cores (stream-K
+ * split, wrapping atomics). Same contract as zpir_gemv (protocol.py:242-257),
+ * planes from zpir_query_planes. nvec <= 64 (batched queries). */
+int zpir_umma_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* planes,
+                   int64_t nvec, uint32_t* b, void* stream);
+
+/* A byte planes: aplanes[(4k+l)*ld + i] = byte l of A[i*lda + k]. */
+int zpir_build_aplanes(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* aplanes,
+                       void* stream);
+
+/* Global hint on the tensor cores, H[r*n + k] = qmask & -(dbt A)[r,k]
+ * (protocol.py:195-217); n % 64 == 0. */
+int zpir_umma_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* aplanes,
+                          int64_t n, uint32_t* H, uint32_t qmask, void* stream);
+
+/* Compression operand: bc[b*4n + 4k + a] = byte (b-a) of ck_o[k], b < nb
+ * (nb = 16*ceil((4 lm + 3)/16): 144 / 272 / 400 for lm = 32 / 64 / 96). */
+int zpir_build_bc(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, void* stream);
+
+/* Row stage of the answer compression on the tensor cores: same contract as
+ * zpir_answer_rows with wz = lm + 2 (rns.py:163-188 replacement). */
+int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
+                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,16 @@ int multiexp_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
                     int, int, const uint32_t*, uint32_t, const uint32_t*, uint32_t*, void*,
                     int64_t, cudaStream_t);
 
+int query_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t);
+int umma_gemv_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int64_t, uint32_t*,
+                     cudaStream_t);
+int umma_hint_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int64_t, uint32_t*,
+                     uint32_t, cudaStream_t);
+int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, int,
+                            const uint32_t*, uint32_t, int, uint32_t*, cudaStream_t);
+int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
+int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
+
 }  // namespace zpir
 
 using namespace zpir;
@@ -109,6 +119,35 @@ int zpir_multiexp(const uint32_t* bases, int64_t n, const uint32_t* exps, int64_
                   void* workspace, int64_t ws_bytes, void* stream) {
   ZPIR_GUARD(multiexp_launch(bases, n, exps, rows, row_stride, base_stride, limb_stride, elimbs,
                              limbs, N, np, r2, out, workspace, ws_bytes, S(stream)));
+}
+
+int zpir_query_planes(const uint32_t* qu, int64_t ld, int64_t nvec, uint8_t* planes, int64_t prow,
+                      void* stream) {
+  ZPIR_GUARD(query_planes_launch(qu, ld, nvec, planes, prow, S(stream)));
+}
+
+int zpir_umma_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* planes,
+                   int64_t nvec, uint32_t* b, void* stream) {
+  ZPIR_GUARD(umma_gemv_launch(dbt, rows, ld, planes, nvec, b, S(stream)));
+}
+
+int zpir_build_aplanes(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* aplanes,
+                       void* stream) {
+  ZPIR_GUARD(build_aplanes_launch(A, ld, lda, n, aplanes, S(stream)));
+}
+
+int zpir_umma_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* aplanes,
+                          int64_t n, uint32_t* H, uint32_t qmask, void* stream) {
+  ZPIR_GUARD(umma_hint_launch(dbt, rows, ld, aplanes, n, H, qmask, S(stream)));
+}
+
+int zpir_build_bc(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, void* stream) {
+  ZPIR_GUARD(build_bc_launch(cko, n, lm, nb, bc, S(stream)));
+}
+
+int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
+                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, void* stream) {
+  ZPIR_GUARD(umma_answer_rows_launch(H, rows, n, bc, nb, b, qmask, wz, z, S(stream)));
 }
 
 }  // extern "C"

@@ -100,6 +100,23 @@ __global__ void mask_kernel(uint32_t* x, int64_t count, uint32_t mask) {
   if (i < count) x[i] &= mask;
 }
 
+// planes (prow x ld bytes): rows 4v+l = byte plane l of query v, zero rows
+// 4*nvec .. prow-1 (the B operand of the tcgen05 GEMV).
+int query_planes_launch(const uint32_t* qu, int64_t ld, int64_t nvec, uint8_t* planes,
+                        int64_t prow, cudaStream_t st) {
+  if (ld % 64 || prow < 4 * nvec) {
+    set_error("query_planes: ld %% 64 and prow >= 4 nvec required");
+    return kErrInput;
+  }
+  const int64_t words = ld / 4;
+  if (prow > 4 * nvec &&
+      cudaMemsetAsync(planes + 4 * nvec * ld, 0, (prow - 4 * nvec) * ld, st) != cudaSuccess)
+    return check_launch("query_planes memset");
+  qplanes_kernel<<<(unsigned)ceil_div(words, 256), 256, 0, st>>>(
+      qu, words, nvec, reinterpret_cast<uint32_t*>(planes));
+  return check_launch("query_planes");
+}
+
 int gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* qu, int64_t nvec,
                 uint32_t* out, uint32_t qmask, uint32_t* qp, cudaStream_t st) {
   constexpr int R = 8;

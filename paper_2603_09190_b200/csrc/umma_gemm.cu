@@ -1,0 +1,491 @@
+// tcgen05 (UMMA) int8 GEMM with byte-limb epilogues -- the tensor-core engine
+// behind the online GEMV, batched queries, the global hint and the answer
+// compression.
+//
+//   P[r, j] = sum_k A[r, k] * B[j, k]      u8 x u8 -> s32 in TMEM (kind::i8)
+//
+// A = DB (rows x ld bytes) or H viewed as bytes (rows x 4n); B holds byte
+// planes of the other operand so that every 32-bit quantity is an exact sum
+// of shifted byte products:
+//   * u32 vector x (query qu, or a column of A): plane l = byte l of x, and
+//     sum_l 2^(8l) P[r, 4v+l] = (A x_v)[r] (mod 2^32)          -> LIMB modes
+//   * big integer ck_o[k] (lm 32-bit limbs): H[r,k] = sum_a 2^(8a) byte_a,
+//     B[b, (k,a)] = byte_(b-a)(ck_o[k]) so sum_b 2^(8b) P[r, b]
+//     = sum_k H[r,k] ck_o[k] = y_r exactly                      -> BIGINT mode
+// Every product is < 2^16 and the K extents keep s32 partial sums far below
+// 2^31 for the BIGINT mode (4n <= 2^14 bytes: < 2^30); the LIMB modes only
+// need sums mod 2^32, which wrapping s32 accumulation (no .satfinite) gives.
+//
+// Kernel structure (one CTA per SM, 192 threads, persistent):
+//   warp 0  TMA producer: A tile 128 x 128 B and B tile NT x 128 B per stage,
+//           SWIZZLE_128B, mbarrier complete_tx
+//   warp 1  TMEM allocator + single-thread MMA issuer: 4 x (M=128, N<=256,
+//           K=32) MMAs per 128-byte k-block, tcgen05.commit frees the stage
+//   warps 2-5  epilogue: tcgen05.ld 32x32b (warp w owns TMEM lanes 32(w%4)..)
+//           -> limb recombination -> global (store or wrapping atomic add)
+// Work: persistent CTAs walk a contiguous range of (tile, k-block) units
+// ("stream-K", split = 1; exact because the LIMB outputs are sums mod 2^32
+// and are combined with wrapping atomics) or of whole tiles (split = 0).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "umma.cuh"
+
+namespace zpir {
+
+using namespace sm100;
+
+enum UmmaMode : int {
+  kLimbCols = 0,     // out[(n*NT/4 + j) * ldo + r]  (+)= sum_l P[r,4j+l] << 8l
+  kLimbRowsNeg = 1,  // out[r * ldo + n*NT/4 + j]  = qmask & -(sum_l ...)   (whole tiles)
+  kBigint = 2        // z[r * wz + i] = limbs of (b[r] & qmask) + sum_b P[r,b] << 8b
+};
+
+struct UmmaArgs {
+  int m_tiles, n_tiles, kblocks;
+  int split;
+  uint32_t* out;
+  int64_t ldo;
+  int nout;
+  uint32_t qmask;
+  const uint32_t* b;
+  int wz;
+};
+
+constexpr int kBM = 128;   // rows per tile (TMEM lanes)
+constexpr int kBK = 128;   // bytes of K per stage (one 128-byte swizzle row)
+constexpr int kThreads = 192;
+
+template <int NT>
+struct UmmaCfg {
+  static constexpr int kABytes = kBM * kBK;
+  static constexpr int kBBytes = NT * kBK;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = std::min(12, (200 * 1024) / kStageBytes);
+  static constexpr int kAcc = (2 * NT <= 512) ? 2 : 1;
+  static constexpr int kTmemCols = (kAcc * NT <= 32) ? 32 : (kAcc * NT <= 64) ? 64
+                                 : (kAcc * NT <= 128) ? 128 : (kAcc * NT <= 256) ? 256 : 512;
+  // TMA box height for B: largest multiple-of-8 divisor of NT that is <= 256
+  static constexpr int boxB() {
+    for (int h = 256; h >= 8; h -= 8)
+      if (NT % h == 0) return h;
+    return 8;
+  }
+  static constexpr int kBoxB = boxB();
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
+
+struct SegIter {
+  int64_t u, u1;
+  int kb;
+  bool split;
+  __device__ bool next(int64_t& t, int& k0, int& k1) {
+    if (u >= u1) return false;
+    if (split) {
+      t = u / kb;
+      k0 = (int)(u - t * kb);
+      const int64_t left = u1 - u;
+      k1 = (int)((int64_t)kb < k0 + left ? (int64_t)kb : k0 + left);
+      u += k1 - k0;
+    } else {
+      t = u;
+      k0 = 0;
+      k1 = kb;
+      u += 1;
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ SegIter seg_range(const UmmaArgs& a) {
+  const int64_t T = (int64_t)a.m_tiles * a.n_tiles;
+  const int64_t U = a.split ? T * a.kblocks : T;
+  const int64_t G = gridDim.x, s = blockIdx.x;
+  SegIter it;
+  it.u = s * U / G;
+  it.u1 = (s + 1) * U / G;
+  it.kb = a.kblocks;
+  it.split = a.split != 0;
+  return it;
+}
+
+template <int NT, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                 const UmmaArgs args) {
+  using C = UmmaCfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kAcc;
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(tempty + C::kAcc);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::kAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tbase_smem, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tbase_smem;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const uint64_t pol_a = l2_evict_first();
+      SegIter it = seg_range(args);
+      int64_t t;
+      int k0, k1, stage = 0;
+      uint32_t phase = 0;
+      while (it.next(t, k0, k1)) {
+        const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+        for (int kb = k0; kb < k1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::kStageBytes);
+          tma_load_2d_hint(sA + stage * C::kABytes, &mapA, &full[stage], kb * kBK, m * kBM, pol_a);
+#pragma unroll
+          for (int p = 0; p < NT / C::kBoxB; ++p)
+            tma_load_2d(sB + stage * C::kBBytes + p * C::kBoxB * kBK, &mapB, &full[stage],
+                        kb * kBK, n * NT + p * C::kBoxB);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      SegIter it = seg_range(args);
+      int64_t t;
+      int k0, k1, stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      while (it.next(t, k0, k1)) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * NT);
+        for (int kb = k0; kb < k1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k) {
+            const uint64_t ad = desc_sw128(a0 + k * 32);
+#pragma unroll
+            for (int p = 0; p < (NT + 255) / 256; ++p) {
+              const int np_ = (NT - p * 256) < 256 ? (NT - p * 256) : 256;
+              const uint64_t bd = desc_sw128(b0 + p * 256 * kBK + k * 32);
+              umma_i8(d + p * 256, ad, bd, idesc_u8(kBM, np_), (kb > k0 || k > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == C::kAcc) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5, 128 threads) ----------------
+    const int quarter = warp & 3;
+    const int lrow = quarter * 32 + lane;
+    SegIter it = seg_range(args);
+    int64_t t;
+    int k0, k1, acc = 0;
+    uint32_t aphase = 0;
+    while (it.next(t, k0, k1)) {
+      const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+      const int64_t row = (int64_t)m * kBM + lrow;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * NT);
+      if constexpr (MODE == kLimbCols || MODE == kLimbRowsNeg) {
+        const bool partial = args.split != 0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c0, r);
+          tmem_wait_ld();
+          uint32_t v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            v[j] = r[4 * j] + (r[4 * j + 1] << 8) + (r[4 * j + 2] << 16) + (r[4 * j + 3] << 24);
+          const int jg = n * (NT / 4) + c0 / 4;
+          if constexpr (MODE == kLimbCols) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (c0 / 4 + j < args.nout) {
+                uint32_t* dst = args.out + (int64_t)(jg + j) * args.ldo + row;
+                if (partial) atomicAdd(dst, v[j]);
+                else *dst = v[j];
+              }
+            }
+          } else {
+            uint4 w = make_uint4((0u - v[0]) & args.qmask, (0u - v[1]) & args.qmask,
+                                 (0u - v[2]) & args.qmask, (0u - v[3]) & args.qmask);
+            if (jg + 3 < args.nout) {
+              *reinterpret_cast<uint4*>(args.out + row * args.ldo + jg) = w;
+            } else {
+              const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+              for (int j = 0; j < 4; ++j)
+                if (jg + j < args.nout) args.out[row * args.ldo + jg + j] = wv[j];
+            }
+          }
+        }
+      } else {
+        // BIGINT: z_r = (b_r & qmask) + sum_b P[r, b] 2^(8b), carry-propagated
+        unsigned long long carry = args.b[row] & args.qmask;
+        uint32_t* zr = args.out + row * args.wz;
+#pragma unroll 1
+        for (int c0 = 0; c0 < NT; c0 += 16) {
+          uint32_t r[16];
+          tmem_ld16(taddr + c0, r);
+          tmem_wait_ld();
+          uint32_t limb[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned long long s = (unsigned long long)r[4 * i] +
+                                         ((unsigned long long)r[4 * i + 1] << 8) +
+                                         ((unsigned long long)r[4 * i + 2] << 16) +
+                                         ((unsigned long long)r[4 * i + 3] << 24) + carry;
+            limb[i] = (uint32_t)s;
+            carry = s >> 32;
+          }
+          const int li = c0 / 4;
+          if (li + 3 < args.wz) {
+            *reinterpret_cast<uint4*>(zr + li) = make_uint4(limb[0], limb[1], limb[2], limb[3]);
+          } else {
+            for (int i = 0; i < 4; ++i)
+              if (li + i < args.wz) zr[li + i] = limb[i];
+          }
+        }
+        for (int li = NT / 4; li < args.wz; ++li) {
+          zr[li] = (uint32_t)carry;
+          carry >>= 32;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == C::kAcc) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// operand builders
+
+// Bc[b * (4n) + 4k + a] = byte (b - a) of ck_o[k] (0 outside [0, 4 lm)), b < nb.
+__global__ void build_bc_kernel(const uint32_t* __restrict__ cko, int64_t n, int lm, int nb,
+                                uint32_t* __restrict__ bc) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (k >= n) return;
+  const uint32_t* c = cko + k * lm;
+  uint32_t w = 0;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int j = b - a;
+    if (j >= 0 && j < 4 * lm) w |= ((c[j >> 2] >> (8 * (j & 3))) & 0xffu) << (8 * a);
+  }
+  bc[(int64_t)b * n + k] = w;
+}
+
+// Ap[(4k + l) * ld + i] = byte l of A[i * lda + k], k < n, i < ld.
+__global__ void __launch_bounds__(256)
+build_aplanes_kernel(const uint32_t* __restrict__ A, int64_t ld, int64_t lda, int64_t n,
+                     uint8_t* __restrict__ ap) {
+  __shared__ uint32_t tile[64][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 64, k0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int r = ty; r < 64; r += 8) {
+    const int64_t i = i0 + r, k = k0 + tx;
+    tile[r][tx] = (i < ld && k < n) ? A[i * lda + k] : 0u;
+  }
+  __syncthreads();
+  // thread -> (k = k0 + c, quad q of 4 consecutive i), writes 4 plane words
+  for (int idx = threadIdx.x; idx < 32 * 16; idx += 256) {
+    const int c = idx >> 4, q = idx & 15;
+    const int64_t k = k0 + c;
+    if (k >= n || i0 + 4 * q >= ld) continue;
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      uint32_t w = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w |= ((tile[4 * q + e][c] >> (8 * l)) & 0xffu) << (8 * e);
+      *reinterpret_cast<uint32_t*>(ap + (4 * k + l) * ld + i0 + 4 * q) = w;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D u8 tensor (rows x cols, row pitch `pitch` bytes), box = box_rows x 128 bytes.
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t pitch,
+                    int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return kErrCuda;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld pitch=%lld box=%d", (int)r,
+              (long long)rows, (long long)cols, (long long)pitch, box_rows);
+    return kErrCuda;
+  }
+  return kOk;
+}
+
+static int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+template <int NT, int MODE>
+static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes, const uint8_t* B,
+                    int64_t brows, int64_t ldb_bytes, UmmaArgs args, cudaStream_t st) {
+  using Cfg = UmmaCfg<NT>;
+  if (rows % kBM || brows % NT) {
+    set_error("umma: rows %% 128 / brows %% NT (rows=%lld brows=%lld NT=%d)", (long long)rows,
+              (long long)brows, NT);
+    return kErrInput;
+  }
+  CUtensorMap ma, mb;
+  if (int e = make_map(&ma, A, rows, K, lda_bytes, kBM)) return e;
+  if (int e = make_map(&mb, B, brows, K, ldb_bytes, Cfg::kBoxB)) return e;
+  args.m_tiles = (int)(rows / kBM);
+  args.n_tiles = (int)(brows / NT);
+  args.kblocks = (int)ceil_div(K, kBK);
+  const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
+  const int64_t U = args.split ? T * args.kblocks : T;
+  const int grid = (int)std::min<int64_t>(num_sms(), U);
+  auto kern = umma_gemm_kernel<NT, MODE>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mb, args);
+  return check_launch("umma_gemm");
+}
+
+// b[v * rows + r] = qmask & (DB qu_v)[r] for nvec <= 4 (N = 16) or 64 (N = 256)
+int umma_gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* qplanes,
+                     int64_t nvec, uint32_t* out, cudaStream_t st) {
+  if (cudaMemsetAsync(out, 0, rows * nvec * sizeof(uint32_t), st) != cudaSuccess)
+    return check_launch("umma_gemv memset");
+  UmmaArgs a{};
+  a.split = 1;
+  a.out = out;
+  a.ldo = rows;
+  a.nout = (int)nvec;
+  a.qmask = 0xffffffffu;
+  if (nvec <= 4) return umma_run<16, kLimbCols>(dbt, rows, ld, ld, qplanes, 16, ld, a, st);
+  if (nvec <= 64) return umma_run<256, kLimbCols>(dbt, rows, ld, ld, qplanes, 256, ld, a, st);
+  set_error("umma_gemv: at most 64 query vectors per launch (got %lld)", (long long)nvec);
+  return kErrInput;
+}
+
+// H[r * n + k] = qmask & -(DB A)[r, k]; aplanes = (4n x ld) byte planes of A.
+int umma_hint_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* aplanes,
+                     int64_t n, uint32_t* H, uint32_t qmask, cudaStream_t st) {
+  if ((4 * n) % 256) {
+    set_error("umma_hint: 4n must be a multiple of 256 (n=%lld)", (long long)n);
+    return kErrUnsupported;
+  }
+  UmmaArgs a{};
+  a.split = 0;
+  a.out = H;
+  a.ldo = n;
+  a.nout = (int)n;
+  a.qmask = qmask;
+  return umma_run<256, kLimbRowsNeg>(dbt, rows, ld, ld, aplanes, 4 * n, ld, a, st);
+}
+
+// z[r * wz + i] = limbs of (b[r] & qmask) + sum_k H[r,k] ck_o[k]; bc from build_bc.
+int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
+                            const uint32_t* b, uint32_t qmask, int wz, uint32_t* z,
+                            cudaStream_t st) {
+  UmmaArgs a{};
+  a.split = 0;
+  a.out = z;
+  a.b = b;
+  a.qmask = qmask;
+  a.wz = wz;
+  const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
+  switch (nb) {
+    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st);
+    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st);
+    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st);
+    default:
+      set_error("umma_answer_rows: unsupported B width %d", nb);
+      return kErrUnsupported;
+  }
+}
+
+int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)nb);
+  build_bc_kernel<<<grid, 256, 0, st>>>(cko, n, lm, nb, reinterpret_cast<uint32_t*>(bc));
+  return check_launch("build_bc");
+}
+
+int build_aplanes_launch(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* ap,
+                         cudaStream_t st) {
+  dim3 grid((unsigned)ceil_div(ld, 64), (unsigned)ceil_div(n, 32));
+  build_aplanes_kernel<<<grid, 256, 0, st>>>(A, ld, lda, n, ap);
+  return check_launch("build_aplanes");
+}
+
+}  // namespace zpir

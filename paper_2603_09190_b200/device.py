@@ -111,3 +111,51 @@ def multiexp(bases, E, rows, rs, bs, ls, elimbs, kctx, stream=None):
               _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_r2sq), _lib.ptr(out),
               _lib.ptr(ws), ws_bytes, _s(stream))
     return out
+
+
+# ---- tcgen05 (UMMA) engine ----------------------------------------------------
+
+UMMA_NB = {32: 144, 64: 272, 96: 400}
+
+
+def query_planes(qu_dev, prow, stream=None):
+    nvec, ld = qu_dev.shape
+    planes = torch.empty((prow, ld), dtype=torch.uint8, device=qu_dev.device)
+    _lib.call("zpir_query_planes", _lib.ptr(qu_dev), ld, nvec, _lib.ptr(planes), prow, _s(stream))
+    return planes
+
+
+def umma_gemv(dbt, planes, nvec, out=None, stream=None):
+    rows, ld = dbt.shape
+    if out is None:
+        out = torch.empty((nvec, rows), dtype=torch.int32, device=dbt.device)
+    _lib.call("zpir_umma_gemv", _lib.ptr(dbt), rows, ld, _lib.ptr(planes), nvec, _lib.ptr(out),
+              _s(stream))
+    return out
+
+
+def umma_global_hint(dbt, A_dev, n, qmask, stream=None):
+    rows, ld = dbt.shape
+    ap = torch.empty((4 * n, ld), dtype=torch.uint8, device=dbt.device)
+    _lib.call("zpir_build_aplanes", _lib.ptr(A_dev), ld, A_dev.shape[1], n, _lib.ptr(ap), _s(stream))
+    H = torch.empty((rows, n), dtype=torch.int32, device=dbt.device)
+    _lib.call("zpir_umma_global_hint", _lib.ptr(dbt), rows, ld, _lib.ptr(ap), n, _lib.ptr(H), qmask,
+              _s(stream))
+    return H
+
+
+def build_bc(cko, lm, stream=None):
+    n = cko.shape[0]
+    nb = UMMA_NB[lm]
+    bc = torch.empty((nb, 4 * n), dtype=torch.uint8, device=cko.device)
+    _lib.call("zpir_build_bc", _lib.ptr(cko), n, lm, nb, _lib.ptr(bc), _s(stream))
+    return bc
+
+
+def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None):
+    rows, n = H.shape
+    if out is None:
+        out = torch.empty((rows, lm + 2), dtype=torch.int32, device=H.device)
+    _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0], _lib.ptr(b),
+              qmask, lm + 2, _lib.ptr(out), _s(stream))
+    return out

@@ -23,6 +23,7 @@ raises.
 
 from dataclasses import dataclass, field
 import hashlib
+import os
 import threading
 import time
 
@@ -37,6 +38,10 @@ from .prg import Stream, DOM_PUBLIC_MATRIX
 
 SEPARATE = "separate"
 COMBINED = "combined"
+
+# "umma": tcgen05 tensor-core engine (default); "cuda_core": the IDP4A / IMAD
+# kernels, kept as the measured alternative (design evidence).
+ENGINE = os.environ.get("ZPIR_ENGINE", "umma")
 
 
 @dataclass
@@ -124,7 +129,8 @@ def _d2h_u32(t: torch.Tensor, key, stream) -> np.ndarray:
 class ServerGlobalState:
     """Database-derived state, immutable between update_database calls."""
 
-    def __init__(self, params, db, basis=None, db_version: int = 0, device_=None):
+    def __init__(self, params, db, basis=None, db_version: int = 0, device_=None,
+                 engine=None):
         lwe = params.lwe
         db = np.asarray(db)
         if db.shape != (params.d0, params.d1):
@@ -149,7 +155,13 @@ class ServerGlobalState:
         db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
         self.dbt = device.transpose_db(db_dev, d0, d1, lay.rows, lay.ld, stream)
         del db_dev
-        self.H_dev = device.global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
+        self.engine = engine or ENGINE
+        if self.engine not in ("umma", "cuda_core"):
+            raise ValueError(f"unknown engine {self.engine!r}")
+        if self.engine == "umma" and n % 64 == 0:
+            self.H_dev = device.umma_global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
+        else:
+            self.H_dev = device.global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
         stream.synchronize()
         self.hint_time = time.perf_counter() - t0
         self._H_host = None
@@ -201,8 +213,17 @@ class ServerGlobalState:
         """b = db^T qu mod q (protocol.py:242-257), uint64 (d1,)."""
         stream = torch.cuda.current_stream(self.device)
         qd = self._stage_query(qu, stream)
-        b = device.gemv(self.dbt, qd, self.layout.qmask, stream=stream)
+        b = self.gemv_device(qd, stream)
         return _d2h_u32(b[0, : self.layout.d1], "b", stream).astype(np.uint64)
+
+    def gemv_device(self, qu_dev, stream):
+        """b (nvec x rows) for staged queries qu_dev (nvec x ld)."""
+        lay = self.layout
+        nvec = qu_dev.shape[0]
+        if self.engine == "umma" and nvec <= 64 and lay.qmask == 0xFFFFFFFF:
+            planes = device.query_planes(qu_dev, 16 if nvec <= 4 else 256, stream)
+            return device.umma_gemv(self.dbt, planes, nvec, stream=stream)
+        return device.gemv(self.dbt, qu_dev, lay.qmask, stream=stream)
 
     def scaled_b(self, b) -> list:
         """Group b into d1' packed integers (protocol.py:259-269), host view."""
@@ -216,10 +237,14 @@ class ServerGlobalState:
         lay = self.layout
         if events:
             events[0].record(stream)
-        b = device.gemv(self.dbt, qu_dev, lay.qmask, stream=stream)
+        b = self.gemv_device(qu_dev, stream)
         if events:
             events[1].record(stream)
-        z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, kctx.lm, stream=stream)
+        if self.engine == "umma" and kctx.lm in device.UMMA_NB:
+            bc = device.build_bc(cko_dev, kctx.lm, stream=stream)
+            z = device.umma_answer_rows(self.H_dev, bc, b[0], lay.qmask, kctx.lm, stream=stream)
+        else:
+            z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, kctx.lm, stream=stream)
         t = device.answer_groups(z, lay.d1, lay.cap, lay.groups, kctx, t_ld, stream=stream)
         if events:
             events[2].record(stream)

@@ -1,0 +1,117 @@
+"""Kernel-level GPU parity through the C ABI: tcgen05 (UMMA) engine vs the
+CUDA-core engine vs the oracle, at shapes the golden cases do not reach:
+K > 2^15 (s32 wrap of the byte-plane sums), ragged d0/d1, all-255 inputs,
+every supported Paillier limb width."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import c as oracle_c
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    from paper_2603_09190_b200 import _lib, build, device
+    build.build()
+    _lib.load()
+    return torch, device
+
+
+def _dbt(torch, device, db, rows, ld):
+    d0, d1 = db.shape
+    dev = torch.device("cuda", 0)
+    db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+    return device.transpose_db(db_dev, d0, d1, rows, ld)
+
+
+def _rup(x, m):
+    return -(-x // m) * m
+
+
+@pytest.mark.parametrize("d0,d1,fill", [(1000, 300, None), (70000, 256, None),
+                                        (66000, 130, 255), (32768, 1024, None)])
+def test_gemv_engines_vs_oracle(env, d0, d1, fill):
+    torch, device = env
+    rng = np.random.default_rng(d0 + d1)
+    db = (np.full((d0, d1), fill, np.uint8) if fill is not None
+          else rng.integers(0, 256, (d0, d1), dtype=np.uint8))
+    qu = (np.full(d0, 0xFFFFFFFF, np.uint64) if fill is not None
+          else rng.integers(0, 1 << 32, d0, dtype=np.uint64))
+    want = oracle_c.db_matvec(db, qu)
+    rows, ld = _rup(d1, 128), _rup(d0, 64)
+    dbt = _dbt(torch, device, db, rows, ld)
+    q = np.zeros((1, ld), np.uint32)
+    q[0, :d0] = qu
+    qd = device.u32_tensor(q, dbt.device)
+    b1 = device.to_host_u32(device.gemv(dbt, qd, 0xFFFFFFFF))[0, :d1]
+    planes = device.query_planes(qd, 16)
+    b2 = device.to_host_u32(device.umma_gemv(dbt, planes, 1))[0, :d1]
+    assert np.array_equal(b1.astype(np.uint64), want)
+    assert np.array_equal(b2.astype(np.uint64), want)
+
+
+@pytest.mark.parametrize("nvec", [3, 64])
+def test_batched_gemv(env, nvec):
+    torch, device = env
+    rng = np.random.default_rng(nvec)
+    d0, d1 = 4096, 512
+    db = rng.integers(0, 256, (d0, d1), dtype=np.uint8)
+    Q = rng.integers(0, 1 << 32, (nvec, d0), dtype=np.uint64)
+    dbt = _dbt(torch, device, db, d1, d0)
+    qd = device.u32_tensor(Q.astype(np.uint32), dbt.device)
+    planes = device.query_planes(qd, 16 if nvec <= 4 else 256)
+    got = device.to_host_u32(device.umma_gemv(dbt, planes, nvec))
+    for v in range(nvec):
+        assert np.array_equal(got[v].astype(np.uint64), ref.db_matvec(db, Q[v], 1 << 32)), v
+
+
+@pytest.mark.parametrize("d0,d1,n", [(777, 130, 256), (4096, 384, 1024), (40000, 128, 64)])
+def test_global_hint_engines(env, d0, d1, n):
+    torch, device = env
+    rng = np.random.default_rng(n)
+    db = rng.integers(0, 256, (d0, d1), dtype=np.uint8)
+    A = rng.integers(0, 1 << 32, (d0, n), dtype=np.uint64)
+    rows, ld, lda = _rup(d1, 128), _rup(d0, 64), _rup(n, 128)
+    dbt = _dbt(torch, device, db, rows, ld)
+    Ap = np.zeros((ld, lda), np.uint32)
+    Ap[:d0, :n] = A
+    Ad = device.u32_tensor(Ap, dbt.device)
+    H1 = device.to_host_u32(device.global_hint(dbt, Ad, n, 0xFFFFFFFF))[:d1]
+    H2 = device.to_host_u32(device.umma_global_hint(dbt, Ad, n, 0xFFFFFFFF))[:d1]
+    cols = sorted({0, 1, d1 // 2, d1 - 1} | set(rng.integers(0, d1, 12).tolist()))
+    want = oracle_c.hint_cols(db, A, cols)
+    assert np.array_equal(H1[cols].astype(np.uint64), want)
+    assert np.array_equal(H2, H1)
+    # pad rows of H are zero (multiexp reads them as zero exponent limbs)
+    assert not device.to_host_u32(device.umma_global_hint(dbt, Ad, n, 0xFFFFFFFF))[d1:].any()
+
+
+@pytest.mark.parametrize("lm,n", [(32, 64), (64, 1024), (96, 256), (64, 4096)])
+def test_answer_rows_engines(env, lm, n):
+    torch, device = env
+    rng = np.random.default_rng(lm * n)
+    rows = 256
+    H = rng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
+    H[0] = 0xFFFFFFFF
+    b = rng.integers(0, 1 << 32, rows, dtype=np.uint64).astype(np.uint32)
+    r = random.Random(lm)
+    ck = [r.randrange(1 << (32 * lm)) for _ in range(n)]
+    ck[0] = (1 << (32 * lm)) - 1
+    from paper_2603_09190_b200.bigint import ints_to_limbs, limbs_to_ints
+    dev = torch.device("cuda", 0)
+    Hd = device.u32_tensor(H, dev)
+    bd = device.u32_tensor(b, dev)
+    cd = device.u32_tensor(ints_to_limbs(ck, lm), dev)
+    z1 = device.to_host_u32(device.answer_rows(Hd, bd, 0xFFFFFFFF, cd, lm))
+    bc = device.build_bc(cd, lm)
+    z2 = device.to_host_u32(device.umma_answer_rows(Hd, bc, bd, 0xFFFFFFFF, lm))
+    assert np.array_equal(z1, z2)
+    zi = limbs_to_ints(z1)
+    for row in (0, 1, 77, 255):
+        assert zi[row] == int(b[row]) + sum(int(h) * c for h, c in zip(H[row], ck))
