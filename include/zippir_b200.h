@@ -51,7 +51,7 @@ int64_t zpir_gemv_workspace_bytes(int64_t ld, int64_t nvec);
 int zpir_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* qu, int64_t nvec,
               uint32_t* b, uint32_t qmask, void* workspace, void* stream);
 
-/* Answer compression, row stage: z[c, 0..lm+2) = (b[c] & qmask) +
+/* Answer compression, row stage: z[c, 0..lm+4) = (b[c] & qmask) +
  * sum_k H[c,k] * cko[k, 0..lm) exactly (rows % 32 == 0, lm % 32 == 0).
  * Replaces rns.rns_matmul_mod's residue products (rns.py:163-188). */
 int zpir_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint32_t* b,
@@ -116,7 +116,7 @@ int zpir_umma_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const ui
 int zpir_build_bc(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, void* stream);
 
 /* Row stage of the answer compression on the tensor cores: same contract as
- * zpir_answer_rows with wz = lm + 2 (rns.py:163-188 replacement). */
+ * zpir_answer_rows with wz = lm + 4 (rns.py:163-188 replacement). */
 int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
                           const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, void* stream);
 

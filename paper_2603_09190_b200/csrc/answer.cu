@@ -10,7 +10,8 @@
 // (SURVEY 8c(ii)); the device reads H (4 bytes/entry, 128 MB at 1 GiB)
 // instead of H_rns.
 //
-//   answer_rows   z_c = b_c + y_c as (Lm + 2) 32-bit limbs, Lm = limbs of m.
+//   answer_rows   z_c = b_c + y_c as Lm + 4 32-bit limbs (top two always zero;
+//                 the padding keeps z rows 16-byte aligned), Lm = limbs of m.
 //   answer_groups X_g = sum_j 2^(32j) z_{g*cap+j}; t_g = X_g mod m via
 //                 t = sum_s mont(X_s, R^(s+1) mod m) over Lm-limb chunks X_s.
 //   combine       K_g = (1 + t_g m) * k_g mod m^2 (paillier.py:104-123).
@@ -18,7 +19,7 @@
 
 namespace zpir {
 
-// z[c, 0..Lm+2) = (b[c] & qmask) + sum_k H[c,k] * cko[k, 0..Lm)
+// z[c, 0..Lm+4) = (b[c] & qmask) + sum_k H[c,k] * cko[k, 0..Lm)
 // 128 threads, tile = 32 rows x 64 limbs, each thread 4 rows x 4 limbs with
 // 96-bit accumulators; row-wise carry propagation in shared memory.
 __global__ void __launch_bounds__(128)
@@ -30,7 +31,7 @@ answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __
   __shared__ uint32_t sS[32][64][3];
   const int t = threadIdx.x, tr = t >> 4, tc = t & 15;
   const int64_t row0 = (int64_t)blockIdx.x * 32;
-  const int wz = lm + 2;
+  const int wz = lm + 4;
   // row-carry state, owned by threads 0..31 (one row each)
   unsigned __int128 carry = 0;
   if (t < 32) carry = (unsigned __int128)(b[row0 + t] & qmask);
@@ -103,6 +104,8 @@ answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __
     uint32_t* zr = z + (row0 + t) * wz;
     zr[lm] = (uint32_t)carry;
     zr[lm + 1] = (uint32_t)(carry >> 32);
+    zr[lm + 2] = (uint32_t)(carry >> 64);
+    zr[lm + 3] = 0;
   }
 }
 
@@ -122,7 +125,7 @@ answer_groups_kernel(const uint32_t* __restrict__ z, int64_t d1, int cap, int64_
   if (g >= groups) return;
   const int nx = nchunks * LM;
   unsigned long long* S = smem_u64 + (size_t)wid * nx;
-  const int wz = LM + 2;
+  const int wz = LM + 4;
   const int64_t c0 = g * cap;
   const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
   for (int P = lane; P < nx; P += 32) {
@@ -232,7 +235,7 @@ int answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint32_
 int answer_groups_launch(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
                          const uint32_t* mod, uint32_t np, const uint32_t* rpow, int nchunks,
                          uint32_t* t, int64_t t_ld, cudaStream_t st) {
-  if (lm % 32 || nchunks * lm < cap + lm + 2 || t_ld < lm || cap <= 0) {
+  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0) {
     set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
     return kErrInput;
   }

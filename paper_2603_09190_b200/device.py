@@ -66,7 +66,7 @@ def gemv(dbt, qu_dev, qmask, out=None, ws=None, stream=None):
 def answer_rows(H, b, qmask, cko, lm, out=None, stream=None):
     rows, n = H.shape
     if out is None:
-        out = torch.empty((rows, lm + 2), dtype=torch.int32, device=H.device)
+        out = torch.empty((rows, lm + 4), dtype=torch.int32, device=H.device)
     _lib.call("zpir_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(b), qmask, _lib.ptr(cko), lm,
               _lib.ptr(out), _s(stream))
     return out
@@ -74,7 +74,7 @@ def answer_rows(H, b, qmask, cko, lm, out=None, stream=None):
 
 def answer_groups(z, d1, cap, groups, kctx, t_ld, out=None, stream=None):
     lm = kctx.lm
-    nchunks = -(-(cap + lm + 2) // lm)
+    nchunks = -(-(cap + lm + 4) // lm)
     rpow = kctx.d_rpow(nchunks)
     if out is None:
         out = torch.empty((groups, t_ld), dtype=torch.int32, device=z.device)
@@ -155,7 +155,7 @@ def build_bc(cko, lm, stream=None):
 def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None):
     rows, n = H.shape
     if out is None:
-        out = torch.empty((rows, lm + 2), dtype=torch.int32, device=H.device)
+        out = torch.empty((rows, lm + 4), dtype=torch.int32, device=H.device)
     _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0], _lib.ptr(b),
-              qmask, lm + 2, _lib.ptr(out), _s(stream))
+              qmask, lm + 4, _lib.ptr(out), _s(stream))
     return out
