@@ -371,7 +371,7 @@ def run_b200(args):
                        "parallelism": f"db-row shards x{world}",
                        "l2": "no flush: DB (1 GiB/GPU) > L2 (126 MB)"},
             "gpu_launches": 4 * args.steps,
-            "roofline": {"bound": "hbm", "kernel": "gemv_dp4a_kernel (+qplanes)",
+            "roofline": {"bound": "hbm", "kernel": "umma_gemm_kernel<16,0> (tcgen05 GEMV, + query planes)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic(),
                          "peak_source": peak_src,

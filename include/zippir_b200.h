@@ -51,20 +51,24 @@ int64_t zpir_gemv_workspace_bytes(int64_t ld, int64_t nvec);
 int zpir_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_t* qu, int64_t nvec,
               uint32_t* b, uint32_t qmask, void* workspace, void* stream);
 
-/* Answer compression, row stage: z[c, 0..lm+4) = (b[c] & qmask) +
- * sum_k H[c,k] * cko[k, 0..lm) exactly (rows % 32 == 0, lm % 32 == 0).
+/* Answer compression, row stage: z[c, 0..lm+4) = sum_k H[c,k] * cko[k, 0..lm)
+ * exactly (rows % 32 == 0, lm % 32 == 0); b and qmask are accepted for
+ * ABI stability and ignored (the group stage adds b).
  * Replaces rns.rns_matmul_mod's residue products (rns.py:163-188). */
 int zpir_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint32_t* b,
                      uint32_t qmask, const uint32_t* cko, int lm, uint32_t* z, void* stream);
 
-/* Answer compression, group stage: t[g] = (sum_j 2^(32j) z[g*cap+j]) mod m,
+/* Answer compression, group stage:
+ * t[g] = (sum_j 2^(32j) ((b[c] & qmask) + z[c])) mod m, c = g*cap + j < d1;
  * m given as lm limbs with np = -m^-1 mod 2^32 and rpow[s] = R^(s+1) mod m
- * (R = 2^(32 lm)) for s < nchunks. t rows have stride t_ld (zero-extended).
- * Replaces Garner reconstruction + scaled_b + the final add (rns.py:94-127,
- * protocol.py:259-269, :349-350) for gamma = q = 2^32. */
-int zpir_answer_groups(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
-                       const uint32_t* m, uint32_t np, const uint32_t* rpow, int nchunks,
-                       uint32_t* t, int64_t t_ld, void* stream);
+ * (R = 2^(32 lm)) for s < nchunks (2 or 3); fast0 = 1 iff R < 2m. t rows
+ * have stride t_ld (zero-extended). Replaces Garner reconstruction +
+ * scaled_b + the final add (rns.py:94-127, protocol.py:259-269, :349-350)
+ * for gamma = q = 2^32. */
+int zpir_answer_groups(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1, int cap,
+                       int64_t groups, int lm, const uint32_t* m, uint32_t np,
+                       const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
+                       void* stream);
 
 /* COMBINED response K[g] = (1 + t[g] m) k[g] mod m^2; m^2 as l2 limbs with
  * np2, r2 = R^2 mod m^2, mr = m R mod m^2 (R = 2^(32 l2)); t zero-extended
@@ -98,9 +102,11 @@ int zpir_query_planes(const uint32_t* qu, int64_t ld, int64_t nvec, uint8_t* pla
 
 /* b[v*rows + r] = (dbt * qu_v)[r] mod 2^32 on the tensor cores (stream-K
  * split, wrapping atomics). Same contract as zpir_gemv (protocol.py:242-257),
- * planes from zpir_query_planes. nvec <= 64 (batched queries). */
+ * planes from zpir_query_planes. nvec <= 64 (batched queries). ctas caps the
+ * persistent grid (0 = one CTA per SM) so the compression GEMM can run
+ * concurrently on the remaining SMs. */
 int zpir_umma_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* planes,
-                   int64_t nvec, uint32_t* b, void* stream);
+                   int64_t nvec, uint32_t* b, int ctas, void* stream);
 
 /* A byte planes: aplanes[(4k+l)*ld + i] = byte l of A[i*lda + k]. */
 int zpir_build_aplanes(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* aplanes,
@@ -116,9 +122,10 @@ int zpir_umma_global_hint(const uint8_t* dbt, int64_t rows, int64_t ld, const ui
 int zpir_build_bc(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, void* stream);
 
 /* Row stage of the answer compression on the tensor cores: same contract as
- * zpir_answer_rows with wz = lm + 4 (rns.py:163-188 replacement). */
+ * zpir_answer_rows (b unused) with wz = lm + 4 (rns.py:163-188 replacement). */
 int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
-                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, void* stream);
+                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
+                          void* stream);
 
 #ifdef __cplusplus
 }

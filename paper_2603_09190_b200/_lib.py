@@ -27,20 +27,20 @@ _SIGS = {
     "zpir_gemv_workspace_bytes": ([_c_i64, _c_i64], _c_i64),
     "zpir_gemv": ([_p, _c_i64, _c_i64, _p, _c_i64, _p, _c_u32, _p, _p], _c_int),
     "zpir_answer_rows": ([_p, _c_i64, _c_i64, _p, _c_u32, _p, _c_int, _p, _p], _c_int),
-    "zpir_answer_groups": ([_p, _c_i64, _c_int, _c_i64, _c_int, _p, _c_u32, _p, _c_int, _p,
-                            _c_i64, _p], _c_int),
+    "zpir_answer_groups": ([_p, _p, _c_u32, _c_i64, _c_int, _c_i64, _c_int, _p, _c_u32, _p,
+                            _c_int, _c_int, _p, _c_i64, _p], _c_int),
     "zpir_combine": ([_p, _p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p, _p], _c_int),
     "zpir_mulmod": ([_p, _p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p], _c_int),
     "zpir_multiexp_workspace_bytes": ([_c_i64, _c_i64, _c_int, _c_int], _c_i64),
     "zpir_multiexp": ([_p, _c_i64, _p, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _p,
                        _c_u32, _p, _p, _p, _c_i64, _p], _c_int),
     "zpir_query_planes": ([_p, _c_i64, _c_i64, _p, _c_i64, _p], _c_int),
-    "zpir_umma_gemv": ([_p, _c_i64, _c_i64, _p, _c_i64, _p, _p], _c_int),
+    "zpir_umma_gemv": ([_p, _c_i64, _c_i64, _p, _c_i64, _p, _c_int, _p], _c_int),
     "zpir_build_aplanes": ([_p, _c_i64, _c_i64, _c_i64, _p, _p], _c_int),
     "zpir_umma_global_hint": ([_p, _c_i64, _c_i64, _p, _c_i64, _p, _c_u32, _p], _c_int),
     "zpir_build_bc": ([_p, _c_i64, _c_int, _c_int, _p, _p], _c_int),
-    "zpir_umma_answer_rows": ([_p, _c_i64, _c_i64, _p, _c_int, _p, _c_u32, _c_int, _p, _p],
-                              _c_int),
+    "zpir_umma_answer_rows": ([_p, _c_i64, _c_i64, _p, _c_int, _p, _c_u32, _c_int, _p, _c_int,
+                               _p], _c_int),
 }
 
 EXPORTED = tuple(_SIGS)

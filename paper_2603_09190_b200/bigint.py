@@ -22,19 +22,34 @@ def limbs_for_bits(bits: int) -> int:
     raise NotImplementedError(f"{bits}-bit moduli exceed the widest kernel (8192 bits)")
 
 
-def ints_to_limbs(values, nlimbs: int) -> np.ndarray:
-    """(len(values), nlimbs) uint32, little-endian limbs."""
-    width = 4 * nlimbs
-    buf = b"".join(int(v).to_bytes(width, "little") for v in values)
-    return np.frombuffer(buf, dtype="<u4").reshape(len(values), nlimbs)
+def _conv():
+    global _CONV
+    if _CONV is None:
+        from . import build
+        build.build_conv()
+        from . import _zpir_conv
+        _CONV = _zpir_conv
+    return _CONV
+
+
+_CONV = None
+
+
+def ints_to_limbs(values, nlimbs: int, out=None) -> np.ndarray:
+    """(len(values), nlimbs) uint32, little-endian limbs (C loop over
+    _PyLong_AsByteArray). ValueError on negative or too-wide values."""
+    if not isinstance(values, (list, tuple)):
+        values = list(values)
+    if out is None:
+        out = np.empty((len(values), nlimbs), dtype=np.uint32)
+    _conv().ints_into(values, out, nlimbs)
+    return out
 
 
 def limbs_to_ints(arr) -> list:
     a = np.ascontiguousarray(arr, dtype="<u4")
     rows, nl = a.shape
-    raw = a.tobytes()
-    w = 4 * nl
-    return [int.from_bytes(raw[i * w:(i + 1) * w], "little") for i in range(rows)]
+    return _conv().ints_from(a, rows, nl)
 
 
 class ModCtx:

@@ -32,7 +32,27 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def conv_path():
+    import sysconfig
+    return os.path.join(HERE, "_zpir_conv" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_conv(force=False):
+    """CPython extension for int <-> limb conversion at the API boundary."""
+    import sysconfig
+    out = conv_path()
+    src = os.path.join(CSRC, "pyconv.c")
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    tmp = out + ".tmp"
+    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+                           src, "-o", tmp])
+    os.replace(tmp, out)
+    return out
+
+
 def build(verbose=False, force=False):
+    build_conv(force)
     if not force and not needs_build():
         return LIB
     objs = []

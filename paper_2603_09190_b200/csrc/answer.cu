@@ -10,16 +10,16 @@
 // (SURVEY 8c(ii)); the device reads H (4 bytes/entry, 128 MB at 1 GiB)
 // instead of H_rns.
 //
-//   answer_rows   z_c = b_c + y_c as Lm + 4 32-bit limbs (top two always zero;
+//   answer_rows   z_c = y_c as Lm + 4 32-bit limbs (top two always zero;
 //                 the padding keeps z rows 16-byte aligned), Lm = limbs of m.
-//   answer_groups X_g = sum_j 2^(32j) z_{g*cap+j}; t_g = X_g mod m via
+//   answer_groups X_g = sum_j 2^(32j) (b_c + z_c); t_g = X_g mod m via
 //                 t = sum_s mont(X_s, R^(s+1) mod m) over Lm-limb chunks X_s.
 //   combine       K_g = (1 + t_g m) * k_g mod m^2 (paillier.py:104-123).
 #include "bignum.cuh"
 
 namespace zpir {
 
-// z[c, 0..Lm+4) = (b[c] & qmask) + sum_k H[c,k] * cko[k, 0..Lm)
+// z[c, 0..Lm+4) = y_c = sum_k H[c,k] * cko[k, 0..Lm) (b is added by the group stage)
 // 128 threads, tile = 32 rows x 64 limbs, each thread 4 rows x 4 limbs with
 // 96-bit accumulators; row-wise carry propagation in shared memory.
 __global__ void __launch_bounds__(128)
@@ -34,7 +34,8 @@ answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __
   const int wz = lm + 4;
   // row-carry state, owned by threads 0..31 (one row each)
   unsigned __int128 carry = 0;
-  if (t < 32) carry = (unsigned __int128)(b[row0 + t] & qmask);
+  (void)b;
+  (void)qmask;
 
   for (int ch = 0; ch < lm; ch += 64) {
     uint32_t lo[4][4], mi[4][4], hi[4][4];
@@ -109,58 +110,83 @@ answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __
   }
 }
 
-// One warp per group. Shared memory per warp: nchunks*Lm u64 position sums
-// (reused as the X limbs). t is written with row stride t_ld (>= Lm),
-// zero-extended.
-template <int LPL>
+// One CTA (4 warps) per group g, latency-oriented (521 groups at 1 GiB):
+//   1. all threads: position sums S[P] = sum_j z[g*cap + j][P - j] (+ b at
+//      P < rows of the group), split as lo/hi 32-bit words in shared memory
+//   2. warp 0: X = LO + (HI << 32) with a ballot carry-lookahead add
+//      (NCH*LM limbs held as LPL*NCH limbs per lane)
+//   3. warp s < NCH: r_s = mont(X_s, R^(s+1) mod m) -- the chunk products run
+//      concurrently in different warps; chunk 0 only needs a conditional
+//      subtraction when R < 2m (m of exactly 32*LM bits)
+//   4. warp 0: t = sum_s r_s mod m
+template <int LPL, int NCH>
 __global__ void __launch_bounds__(128)
-answer_groups_kernel(const uint32_t* __restrict__ z, int64_t d1, int cap, int64_t groups,
+answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict__ b,
+                     uint32_t qmask, int64_t d1, int cap, int64_t groups,
                      const uint32_t* __restrict__ mod, uint32_t np,
-                     const uint32_t* __restrict__ rpow, int nchunks, uint32_t* __restrict__ t,
+                     const uint32_t* __restrict__ rpow, int fast0, uint32_t* __restrict__ t,
                      int64_t t_ld) {
   constexpr int LM = 32 * LPL;
-  extern __shared__ unsigned long long smem_u64[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-  if (g >= groups) return;
-  const int nx = nchunks * LM;
-  unsigned long long* S = smem_u64 + (size_t)wid * nx;
+  constexpr int NX = NCH * LM;
+  constexpr int LX = NCH * LPL;
+  __shared__ __align__(16) uint32_t lo[NX], hi[NX + 1], X[NX], R[NCH][LM];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t g = blockIdx.x;
   const int wz = LM + 4;
   const int64_t c0 = g * cap;
   const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
-  for (int P = lane; P < nx; P += 32) {
-    unsigned long long s = 0;
+  for (int P = tid; P < NX; P += blockDim.x) {
+    unsigned long long s = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
     const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
     for (int j = jlo; j <= jhi; ++j) s += z[(c0 + j) * wz + (P - j)];
-    S[P] = s;
+    lo[P] = (uint32_t)s;
+    hi[P + 1] = (uint32_t)(s >> 32);
   }
-  __syncwarp();
-  if (lane == 0) {
-    uint32_t* X = reinterpret_cast<uint32_t*>(S);  // in-place: X[P] written after S[P] read
-    unsigned long long c = 0;
-    for (int P = 0; P < nx; ++P) {
-      const unsigned long long s = S[P];
-      const unsigned __int128 v = (unsigned __int128)s + c;
-      X[P] = (uint32_t)v;
-      c = (unsigned long long)(v >> 32);
-    }
-  }
-  __syncwarp();
-  const uint32_t* X = reinterpret_cast<const uint32_t*>(S);
-  uint32_t n_[LPL], res[LPL], x[LPL], rp[LPL];
-  big_load<LPL>(n_, mod, lane);
-  big_set_small<LPL>(res, 0, lane);
-  for (int s = 0; s < nchunks; ++s) {
+  if (tid == 0) hi[0] = 0;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t x[LX], y[LX];
 #pragma unroll
-    for (int i = 0; i < LPL; ++i) x[i] = X[s * LM + lane * LPL + i];
-    big_load<LPL>(rp, rpow + (size_t)s * LM, lane);
-    mont_mul<LPL>(x, x, rp, n_, np, lane);
-    const uint32_t cy = big_add<LPL>(res, x, lane);
-    big_cond_sub<LPL>(res, cy, n_, lane);
+    for (int i = 0; i < LX; ++i) {
+      x[i] = lo[lane * LX + i];
+      y[i] = hi[lane * LX + i];
+    }
+    big_add<LX>(x, y, lane);
+#pragma unroll
+    for (int i = 0; i < LX; ++i) X[lane * LX + i] = x[i];
   }
-  uint32_t* out = t + g * t_ld;
-  big_store<LPL>(out, res, lane);
-  for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
+  __syncthreads();
+  if (warp < NCH) {
+    uint32_t n_[LPL], x[LPL], rp[LPL];
+    big_load<LPL>(n_, mod, lane);
+#pragma unroll
+    for (int i = 0; i < LPL; ++i) x[i] = X[warp * LM + lane * LPL + i];
+    if (warp == 0 && fast0) {
+      big_cond_sub<LPL>(x, 0u, n_, lane);  // X_0 < R < 2m
+    } else {
+      big_load<LPL>(rp, rpow + (size_t)warp * LM, lane);
+      mont_mul<LPL>(x, x, rp, n_, np, lane);
+    }
+#pragma unroll
+    for (int i = 0; i < LPL; ++i) R[warp][lane * LPL + i] = x[i];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t n_[LPL], res[LPL], x[LPL];
+    big_load<LPL>(n_, mod, lane);
+#pragma unroll
+    for (int i = 0; i < LPL; ++i) res[i] = R[0][lane * LPL + i];
+#pragma unroll
+    for (int s = 1; s < NCH; ++s) {
+#pragma unroll
+      for (int i = 0; i < LPL; ++i) x[i] = R[s][lane * LPL + i];
+      const uint32_t cy = big_add<LPL>(res, x, lane);
+      big_cond_sub<LPL>(res, cy, n_, lane);
+    }
+    uint32_t* out = t + g * t_ld;
+    big_store<LPL>(out, res, lane);
+    for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
+  }
 }
 
 // K_g = (1 + t_g m) k_g mod m^2, one warp per group, with m^2 context
@@ -232,21 +258,27 @@ int answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint32_
       return kErrUnsupported;                                          \
   }
 
-int answer_groups_launch(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
-                         const uint32_t* mod, uint32_t np, const uint32_t* rpow, int nchunks,
-                         uint32_t* t, int64_t t_ld, cudaStream_t st) {
-  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0) {
+int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1,
+                         int cap, int64_t groups, int lm, const uint32_t* mod, uint32_t np,
+                         const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
+                         cudaStream_t st) {
+  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
+      nchunks > 3) {
     set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
     return kErrInput;
   }
-  const size_t smem = (size_t)4 * nchunks * lm * sizeof(unsigned long long);
-  const unsigned grid = (unsigned)ceil_div(groups, 4);
-  ZPIR_LPL_DISPATCH(lm / 32, {
-    cudaFuncSetAttribute(answer_groups_kernel<LPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    answer_groups_kernel<LPL><<<grid, 128, smem, st>>>(z, d1, cap, groups, mod, np, rpow, nchunks,
-                                                       t, t_ld);
-  });
+  const unsigned grid = (unsigned)groups;
+#define ZPIR_GROUPS(NCHV)                                                                    \
+  ZPIR_LPL_DISPATCH(lm / 32, {                                                               \
+    answer_groups_kernel<LPL, NCHV><<<grid, 128, 0, st>>>(z, b, qmask, d1, cap, groups, mod, \
+                                                          np, rpow, fast0, t, t_ld);         \
+  })
+  if (nchunks == 2) {
+    ZPIR_GROUPS(2);
+  } else {
+    ZPIR_GROUPS(3);
+  }
+#undef ZPIR_GROUPS
   return check_launch("answer_groups");
 }
 

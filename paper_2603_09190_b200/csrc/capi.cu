@@ -25,8 +25,9 @@ int gemv_launch(const uint8_t*, int64_t, int64_t, const uint32_t*, int64_t, uint
                 uint32_t*, cudaStream_t);
 int answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint32_t*, uint32_t,
                        const uint32_t*, int, uint32_t*, cudaStream_t);
-int answer_groups_launch(const uint32_t*, int64_t, int, int64_t, int, const uint32_t*, uint32_t,
-                         const uint32_t*, int, uint32_t*, int64_t, cudaStream_t);
+int answer_groups_launch(const uint32_t*, const uint32_t*, uint32_t, int64_t, int, int64_t, int,
+                         const uint32_t*, uint32_t, const uint32_t*, int, int, uint32_t*, int64_t,
+                         cudaStream_t);
 int combine_launch(const uint32_t*, const uint32_t*, int64_t, int, const uint32_t*, uint32_t,
                    const uint32_t*, const uint32_t*, uint32_t*, cudaStream_t);
 int mulmod_launch(const uint32_t*, const uint32_t*, int64_t, int, const uint32_t*, uint32_t,
@@ -37,12 +38,12 @@ int multiexp_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
                     int64_t, cudaStream_t);
 
 int query_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t);
-int umma_gemv_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int64_t, uint32_t*,
+int umma_gemv_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int64_t, uint32_t*, int,
                      cudaStream_t);
 int umma_hint_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int64_t, uint32_t*,
                      uint32_t, cudaStream_t);
 int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, int,
-                            const uint32_t*, uint32_t, int, uint32_t*, cudaStream_t);
+                            const uint32_t*, uint32_t, int, uint32_t*, int, cudaStream_t);
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 
@@ -91,11 +92,12 @@ int zpir_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint32_t*
   ZPIR_GUARD(answer_rows_launch(H, rows, n, b, qmask, cko, lm, z, S(stream)));
 }
 
-int zpir_answer_groups(const uint32_t* z, int64_t d1, int cap, int64_t groups, int lm,
-                       const uint32_t* m, uint32_t np, const uint32_t* rpow, int nchunks,
-                       uint32_t* t, int64_t t_ld, void* stream) {
-  ZPIR_GUARD(
-      answer_groups_launch(z, d1, cap, groups, lm, m, np, rpow, nchunks, t, t_ld, S(stream)));
+int zpir_answer_groups(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1, int cap,
+                       int64_t groups, int lm, const uint32_t* m, uint32_t np,
+                       const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
+                       void* stream) {
+  ZPIR_GUARD(answer_groups_launch(z, b, qmask, d1, cap, groups, lm, m, np, rpow, nchunks, fast0, t,
+                                  t_ld, S(stream)));
 }
 
 int zpir_combine(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* m2,
@@ -127,8 +129,8 @@ int zpir_query_planes(const uint32_t* qu, int64_t ld, int64_t nvec, uint8_t* pla
 }
 
 int zpir_umma_gemv(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* planes,
-                   int64_t nvec, uint32_t* b, void* stream) {
-  ZPIR_GUARD(umma_gemv_launch(dbt, rows, ld, planes, nvec, b, S(stream)));
+                   int64_t nvec, uint32_t* b, int ctas, void* stream) {
+  ZPIR_GUARD(umma_gemv_launch(dbt, rows, ld, planes, nvec, b, ctas, S(stream)));
 }
 
 int zpir_build_aplanes(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* aplanes,
@@ -146,8 +148,9 @@ int zpir_build_bc(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, v
 }
 
 int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
-                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, void* stream) {
-  ZPIR_GUARD(umma_answer_rows_launch(H, rows, n, bc, nb, b, qmask, wz, z, S(stream)));
+                          const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
+                          void* stream) {
+  ZPIR_GUARD(umma_answer_rows_launch(H, rows, n, bc, nb, b, qmask, wz, z, ctas, S(stream)));
 }
 
 }  // extern "C"

@@ -1,0 +1,179 @@
+/* _zpir_conv: Python int <-> little-endian u32 limb buffers, in C.
+ *
+ * The reference API carries big integers as Python ints (QueryMessage.ck_o,
+ * ResponseMessage.t, PaillierCiphertext.c); converting 1024 x 2048-bit ints
+ * with int.to_bytes / int.from_bytes costs ~0.4 ms each way in CPython,
+ * more than the whole device answer. These two loops use CPython's
+ * _PyLong_AsByteArray / _PyLong_FromByteArray directly.
+ *
+ *   ints_into(seq, buf, nlimbs)   writes len(seq) x nlimbs u32 LE into a
+ *                                 writable buffer (numpy / pinned tensor);
+ *                                 ValueError on negative or too-wide ints
+ *   ints_from(buf, count, nlimbs) -> list of count Python ints
+ */
+#define PY_SSIZE_T_CLEAN
+#include <Python.h>
+#include <stdint.h>
+#include <string.h>
+
+/* CPython 3.12/3.13 store ints as 30-bit digits behind lv_tag (ndigits << 3 |
+ * sign); converting digits <-> 32-bit limbs directly is ~4x faster than the
+ * byte-array API. Other versions use the byte-array API. */
+#if PY_VERSION_HEX >= 0x030C0000 && PY_VERSION_HEX < 0x030E0000 && PYLONG_BITS_IN_DIGIT == 30
+#define ZPIR_FAST_DIGITS 1
+#include "cpython/longintrepr.h"
+
+/* returns 0 ok, -1 negative, -2 too wide */
+static int long_to_limbs(PyObject* v, uint32_t* o, Py_ssize_t nlimbs) {
+  PyLongObject* L = (PyLongObject*)v;
+  const uintptr_t tag = L->long_value.lv_tag;
+  if ((tag & 3) == 2) return -1;
+  const Py_ssize_t nd = (Py_ssize_t)(tag >> 3);
+  const digit* d = L->long_value.ob_digit;
+  uint64_t acc = 0;
+  int bits = 0;
+  Py_ssize_t li = 0;
+  for (Py_ssize_t i = 0; i < nd; ++i) {
+    acc |= (uint64_t)d[i] << bits;
+    bits += 30;
+    if (bits >= 32) {
+      if (li >= nlimbs) return -2;
+      o[li++] = (uint32_t)acc;
+      acc >>= 32;
+      bits -= 32;
+    }
+  }
+  if (acc) {
+    if (li >= nlimbs) return -2;
+    o[li++] = (uint32_t)acc;
+  }
+  if (li < nlimbs) memset(o + li, 0, (size_t)(nlimbs - li) * 4);
+  return 0;
+}
+
+static PyObject* limbs_to_long(const uint32_t* l, Py_ssize_t nlimbs) {
+  digit dig[1024];
+  Py_ssize_t k = 0;
+  uint64_t acc = 0;
+  int bits = 0;
+  if (nlimbs > 900) return _PyLong_FromByteArray((const unsigned char*)l, (size_t)nlimbs * 4, 1, 0);
+  for (Py_ssize_t i = 0; i < nlimbs; ++i) {
+    acc |= (uint64_t)l[i] << bits;
+    bits += 32;
+    while (bits >= 30) {
+      dig[k++] = (digit)(acc & 0x3fffffffu);
+      acc >>= 30;
+      bits -= 30;
+    }
+  }
+  if (bits > 0) dig[k++] = (digit)acc;
+  while (k > 0 && dig[k - 1] == 0) --k;
+  if (k == 0) return PyLong_FromLong(0);
+  return (PyObject*)_PyLong_FromDigits(0, k, dig);
+}
+#endif
+
+static PyObject* ints_into(PyObject* self, PyObject* args) {
+  PyObject* seq;
+  Py_buffer view;
+  Py_ssize_t nlimbs;
+  if (!PyArg_ParseTuple(args, "Ow*n", &seq, &view, &nlimbs)) return NULL;
+  PyObject* fast = PySequence_Fast(seq, "expected a sequence of ints");
+  if (!fast) {
+    PyBuffer_Release(&view);
+    return NULL;
+  }
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
+  const size_t width = (size_t)nlimbs * 4;
+  if ((size_t)view.len < (size_t)n * width) {
+    PyErr_SetString(PyExc_ValueError, "buffer too small");
+    goto fail;
+  }
+  PyObject** items = PySequence_Fast_ITEMS(fast);
+  unsigned char* out = (unsigned char*)view.buf;
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* v = items[i];
+    PyObject* tmp = NULL;
+    if (!PyLong_Check(v)) {
+      PyObject* c = PyObject_GetAttrString(v, "c"); /* PaillierCiphertext */
+      if (!c) goto fail;
+      tmp = PyNumber_Index(c);
+      Py_DECREF(c);
+      if (!tmp) goto fail;
+      v = tmp;
+    }
+#ifdef ZPIR_FAST_DIGITS
+    {
+      const int rc = long_to_limbs(v, (uint32_t*)(out + (size_t)i * width), nlimbs);
+      if (rc) {
+        Py_XDECREF(tmp);
+        PyErr_SetString(PyExc_ValueError, rc == -1 ? "negative integers are not encodable"
+                                                   : "integer wider than the limb width");
+        goto fail;
+      }
+    }
+#else
+    if (_PyLong_Sign(v) < 0) {
+      Py_XDECREF(tmp);
+      PyErr_SetString(PyExc_ValueError, "negative integers are not encodable");
+      goto fail;
+    }
+    if (_PyLong_AsByteArray((PyLongObject*)v, out + (size_t)i * width, width, 1, 0) < 0) {
+      Py_XDECREF(tmp);
+      PyErr_Clear();
+      PyErr_SetString(PyExc_ValueError, "integer wider than the limb width");
+      goto fail;
+    }
+#endif
+    Py_XDECREF(tmp);
+  }
+  Py_DECREF(fast);
+  PyBuffer_Release(&view);
+  Py_RETURN_NONE;
+fail:
+  Py_DECREF(fast);
+  PyBuffer_Release(&view);
+  return NULL;
+}
+
+static PyObject* ints_from(PyObject* self, PyObject* args) {
+  Py_buffer view;
+  Py_ssize_t count, nlimbs;
+  if (!PyArg_ParseTuple(args, "y*nn", &view, &count, &nlimbs)) return NULL;
+  const size_t width = (size_t)nlimbs * 4;
+  if ((size_t)view.len < (size_t)count * width) {
+    PyBuffer_Release(&view);
+    PyErr_SetString(PyExc_ValueError, "buffer too small");
+    return NULL;
+  }
+  PyObject* list = PyList_New(count);
+  if (!list) {
+    PyBuffer_Release(&view);
+    return NULL;
+  }
+  const unsigned char* p = (const unsigned char*)view.buf;
+  for (Py_ssize_t i = 0; i < count; ++i) {
+#ifdef ZPIR_FAST_DIGITS
+    PyObject* v = limbs_to_long((const uint32_t*)(p + (size_t)i * width), nlimbs);
+#else
+    PyObject* v = _PyLong_FromByteArray(p + (size_t)i * width, width, 1, 0);
+#endif
+    if (!v) {
+      Py_DECREF(list);
+      PyBuffer_Release(&view);
+      return NULL;
+    }
+    PyList_SET_ITEM(list, i, v);
+  }
+  PyBuffer_Release(&view);
+  return list;
+}
+
+static PyMethodDef methods[] = {
+    {"ints_into", ints_into, METH_VARARGS, "ints -> u32 LE limbs written into a buffer"},
+    {"ints_from", ints_from, METH_VARARGS, "u32 LE limbs -> list of ints"},
+    {NULL, NULL, 0, NULL}};
+
+static struct PyModuleDef mod = {PyModuleDef_HEAD_INIT, "_zpir_conv", NULL, -1, methods};
+
+PyMODINIT_FUNC PyInit__zpir_conv(void) { return PyModule_Create(&mod); }

@@ -39,7 +39,7 @@ using namespace sm100;
 enum UmmaMode : int {
   kLimbCols = 0,     // out[(n*NT/4 + j) * ldo + r]  (+)= sum_l P[r,4j+l] << 8l
   kLimbRowsNeg = 1,  // out[r * ldo + n*NT/4 + j]  = qmask & -(sum_l ...)   (whole tiles)
-  kBigint = 2        // z[r * wz + i] = limbs of (b[r] & qmask) + sum_b P[r,b] << 8b
+  kBigint = 2        // z[r * wz + i] = limbs of sum_b P[r,b] << 8b
 };
 
 struct UmmaArgs {
@@ -258,8 +258,9 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           }
         }
       } else {
-        // BIGINT: z_r = (b_r & qmask) + sum_b P[r, b] 2^(8b), carry-propagated
-        unsigned long long carry = args.b[row] & args.qmask;
+        // BIGINT: z_r = sum_b P[r, b] 2^(8b), carry-propagated (b is added by
+        // the group stage, so this GEMM does not depend on the GEMV)
+        unsigned long long carry = 0;
         uint32_t* zr = args.out + row * args.wz;
 #pragma unroll 1
         for (int c0 = 0; c0 < NT; c0 += 16) {
@@ -309,19 +310,33 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 // operand builders
 
 // Bc[b * (4n) + 4k + a] = byte (b - a) of ck_o[k] (0 outside [0, 4 lm)), b < nb.
-__global__ void build_bc_kernel(const uint32_t* __restrict__ cko, int64_t n, int lm, int nb,
-                                uint32_t* __restrict__ bc) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int b = blockIdx.y;
-  if (k >= n) return;
-  const uint32_t* c = cko + k * lm;
-  uint32_t w = 0;
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int j = b - a;
-    if (j >= 0 && j < 4 * lm) w |= ((c[j >> 2] >> (8 * (j & 3))) & 0xffu) << (8 * a);
+// One CTA per 32 values of k and 32 rows b: the 32 ck_o rows are staged in
+// shared memory (row pitch lm + 1 words against bank conflicts), each warp
+// then writes 32 consecutive output words of one row b.
+__global__ void __launch_bounds__(256)
+build_bc_kernel(const uint32_t* __restrict__ cko, int64_t n, int lm, int nb,
+                uint32_t* __restrict__ bc) {
+  extern __shared__ uint32_t sck[];
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  const int pitch = lm + 1;
+  for (int idx = threadIdx.x; idx < 32 * lm; idx += blockDim.x) {
+    const int kk = idx / lm, j = idx - kk * lm;
+    sck[kk * pitch + j] = (k0 + kk < n) ? cko[(k0 + kk) * lm + j] : 0u;
   }
-  bc[(int64_t)b * n + k] = w;
+  __syncthreads();
+  const int kk = threadIdx.x & 31;
+  const uint8_t* by = reinterpret_cast<const uint8_t*>(sck + kk * pitch);
+  if (k0 + kk >= n) return;
+  const int b1 = min(nb, (int)(blockIdx.y + 1) * 32);
+  for (int bb = blockIdx.y * 32 + (threadIdx.x >> 5); bb < b1; bb += blockDim.x >> 5) {
+    uint32_t w = 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int j = bb - a;
+      if (j >= 0 && j < 4 * lm) w |= (uint32_t)by[j] << (8 * a);
+    }
+    bc[(int64_t)bb * n + k0 + kk] = w;
+  }
 }
 
 // Ap[(4k + l) * ld + i] = byte l of A[i * lda + k], k < n, i < ld.
@@ -399,7 +414,8 @@ static int num_sms() {
 
 template <int NT, int MODE>
 static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes, const uint8_t* B,
-                    int64_t brows, int64_t ldb_bytes, UmmaArgs args, cudaStream_t st) {
+                    int64_t brows, int64_t ldb_bytes, UmmaArgs args, cudaStream_t st,
+                    int max_ctas = 0) {
   using Cfg = UmmaCfg<NT>;
   if (rows % kBM || brows % NT) {
     set_error("umma: rows %% 128 / brows %% NT (rows=%lld brows=%lld NT=%d)", (long long)rows,
@@ -414,7 +430,9 @@ static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes
   args.kblocks = (int)ceil_div(K, kBK);
   const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
   const int64_t U = args.split ? T * args.kblocks : T;
-  const int grid = (int)std::min<int64_t>(num_sms(), U);
+  const int sms = num_sms();
+  const int cap = (max_ctas > 0 && max_ctas < sms) ? max_ctas : sms;
+  const int grid = (int)std::min<int64_t>(cap, U);
   auto kern = umma_gemm_kernel<NT, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
   kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mb, args);
@@ -423,7 +441,7 @@ static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes
 
 // b[v * rows + r] = qmask & (DB qu_v)[r] for nvec <= 4 (N = 16) or 64 (N = 256)
 int umma_gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* qplanes,
-                     int64_t nvec, uint32_t* out, cudaStream_t st) {
+                     int64_t nvec, uint32_t* out, int ctas, cudaStream_t st) {
   if (cudaMemsetAsync(out, 0, rows * nvec * sizeof(uint32_t), st) != cudaSuccess)
     return check_launch("umma_gemv memset");
   UmmaArgs a{};
@@ -432,8 +450,9 @@ int umma_gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t
   a.ldo = rows;
   a.nout = (int)nvec;
   a.qmask = 0xffffffffu;
-  if (nvec <= 4) return umma_run<16, kLimbCols>(dbt, rows, ld, ld, qplanes, 16, ld, a, st);
-  if (nvec <= 64) return umma_run<256, kLimbCols>(dbt, rows, ld, ld, qplanes, 256, ld, a, st);
+  if (nvec <= 4) return umma_run<16, kLimbCols>(dbt, rows, ld, ld, qplanes, 16, ld, a, st, ctas);
+  if (nvec <= 64)
+    return umma_run<256, kLimbCols>(dbt, rows, ld, ld, qplanes, 256, ld, a, st, ctas);
   set_error("umma_gemv: at most 64 query vectors per launch (got %lld)", (long long)nvec);
   return kErrInput;
 }
@@ -456,7 +475,7 @@ int umma_hint_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t
 
 // z[r * wz + i] = limbs of (b[r] & qmask) + sum_k H[r,k] ck_o[k]; bc from build_bc.
 int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
-                            const uint32_t* b, uint32_t qmask, int wz, uint32_t* z,
+                            const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
                             cudaStream_t st) {
   UmmaArgs a{};
   a.split = 0;
@@ -466,9 +485,9 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
   a.wz = wz;
   const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
   switch (nb) {
-    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st);
-    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st);
-    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st);
+    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
+    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
+    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st, ctas);
     default:
       set_error("umma_answer_rows: unsupported B width %d", nb);
       return kErrUnsupported;
@@ -476,8 +495,10 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
 }
 
 int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st) {
-  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)nb);
-  build_bc_kernel<<<grid, 256, 0, st>>>(cko, n, lm, nb, reinterpret_cast<uint32_t*>(bc));
+  const size_t smem = (size_t)32 * (lm + 1) * sizeof(uint32_t);
+  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(nb, 32));
+  build_bc_kernel<<<grid, 256, smem, st>>>(cko, n, lm, nb,
+                                                               reinterpret_cast<uint32_t*>(bc));
   return check_launch("build_bc");
 }
 

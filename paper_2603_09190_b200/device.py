@@ -72,14 +72,16 @@ def answer_rows(H, b, qmask, cko, lm, out=None, stream=None):
     return out
 
 
-def answer_groups(z, d1, cap, groups, kctx, t_ld, out=None, stream=None):
+def answer_groups(z, b, qmask, d1, cap, groups, kctx, t_ld, out=None, stream=None):
     lm = kctx.lm
-    nchunks = -(-(cap + lm + 4) // lm)
+    nchunks = max(2, -(-(cap + lm + 4) // lm))
     rpow = kctx.d_rpow(nchunks)
+    fast0 = 1 if kctx.cm.R < 2 * kctx.m else 0
     if out is None:
         out = torch.empty((groups, t_ld), dtype=torch.int32, device=z.device)
-    _lib.call("zpir_answer_groups", _lib.ptr(z), d1, cap, groups, lm, _lib.ptr(kctx.d_m),
-              kctx.cm.np, _lib.ptr(rpow), nchunks, _lib.ptr(out), t_ld, _s(stream))
+    _lib.call("zpir_answer_groups", _lib.ptr(z), _lib.ptr(b), qmask, d1, cap, groups, lm,
+              _lib.ptr(kctx.d_m), kctx.cm.np, _lib.ptr(rpow), nchunks, fast0, _lib.ptr(out), t_ld,
+              _s(stream))
     return out
 
 
@@ -118,19 +120,20 @@ def multiexp(bases, E, rows, rs, bs, ls, elimbs, kctx, stream=None):
 UMMA_NB = {32: 144, 64: 272, 96: 400}
 
 
-def query_planes(qu_dev, prow, stream=None):
+def query_planes(qu_dev, prow, stream=None, planes=None):
     nvec, ld = qu_dev.shape
-    planes = torch.empty((prow, ld), dtype=torch.uint8, device=qu_dev.device)
+    if planes is None:
+        planes = torch.empty((prow, ld), dtype=torch.uint8, device=qu_dev.device)
     _lib.call("zpir_query_planes", _lib.ptr(qu_dev), ld, nvec, _lib.ptr(planes), prow, _s(stream))
     return planes
 
 
-def umma_gemv(dbt, planes, nvec, out=None, stream=None):
+def umma_gemv(dbt, planes, nvec, out=None, stream=None, ctas=0):
     rows, ld = dbt.shape
     if out is None:
         out = torch.empty((nvec, rows), dtype=torch.int32, device=dbt.device)
     _lib.call("zpir_umma_gemv", _lib.ptr(dbt), rows, ld, _lib.ptr(planes), nvec, _lib.ptr(out),
-              _s(stream))
+              ctas, _s(stream))
     return out
 
 
@@ -144,18 +147,19 @@ def umma_global_hint(dbt, A_dev, n, qmask, stream=None):
     return H
 
 
-def build_bc(cko, lm, stream=None):
+def build_bc(cko, lm, stream=None, bc=None):
     n = cko.shape[0]
     nb = UMMA_NB[lm]
-    bc = torch.empty((nb, 4 * n), dtype=torch.uint8, device=cko.device)
+    if bc is None:
+        bc = torch.empty((nb, 4 * n), dtype=torch.uint8, device=cko.device)
     _lib.call("zpir_build_bc", _lib.ptr(cko), n, lm, nb, _lib.ptr(bc), _s(stream))
     return bc
 
 
-def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None):
+def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None, ctas=0):
     rows, n = H.shape
     if out is None:
         out = torch.empty((rows, lm + 4), dtype=torch.int32, device=H.device)
     _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0], _lib.ptr(b),
-              qmask, lm + 4, _lib.ptr(out), _s(stream))
+              qmask, lm + 4, _lib.ptr(out), ctas, _s(stream))
     return out

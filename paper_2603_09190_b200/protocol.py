@@ -42,6 +42,9 @@ COMBINED = "combined"
 # "umma": tcgen05 tensor-core engine (default); "cuda_core": the IDP4A / IMAD
 # kernels, kept as the measured alternative (design evidence).
 ENGINE = os.environ.get("ZPIR_ENGINE", "umma")
+# SMs given to the compression GEMM while the GEMV streams the DB on the rest
+# (both are HBM-bound; H is ~1/8 of the DB bytes). 0 = run them back to back.
+COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "36"))
 
 
 @dataclass
@@ -167,6 +170,7 @@ class ServerGlobalState:
         self._H_host = None
         self._H_scaled = None
         self._lock = threading.Lock()
+        self._tls = threading.local()
 
     # -- reference-compatible views (materialised lazily on the host) ------
 
@@ -232,20 +236,66 @@ class ServerGlobalState:
         return [int.from_bytes(arr[g * lay.cap:(g + 1) * lay.cap].tobytes(), "little")
                 for g in range(lay.groups)]
 
+    def _workspace(self, lm):
+        """Per-thread device buffers and side stream for the online path."""
+        tl = self._tls
+        ws = getattr(tl, "ws", None)
+        if ws is None:
+            ws = tl.ws = {}
+        w = ws.get(lm)
+        if w is None:
+            lay = self.layout
+            dev = self.device
+            w = ws[lm] = {
+                "side": torch.cuda.Stream(dev),
+                "ev_in": torch.cuda.Event(), "ev_comp": torch.cuda.Event(),
+                "planes": torch.empty((16, lay.ld), dtype=torch.uint8, device=dev),
+                "b": torch.empty((1, lay.rows), dtype=torch.int32, device=dev),
+                "z": torch.empty((lay.rows, lm + 4), dtype=torch.int32, device=dev),
+                "bc": (torch.empty((device.UMMA_NB[lm], 4 * lay.n), dtype=torch.uint8,
+                                   device=dev) if lm in device.UMMA_NB else None),
+            }
+        return w
+
     def answer_device(self, qu_dev, cko_dev, kctx, t_ld, stream, events=None):
-        """t (groups x t_ld u32 limbs) for one staged query; all on device."""
+        """t (groups x t_ld u32 limbs) for one staged query; all on device.
+
+        UMMA engine: the compression GEMM (H, 1/8 of the bytes) runs on a side
+        stream on COMPRESS_CTAS SMs while the GEMV streams the DB on the other
+        SMs; the group stage joins both."""
         lay = self.layout
+        lm = kctx.lm
         if events:
             events[0].record(stream)
-        b = self.gemv_device(qu_dev, stream)
-        if events:
-            events[1].record(stream)
-        if self.engine == "umma" and kctx.lm in device.UMMA_NB:
-            bc = device.build_bc(cko_dev, kctx.lm, stream=stream)
-            z = device.umma_answer_rows(self.H_dev, bc, b[0], lay.qmask, kctx.lm, stream=stream)
+        if (self.engine == "umma" and lm in device.UMMA_NB and qu_dev.shape[0] == 1
+                and lay.qmask == 0xFFFFFFFF):
+            w = self._workspace(lm)
+            side = w["side"]
+            split = COMPRESS_CTAS > 0
+            cs = side if split else stream
+            if split:
+                w["ev_in"].record(stream)
+                side.wait_event(w["ev_in"])
+            bc = device.build_bc(cko_dev, lm, stream=cs, bc=w["bc"])
+            z = device.umma_answer_rows(self.H_dev, bc, w["b"][0], lay.qmask, lm, out=w["z"],
+                                        stream=cs, ctas=COMPRESS_CTAS if split else 0)
+            if split:
+                w["ev_comp"].record(side)
+            planes = device.query_planes(qu_dev, 16, stream, planes=w["planes"])
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            b = device.umma_gemv(self.dbt, planes, 1, out=w["b"], stream=stream,
+                                 ctas=(sms - COMPRESS_CTAS) if split else 0)
+            if events:
+                events[1].record(stream)
+            if split:
+                stream.wait_event(w["ev_comp"])
         else:
-            z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, kctx.lm, stream=stream)
-        t = device.answer_groups(z, lay.d1, lay.cap, lay.groups, kctx, t_ld, stream=stream)
+            b = self.gemv_device(qu_dev, stream)
+            if events:
+                events[1].record(stream)
+            z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, lm, stream=stream)
+        t = device.answer_groups(z, b[0], lay.qmask, lay.d1, lay.cap, lay.groups, kctx, t_ld,
+                                 stream=stream)
         if events:
             events[2].record(stream)
         return t
