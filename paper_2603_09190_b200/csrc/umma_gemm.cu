@@ -63,7 +63,13 @@ struct UmmaCfg {
   static constexpr int kBBytes = NT * kBK;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = std::min(12, (200 * 1024) / kStageBytes);
-  static constexpr int kAcc = (2 * NT <= 512) ? 2 : 1;
+  // Two accumulator buffers when they fit side by side in the 512 TMEM
+  // columns; for 256 < NT <= 272 they overlap by kOv = 2 NT - 512 <= 32
+  // columns at [512 - NT, NT): the epilogue drains that overlap first and
+  // releases it early (bar "oempty") so the next tile's MMAs can start.
+  static constexpr int kAcc = (2 * NT <= 512 + 32) ? 2 : 1;
+  static constexpr int kOv = (kAcc == 2 && 2 * NT > 512) ? 2 * NT - 512 : 0;
+  static constexpr int kAccOff1 = (kOv > 0) ? 512 - NT : NT;
   static constexpr int kTmemCols = (kAcc * NT <= 32) ? 32 : (kAcc * NT <= 64) ? 64
                                  : (kAcc * NT <= 128) ? 128 : (kAcc * NT <= 256) ? 256 : 512;
   // TMA box height for B: largest multiple-of-8 divisor of NT that is <= 256
@@ -115,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const UmmaArgs args) {
   using C = UmmaCfg<NT>;
+  static_assert(C::kOv == 0 || MODE == kBigint, "overlapped accumulators need the BIGINT epilogue");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
@@ -124,7 +131,8 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
   uint64_t* tempty = tfull + C::kAcc;
-  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(tempty + C::kAcc);
+  uint64_t* oempty = tempty + C::kAcc;
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(oempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
@@ -138,6 +146,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
     }
+    mbar_init(oempty, 128);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tbase_smem, C::kTmemCols);
@@ -178,10 +187,16 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       int64_t t;
       int k0, k1, stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0;
+      int seg = 0;
       while (it.next(t, k0, k1)) {
         mbar_wait(&tempty[acc], aphase ^ 1);
+        if constexpr (C::kOv > 0) {
+          // the previous segment (other buffer) must have drained the overlap
+          if (seg > 0) mbar_wait(oempty, (uint32_t)((seg - 1) & 1));
+        }
         tc_fence_after();
-        const uint32_t d = tbase + (uint32_t)(acc * NT);
+        const uint32_t d = tbase + (uint32_t)(acc * C::kAccOff1);
+        ++seg;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -223,7 +238,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       const int64_t row = (int64_t)m * kBM + lrow;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * NT);
+      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * C::kAccOff1);
       if constexpr (MODE == kLimbCols || MODE == kLimbRowsNeg) {
         const bool partial = args.split != 0;
 #pragma unroll 1
@@ -260,13 +275,34 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
       } else {
         // BIGINT: z_r = sum_b P[r, b] 2^(8b), carry-propagated (b is added by
         // the group stage, so this GEMM does not depend on the GEMV)
+        constexpr int kOvChunks = C::kOv / 16;
+        uint32_t ov[kOvChunks > 0 ? kOvChunks : 1][16];
+        const int first = (acc == 0) ? (NT - C::kOv) : 0;
+        if constexpr (kOvChunks > 0) {
+          // drain the TMEM columns shared with the other buffer first
+#pragma unroll
+          for (int q = 0; q < kOvChunks; ++q) tmem_ld16(taddr + first + 16 * q, ov[q]);
+          tmem_wait_ld();
+          tc_fence_before();
+          mbar_arrive(oempty);
+        }
         unsigned long long carry = 0;
         uint32_t* zr = args.out + row * args.wz;
 #pragma unroll 1
         for (int c0 = 0; c0 < NT; c0 += 16) {
           uint32_t r[16];
-          tmem_ld16(taddr + c0, r);
-          tmem_wait_ld();
+          const bool in_ov = kOvChunks > 0 && c0 >= first && c0 < first + C::kOv;
+          if (in_ov) {
+            const int qi = (c0 - first) >> 4;
+#pragma unroll
+            for (int q = 0; q < (kOvChunks > 0 ? kOvChunks : 1); ++q)
+              if (q == qi)
+#pragma unroll
+                for (int i = 0; i < 16; ++i) r[i] = ov[q][i];
+          } else {
+            tmem_ld16(taddr + c0, r);
+            tmem_wait_ld();
+          }
           uint32_t limb[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
