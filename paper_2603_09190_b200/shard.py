@@ -44,7 +44,10 @@ def gather_groups(t_local: torch.Tensor, bounds, rank: int, group=None) -> torch
     pad = torch.zeros((gmax, L), dtype=t_local.dtype, device=t_local.device)
     pad[: t_local.shape[0]] = t_local
     full = torch.empty((world * gmax, L), dtype=t_local.dtype, device=t_local.device)
-    dist.all_gather_into_tensor(full, pad, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(full, pad, group=group)
+    else:  # gloo (CPU tests of the multi-rank host logic)
+        dist.all_gather(list(full.split(gmax)), pad, group=group)
     parts = [full[s * gmax: s * gmax + (b[3] - b[2])] for s, b in enumerate(bounds)]
     return torch.cat(parts, 0)
 

@@ -115,3 +115,39 @@ def test_answer_rows_engines(env, lm, n):
     zi = limbs_to_ints(z1)
     for row in (0, 1, 77, 255):
         assert zi[row] == sum(int(h) * c for h, c in zip(H[row], ck))
+
+
+@pytest.mark.parametrize("lm", [32, 64, 96])
+@pytest.mark.parametrize("ctas", [1, 3])
+def test_umma_few_ctas_multi_tile(env, lm, ctas):
+    """Few persistent CTAs -> each walks several tiles, cycling both TMEM
+    accumulator buffers (and, for lm = 64, the 32-column overlap hand-off)."""
+    torch, device = env
+    rng = np.random.default_rng(lm + ctas)
+    rows, n = 640, 256
+    H = rng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
+    r = random.Random(lm * ctas)
+    ck = [r.randrange(1 << (32 * lm)) for _ in range(n)]
+    from paper_2603_09190_b200.bigint import ints_to_limbs, limbs_to_ints
+    dev = torch.device("cuda", 0)
+    Hd = device.u32_tensor(H, dev)
+    cd = device.u32_tensor(ints_to_limbs(ck, lm), dev)
+    bd = torch.zeros(rows, dtype=torch.int32, device=dev)
+    z_ref = device.to_host_u32(device.answer_rows(Hd, bd, 0xFFFFFFFF, cd, lm))
+    bc = device.build_bc(cd, lm)
+    z = device.to_host_u32(device.umma_answer_rows(Hd, bc, bd, 0xFFFFFFFF, lm, ctas=ctas))
+    assert np.array_equal(z, z_ref)
+    zi = limbs_to_ints(z)
+    for row in (0, 129, 383, 639):
+        assert zi[row] == sum(int(h) * c for h, c in zip(H[row], ck))
+    # GEMV stream-K on the same few CTAs
+    d0 = 5000
+    db = rng.integers(0, 256, (d0, rows), dtype=np.uint8)
+    qu = rng.integers(0, 1 << 32, d0, dtype=np.uint64)
+    ld = _rup(d0, 64)
+    dbt = _dbt(torch, device, db, rows, ld)
+    q = np.zeros((1, ld), np.uint32)
+    q[0, :d0] = qu
+    planes = device.query_planes(device.u32_tensor(q, dev), 16)
+    b = device.to_host_u32(device.umma_gemv(dbt, planes, 1, ctas=ctas))[0]
+    assert np.array_equal(b.astype(np.uint64), oracle_c.db_matvec(db, qu))
