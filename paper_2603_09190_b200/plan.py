@@ -1,0 +1,110 @@
+"""Captured online-answer plans: fixed device buffers + CUDA graphs.
+
+One plan per (state, thread, key width, output stride). Its input buffers
+(qu, cko) and output (t) have fixed addresses, so the whole device sequence
+-- query planes, compression operand, the two tcgen05 GEMMs, the group
+stage -- is captured once into CUDA graphs and replayed per query:
+
+  full graph     GEMV on (SMs - COMPRESS_CTAS) SMs || compression on a side
+                 stream on COMPRESS_CTAS SMs, joined by the group stage
+                 (device-resident throughput; bench `value`)
+  gemv graph     query planes + GEMV on all SMs
+  compress graph compression operand + compression GEMM (all SMs) + groups
+                 (respond(): the host converts ck_o while the gemv graph runs)
+
+The eager sequence is run once before capture (sets kernel attributes,
+warms the TMA-descriptor path). ZPIR_GRAPHS=0 disables capture.
+"""
+
+import os
+
+import torch
+
+from . import device
+
+USE_GRAPHS = os.environ.get("ZPIR_GRAPHS", "1") != "0"
+
+
+class AnswerPlan:
+    def __init__(self, state, kctx, t_ld, compress_ctas):
+        lay = state.layout
+        dev = state.device
+        lm = kctx.lm
+        if lm not in device.UMMA_NB or lay.qmask != 0xFFFFFFFF or state.engine != "umma":
+            raise NotImplementedError("plans cover the tcgen05 path (lm 32/64/96, q = 2^32)")
+        self.state, self.kctx, self.t_ld = state, kctx, t_ld
+        self.ctas = compress_ctas
+        self.sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.qu = torch.zeros((1, lay.ld), dtype=torch.int32, device=dev)
+        self.cko = torch.zeros((lay.n, lm), dtype=torch.int32, device=dev)
+        self.planes = torch.empty((16, lay.ld), dtype=torch.uint8, device=dev)
+        self.b = torch.empty((1, lay.rows), dtype=torch.int32, device=dev)
+        self.bc = torch.empty((device.UMMA_NB[lm], 4 * lay.n), dtype=torch.uint8, device=dev)
+        self.z = torch.empty((lay.rows, lm + 4), dtype=torch.int32, device=dev)
+        self.t = torch.empty((lay.groups, t_ld), dtype=torch.int32, device=dev)
+        # pinned host mirrors for respond(): written in place, copied async
+        self.h_qu = torch.zeros((lay.ld,), dtype=torch.int32).pin_memory()
+        self.h_cko = torch.empty((lay.n, lm), dtype=torch.int32).pin_memory()
+        self.h_t = torch.empty((lay.groups, t_ld), dtype=torch.int32).pin_memory()
+        self.h_K = torch.empty((lay.groups, kctx.l2), dtype=torch.int32).pin_memory()
+        self.side = torch.cuda.Stream(dev)
+        self.ev_in = torch.cuda.Event()
+        self.ev_comp = torch.cuda.Event()
+        self.graphs = {}
+
+    # -- eager pieces (also what gets captured) -----------------------------
+
+    def _gemv(self, stream, ctas):
+        device.query_planes(self.qu, 16, stream, planes=self.planes)
+        device.umma_gemv(self.state.dbt, self.planes, 1, out=self.b, stream=stream, ctas=ctas)
+
+    def _compress(self, stream, ctas):
+        st, lm = self.state, self.kctx.lm
+        device.build_bc(self.cko, lm, stream=stream, bc=self.bc)
+        device.umma_answer_rows(st.H_dev, self.bc, self.b[0], st.layout.qmask, lm, out=self.z,
+                                stream=stream, ctas=ctas)
+
+    def _groups(self, stream):
+        lay = self.state.layout
+        device.answer_groups(self.z, self.b[0], lay.qmask, lay.d1, lay.cap, lay.groups, self.kctx,
+                             self.t_ld, out=self.t, stream=stream)
+
+    def _seq(self, which, stream):
+        if which == "full":
+            if self.ctas > 0:
+                self.ev_in.record(stream)
+                self.side.wait_event(self.ev_in)
+                self._compress(self.side, self.ctas)
+                self.ev_comp.record(self.side)
+                self._gemv(stream, self.sms - self.ctas)
+                stream.wait_event(self.ev_comp)
+            else:
+                self._gemv(stream, 0)
+                self._compress(stream, 0)
+            self._groups(stream)
+        elif which == "gemv":
+            self._gemv(stream, 0)
+        elif which == "compress":
+            self._compress(stream, 0)
+            self._groups(stream)
+        else:
+            raise ValueError(which)
+
+    # -- graph replay ----------------------------------------------------------
+
+    def run(self, which, stream):
+        if not USE_GRAPHS:
+            return self._seq(which, stream)
+        g = self.graphs.get(which)
+        if g is None:
+            self._seq(which, stream)  # eager warm-up on the caller's stream
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream(self.state.device)
+            cap.wait_stream(stream)
+            with torch.cuda.graph(g, stream=cap):
+                self._seq(which, cap)
+            stream.wait_stream(cap)
+            self.graphs[which] = g
+        with torch.cuda.stream(stream):
+            g.replay()

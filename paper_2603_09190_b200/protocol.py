@@ -34,6 +34,7 @@ from . import counters, device
 from .bigint import ints_to_limbs, key_ctx, limbs_to_ints
 from .paillier import PaillierCiphertext, PaillierPublicKey, sample_ciphertext  # noqa: F401
 from .params import Layout, LweParams, ProtocolParams  # noqa: F401
+from .plan import AnswerPlan
 from .prg import Stream, DOM_PUBLIC_MATRIX
 
 SEPARATE = "separate"
@@ -257,6 +258,20 @@ class ServerGlobalState:
             }
         return w
 
+    def answer_plan(self, kctx, t_ld):
+        """Per-thread captured plan for the tcgen05 path, or None."""
+        if not (self.engine == "umma" and kctx.lm in device.UMMA_NB
+                and self.layout.qmask == 0xFFFFFFFF):
+            return None
+        plans = getattr(self._tls, "plans", None)
+        if plans is None:
+            plans = self._tls.plans = {}
+        key = (kctx.lm, t_ld)
+        p = plans.get(key)
+        if p is None:
+            p = plans[key] = AnswerPlan(self, kctx, t_ld, COMPRESS_CTAS)
+        return p
+
     def answer_device(self, qu_dev, cko_dev, kctx, t_ld, stream, events=None):
         """t (groups x t_ld u32 limbs) for one staged query; all on device.
 
@@ -349,21 +364,51 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     kctx = key_ctx(reg.pk.m, dev)
     t_total = time.perf_counter()
     events = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timings is not None else None
-    qu_dev = state._stage_query(qmsg.qu0, stream)
-    cko = _h2d(ints_to_limbs(qmsg.ck_o, kctx.lm), dev, "cko", stream).view(torch.int32)
-    cko = cko.reshape(lay.n, kctx.lm)
-    if mode == SEPARATE:
-        t_dev = state.answer_device(qu_dev, cko, kctx, kctx.lm, stream, events)
-        t = limbs_to_ints(_d2h_u32(t_dev, "t", stream))
-        out = ResponseMessage(SEPARATE, qmsg.query_index, t, stored.entries)
+    t_ld = kctx.lm if mode == SEPARATE else kctx.l2
+    plan = state.answer_plan(kctx, t_ld)
+    if plan is not None:
+        # qu -> pinned -> device, GEMV graph; the host converts ck_o meanwhile
+        qu = np.asarray(qmsg.qu0)
+        hq = plan.h_qu.numpy().view(np.uint32)
+        np.copyto(hq[: lay.d0], qu, casting="unsafe")
+        with torch.cuda.stream(stream):
+            plan.qu.view(-1).copy_(plan.h_qu, non_blocking=True)
+        if events:
+            events[0].record(stream)
+        plan.run("gemv", stream)
+        if events:
+            events[1].record(stream)
+        ints_to_limbs(qmsg.ck_o, kctx.lm, out=plan.h_cko.numpy().view(np.uint32))
+        with torch.cuda.stream(stream):
+            plan.cko.copy_(plan.h_cko, non_blocking=True)
+        plan.run("compress", stream)
+        if events:
+            events[2].record(stream)
+        t_dev, h_out = plan.t, plan.h_t
+        if mode == COMBINED:
+            k_dev = _stored_device(stored, kctx, dev, stream)
+            t_dev = device.combine(plan.t, k_dev, kctx, stream=stream)
+            h_out = plan.h_K
+        with torch.cuda.stream(stream):
+            h_out.copy_(t_dev, non_blocking=True)
+        stream.synchronize()
+        vals = limbs_to_ints(h_out.numpy().view(np.uint32))
     else:
-        t_dev = state.answer_device(qu_dev, cko, kctx, kctx.l2, stream, events)
-        k_dev = _stored_device(stored, kctx, dev, stream)
-        K = device.combine(t_dev, k_dev, kctx, stream=stream)
-        vals = limbs_to_ints(_d2h_u32(K, "K", stream))
+        qu_dev = state._stage_query(qmsg.qu0, stream)
+        cko = _h2d(ints_to_limbs(qmsg.ck_o, kctx.lm), dev, "cko", stream).view(torch.int32)
+        cko = cko.reshape(lay.n, kctx.lm)
+        t_dev = state.answer_device(qu_dev, cko, kctx, t_ld, stream, events)
+        if mode == COMBINED:
+            k_dev = _stored_device(stored, kctx, dev, stream)
+            t_dev = device.combine(t_dev, k_dev, kctx, stream=stream)
+        vals = limbs_to_ints(_d2h_u32(t_dev, "t", stream))
+    if mode == SEPARATE:
+        out = ResponseMessage(SEPARATE, qmsg.query_index, vals, stored.entries)
+    else:
         counters.bump("add", lay.groups)
         counters.bump("group_mult", lay.groups)
-        out = ResponseMessage(COMBINED, qmsg.query_index, [], [PaillierCiphertext(v) for v in vals])
+        out = ResponseMessage(COMBINED, qmsg.query_index, [],
+                              [PaillierCiphertext(v) for v in vals])
     if timings is not None:
         stream.synchronize()
         timings["db_matvec"] = events[0].elapsed_time(events[1]) / 1e3

@@ -97,6 +97,48 @@ def test_respond_separate_and_combined(z, golden, name):
                           k=[c.c for c in r.k]) == list(g.arr["record"])
 
 
+@pytest.mark.parametrize("name", ["ragged", "tiny"])
+def test_cuda_core_engine_bit_exact(z, golden, name):
+    """The CUDA-core engine (IDP4A GEMV, IMAD hint and compression) -- the
+    measured alternative to the tcgen05 path -- matches the reference too."""
+    g = golden(name)
+    st = z.ServerGlobalState(g.params(z), g.db, engine="cuda_core")
+    assert np.array_equal(st.H, g.arr["H"]) if "H" in g.arr else True
+    assert np.array_equal(st.db_matvec(g.arr["qu0"]), g.arr["b"])
+    reg = _reg(z, g)
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(k) for k in g.ints("k")])
+    q = z.QueryMessage(reg.client_id, 0, z.SEPARATE, g.ints("ck_o"), g.arr["qu0"])
+    assert z.respond(st, reg, q).t == g.ints("t")
+    assert [c.c for c in z.respond(st, reg, q, mode=z.COMBINED).k] == g.ints("K")
+
+
+def test_respond_repeated_and_threads(z, golden):
+    """Graph-replayed answers are stable across calls and threads."""
+    import threading
+    g = golden("tiny")
+    st = _state(z, g)
+    reg = _reg(z, g)
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(k) for k in g.ints("k")])
+    q = z.QueryMessage(reg.client_id, 0, z.SEPARATE, g.ints("ck_o"), g.arr["qu0"])
+    want = g.ints("t")
+    for _ in range(3):
+        assert z.respond(st, reg, q).t == want
+    errs = []
+
+    def worker():
+        try:
+            for _ in range(3):
+                assert z.respond(st, reg, q).t == want
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+    th = [threading.Thread(target=worker) for _ in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+
+
 def test_respond_errors(z, golden):
     g = golden("desk_reduced")
     st = _state(z, g)
