@@ -127,6 +127,10 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
                           const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
                           void* stream);
 
+/* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
+ * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
+int zpir_probe_imad(int blocks, int iters, float* ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,7 +86,7 @@ class KeyCtx:
         self.cm = ModCtx(m, self.lm)
         self.c2 = ModCtx(self.m2, self.l2)
         self.mr = ints_to_limbs([m * self.c2.R % self.m2], self.l2)[0]
-        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(device)
+        dev = lambda a: torch.from_numpy(np.array(a, dtype=np.uint32).view(np.int32)).to(device)
         self.d_m = dev(self.cm.n_limbs)
         self.d_m2 = dev(self.c2.n_limbs)
         self.d_r2sq = dev(self.c2.r2)

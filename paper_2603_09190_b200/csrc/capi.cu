@@ -46,6 +46,7 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
                             const uint32_t*, uint32_t, int, uint32_t*, int, cudaStream_t);
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
+int imad_probe(int, int, float*);
 
 }  // namespace zpir
 
@@ -152,5 +153,7 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
                           void* stream) {
   ZPIR_GUARD(umma_answer_rows_launch(H, rows, n, bc, nb, b, qmask, wz, z, ctas, S(stream)));
 }
+
+int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(blocks, iters, ms)); }
 
 }  // extern "C"

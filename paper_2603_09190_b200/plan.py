@@ -17,12 +17,14 @@ warms the TMA-descriptor path). ZPIR_GRAPHS=0 disables capture.
 """
 
 import os
+import threading
 
 import torch
 
 from . import device
 
 USE_GRAPHS = os.environ.get("ZPIR_GRAPHS", "1") != "0"
+_capture_lock = threading.Lock()
 
 
 class AnswerPlan:
@@ -102,7 +104,9 @@ class AnswerPlan:
             g = torch.cuda.CUDAGraph()
             cap = torch.cuda.Stream(self.state.device)
             cap.wait_stream(stream)
-            with torch.cuda.graph(g, stream=cap):
+            # thread_local: connection threads keep answering while one captures
+            with _capture_lock, torch.cuda.graph(g, stream=cap,
+                                                 capture_error_mode="thread_local"):
                 self._seq(which, cap)
             stream.wait_stream(cap)
             self.graphs[which] = g

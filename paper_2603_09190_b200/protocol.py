@@ -26,6 +26,7 @@ import hashlib
 import os
 import threading
 import time
+import warnings
 
 import numpy as np
 import torch
@@ -156,7 +157,9 @@ class ServerGlobalState:
         A_pad[:d0, :n] = A32
         t0 = time.perf_counter()
         self.A_dev = device.u32_tensor(A_pad, dev)
-        db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+        with warnings.catch_warnings():  # read-only numpy views are only read here
+            warnings.simplefilter("ignore", UserWarning)
+            db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
         self.dbt = device.transpose_db(db_dev, d0, d1, lay.rows, lay.ld, stream)
         del db_dev
         self.engine = engine or ENGINE

@@ -128,9 +128,11 @@ def test_respond_repeated_and_threads(z, golden):
     def worker():
         try:
             for _ in range(3):
-                assert z.respond(st, reg, q).t == want
+                got = z.respond(st, reg, q).t
+                if got != want:
+                    errs.append("mismatch")
         except Exception as e:  # noqa: BLE001
-            errs.append(e)
+            errs.append(repr(e))
     th = [threading.Thread(target=worker) for _ in range(3)]
     for t in th:
         t.start()
