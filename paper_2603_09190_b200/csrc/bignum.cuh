@@ -17,6 +17,7 @@
 // answer reduction mod m (protocol.py:348-350) and the COMBINED response
 // (protocol.py:354-358, paillier.py:104-123).
 #pragma once
+#include "mac_asm.cuh"
 #include "zpir_common.cuh"
 
 namespace zpir {
@@ -155,11 +156,11 @@ __device__ __forceinline__ void big_cond_sub(uint32_t (&x)[LPL], uint32_t top,
   for (int i = 0; i < LPL; ++i) x[i] = ge ? d[i] : x[i];
 }
 
-// t += x * y (lane-local LPL limbs); the carry out of the lane goes to the
-// 64-bit spill (s1:s0).
+// t += x * y with 64-bit products (compiles to IMAD.WIDE.U32 chains); measured
+// fewer SASS instructions than the explicit PTX carry chain (mac_asm.cuh).
 template <int LPL>
-__device__ __forceinline__ void mac_row(uint32_t (&t)[LPL], uint32_t& s0, uint32_t& s1,
-                                        uint32_t x, const uint32_t (&y)[LPL]) {
+__device__ __forceinline__ void mac_row_c(uint32_t (&t)[LPL], uint32_t& s0, uint32_t& s1,
+                                          uint32_t x, const uint32_t (&y)[LPL]) {
   uint64_t c = 0;
 #pragma unroll
   for (int k = 0; k < LPL; ++k) {
@@ -170,6 +171,18 @@ __device__ __forceinline__ void mac_row(uint32_t (&t)[LPL], uint32_t& s0, uint32
   const uint64_t s = (((uint64_t)s1 << 32) | s0) + c;
   s0 = (uint32_t)s;
   s1 = (uint32_t)(s >> 32);
+}
+
+// t += x * y (lane-local LPL limbs); the carry out of the lane goes to the
+// 64-bit spill (s1:s0).
+template <int LPL>
+__device__ __forceinline__ void mac_row(uint32_t (&t)[LPL], uint32_t& s0, uint32_t& s1,
+                                        uint32_t x, const uint32_t (&y)[LPL]) {
+#ifdef ZPIR_MAC_ASM
+  mac_row_asm<LPL>(t, s0, s1, x, y);  // PTX carry chains: more SASS (IMAD + IADD3.X pairs)
+#else
+  mac_row_c<LPL>(t, s0, s1, x, y);    // IMAD.WIDE.U32 + 64-bit adds: fewest instructions
+#endif
 }
 
 // r = a * b * R^-1 mod N, canonical. Requires a < R, b < N (then T < 2N).
