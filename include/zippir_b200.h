@@ -127,6 +127,24 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
                           const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
                           void* stream);
 
+/* ---- batched queries (BASELINE configs[3]; no reference counterpart: the
+ * reference answers strictly one query at a time, protocol.py:333) ---------
+ * nq stacked compression operands (nq x nb x 4n bytes) from nq ck_o limb rows. */
+int zpir_build_bc_batch(const uint32_t* cko, int64_t n, int lm, int nb, int nq, uint8_t* bc,
+                        void* stream);
+/* z[q*rows*wz + r*wz + i] for nq queries in one tcgen05 launch (H tiles are
+ * reused from L2 across the queries of a row block). */
+int zpir_umma_answer_rows_batch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc,
+                                int nb, int nq, int wz, uint32_t* z, void* stream);
+/* Group stage for nq queries: z / b strides zq / bq, per-query modulus limbs
+ * mods[q*lm], n' nps[q], R-power tables rpows[q*nchunks*lm], fast0s[q];
+ * t[q*groups*t_ld + g*t_ld]. */
+int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, int64_t bq,
+                             uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
+                             const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
+                             int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
+                             void* stream);
+
 /* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
  * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
 int zpir_probe_imad(int blocks, int iters, float* ms);

@@ -11,11 +11,11 @@ from .paillier import (PaillierPublicKey, PaillierCiphertext, InvalidCiphertext,
                        add_batch)
 from .protocol import (SEPARATE, COMBINED, ServerGlobalState, ClientHint,  # noqa: F401
                        ClientRegistration, QueryMessage, ResponseMessage, HintRequest,
-                       client_id_of, derive_ck_r, hint, respond)
+                       client_id_of, derive_ck_r, hint, respond, respond_batch)
 
 __all__ = [
     "LweParams", "ProtocolParams", "PaillierPublicKey", "PaillierCiphertext", "multiexp",
     "paillier_matmul", "sample_ciphertext", "ServerGlobalState", "ClientHint",
     "ClientRegistration", "QueryMessage", "ResponseMessage", "client_id_of", "derive_ck_r",
-    "hint", "respond", "SEPARATE", "COMBINED",
+    "hint", "respond", "respond_batch", "SEPARATE", "COMBINED",
 ]

@@ -41,6 +41,11 @@ _SIGS = {
     "zpir_build_bc": ([_p, _c_i64, _c_int, _c_int, _p, _p], _c_int),
     "zpir_umma_answer_rows": ([_p, _c_i64, _c_i64, _p, _c_int, _p, _c_u32, _c_int, _p, _c_int,
                                _p], _c_int),
+    "zpir_build_bc_batch": ([_p, _c_i64, _c_int, _c_int, _c_int, _p, _p], _c_int),
+    "zpir_umma_answer_rows_batch": ([_p, _c_i64, _c_i64, _p, _c_int, _c_int, _c_int, _p, _p],
+                                    _c_int),
+    "zpir_answer_groups_batch": ([_p, _c_i64, _p, _c_i64, _c_u32, _c_i64, _c_int, _c_i64, _c_int,
+                                  _p, _p, _p, _c_int, _p, _p, _c_i64, _c_int, _p], _c_int),
     "zpir_probe_imad": ([_c_int, _c_int, ctypes.POINTER(ctypes.c_float)], _c_int),
 }
 

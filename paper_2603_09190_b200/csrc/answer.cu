@@ -119,13 +119,32 @@ answer_rows_kernel(const uint32_t* __restrict__ H, int64_t n, const uint32_t* __
 //      concurrently in different warps; chunk 0 only needs a conditional
 //      subtraction when R < 2m (m of exactly 32*LM bits)
 //   4. warp 0: t = sum_s r_s mod m
+// Batched over queries with blockIdx.y = query q: z, b, t, the modulus, its
+// R-power table, n' and fast0 are offset by the per-query strides (zero
+// strides and a single n'/fast0 for the one-query call).
+struct GroupBatch {
+  int64_t zq, bq, tq, mq, rq;
+  const uint32_t* nps;     // per-query n' (nullptr: use np)
+  const uint8_t* fast0s;   // per-query fast0 (nullptr: use fast0)
+};
+
 template <int LPL, int NCH>
 __global__ void __launch_bounds__(128)
 answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict__ b,
                      uint32_t qmask, int64_t d1, int cap, int64_t groups,
                      const uint32_t* __restrict__ mod, uint32_t np,
                      const uint32_t* __restrict__ rpow, int fast0, uint32_t* __restrict__ t,
-                     int64_t t_ld) {
+                     int64_t t_ld, GroupBatch bt) {
+  {
+    const int64_t q = blockIdx.y;
+    z += q * bt.zq;
+    b += q * bt.bq;
+    t += q * bt.tq;
+    mod += q * bt.mq;
+    rpow += q * bt.rq;
+    if (bt.nps) np = bt.nps[q];
+    if (bt.fast0s) fast0 = bt.fast0s[q];
+  }
   constexpr int LM = 32 * LPL;
   constexpr int NX = NCH * LM;
   constexpr int LX = NCH * LPL;
@@ -261,17 +280,18 @@ int answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint32_
 int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1,
                          int cap, int64_t groups, int lm, const uint32_t* mod, uint32_t np,
                          const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
-                         cudaStream_t st) {
+                         cudaStream_t st, int nq = 1, GroupBatch bt = GroupBatch{0, 0, 0, 0, 0,
+                                                                                nullptr, nullptr}) {
   if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
       nchunks > 3) {
     set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
     return kErrInput;
   }
-  const unsigned grid = (unsigned)groups;
+  const dim3 grid((unsigned)groups, (unsigned)nq);
 #define ZPIR_GROUPS(NCHV)                                                                    \
   ZPIR_LPL_DISPATCH(lm / 32, {                                                               \
     answer_groups_kernel<LPL, NCHV><<<grid, 128, 0, st>>>(z, b, qmask, d1, cap, groups, mod, \
-                                                          np, rpow, fast0, t, t_ld);         \
+                                                          np, rpow, fast0, t, t_ld, bt);     \
   })
   if (nchunks == 2) {
     ZPIR_GROUPS(2);
@@ -280,6 +300,17 @@ int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, i
   }
 #undef ZPIR_GROUPS
   return check_launch("answer_groups");
+}
+
+// Batched group stage: nq queries sharing d1/cap/lm, per-query moduli.
+int answer_groups_batch_launch(const uint32_t* z, int64_t zq, const uint32_t* b, int64_t bq,
+                               uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
+                               const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
+                               int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld,
+                               int nq, cudaStream_t st) {
+  GroupBatch bt{zq, bq, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s};
+  return answer_groups_launch(z, b, qmask, d1, cap, groups, lm, mods, 0, rpows, nchunks, 0, t,
+                              t_ld, st, nq, bt);
 }
 
 int combine_launch(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* n2,

@@ -47,6 +47,13 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
+int umma_answer_rows_batch_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, int, int, int,
+                                  uint32_t*, cudaStream_t);
+int answer_groups_batch_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, uint32_t, int64_t,
+                               int, int64_t, int, const uint32_t*, const uint32_t*,
+                               const uint32_t*, int, const uint8_t*, uint32_t*, int64_t, int,
+                               cudaStream_t);
 
 }  // namespace zpir
 
@@ -155,5 +162,24 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
 }
 
 int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(blocks, iters, ms)); }
+
+int zpir_build_bc_batch(const uint32_t* cko, int64_t n, int lm, int nb, int nq, uint8_t* bc,
+                        void* stream) {
+  ZPIR_GUARD(build_bc_batch_launch(cko, n, lm, nb, nq, bc, S(stream)));
+}
+
+int zpir_umma_answer_rows_batch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc,
+                                int nb, int nq, int wz, uint32_t* z, void* stream) {
+  ZPIR_GUARD(umma_answer_rows_batch_launch(H, rows, n, bc, nb, nq, wz, z, S(stream)));
+}
+
+int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, int64_t bq,
+                             uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
+                             const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
+                             int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
+                             void* stream) {
+  ZPIR_GUARD(answer_groups_batch_launch(z, zq, b, bq, qmask, d1, cap, groups, lm, mods, nps, rpows,
+                                        nchunks, fast0s, t, t_ld, nq, S(stream)));
+}
 
 }  // extern "C"

@@ -51,6 +51,7 @@ struct UmmaArgs {
   uint32_t qmask;
   const uint32_t* b;
   int wz;
+  int64_t zq;  // BIGINT: per-N-tile (= per query) stride of z
 };
 
 constexpr int kBM = 128;   // rows per tile (TMEM lanes)
@@ -287,7 +288,7 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
           mbar_arrive(oempty);
         }
         unsigned long long carry = 0;
-        uint32_t* zr = args.out + row * args.wz;
+        uint32_t* zr = args.out + (int64_t)n * args.zq + row * args.wz;
 #pragma unroll 1
         for (int c0 = 0; c0 < NT; c0 += 16) {
           uint32_t r[16];
@@ -353,6 +354,8 @@ __global__ void __launch_bounds__(256)
 build_bc_kernel(const uint32_t* __restrict__ cko, int64_t n, int lm, int nb,
                 uint32_t* __restrict__ bc) {
   extern __shared__ uint32_t sck[];
+  cko += (int64_t)blockIdx.z * n * lm;   // query q = blockIdx.z
+  bc += (int64_t)blockIdx.z * nb * n;
   const int64_t k0 = (int64_t)blockIdx.x * 32;
   const int pitch = lm + 1;
   for (int idx = threadIdx.x; idx < 32 * lm; idx += blockDim.x) {
@@ -530,12 +533,38 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
   }
 }
 
-int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st) {
+int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st,
+                    int nq = 1) {
   const size_t smem = (size_t)32 * (lm + 1) * sizeof(uint32_t);
-  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(nb, 32));
+  dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(nb, 32), (unsigned)nq);
   build_bc_kernel<<<grid, 256, smem, st>>>(cko, n, lm, nb,
                                                                reinterpret_cast<uint32_t*>(bc));
   return check_launch("build_bc");
+}
+
+int build_bc_batch_launch(const uint32_t* cko, int64_t n, int lm, int nb, int nq, uint8_t* bc,
+                          cudaStream_t st) {
+  return build_bc_launch(cko, n, lm, nb, bc, st, nq);
+}
+
+// z[q][r * wz + i] for nq queries (bc = nq stacked operands): one launch,
+// tiles = (row block, query) with consecutive tiles sharing the H rows.
+int umma_answer_rows_batch_launch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc,
+                                  int nb, int nq, int wz, uint32_t* z, cudaStream_t st) {
+  UmmaArgs a{};
+  a.split = 0;
+  a.out = z;
+  a.wz = wz;
+  a.zq = rows * wz;
+  const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
+  switch (nb) {
+    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st);
+    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st);
+    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400LL * nq, 4 * n, a, st);
+    default:
+      set_error("umma_answer_rows_batch: unsupported B width %d", nb);
+      return kErrUnsupported;
+  }
 }
 
 int build_aplanes_launch(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* ap,

@@ -163,3 +163,38 @@ def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None, ctas=0):
     _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0], _lib.ptr(b),
               qmask, lm + 4, _lib.ptr(out), ctas, _s(stream))
     return out
+
+
+def build_bc_batch(cko_all, lm, stream=None):
+    """cko_all (nq, n, lm) int32 -> (nq, nb, 4n) uint8 stacked operands."""
+    nq, n, _ = cko_all.shape
+    nb = UMMA_NB[lm]
+    bc = torch.empty((nq, nb, 4 * n), dtype=torch.uint8, device=cko_all.device)
+    _lib.call("zpir_build_bc_batch", _lib.ptr(cko_all), n, lm, nb, nq, _lib.ptr(bc), _s(stream))
+    return bc
+
+
+def umma_answer_rows_batch(H, bc, lm, stream=None):
+    rows, n = H.shape
+    nq, nb, _ = bc.shape
+    z = torch.empty((nq, rows, lm + 4), dtype=torch.int32, device=H.device)
+    _lib.call("zpir_umma_answer_rows_batch", _lib.ptr(H), rows, n, _lib.ptr(bc), nb, nq, lm + 4,
+              _lib.ptr(z), _s(stream))
+    return z
+
+
+def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None):
+    """z (nq, rows, lm+4), b (nq, rows); per-query Montgomery contexts."""
+    nq, rows, wz = z.shape
+    lm = kctxs[0].lm
+    nchunks = max(2, -(-(cap + lm + 4) // lm))
+    dev = z.device
+    mods = torch.stack([k.d_m for k in kctxs])
+    rpows = torch.stack([k.d_rpow(nchunks) for k in kctxs])
+    nps = torch.tensor(np.array([k.cm.np for k in kctxs], dtype=np.uint32).view(np.int32), device=dev)
+    f0 = torch.tensor([1 if k.cm.R < 2 * k.m else 0 for k in kctxs], dtype=torch.uint8, device=dev)
+    t = torch.empty((nq, groups, t_ld), dtype=torch.int32, device=dev)
+    _lib.call("zpir_answer_groups_batch", _lib.ptr(z), rows * wz, _lib.ptr(b), b.shape[1], qmask, d1,
+              cap, groups, lm, _lib.ptr(mods), _lib.ptr(nps), _lib.ptr(rpows), nchunks, _lib.ptr(f0),
+              _lib.ptr(t), t_ld, nq, _s(stream))
+    return t

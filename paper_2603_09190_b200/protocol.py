@@ -420,6 +420,85 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     return out
 
 
+MAX_BATCH = 64
+
+
+def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
+                  stream=None) -> list:
+    """Answer many queries together (BASELINE configs[3]); the reference has
+    no batch path and answers one query at a time (protocol.py:333-365).
+
+    Per chunk of <= 64 queries: ONE tensor-core GEMV streams the DB once for
+    all of them (N = 4 byte planes x 64 queries = 256), one compression launch
+    covers every query (H row blocks reused from L2), one group-stage launch
+    with per-query moduli. Same validation / exceptions / counters as respond;
+    returns the list of ResponseMessages in order."""
+    if len(regs) != len(qmsgs):
+        raise ValueError("regs and qmsgs must have the same length")
+    lay = state.layout
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    modes, storeds, kctxs = [], [], []
+    for reg, q in zip(regs, qmsgs):
+        md = mode or q.mode
+        if len(q.ck_o) != lay.n or len(q.qu0) != lay.d0:
+            raise ValueError("query dimensions do not match the parameters")
+        st = reg.hints.get(q.query_index)
+        if st is None or st.db_version != state.db_version:
+            raise KeyError("no hint for this query index and database version")
+        if md not in (SEPARATE, COMBINED):
+            raise ValueError("unknown response mode")
+        modes.append(md)
+        storeds.append(st)
+        kctxs.append(key_ctx(reg.pk.m, dev))
+    if not qmsgs:
+        return []
+    umma_ok = (state.engine == "umma" and lay.qmask == 0xFFFFFFFF
+               and all(k.lm == kctxs[0].lm for k in kctxs) and kctxs[0].lm in device.UMMA_NB)
+    if not umma_ok:
+        return [respond(state, r, q, mode=md, stream=stream)
+                for r, q, md in zip(regs, qmsgs, modes)]
+    out = []
+    lm = kctxs[0].lm
+    for c0 in range(0, len(qmsgs), MAX_BATCH):
+        qs = qmsgs[c0:c0 + MAX_BATCH]
+        ks = kctxs[c0:c0 + MAX_BATCH]
+        nq = len(qs)
+        q32 = np.zeros((nq, lay.ld), dtype=np.uint32)
+        for i, q in enumerate(qs):
+            np.copyto(q32[i, : lay.d0], np.asarray(q.qu0), casting="unsafe")
+        qd = _h2d(q32, dev, "qb", stream).view(torch.int32).reshape(nq, lay.ld)
+        cko = np.empty((nq, lay.n, lm), dtype=np.uint32)
+        for i, q in enumerate(qs):
+            ints_to_limbs(q.ck_o, lm, out=cko[i])
+        cd = _h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, lay.n, lm)
+        planes = device.query_planes(qd, 16 if nq <= 4 else 256, stream)
+        b = device.umma_gemv(state.dbt, planes, nq, stream=stream)
+        bc = device.build_bc_batch(cd, lm, stream)
+        z = device.umma_answer_rows_batch(state.H_dev, bc, lm, stream)
+        t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, ks,
+                                       ks[0].l2, stream)
+        res = []
+        for i in range(nq):
+            md = modes[c0 + i]
+            if md == SEPARATE:
+                res.append(t[i, :, :lm])
+            else:
+                k_dev = _stored_device(storeds[c0 + i], ks[i], dev, stream)
+                res.append(device.combine(t[i], k_dev, ks[i], stream=stream))
+        for i in range(nq):
+            vals = limbs_to_ints(_d2h_u32(res[i].contiguous(), "tb", stream))
+            md = modes[c0 + i]
+            qi = qs[i].query_index
+            if md == SEPARATE:
+                out.append(ResponseMessage(SEPARATE, qi, vals, storeds[c0 + i].entries))
+            else:
+                counters.bump("add", lay.groups)
+                counters.bump("group_mult", lay.groups)
+                out.append(ResponseMessage(COMBINED, qi, [], [PaillierCiphertext(v) for v in vals]))
+    return out
+
+
 def client_storage_hint_transfer(reg, query_index: int) -> ClientHint:
     """Hand the stored hint to the client; single use (protocol.py:399-408)."""
     if query_index in reg.consumed:

@@ -217,3 +217,45 @@ def test_end_to_end_seeded_queries(z):
             rec = client.extract(sk, 1 << 32, 256, params.capacity, 1 << 32, 48,
                                  combined=[c.c for c in r.k])
         assert rec == [int(x) for x in db[i0]]
+
+
+@pytest.mark.parametrize("nq", [1, 5, 64, 70])
+def test_respond_batch_bit_exact(z, golden, nq):
+    """Batched answers (one GEMV for all queries, one compression launch) equal
+    the per-query reference answers; mixed modes; different clients/moduli."""
+    g = golden("tiny")
+    st = _state(z, g)
+    rng = random.Random(nq)
+    A = st.A
+    lw = g.lwe
+    regs, qs, wants, modes = [], [], [], []
+    keys = [client.SecretKey(g.p, g.q)] + [client.keygen(2048, random.Random(1000 + j))
+                                            for j in range(2)]
+    for i in range(nq):
+        sk = keys[i % len(keys)]
+        pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+        seed = bytes([i % 7] * 16)
+        reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
+        reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(rng.randrange(sk.m * sk.m))
+                                           for _ in range(g.groups)])
+        qu = np.array([rng.randrange(1 << 32) for _ in range(g.d0)], dtype=np.uint64)
+        ck = [rng.randrange(sk.m) for _ in range(lw["n"])]
+        mode = z.SEPARATE if i % 3 else z.COMBINED
+        regs.append(reg)
+        qs.append(z.QueryMessage(reg.client_id, 0, mode, ck, qu))
+        modes.append(mode)
+    got = z.respond_batch(st, regs, qs)
+    for i in (0, 1, nq // 2, nq - 1):
+        want = z.respond(st, regs[i], qs[i])
+        assert got[i].mode == modes[i]
+        assert got[i].t == want.t and [c.c for c in got[i].k] == [c.c for c in want.k], i
+    # and against the oracle for one query
+    b = ref.db_matvec(g.db, qs[-1].qu0, 1 << 32)
+    H = st.H
+    sk = keys[(nq - 1) % len(keys)]
+    t = ref.answer_t(H, b, qs[-1].ck_o, sk.m, g.cap, g.gamma, g.d1)
+    if modes[-1] == z.SEPARATE:
+        assert got[-1].t == t
+    else:
+        k = [c.c for c in regs[-1].hints[0].entries]
+        assert [c.c for c in got[-1].k] == ref.combined(t, k, sk.m)
