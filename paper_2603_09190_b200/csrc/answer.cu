@@ -277,11 +277,11 @@ int answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint32_
       return kErrUnsupported;                                          \
   }
 
-int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1,
-                         int cap, int64_t groups, int lm, const uint32_t* mod, uint32_t np,
-                         const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
-                         cudaStream_t st, int nq = 1, GroupBatch bt = GroupBatch{0, 0, 0, 0, 0,
-                                                                                nullptr, nullptr}) {
+static int answer_groups_launch_ex(const uint32_t* z, const uint32_t* b, uint32_t qmask,
+                                   int64_t d1, int cap, int64_t groups, int lm,
+                                   const uint32_t* mod, uint32_t np, const uint32_t* rpow,
+                                   int nchunks, int fast0, uint32_t* t, int64_t t_ld,
+                                   cudaStream_t st, int nq, GroupBatch bt) {
   if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
       nchunks > 3) {
     set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
@@ -309,8 +309,16 @@ int answer_groups_batch_launch(const uint32_t* z, int64_t zq, const uint32_t* b,
                                int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld,
                                int nq, cudaStream_t st) {
   GroupBatch bt{zq, bq, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s};
-  return answer_groups_launch(z, b, qmask, d1, cap, groups, lm, mods, 0, rpows, nchunks, 0, t,
-                              t_ld, st, nq, bt);
+  return answer_groups_launch_ex(z, b, qmask, d1, cap, groups, lm, mods, 0, rpows, nchunks, 0, t,
+                                 t_ld, st, nq, bt);
+}
+
+int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1,
+                         int cap, int64_t groups, int lm, const uint32_t* mod, uint32_t np,
+                         const uint32_t* rpow, int nchunks, int fast0, uint32_t* t, int64_t t_ld,
+                         cudaStream_t st) {
+  return answer_groups_launch_ex(z, b, qmask, d1, cap, groups, lm, mod, np, rpow, nchunks, fast0,
+                                 t, t_ld, st, 1, GroupBatch{0, 0, 0, 0, 0, nullptr, nullptr});
 }
 
 int combine_launch(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* n2,
