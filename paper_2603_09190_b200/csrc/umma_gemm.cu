@@ -533,8 +533,8 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
   }
 }
 
-int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st,
-                    int nq = 1) {
+static int build_bc_launch_ex(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc,
+                              cudaStream_t st, int nq) {
   const size_t smem = (size_t)32 * (lm + 1) * sizeof(uint32_t);
   dim3 grid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(nb, 32), (unsigned)nq);
   build_bc_kernel<<<grid, 256, smem, st>>>(cko, n, lm, nb,
@@ -542,9 +542,13 @@ int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc,
   return check_launch("build_bc");
 }
 
+int build_bc_launch(const uint32_t* cko, int64_t n, int lm, int nb, uint8_t* bc, cudaStream_t st) {
+  return build_bc_launch_ex(cko, n, lm, nb, bc, st, 1);
+}
+
 int build_bc_batch_launch(const uint32_t* cko, int64_t n, int lm, int nb, int nq, uint8_t* bc,
                           cudaStream_t st) {
-  return build_bc_launch(cko, n, lm, nb, bc, st, nq);
+  return build_bc_launch_ex(cko, n, lm, nb, bc, st, nq);
 }
 
 // z[q][r * wz + i] for nq queries (bc = nq stacked operands): one launch,
