@@ -245,7 +245,7 @@ def test_respond_batch_bit_exact(z, golden, nq):
         qs.append(z.QueryMessage(reg.client_id, 0, mode, ck, qu))
         modes.append(mode)
     got = z.respond_batch(st, regs, qs)
-    for i in (0, 1, nq // 2, nq - 1):
+    for i in sorted({0, min(1, nq - 1), nq // 2, nq - 1}):
         want = z.respond(st, regs[i], qs[i])
         assert got[i].mode == modes[i]
         assert got[i].t == want.t and [c.c for c in got[i].k] == [c.c for c in want.k], i
