@@ -95,17 +95,25 @@ def client_id_of(pk) -> bytes:
 
 
 class _Staging(threading.local):
-    """Per-thread pinned host buffers for the per-query H2D / D2H copies."""
+    """Per-thread pinned host buffers for H2D / D2H staging. Each buffer
+    carries the event of the last async copy that read or wrote it; get()
+    waits for it, so a buffer is never rewritten while a copy is in flight."""
 
     def __init__(self):
         self.bufs = {}
 
     def get(self, key, nbytes):
-        buf = self.bufs.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 4096), dtype=torch.uint8).pin_memory()
-            self.bufs[key] = buf
-        return buf[:nbytes]
+        ent = self.bufs.get(key)
+        if ent is not None:
+            ent[1].synchronize()
+        if ent is None or ent[0].numel() < nbytes:
+            ent = (torch.empty(max(nbytes, 4096), dtype=torch.uint8).pin_memory(),
+                   torch.cuda.Event())
+            self.bufs[key] = ent
+        return ent[0][:nbytes]
+
+    def mark(self, key, stream):
+        self.bufs[key][1].record(stream)
 
 
 _staging = _Staging()
@@ -119,6 +127,7 @@ def _h2d(arr: np.ndarray, dev, key, stream) -> torch.Tensor:
     out = torch.empty(raw.nbytes, dtype=torch.uint8, device=dev)
     with torch.cuda.stream(stream):
         out.copy_(pinned, non_blocking=True)
+    _staging.mark(key, stream)
     return out
 
 
