@@ -49,6 +49,14 @@ class AnswerPlan:
         self.h_cko = torch.empty((lay.n, lm), dtype=torch.int32).pin_memory()
         self.h_t = torch.empty((lay.groups, t_ld), dtype=torch.int32).pin_memory()
         self.h_K = torch.empty((lay.groups, kctx.l2), dtype=torch.int32).pin_memory()
+        # the client's modulus constants live in plan buffers read by the
+        # captured group stage (refreshed by set_key when the client changes)
+        self.nchunks = max(2, -(-(lay.cap + lm + 4) // lm))
+        self.d_m = torch.zeros((1, lm), dtype=torch.int32, device=dev)
+        self.d_rpow = torch.zeros((1, self.nchunks, lm), dtype=torch.int32, device=dev)
+        self.d_np = torch.zeros((1,), dtype=torch.int32, device=dev)
+        self.d_f0 = torch.zeros((1,), dtype=torch.uint8, device=dev)
+        self.key_m = None
         self.side = torch.cuda.Stream(dev)
         self.ev_in = torch.cuda.Event()
         self.ev_comp = torch.cuda.Event()
@@ -66,10 +74,25 @@ class AnswerPlan:
         device.umma_answer_rows(st.H_dev, self.bc, self.b[0], st.layout.qmask, lm, out=self.z,
                                 stream=stream, ctas=ctas)
 
+    def set_key(self, kctx, stream):
+        """Load a client's modulus constants into the plan buffers (in-stream)."""
+        if self.key_m == kctx.m:
+            return
+        import numpy as np
+        with torch.cuda.stream(stream):
+            self.d_m[0].copy_(kctx.d_m)
+            self.d_rpow[0].copy_(kctx.d_rpow(self.nchunks))
+            self.d_np.copy_(torch.tensor(np.array([kctx.cm.np], np.uint32).view(np.int32)),
+                            non_blocking=False)
+            self.d_f0.fill_(1 if kctx.cm.R < 2 * kctx.m else 0)
+        self.kctx = kctx
+        self.key_m = kctx.m
+
     def _groups(self, stream):
         lay = self.state.layout
-        device.answer_groups(self.z, self.b[0], lay.qmask, lay.d1, lay.cap, lay.groups, self.kctx,
-                             self.t_ld, out=self.t, stream=stream)
+        device.answer_groups_plan(self.z, self.b, lay.qmask, lay.d1, lay.cap, lay.groups,
+                                  self.kctx.lm, self.d_m, self.d_np, self.d_rpow, self.nchunks,
+                                  self.d_f0, self.t, self.t_ld, stream)
 
     def _seq(self, which, stream):
         if which == "full":
@@ -95,6 +118,8 @@ class AnswerPlan:
     # -- graph replay ----------------------------------------------------------
 
     def run(self, which, stream):
+        if self.key_m is None:
+            self.set_key(self.kctx, stream)
         if not USE_GRAPHS:
             return self._seq(which, stream)
         g = self.graphs.get(which)

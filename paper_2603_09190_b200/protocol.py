@@ -379,6 +379,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     t_ld = kctx.lm if mode == SEPARATE else kctx.l2
     plan = state.answer_plan(kctx, t_ld)
     if plan is not None:
+        plan.set_key(kctx, stream)
         # qu -> pinned -> device, GEMV graph; the host converts ck_o meanwhile
         qu = np.asarray(qmsg.qu0)
         hq = plan.h_qu.numpy().view(np.uint32)
