@@ -54,6 +54,10 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--workload", default="1g", choices=["1g", "batch64", "8g", "hint"],
+                    help="1g: BASELINE configs[1] (default, the driver's line); batch64: "
+                         "configs[3]; 8g: configs[2] (92682^2, strong-scaled over --gpus); "
+                         "hint: configs[4] offline hint generation")
     return ap.parse_args()
 
 
@@ -411,10 +415,145 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def run_extra(args):
+    """Non-default workloads (printed as one JSON line each, rank 0)."""
+    import torch
+    rank, world, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import _lib, build as zb
+    from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
+    zb.build()
+    _lib.load()
+    stream = torch.cuda.current_stream(dev)
+    m = paillier_modulus(BITS, 2048)
+    kctx = key_ctx(m, dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    peak, peak_src = _peaks()
+    if args.workload == "8g":
+        d = 92682
+        params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), d, d, BITS)
+        from paper_2603_09190_b200.shard import ShardedServer, shard_bounds
+        bounds = shard_bounds(d, params.capacity, world)
+        lo, hi, _, _ = bounds[rank]
+        db = np.frombuffer(np.random.default_rng(8).bytes(d * d), dtype=np.uint8).reshape(d, d)
+        t0 = time.perf_counter()
+        srv = ShardedServer(params, db[:, lo:hi], rank, world)
+        setup = time.perf_counter() - t0
+        del db
+        st = srv.state
+        plan = st.answer_plan(kctx, kctx.lm)
+        rng = np.random.default_rng(3)
+        q32 = np.zeros(st.layout.ld, np.uint32)
+        q32[:d] = rng.integers(0, 1 << 32, d, dtype=np.uint64)
+        plan.qu.copy_(torch.from_numpy(q32.view(np.int32)).to(dev).reshape(1, -1))
+        r = random.Random(4)
+        plan.cko.copy_(torch.from_numpy(ints_to_limbs([r.randrange(m) for _ in range(N_LWE)],
+                                                      kctx.lm).view(np.int32)).to(dev))
+
+        def step():
+            plan.run("full", stream)
+            if world > 1:
+                from paper_2603_09190_b200.shard import gather_groups
+                with torch.cuda.stream(stream):
+                    gather_groups(plan.t, bounds, rank)
+        for _ in range(max(args.warmup, 3)):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        out = {"workload": "BASELINE configs[2]: 8 GiB DB 92682 x 92682 u8, n=1024, 2048-bit, "
+                           "rows sharded group-aligned", "n_gpus": world, "scaling": "strong",
+               "metric": "online server throughput (DB GB/s per query)",
+               "value": d * d / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+               "per_gpu_hbm_frac": (d * (hi - lo)) / (ms / 1e3) / 1e9 / peak, "setup_s": setup}
+    elif args.workload == "batch64":
+        params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
+        st = z.ServerGlobalState(params, db_slice(0, D1))
+        nq = 64
+        rng = np.random.default_rng(5)
+        q32 = np.zeros((nq, st.layout.ld), np.uint32)
+        q32[:, :D0] = rng.integers(0, 1 << 32, (nq, D0), dtype=np.uint64)
+        qd = torch.from_numpy(q32.view(np.int32)).to(dev)
+        r = random.Random(6)
+        cko = np.stack([ints_to_limbs([r.randrange(m) for _ in range(N_LWE)], kctx.lm)
+                        for _ in range(nq)])
+        cd = torch.from_numpy(cko.view(np.int32)).to(dev)
+        ks = [kctx] * nq
+        for _ in range(max(args.warmup, 3)):
+            st.answer_batch_device(qd, cd, ks, kctx.lm, stream)
+        torch.cuda.synchronize()
+        steps = max(3, args.steps // 20)
+        evs = [[ev(), ev(), ev()] for _ in range(steps)]
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for i in range(steps):
+            st.answer_batch_device(qd, cd, ks, kctx.lm, stream, evs[i])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        gemv = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+        comp = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+        ops = 2 * 64 * D0 * D1
+        out = {"workload": "BASELINE configs[3]: 1 GiB DB, 64 queries per step (N = 256 byte-plane "
+                           "GEMV) + 64 compressions", "n_gpus": 1,
+               "metric": "online server throughput (DB GB/s per query, 64 queries)",
+               "value": nq * D0 * D1 / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
+               "gemv_ms": gemv, "compress_ms": comp,
+               "gemv_u8xu32_macs_per_s": ops / 2 / (gemv / 1e3),
+               "gemv_hbm_frac": (D0 * D1) / (gemv / 1e3) / 1e9 / peak}
+    else:  # hint
+        params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
+        t0 = time.perf_counter()
+        st = z.ServerGlobalState(params, db_slice(0, D1))
+        setup = time.perf_counter() - t0
+        nclients = 4
+        times = []
+        for j in range(nclients):
+            mj = paillier_modulus(BITS, 3000 + j)
+            pk = z.PaillierPublicKey(mj, mj.bit_length())
+            reg = z.ClientRegistration(pk, bytes([j]) * 16, z.client_id_of(pk))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            z.hint(st, reg, 0)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t1)
+        per = statistics.median(times)
+        ref_mulmods = 361620 * params.d1_prime
+        imad = None
+        try:
+            imad = json.load(open(os.path.join(ROOT, "profiles", "imad_peak.json")))["imad_per_s"]
+        except Exception:
+            pass
+        out = {"workload": "BASELINE configs[4]: global H = DB A (1 GiB, n=1024) + per-client "
+                           "compressed hint (521 entries, 2048-bit)", "n_gpus": 1,
+               "global_hint_s": st.hint_time, "setup_s": setup,
+               "hint_s_per_client": per, "clients_sampled": nclients,
+               "extrapolated_256_clients_s": 256 * per,
+               "reference_equivalent_mulmods_per_s": ref_mulmods / per,
+               "imad_peak_per_s": imad,
+               "imad_util_reference_equivalent": (ref_mulmods / per * 65792 / imad) if imad else None}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
 def main():
     args = _args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "1g":
+        run_extra(args)
     else:
         run_b200(args)
 

@@ -284,6 +284,26 @@ class ServerGlobalState:
             p = plans[key] = AnswerPlan(self, kctx, t_ld, COMPRESS_CTAS)
         return p
 
+    def answer_batch_device(self, qu_dev, cko_dev, kctxs, t_ld, stream, events=None):
+        """t (nq x groups x t_ld) for nq <= 64 staged queries (tcgen05 path):
+        one N = 4*nq GEMV over the DB, one compression launch, one group launch."""
+        lay = self.layout
+        nq = qu_dev.shape[0]
+        lm = kctxs[0].lm
+        if events:
+            events[0].record(stream)
+        planes = device.query_planes(qu_dev, 16 if nq <= 4 else 256, stream)
+        b = device.umma_gemv(self.dbt, planes, nq, stream=stream)
+        if events:
+            events[1].record(stream)
+        bc = device.build_bc_batch(cko_dev, lm, stream)
+        z = device.umma_answer_rows_batch(self.H_dev, bc, lm, stream)
+        t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctxs, t_ld,
+                                       stream)
+        if events:
+            events[2].record(stream)
+        return t
+
     def answer_device(self, qu_dev, cko_dev, kctx, t_ld, stream, events=None):
         """t (groups x t_ld u32 limbs) for one staged query; all on device.
 
@@ -482,12 +502,7 @@ def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
         for i, q in enumerate(qs):
             ints_to_limbs(q.ck_o, lm, out=cko[i])
         cd = _h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, lay.n, lm)
-        planes = device.query_planes(qd, 16 if nq <= 4 else 256, stream)
-        b = device.umma_gemv(state.dbt, planes, nq, stream=stream)
-        bc = device.build_bc_batch(cd, lm, stream)
-        z = device.umma_answer_rows_batch(state.H_dev, bc, lm, stream)
-        t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, ks,
-                                       ks[0].l2, stream)
+        t = state.answer_batch_device(qd, cd, ks, ks[0].l2, stream)
         res = []
         for i in range(nq):
             md = modes[c0 + i]
