@@ -145,6 +145,30 @@ int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, i
                              int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
                              void* stream);
 
+/* ---- slot-decomposed hints and incremental DB update (BASELINE configs[4];
+ * the reference rebuilds everything on update, server.py:115-124) ---------
+ * Multiexp over an explicit list of exponent rows (row_ids, nullable = 0..rows-1);
+ * out[row_ids[i]] gets row i's product, kept in Montgomery form when keep_mont
+ * (all-zero rows then get one_m = R mod N). */
+int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
+                       const int32_t* row_ids, int64_t rows, int64_t row_stride,
+                       int64_t base_stride, int64_t limb_stride, int elimbs, int limbs,
+                       const uint32_t* N, uint32_t np, const uint32_t* r2, const uint32_t* one_m,
+                       int keep_mont, uint32_t* out, void* workspace, int64_t ws_bytes,
+                       void* stream);
+/* k[g] = prod_j W[g*cap + j]^(2^(32 j)) mod N (W in Montgomery form; k canonical)
+ * for the groups in group_ids (nullable = all ngroups): the hint entry
+ * k_g = prod_k ck_r[k]^H_scaled[g][k] (paillier.py:134-203) rebuilt from its
+ * per-DB-row factors W[c] = prod_k ck_r[k]^H[c][k]. */
+int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
+                      int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream);
+/* flags[r] = (row r of a != row r of b), rows of ld bytes. */
+int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,
+                     void* stream);
+/* Row gather (scatter = 0: dst[i] = src[ids[i]]) / scatter (dst[ids[i]] = src[i]). */
+int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_t* ids,
+                   int64_t nrows, int scatter, void* stream);
+
 /* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
  * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
 int zpir_probe_imad(int blocks, int iters, float* ms);

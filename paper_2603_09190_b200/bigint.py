@@ -91,6 +91,7 @@ class KeyCtx:
         self.d_m2 = dev(self.c2.n_limbs)
         self.d_r2sq = dev(self.c2.r2)
         self.d_mr = dev(self.mr)
+        self.d_one2 = dev(ints_to_limbs([self.c2.R % self.m2], self.l2)[0])  # Montgomery 1
         self._rpow = {}
         self._dev = dev
         self._lock = threading.Lock()

@@ -47,6 +47,13 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_t*, int64_t, int64_t,
+                         int64_t, int64_t, int, int, const uint32_t*, uint32_t, const uint32_t*,
+                         const uint32_t*, int, uint32_t*, void*, int64_t, cudaStream_t);
+int slot_combine_launch(const uint32_t*, int, const int32_t*, int64_t, int, const uint32_t*,
+                        uint32_t, uint32_t*, cudaStream_t);
+int rows_differ_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
+int move_rows_launch(const uint8_t*, uint8_t*, int64_t, const int32_t*, int64_t, int, cudaStream_t);
 int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
 int umma_answer_rows_batch_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, int, int, int,
                                   uint32_t*, cudaStream_t);
@@ -180,6 +187,32 @@ int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, i
                              void* stream) {
   ZPIR_GUARD(answer_groups_batch_launch(z, zq, b, bq, qmask, d1, cap, groups, lm, mods, nps, rpows,
                                         nchunks, fast0s, t, t_ld, nq, S(stream)));
+}
+
+int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
+                       const int32_t* row_ids, int64_t rows, int64_t row_stride,
+                       int64_t base_stride, int64_t limb_stride, int elimbs, int limbs,
+                       const uint32_t* N, uint32_t np, const uint32_t* r2, const uint32_t* one_m,
+                       int keep_mont, uint32_t* out, void* workspace, int64_t ws_bytes,
+                       void* stream) {
+  ZPIR_GUARD(multiexp_rows_launch(bases, n, exps, row_ids, rows, row_stride, base_stride,
+                                  limb_stride, elimbs, limbs, N, np, r2, one_m, keep_mont, out,
+                                  workspace, ws_bytes, S(stream)));
+}
+
+int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
+                      int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream) {
+  ZPIR_GUARD(slot_combine_launch(W, cap, group_ids, ngroups, limbs, N, np, out, S(stream)));
+}
+
+int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,
+                     void* stream) {
+  ZPIR_GUARD(rows_differ_launch(a, b, rows, ld, flags, S(stream)));
+}
+
+int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_t* ids,
+                   int64_t nrows, int scatter, void* stream) {
+  ZPIR_GUARD(move_rows_launch(src, dst, pitch, ids, nrows, scatter, S(stream)));
 }
 
 }  // extern "C"

@@ -114,4 +114,56 @@ int hint_gemm_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint32_
   return check_launch("global_hint");
 }
 
+// ---- incremental database update helpers (server.py:115-124 does a full
+// rebuild; here only the DB rows that changed are re-multiplied) -----------
+
+// flags[r] = 1 iff rows r of a and b (ld bytes, ld % 16 == 0) differ.
+__global__ void __launch_bounds__(256)
+rows_differ_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t ld,
+                   uint32_t* __restrict__ flags) {
+  const int64_t r = blockIdx.x;
+  const uint4* pa = reinterpret_cast<const uint4*>(a + r * ld);
+  const uint4* pb = reinterpret_cast<const uint4*>(b + r * ld);
+  int diff = 0;
+  for (int64_t i = threadIdx.x; i < ld / 16; i += blockDim.x) {
+    const uint4 x = pa[i], y = pb[i];
+    diff |= (x.x != y.x) | (x.y != y.y) | (x.z != y.z) | (x.w != y.w);
+  }
+  diff = __syncthreads_or(diff);
+  if (threadIdx.x == 0) flags[r] = diff ? 1u : 0u;
+}
+
+// dst row i = src row ids[i] (gather) or dst row ids[i] = src row i (scatter),
+// rows of `pitch` bytes (pitch % 16 == 0).
+__global__ void move_rows_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                                 int64_t pitch, const int32_t* __restrict__ ids, int scatter) {
+  const int64_t i = blockIdx.x;
+  const int64_t si = scatter ? i : (int64_t)ids[i];
+  const int64_t di = scatter ? (int64_t)ids[i] : i;
+  const uint4* s = reinterpret_cast<const uint4*>(src + si * pitch);
+  uint4* d = reinterpret_cast<uint4*>(dst + di * pitch);
+  for (int64_t k = threadIdx.x; k < pitch / 16; k += blockDim.x) d[k] = s[k];
+}
+
+int rows_differ_launch(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld,
+                       uint32_t* flags, cudaStream_t st) {
+  if (ld % 16 || rows <= 0) {
+    set_error("rows_differ: ld %% 16 required");
+    return kErrInput;
+  }
+  rows_differ_kernel<<<(unsigned)rows, 256, 0, st>>>(a, b, ld, flags);
+  return check_launch("rows_differ");
+}
+
+int move_rows_launch(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_t* ids,
+                     int64_t nrows, int scatter, cudaStream_t st) {
+  if (pitch % 16 || nrows < 0) {
+    set_error("move_rows: pitch %% 16 required");
+    return kErrInput;
+  }
+  if (nrows == 0) return kOk;
+  move_rows_kernel<<<(unsigned)nrows, 256, 0, st>>>(src, dst, pitch, ids, scatter);
+  return check_launch("move_rows");
+}
+
 }  // namespace zpir

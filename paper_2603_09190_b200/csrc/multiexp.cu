@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(128)
 window_kernel(const uint32_t* __restrict__ bases, int64_t n, const uint32_t* __restrict__ E,
               int64_t rows, int64_t rs, int64_t bs, int64_t ls, int elimbs, int nwin,
               const uint32_t* __restrict__ N, uint32_t np, uint32_t* __restrict__ W,
-              uint8_t* __restrict__ flags) {
+              uint8_t* __restrict__ flags, const int32_t* __restrict__ row_ids) {
   constexpr int L = 32 * LPL;
   extern __shared__ uint32_t smem_u32[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -73,8 +73,9 @@ window_kernel(const uint32_t* __restrict__ bases, int64_t n, const uint32_t* __r
   const int64_t tasks = rows * nwin;
   for (int64_t task = (int64_t)blockIdx.x * wpb + wid; task < tasks;
        task += (int64_t)gridDim.x * wpb) {
-    const int64_t g = task / nwin;
-    const int win = (int)(task - g * nwin);
+    const int64_t gi = task / nwin;
+    const int win = (int)(task - gi * nwin);
+    const int64_t g = row_ids ? (int64_t)row_ids[gi] : gi;  // exponent row
     const int bitpos = win * kWin;
     cnt[lane] = 0;
     cnt[lane + 32] = 0;
@@ -133,7 +134,8 @@ template <int LPL>
 __global__ void __launch_bounds__(128)
 combine_windows_kernel(const uint32_t* __restrict__ W, const uint8_t* __restrict__ flags,
                        int64_t rows, int nwin, const uint32_t* __restrict__ N, uint32_t np,
-                       uint32_t* __restrict__ out) {
+                       uint32_t* __restrict__ out, const int32_t* __restrict__ row_ids,
+                       int keep_mont, const uint32_t* __restrict__ one_m) {
   constexpr int L = 32 * LPL;
   const int lane = threadIdx.x & 31;
   const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -152,12 +154,42 @@ combine_windows_kernel(const uint32_t* __restrict__ W, const uint8_t* __restrict
       has = true;
     }
   }
-  if (has) {
+  if (keep_mont) {
+    if (!has) big_load<LPL>(acc, one_m, lane);   // Montgomery form of 1
+  } else if (has) {
     big_set_small<LPL>(x, 1, lane);
     mont_mul<LPL>(acc, acc, x, n_, np, lane);  // leave Montgomery form
   } else {
     big_set_small<LPL>(acc, 1, lane);          // all exponents zero -> 1 (paillier.py:145-146)
   }
+  const int64_t orow = row_ids ? (int64_t)row_ids[g] : g;
+  big_store<LPL>(out + orow * L, acc, lane);
+}
+
+// Slot-decomposed hint: k_g = prod_j W[g*cap + j]^(2^(32 j)) mod N, with the
+// per-slot products W (Montgomery form) from a 32-bit multiexp per DB row.
+// Horner from the top slot: acc = acc^(2^32) * W_j. One warp per group.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __restrict__ group_ids,
+                    int64_t ngroups, const uint32_t* __restrict__ N, uint32_t np,
+                    uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gi >= ngroups) return;
+  const int64_t g = group_ids ? (int64_t)group_ids[gi] : gi;
+  uint32_t n_[LPL], acc[LPL], x[LPL];
+  big_load<LPL>(n_, N, lane);
+  const uint32_t* Wg = W + (size_t)g * cap * L;
+  big_load<LPL>(acc, Wg + (size_t)(cap - 1) * L, lane);
+  for (int j = cap - 2; j >= 0; --j) {
+    for (int s = 0; s < 32; ++s) mont_mul<LPL>(acc, acc, acc, n_, np, lane);
+    big_load<LPL>(x, Wg + (size_t)j * L, lane);
+    mont_mul<LPL>(acc, acc, x, n_, np, lane);
+  }
+  big_set_small<LPL>(x, 1, lane);
+  mont_mul<LPL>(acc, acc, x, n_, np, lane);  // leave Montgomery form
   big_store<LPL>(out + g * L, acc, lane);
 }
 
@@ -182,11 +214,12 @@ int64_t multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs)
       return kErrUnsupported;                                          \
   }
 
-int multiexp_launch(const uint32_t* bases, int64_t n, const uint32_t* E, int64_t rows, int64_t rs,
-                    int64_t bs, int64_t ls, int elimbs, int limbs, const uint32_t* N, uint32_t np,
-                    const uint32_t* r2, uint32_t* out, void* ws, int64_t ws_bytes,
-                    cudaStream_t st) {
-  if (limbs % 32 || n <= 0 || rows <= 0 || elimbs <= 0) {
+int multiexp_rows_launch(const uint32_t* bases, int64_t n, const uint32_t* E,
+                         const int32_t* row_ids, int64_t rows, int64_t rs, int64_t bs, int64_t ls,
+                         int elimbs, int limbs, const uint32_t* N, uint32_t np,
+                         const uint32_t* r2, const uint32_t* one_m, int keep_mont, uint32_t* out,
+                         void* ws, int64_t ws_bytes, cudaStream_t st) {
+  if (limbs % 32 || n <= 0 || rows <= 0 || elimbs <= 0 || (keep_mont && !one_m)) {
     set_error("multiexp: bad shapes (n=%lld rows=%lld elimbs=%d limbs=%d)", (long long)n,
               (long long)rows, elimbs, limbs);
     return kErrInput;
@@ -214,12 +247,33 @@ int multiexp_launch(const uint32_t* bases, int64_t n, const uint32_t* E, int64_t
     const int64_t tasks = rows * nwin;
     const int64_t grid = std::min<int64_t>(ceil_div(tasks, 4), (int64_t)sms * 32);
     window_kernel<LPL><<<(unsigned)grid, 128, smem, st>>>(bm, n, E, rows, rs, bs, ls, elimbs,
-                                                          nwin, N, np, W, flags);
+                                                          nwin, N, np, W, flags, row_ids);
     if (int e = check_launch("multiexp window")) return e;
-    combine_windows_kernel<LPL><<<(unsigned)ceil_div(rows, 4), 128, 0, st>>>(W, flags, rows, nwin,
-                                                                             N, np, out);
+    combine_windows_kernel<LPL><<<(unsigned)ceil_div(rows, 4), 128, 0, st>>>(
+        W, flags, rows, nwin, N, np, out, row_ids, keep_mont, one_m);
   });
   return check_launch("multiexp combine");
+}
+
+int multiexp_launch(const uint32_t* bases, int64_t n, const uint32_t* E, int64_t rows, int64_t rs,
+                    int64_t bs, int64_t ls, int elimbs, int limbs, const uint32_t* N, uint32_t np,
+                    const uint32_t* r2, uint32_t* out, void* ws, int64_t ws_bytes,
+                    cudaStream_t st) {
+  return multiexp_rows_launch(bases, n, E, nullptr, rows, rs, bs, ls, elimbs, limbs, N, np, r2,
+                              nullptr, 0, out, ws, ws_bytes, st);
+}
+
+int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
+                        int limbs, const uint32_t* N, uint32_t np, uint32_t* out, cudaStream_t st) {
+  if (limbs % 32 || cap <= 0 || ngroups <= 0) {
+    set_error("slot_combine: bad shapes");
+    return kErrInput;
+  }
+  ZPIR_LPL_DISPATCH2(limbs / 32, {
+    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(W, cap, group_ids,
+                                                                            ngroups, N, np, out);
+  });
+  return check_launch("slot_combine");
 }
 
 }  // namespace zpir

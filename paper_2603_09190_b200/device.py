@@ -209,3 +209,39 @@ def answer_groups_plan(z, b, qmask, d1, cap, groups, lm, d_m, d_np, d_rpow, nchu
               cap, groups, lm, _lib.ptr(d_m), _lib.ptr(d_np), _lib.ptr(d_rpow), nchunks,
               _lib.ptr(d_f0), _lib.ptr(t), t_ld, 1, _s(stream))
     return t
+
+
+# ---- slot-decomposed hints / incremental update ------------------------------
+
+def multiexp_rows(bases, E, row_ids, rows, rs, bs, ls, elimbs, kctx, out, keep_mont, stream=None):
+    n = bases.shape[0]
+    l2 = kctx.l2
+    ws_bytes = int(_lib.lib().zpir_multiexp_workspace_bytes(n, rows, elimbs, l2))
+    ws = torch.empty(ws_bytes // 4 + 64, dtype=torch.int32, device=bases.device)
+    _lib.call("zpir_multiexp_rows", _lib.ptr(bases), n, _lib.ptr(E),
+              _lib.ptr(row_ids) if row_ids is not None else None, rows, rs, bs, ls, elimbs, l2,
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_r2sq), _lib.ptr(kctx.d_one2),
+              1 if keep_mont else 0, _lib.ptr(out), _lib.ptr(ws), ws_bytes, _s(stream))
+    return out
+
+
+def slot_combine(W, cap, group_ids, ngroups, kctx, out, stream=None):
+    _lib.call("zpir_slot_combine", _lib.ptr(W), cap,
+              _lib.ptr(group_ids) if group_ids is not None else None, ngroups, kctx.l2,
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(out), _s(stream))
+    return out
+
+
+def rows_differ(a, b, stream=None):
+    rows, ld = a.shape
+    flags = torch.empty(rows, dtype=torch.int32, device=a.device)
+    _lib.call("zpir_rows_differ", _lib.ptr(a), _lib.ptr(b), rows, ld, _lib.ptr(flags), _s(stream))
+    return flags
+
+
+def move_rows(src, dst, ids, scatter, stream=None):
+    """Row gather (dst[i] = src[ids[i]]) or scatter (dst[ids[i]] = src[i])."""
+    pitch = src.shape[1] * src.element_size()
+    _lib.call("zpir_move_rows", _lib.ptr(src), _lib.ptr(dst), pitch, _lib.ptr(ids), ids.numel(),
+              1 if scatter else 0, _s(stream))
+    return dst

@@ -71,6 +71,11 @@ class ClientHint:
     entries: list    # d1' PaillierCiphertexts
     # device copy of the entries (groups x l2 u32 limbs), kept for COMBINED
     dev: object = field(default=None, repr=False, compare=False)
+    # slot decomposition (hint(..., keep_slots=True)): per-DB-row factors
+    # W[c] = prod_k ck_r[k]^H[c][k] (Montgomery form) and the canonical bases,
+    # enabling refresh_hint() after a row update without a full recompute
+    slots: object = field(default=None, repr=False, compare=False)
+    bases: object = field(default=None, repr=False, compare=False)
 
 
 @dataclass
@@ -184,6 +189,54 @@ class ServerGlobalState:
         self._H_scaled = None
         self._lock = threading.Lock()
         self._tls = threading.local()
+
+    # -- incremental update ------------------------------------------------
+
+    def updated(self, db, db_version: int = None):
+        """New state for database `db` built incrementally from this one:
+        the DB rows (db columns) that changed are found on the device
+        (rows_differ) and only their H rows are recomputed (gather -> hint
+        GEMM -> scatter). Returns (new_state, changed_rows). Equivalent to
+        ServerGlobalState(params, db, basis, db_version + 1) (server.py:116)."""
+        params = self.params
+        db = np.asarray(db)
+        if db.shape != (params.d0, params.d1):
+            raise ValueError("database shape mismatch")
+        if int(db.max(initial=0)) >= params.lwe.p:
+            raise ValueError("database symbol out of range")
+        lay = self.layout
+        dev = self.device
+        stream = torch.cuda.current_stream(dev)
+        t0 = time.perf_counter()
+        new = object.__new__(ServerGlobalState)
+        new.__dict__.update(params=params, db=db, basis=self.basis, layout=lay, device=dev,
+                            engine=self.engine, _A32=self._A32, _A64=self._A64, A_dev=self.A_dev,
+                            _H_host=None, _H_scaled=None, _lock=threading.Lock(),
+                            _tls=threading.local())
+        new.db_version = self.db_version + 1 if db_version is None else db_version
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+        new.dbt = device.transpose_db(db_dev, lay.d0, lay.d1, lay.rows, lay.ld, stream)
+        del db_dev
+        flags = device.rows_differ(new.dbt, self.dbt, stream)
+        changed = np.nonzero(flags[: lay.d1].cpu().numpy())[0].astype(np.int64)
+        H = self.H_dev.clone()
+        if changed.size:
+            R = changed.size
+            Rp = -(-R // 128) * 128
+            ids = torch.from_numpy(changed.astype(np.int32)).to(dev)
+            part = torch.zeros((Rp, lay.ld), dtype=torch.uint8, device=dev)
+            device.move_rows(new.dbt, part, ids, scatter=False, stream=stream)
+            if self.engine == "umma" and lay.n % 64 == 0:
+                Hp = device.umma_global_hint(part, self.A_dev, lay.n, lay.qmask, stream)
+            else:
+                Hp = device.global_hint(part, self.A_dev, lay.n, lay.qmask, stream)
+            device.move_rows(Hp, H, ids, scatter=True, stream=stream)
+        new.H_dev = H
+        stream.synchronize()
+        new.hint_time = time.perf_counter() - t0
+        return new, changed
 
     # -- reference-compatible views (materialised lazily on the host) ------
 
@@ -353,9 +406,14 @@ def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
     return [sample_ciphertext(pk, seed, (query_index << 32) | i) for i in range(n)]
 
 
-def hint(state: ServerGlobalState, reg, query_index: int, stream=None) -> ClientHint:
+def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
+         keep_slots: bool = False) -> ClientHint:
     """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups in one
-    device multi-exponentiation; exponents read in place from H."""
+    device multi-exponentiation; exponents read in place from H.
+
+    keep_slots=True computes the same entries through the slot decomposition
+    k_g = prod_j W[g*cap+j]^(2^(32 j)), W[c] = prod_k ck_r[k]^H[c][k] (32-bit
+    exponents), and keeps W (groups*cap x l2) on the device for refresh_hint."""
     lay = state.layout
     dev = state.device
     stream = stream or torch.cuda.current_stream(dev)
@@ -363,12 +421,57 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None) -> Client
     ck_r = [c.c for c in derive_ck_r(reg.pk, reg.seed, query_index, lay.n)]
     bases = _h2d(ints_to_limbs(ck_r, kctx.l2), dev, "bases", stream).view(torch.int32)
     bases = bases.reshape(lay.n, kctx.l2)
+    if keep_slots:
+        nslot = lay.groups * lay.cap
+        W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
+        device.multiexp_rows(bases, state.H_dev, None, nslot, lay.n, 1, lay.n, 1, kctx, W, True,
+                             stream)
+        out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
+        device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, stream)
+        entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
+        counters.bump("group_mult", lay.groups * lay.n)
+        return ClientHint(query_index, state.db_version,
+                          [PaillierCiphertext(e) for e in entries], dev=out, slots=W,
+                          bases=bases.clone())
     out = device.multiexp(bases, state.H_dev, lay.groups, lay.cap * lay.n, 1, lay.n, lay.cap,
                           kctx, stream)
     entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
     counters.bump("group_mult", lay.groups * lay.n)
     return ClientHint(query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
                       dev=out)
+
+
+def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
+                 stream=None) -> ClientHint:
+    """Incremental hint refresh after a DB-row update (no reference
+    counterpart: the reference regenerates every hint, server.py:115-124).
+
+    `old` must carry its slot decomposition (hint(..., keep_slots=True)) and
+    `state` is the updated state (ServerGlobalState.updated). Only the
+    changed DB rows' factors W[c] are recomputed (one 32-bit multiexp each) and
+    only their groups are recombined; bit-identical to a full hint() on the
+    new state."""
+    if old.slots is None or old.bases is None:
+        raise ValueError("refresh_hint needs a hint computed with keep_slots=True")
+    lay = state.layout
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    kctx = key_ctx(reg.pk.m, dev)
+    rows = np.unique(np.asarray(changed_rows, dtype=np.int64))
+    W = old.slots.clone()
+    k = old.dev.clone()
+    if rows.size:
+        if rows.min() < 0 or rows.max() >= lay.d1:
+            raise ValueError("changed row out of range")
+        rid = torch.from_numpy(rows.astype(np.int32)).to(dev)
+        device.multiexp_rows(old.bases, state.H_dev, rid, rows.size, lay.n, 1, lay.n, 1, kctx, W,
+                             True, stream)
+        groups = np.unique(rows // lay.cap).astype(np.int32)
+        gid = torch.from_numpy(groups).to(dev)
+        device.slot_combine(W, lay.cap, gid, groups.size, kctx, k, stream)
+    entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
+    return ClientHint(old.query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
+                      dev=k, slots=W, bases=old.bases)
 
 
 def _stored_device(stored, kctx, dev, stream):

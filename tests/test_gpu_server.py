@@ -54,3 +54,36 @@ def test_server_update_and_regenerate():
         assert ask(9, 3, z.SEPARATE) == [int(x) for x in db2[3]]
     finally:
         srv.close()
+
+
+@pytest.mark.parametrize("name", ["ragged", "tiny"])
+def test_incremental_update_bit_exact(golden, name):
+    """updated() + refresh_hint() == full rebuild + full hint, bit for bit."""
+    import paper_2603_09190_b200 as z
+    from conftest import Golden
+    g = golden(name)
+    params = g.params(z)
+    st = z.ServerGlobalState(params, g.db)
+    pk = z.PaillierPublicKey(g.m, g.m.bit_length())
+    reg = z.ClientRegistration(pk, g.seed, z.client_id_of(pk))
+    h_slots = z.hint(st, reg, 0, keep_slots=True)
+    assert [c.c for c in h_slots.entries] == g.ints("k")          # slot path == reference
+    rng = np.random.default_rng(9)
+    db2 = np.array(g.db, dtype=np.uint8, copy=True)
+    rows = sorted(set(rng.choice(g.d1, size=max(1, g.d1 // 100), replace=False).tolist())
+                  | {0, g.d1 - 1})
+    for c in rows:
+        db2[:, c] = rng.integers(0, 256, g.d0, dtype=np.uint8)
+    st2, changed = st.updated(db2)
+    full = z.ServerGlobalState(params, db2, db_version=1)
+    assert st2.db_version == 1
+    assert np.array_equal(st2.H, full.H)
+    assert set(changed.tolist()) <= set(rows)
+    h2 = z.refresh_hint(st2, reg, h_slots, changed)
+    h_full = z.hint(full, reg, 0)
+    assert [c.c for c in h2.entries] == [c.c for c in h_full.entries]
+    assert h2.db_version == 1
+    # answers against the updated state use the refreshed hint
+    reg.hints[0] = h2
+    q = z.QueryMessage(reg.client_id, 0, z.SEPARATE, g.ints("ck_o"), g.arr["qu0"])
+    assert z.respond(st2, reg, q).t == z.respond(full, reg, q).t
