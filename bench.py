@@ -54,7 +54,7 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
-    ap.add_argument("--workload", default="1g", choices=["1g", "batch64", "8g", "hint"],
+    ap.add_argument("--workload", default="1g", choices=["1g", "batch64", "8g", "hint", "update"],
                     help="1g: BASELINE configs[1] (default, the driver's line); batch64: "
                          "configs[3]; 8g: configs[2] (92682^2, strong-scaled over --gpus); "
                          "hint: configs[4] offline hint generation")
@@ -513,6 +513,49 @@ def run_extra(args):
                "gemv_ms": gemv, "compress_ms": comp,
                "gemv_u8xu32_macs_per_s": ops / 2 / (gemv / 1e3),
                "gemv_hbm_frac": (D0 * D1) / (gemv / 1e3) / 1e9 / peak}
+    elif args.workload == "update":
+        params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
+        db = db_slice(0, D1)
+        st = z.ServerGlobalState(params, db)
+        nclients = 4
+        regs, hints, t_full = [], [], []
+        for j in range(nclients):
+            mj = paillier_modulus(BITS, 3000 + j)
+            pk = z.PaillierPublicKey(mj, mj.bit_length())
+            reg = z.ClientRegistration(pk, bytes([j]) * 16, z.client_id_of(pk))
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            hints.append(z.hint(st, reg, 0, keep_slots=True))
+            torch.cuda.synchronize()
+            t_full.append(time.perf_counter() - t1)
+            regs.append(reg)
+        # update 1% of DB rows (DB = db^T rows = db columns), re-drawn from a seed
+        rng = np.random.default_rng(77)
+        rows = np.sort(rng.choice(D1, size=D1 // 100, replace=False))
+        db2 = db.copy()
+        db2[:, rows] = rng.integers(0, 256, (D0, rows.size), dtype=np.uint8)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        st2, changed = st.updated(db2)
+        torch.cuda.synchronize()
+        t_state = time.perf_counter() - t1
+        t_ref = []
+        for reg, h in zip(regs, hints):
+            t1 = time.perf_counter()
+            z.refresh_hint(st2, reg, h, changed)
+            torch.cuda.synchronize()
+            t_ref.append(time.perf_counter() - t1)
+        full_rebuild = z.ServerGlobalState(params, db2, db_version=1).hint_time
+        r = statistics.median(t_ref)
+        f = statistics.median(t_full)
+        out = {"workload": "BASELINE configs[4] update: 1 GiB DB, 1% of DB rows (328) re-drawn, "
+                           "incremental state + hint refresh (slot-decomposed hints)",
+               "n_gpus": 1, "changed_rows": int(changed.size),
+               "state_update_s": t_state, "state_full_rebuild_gpu_s": full_rebuild,
+               "hint_full_s_per_client": f, "hint_refresh_s_per_client": r,
+               "refresh_speedup": f / r, "clients_sampled": nclients,
+               "extrapolated_256_clients_refresh_s": 256 * r,
+               "extrapolated_256_clients_full_regen_s": 256 * f}
     else:  # hint
         params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
         t0 = time.perf_counter()
