@@ -162,6 +162,16 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
  * per-DB-row factors W[c] = prod_k ck_r[k]^H[c][k]. */
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
                       int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream);
+/* Fixed-base table for 32-bit exponents: P[i*n + k] = bases[k]^(2^(8 i)) in
+ * Montgomery form, i < 4. */
+int zpir_pow8_table(const uint32_t* bases, int64_t n, int limbs, const uint32_t* N, uint32_t np,
+                    const uint32_t* r2, uint32_t* P, void* stream);
+/* W[r] = prod_k bases[k]^exps[r*row_stride + k] (Montgomery form) for the
+ * listed rows (row_ids nullable = 0..rows-1), one 255-bucket Pippenger over
+ * the 4n byte digits per row using P; all-zero rows get one_m. */
+int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t row_stride,
+                    const int32_t* row_ids, int64_t rows, int limbs, const uint32_t* N,
+                    uint32_t np, const uint32_t* one_m, uint32_t* W, void* stream);
 /* flags[r] = (row r of a != row r of b), rows of ld bytes. */
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,
                      void* stream);

@@ -149,15 +149,27 @@ answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict_
   constexpr int NX = NCH * LM;
   constexpr int LX = NCH * LPL;
   __shared__ __align__(16) uint32_t lo[NX], hi[NX + 1], X[NX], R[NCH][LM];
+  __shared__ unsigned long long S[NX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t g = blockIdx.x;
   const int wz = LM + 4;
   const int64_t c0 = g * cap;
   const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
+  for (int P = tid; P < NX; P += blockDim.x)
+    S[P] = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
+  __syncthreads();
+  // position sums: row j of the group lands at positions j .. j + wz - 1;
+  // rows are read contiguously (coalesced) and accumulated with smem atomics
+  const uint32_t* zg = z + c0 * wz;
+  const int total = nrows * wz;
+  for (int idx = tid; idx < total; idx += blockDim.x) {
+    const int j = idx / wz;
+    const uint32_t v = zg[idx];
+    if (v) atomicAdd(&S[idx - j * wz + j], (unsigned long long)v);
+  }
+  __syncthreads();
   for (int P = tid; P < NX; P += blockDim.x) {
-    unsigned long long s = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
-    const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
-    for (int j = jlo; j <= jhi; ++j) s += z[(c0 + j) * wz + (P - j)];
+    const unsigned long long s = S[P];
     lo[P] = (uint32_t)s;
     hi[P + 1] = (uint32_t)(s >> 32);
   }

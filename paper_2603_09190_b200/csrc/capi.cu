@@ -52,6 +52,10 @@ int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_
                          const uint32_t*, int, uint32_t*, void*, int64_t, cudaStream_t);
 int slot_combine_launch(const uint32_t*, int, const int32_t*, int64_t, int, const uint32_t*,
                         uint32_t, uint32_t*, cudaStream_t);
+int pow8_table_launch(const uint32_t*, int64_t, int, const uint32_t*, uint32_t, const uint32_t*,
+                      uint32_t*, cudaStream_t);
+int slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, const int32_t*, int64_t,
+                      int, const uint32_t*, uint32_t, const uint32_t*, uint32_t*, cudaStream_t);
 int rows_differ_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
 int move_rows_launch(const uint8_t*, uint8_t*, int64_t, const int32_t*, int64_t, int, cudaStream_t);
 int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
@@ -203,6 +207,18 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
                       int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream) {
   ZPIR_GUARD(slot_combine_launch(W, cap, group_ids, ngroups, limbs, N, np, out, S(stream)));
+}
+
+int zpir_pow8_table(const uint32_t* bases, int64_t n, int limbs, const uint32_t* N, uint32_t np,
+                    const uint32_t* r2, uint32_t* P, void* stream) {
+  ZPIR_GUARD(pow8_table_launch(bases, n, limbs, N, np, r2, P, S(stream)));
+}
+
+int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t row_stride,
+                    const int32_t* row_ids, int64_t rows, int limbs, const uint32_t* N,
+                    uint32_t np, const uint32_t* one_m, uint32_t* W, void* stream) {
+  ZPIR_GUARD(slot_fixed_launch(P, n, exps, row_stride, row_ids, rows, limbs, N, np, one_m, W,
+                               S(stream)));
 }
 
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,

@@ -193,6 +193,120 @@ slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __re
   big_store<LPL>(out + g * L, acc, lane);
 }
 
+// ---- fixed-base slot multiexp (w = 8) -------------------------------------
+// P[i][k] = ck_k^(2^(8 i)) in Montgomery form (i < 4), one warp per base.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+pow8_table_kernel(const uint32_t* __restrict__ bases, int64_t n, const uint32_t* __restrict__ N,
+                  uint32_t np, const uint32_t* __restrict__ r2, uint32_t* __restrict__ P) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= n) return;
+  uint32_t n_[LPL], a[LPL], b[LPL];
+  big_load<LPL>(n_, N, lane);
+  big_load<LPL>(a, bases + k * L, lane);
+  big_load<LPL>(b, r2, lane);
+  mont_mul<LPL>(a, a, b, n_, np, lane);
+  big_store<LPL>(P + (size_t)k * L, a, lane);
+  for (int i = 1; i < 4; ++i) {
+    for (int s = 0; s < 8; ++s) mont_mul<LPL>(a, a, a, n_, np, lane);
+    big_store<LPL>(P + ((size_t)i * n + k) * L, a, lane);
+  }
+}
+
+// W[r] = prod_{i<4, k<n} P[i][k]^(byte_i(H[r][k])) -- one Pippenger with 255
+// buckets over the 4n (i, k) digit pairs of the 32-bit exponent row r: no
+// per-window squarings, ~4n + 510 multiplications. One warp per row; the
+// digits are counting-sorted in shared memory (u16 indices i*n + k).
+// Smem per warp: cnt[256] + off[256] (u32) + list[4n] (u16).
+template <int LPL>
+__global__ void __launch_bounds__(128)
+slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __restrict__ E,
+                  int64_t rs, const int32_t* __restrict__ row_ids, int64_t rows,
+                  const uint32_t* __restrict__ N, uint32_t np, const uint32_t* __restrict__ one_m,
+                  uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  extern __shared__ uint32_t smem_u32[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int64_t per_warp = 512 + (4 * n + 1) / 2;
+  uint32_t* cnt = smem_u32 + (size_t)wid * per_warp;
+  uint32_t* off = cnt + 256;
+  uint16_t* list = reinterpret_cast<uint16_t*>(off + 256);
+  uint32_t n_[LPL];
+  big_load<LPL>(n_, N, lane);
+  for (int64_t gi = (int64_t)blockIdx.x * wpb + wid; gi < rows; gi += (int64_t)gridDim.x * wpb) {
+    const int64_t r = row_ids ? (int64_t)row_ids[gi] : gi;
+    const uint32_t* er = E + r * rs;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cnt[lane * 8 + q] = 0;
+    __syncwarp();
+    for (int64_t k = lane; k < n; k += 32) {
+      const uint32_t w = er[k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t d = (w >> (8 * i)) & 0xffu;
+        if (d) atomicAdd(&cnt[d], 1u);
+      }
+    }
+    __syncwarp();
+    // exclusive scan of cnt[0..255]: lane holds entries 8*lane .. 8*lane+7
+    uint32_t c[8], run = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      c[q] = cnt[lane * 8 + q];
+      run += c[q];
+    }
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(ZPIR_FULL, incl, o);
+      if (lane >= o) incl += v;
+    }
+    uint32_t base = incl - run;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      off[lane * 8 + q] = base;
+      base += c[q];
+    }
+    __syncwarp();
+    for (int64_t k = lane; k < n; k += 32) {
+      const uint32_t w = er[k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t d = (w >> (8 * i)) & 0xffu;
+        if (d) list[atomicAdd(&off[d], 1u)] = (uint16_t)(i * n + k);
+      }
+    }
+    __syncwarp();
+    bool has_run = false, has_tot = false;
+    uint32_t run_[LPL], tot[LPL], bkt[LPL], x[LPL];
+    for (int d = 255; d >= 1; --d) {
+      const uint32_t cd = cnt[d];
+      if (cd) {
+        const uint32_t e = off[d], s0 = e - cd;
+        big_load<LPL>(bkt, P + (size_t)list[s0] * L, lane);
+        for (uint32_t i = s0 + 1; i < e; ++i) {
+          big_load<LPL>(x, P + (size_t)list[i] * L, lane);
+          mont_mul<LPL>(bkt, bkt, x, n_, np, lane);
+        }
+        if (has_run) mont_mul<LPL>(run_, run_, bkt, n_, np, lane);
+        else big_copy<LPL>(run_, bkt);
+        has_run = true;
+      }
+      if (has_run) {
+        if (has_tot) mont_mul<LPL>(tot, tot, run_, n_, np, lane);
+        else big_copy<LPL>(tot, run_);
+        has_tot = true;
+      }
+    }
+    if (!has_tot) big_load<LPL>(tot, one_m, lane);
+    big_store<LPL>(out + r * L, tot, lane);
+    __syncwarp();
+  }
+}
+
 int64_t multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs) {
   const int64_t nwin = ceil_div((int64_t)32 * elimbs, kWin);
   const int64_t a = ((n * limbs * 4 + 255) / 256) * 256;
@@ -261,6 +375,41 @@ int multiexp_launch(const uint32_t* bases, int64_t n, const uint32_t* E, int64_t
                     cudaStream_t st) {
   return multiexp_rows_launch(bases, n, E, nullptr, rows, rs, bs, ls, elimbs, limbs, N, np, r2,
                               nullptr, 0, out, ws, ws_bytes, st);
+}
+
+// P = pow8 table (4 x n x limbs) of the canonical bases (Montgomery form).
+int pow8_table_launch(const uint32_t* bases, int64_t n, int limbs, const uint32_t* N, uint32_t np,
+                      const uint32_t* r2, uint32_t* P, cudaStream_t st) {
+  if (limbs % 32 || n <= 0) {
+    set_error("pow8_table: bad shapes");
+    return kErrInput;
+  }
+  ZPIR_LPL_DISPATCH2(limbs / 32, {
+    pow8_table_kernel<LPL><<<(unsigned)ceil_div(n, 4), 128, 0, st>>>(bases, n, N, np, r2, P);
+  });
+  return check_launch("pow8_table");
+}
+
+// W[row] (Montgomery form) for the listed 32-bit exponent rows E[row*rs + k].
+int slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs,
+                      const int32_t* row_ids, int64_t rows, int limbs, const uint32_t* N,
+                      uint32_t np, const uint32_t* one_m, uint32_t* W, cudaStream_t st) {
+  if (limbs % 32 || n <= 0 || rows <= 0 || 4 * n > 65536) {
+    set_error("slot_fixed: bad shapes (n=%lld rows=%lld)", (long long)n, (long long)rows);
+    return kErrInput;
+  }
+  const size_t smem = (size_t)4 * (512 + (4 * n + 1) / 2) * sizeof(uint32_t);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ZPIR_LPL_DISPATCH2(limbs / 32, {
+    cudaFuncSetAttribute(slot_fixed_kernel<LPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    const int64_t grid = std::min<int64_t>(ceil_div(rows, 4), (int64_t)sms * 16);
+    slot_fixed_kernel<LPL><<<(unsigned)grid, 128, smem, st>>>(P, n, E, rs, row_ids, rows, N, np,
+                                                              one_m, W);
+  });
+  return check_launch("slot_fixed");
 }
 
 int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,

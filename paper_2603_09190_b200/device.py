@@ -245,3 +245,18 @@ def move_rows(src, dst, ids, scatter, stream=None):
     _lib.call("zpir_move_rows", _lib.ptr(src), _lib.ptr(dst), pitch, _lib.ptr(ids), ids.numel(),
               1 if scatter else 0, _s(stream))
     return dst
+
+
+def pow8_table(bases, kctx, stream=None):
+    n = bases.shape[0]
+    P = torch.empty((4 * n, kctx.l2), dtype=torch.int32, device=bases.device)
+    _lib.call("zpir_pow8_table", _lib.ptr(bases), n, kctx.l2, _lib.ptr(kctx.d_m2), kctx.c2.np,
+              _lib.ptr(kctx.d_r2sq), _lib.ptr(P), _s(stream))
+    return P
+
+
+def slot_fixed(P, n, E, rs, row_ids, rows, kctx, W, stream=None):
+    _lib.call("zpir_slot_fixed", _lib.ptr(P), n, _lib.ptr(E), rs,
+              _lib.ptr(row_ids) if row_ids is not None else None, rows, kctx.l2,
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_one2), _lib.ptr(W), _s(stream))
+    return W

@@ -72,8 +72,9 @@ class ClientHint:
     # device copy of the entries (groups x l2 u32 limbs), kept for COMBINED
     dev: object = field(default=None, repr=False, compare=False)
     # slot decomposition (hint(..., keep_slots=True)): per-DB-row factors
-    # W[c] = prod_k ck_r[k]^H[c][k] (Montgomery form) and the canonical bases,
-    # enabling refresh_hint() after a row update without a full recompute
+    # W[c] = prod_k ck_r[k]^H[c][k] (Montgomery form) and the fixed-base
+    # table P[i][k] = ck_r[k]^(2^(8i)), enabling refresh_hint() after a row
+    # update without a full recompute
     slots: object = field(default=None, repr=False, compare=False)
     bases: object = field(default=None, repr=False, compare=False)
 
@@ -408,12 +409,17 @@ def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
 
 def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
          keep_slots: bool = False) -> ClientHint:
-    """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups in one
-    device multi-exponentiation; exponents read in place from H.
+    """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups
+    (protocol.py:291-296; paillier_matmul / multiexp, paillier.py:134-203).
 
-    keep_slots=True computes the same entries through the slot decomposition
-    k_g = prod_j W[g*cap+j]^(2^(32 j)), W[c] = prod_k ck_r[k]^H[c][k] (32-bit
-    exponents), and keeps W (groups*cap x l2) on the device for refresh_hint."""
+    Computed through the slot decomposition: with gamma = 2^32,
+    H_scaled[g][k] = sum_j 2^(32j) H[g*cap+j][k], so
+    k_g = prod_j W[g*cap+j]^(2^(32 j)) with W[c] = prod_k ck_r[k]^H[c][k].
+    Each W[c] (32-bit exponents) is one fixed-base Pippenger over the table
+    P[i][k] = ck_r[k]^(2^(8i)) (255 buckets, 4n digits); the groups are then
+    recombined by Horner (slot_combine). Same group element as the
+    reference's windowed multiexp, canonical mod m^2. keep_slots=True keeps W
+    and P on the device for refresh_hint."""
     lay = state.layout
     dev = state.device
     stream = stream or torch.cuda.current_stream(dev)
@@ -421,24 +427,16 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     ck_r = [c.c for c in derive_ck_r(reg.pk, reg.seed, query_index, lay.n)]
     bases = _h2d(ints_to_limbs(ck_r, kctx.l2), dev, "bases", stream).view(torch.int32)
     bases = bases.reshape(lay.n, kctx.l2)
-    if keep_slots:
-        nslot = lay.groups * lay.cap
-        W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
-        device.multiexp_rows(bases, state.H_dev, None, nslot, lay.n, 1, lay.n, 1, kctx, W, True,
-                             stream)
-        out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
-        device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, stream)
-        entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
-        counters.bump("group_mult", lay.groups * lay.n)
-        return ClientHint(query_index, state.db_version,
-                          [PaillierCiphertext(e) for e in entries], dev=out, slots=W,
-                          bases=bases.clone())
-    out = device.multiexp(bases, state.H_dev, lay.groups, lay.cap * lay.n, 1, lay.n, lay.cap,
-                          kctx, stream)
+    nslot = lay.groups * lay.cap
+    W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
+    P = device.pow8_table(bases, kctx, stream)
+    device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
+    out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
+    device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, stream)
     entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
     counters.bump("group_mult", lay.groups * lay.n)
     return ClientHint(query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
-                      dev=out)
+                      dev=out, slots=W if keep_slots else None, bases=P if keep_slots else None)
 
 
 def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
@@ -464,8 +462,7 @@ def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
         if rows.min() < 0 or rows.max() >= lay.d1:
             raise ValueError("changed row out of range")
         rid = torch.from_numpy(rows.astype(np.int32)).to(dev)
-        device.multiexp_rows(old.bases, state.H_dev, rid, rows.size, lay.n, 1, lay.n, 1, kctx, W,
-                             True, stream)
+        device.slot_fixed(old.bases, lay.n, state.H_dev, lay.n, rid, rows.size, kctx, W, stream)
         groups = np.unique(rows // lay.cap).astype(np.int32)
         gid = torch.from_numpy(groups).to(dev)
         device.slot_combine(W, lay.cap, gid, groups.size, kctx, k, stream)
