@@ -517,7 +517,7 @@ def run_extra(args):
         params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
         db = db_slice(0, D1)
         st = z.ServerGlobalState(params, db)
-        nclients = 4
+        nclients = 16
         regs, hints, t_full = [], [], []
         for j in range(nclients):
             mj = paillier_modulus(BITS, 3000 + j)
@@ -539,20 +539,22 @@ def run_extra(args):
         st2, changed = st.updated(db2)
         torch.cuda.synchronize()
         t_state = time.perf_counter() - t1
-        t_ref = []
-        for reg, h in zip(regs, hints):
-            t1 = time.perf_counter()
-            z.refresh_hint(st2, reg, h, changed)
-            torch.cuda.synchronize()
-            t_ref.append(time.perf_counter() - t1)
+        t1 = time.perf_counter()
+        z.refresh_hint(st2, regs[0], hints[0], changed)
+        torch.cuda.synchronize()
+        t_one = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        z.refresh_hints(st2, list(zip(regs, hints)), changed)
+        torch.cuda.synchronize()
+        r = (time.perf_counter() - t1) / nclients
         full_rebuild = z.ServerGlobalState(params, db2, db_version=1).hint_time
-        r = statistics.median(t_ref)
         f = statistics.median(t_full)
         out = {"workload": "BASELINE configs[4] update: 1 GiB DB, 1% of DB rows (328) re-drawn, "
                            "incremental state + hint refresh (slot-decomposed hints)",
                "n_gpus": 1, "changed_rows": int(changed.size),
                "state_update_s": t_state, "state_full_rebuild_gpu_s": full_rebuild,
                "hint_full_s_per_client": f, "hint_refresh_s_per_client": r,
+               "hint_refresh_single_client_s": t_one,
                "refresh_speedup": f / r, "clients_sampled": nclients,
                "extrapolated_256_clients_refresh_s": 256 * r,
                "extrapolated_256_clients_full_regen_s": 256 * f}

@@ -12,7 +12,7 @@ from .paillier import (PaillierPublicKey, PaillierCiphertext, InvalidCiphertext,
 from .protocol import (SEPARATE, COMBINED, ServerGlobalState, ClientHint,  # noqa: F401
                        ClientRegistration, QueryMessage, ResponseMessage, HintRequest,
                        client_id_of, derive_ck_r, hint, respond, respond_batch,
-                       refresh_hint)
+                       refresh_hint, refresh_hints)
 
 __all__ = [
     "LweParams", "ProtocolParams", "PaillierPublicKey", "PaillierCiphertext", "multiexp",

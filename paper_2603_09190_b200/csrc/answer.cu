@@ -149,27 +149,25 @@ answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict_
   constexpr int NX = NCH * LM;
   constexpr int LX = NCH * LPL;
   __shared__ __align__(16) uint32_t lo[NX], hi[NX + 1], X[NX], R[NCH][LM];
-  __shared__ unsigned long long S[NX];
+  extern __shared__ uint32_t zs[];  // the group's z rows (cap x wz), staged
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t g = blockIdx.x;
   const int wz = LM + 4;
   const int64_t c0 = g * cap;
   const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
-  for (int P = tid; P < NX; P += blockDim.x)
-    S[P] = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
-  __syncthreads();
-  // position sums: row j of the group lands at positions j .. j + wz - 1;
-  // rows are read contiguously (coalesced) and accumulated with smem atomics
-  const uint32_t* zg = z + c0 * wz;
-  const int total = nrows * wz;
-  for (int idx = tid; idx < total; idx += blockDim.x) {
-    const int j = idx / wz;
-    const uint32_t v = zg[idx];
-    if (v) atomicAdd(&S[idx - j * wz + j], (unsigned long long)v);
+  {
+    // coalesced 16-byte copy of the group's rows (contiguous in z)
+    const uint4* src = reinterpret_cast<const uint4*>(z + c0 * wz);
+    uint4* dst = reinterpret_cast<uint4*>(zs);
+    const int n16 = nrows * wz / 4;
+    for (int i = tid; i < n16; i += blockDim.x) dst[i] = src[i];
   }
   __syncthreads();
+  // position sums X_P = b_P + sum_j z_j[P - j], split into lo/hi words
   for (int P = tid; P < NX; P += blockDim.x) {
-    const unsigned long long s = S[P];
+    unsigned long long s = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
+    const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
+    for (int j = jlo; j <= jhi; ++j) s += zs[j * wz + (P - j)];
     lo[P] = (uint32_t)s;
     hi[P + 1] = (uint32_t)(s >> 32);
   }
@@ -300,10 +298,14 @@ static int answer_groups_launch_ex(const uint32_t* z, const uint32_t* b, uint32_
     return kErrInput;
   }
   const dim3 grid((unsigned)groups, (unsigned)nq);
+  const size_t zsm = (size_t)cap * (lm + 4) * sizeof(uint32_t);
 #define ZPIR_GROUPS(NCHV)                                                                    \
   ZPIR_LPL_DISPATCH(lm / 32, {                                                               \
-    answer_groups_kernel<LPL, NCHV><<<grid, 128, 0, st>>>(z, b, qmask, d1, cap, groups, mod, \
-                                                          np, rpow, fast0, t, t_ld, bt);     \
+    cudaFuncSetAttribute(answer_groups_kernel<LPL, NCHV>,                                    \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);             \
+    answer_groups_kernel<LPL, NCHV><<<grid, 128, zsm, st>>>(z, b, qmask, d1, cap, groups,    \
+                                                            mod, np, rpow, fast0, t, t_ld,   \
+                                                            bt);                             \
   })
   if (nchunks == 2) {
     ZPIR_GROUPS(2);

@@ -439,6 +439,28 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
                       dev=out, slots=W if keep_slots else None, bases=P if keep_slots else None)
 
 
+def _refresh_device(state, kctx, old, rows, rid, gid, ngroups, stream):
+    lay = state.layout
+    W = old.slots.clone()
+    k = old.dev.clone()
+    if rows:
+        device.slot_fixed(old.bases, lay.n, state.H_dev, lay.n, rid, rows, kctx, W, stream)
+        device.slot_combine(W, lay.cap, gid, ngroups, kctx, k, stream)
+    return W, k
+
+
+def _changed_ids(state, changed_rows):
+    lay = state.layout
+    rows = np.unique(np.asarray(changed_rows, dtype=np.int64))
+    if rows.size and (rows.min() < 0 or rows.max() >= lay.d1):
+        raise ValueError("changed row out of range")
+    groups = np.unique(rows // lay.cap).astype(np.int32)
+    dev = state.device
+    rid = torch.from_numpy(rows.astype(np.int32)).to(dev) if rows.size else None
+    gid = torch.from_numpy(groups).to(dev) if groups.size else None
+    return rows.size, rid, gid, groups.size
+
+
 def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
                  stream=None) -> ClientHint:
     """Incremental hint refresh after a DB-row update (no reference
@@ -446,29 +468,45 @@ def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
 
     `old` must carry its slot decomposition (hint(..., keep_slots=True)) and
     `state` is the updated state (ServerGlobalState.updated). Only the
-    changed DB rows' factors W[c] are recomputed (one 32-bit multiexp each) and
-    only their groups are recombined; bit-identical to a full hint() on the
-    new state."""
-    if old.slots is None or old.bases is None:
-        raise ValueError("refresh_hint needs a hint computed with keep_slots=True")
-    lay = state.layout
+    changed DB rows' factors W[c] are recomputed (one fixed-base 32-bit
+    multiexp each) and only their groups are recombined; bit-identical to a
+    full hint() on the new state."""
+    return refresh_hints(state, [(reg, old)], changed_rows, stream=stream)[0]
+
+
+def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
+                  nstreams: int = 8) -> list:
+    """refresh_hint for many (registration, hint) pairs at once: the clients'
+    kernels are spread over `nstreams` CUDA streams so that small refreshes
+    (a few hundred rows each) fill the GPU together."""
+    for _, old in pairs:
+        if old.slots is None or old.bases is None:
+            raise ValueError("refresh_hint needs a hint computed with keep_slots=True")
     dev = state.device
-    stream = stream or torch.cuda.current_stream(dev)
-    kctx = key_ctx(reg.pk.m, dev)
-    rows = np.unique(np.asarray(changed_rows, dtype=np.int64))
-    W = old.slots.clone()
-    k = old.dev.clone()
-    if rows.size:
-        if rows.min() < 0 or rows.max() >= lay.d1:
-            raise ValueError("changed row out of range")
-        rid = torch.from_numpy(rows.astype(np.int32)).to(dev)
-        device.slot_fixed(old.bases, lay.n, state.H_dev, lay.n, rid, rows.size, kctx, W, stream)
-        groups = np.unique(rows // lay.cap).astype(np.int32)
-        gid = torch.from_numpy(groups).to(dev)
-        device.slot_combine(W, lay.cap, gid, groups.size, kctx, k, stream)
-    entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
-    return ClientHint(old.query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
-                      dev=k, slots=W, bases=old.bases)
+    main = stream or torch.cuda.current_stream(dev)
+    rows, rid, gid, ng = _changed_ids(state, changed_rows)
+    streams = [main] if len(pairs) == 1 else [torch.cuda.Stream(dev)
+                                              for _ in range(min(nstreams, len(pairs)))]
+    ev = torch.cuda.Event()
+    ev.record(main)
+    outs = []
+    for i, (reg, old) in enumerate(pairs):
+        st = streams[i % len(streams)]
+        if st is not main:
+            st.wait_event(ev)
+        kctx = key_ctx(reg.pk.m, dev)
+        with torch.cuda.stream(st):
+            outs.append(_refresh_device(state, kctx, old, rows, rid, gid, ng, st))
+    for st in streams:
+        if st is not main:
+            main.wait_stream(st)
+    res = []
+    for (reg, old), (W, k) in zip(pairs, outs):
+        entries = limbs_to_ints(_d2h_u32(k, "hint", main))
+        res.append(ClientHint(old.query_index, state.db_version,
+                              [PaillierCiphertext(e) for e in entries], dev=k, slots=W,
+                              bases=old.bases))
+    return res
 
 
 def _stored_device(stored, kctx, dev, stream):
