@@ -22,6 +22,7 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--engine", default="umma")
 ap.add_argument("--hint", action="store_true")
 ap.add_argument("--d1", type=int, default=bench.D1)
+ap.add_argument("--plan", default="", help="run the captured plan: full | gemv | compress")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 params = z.ProtocolParams(z.LweParams(1024, 1 << 32, 256, 6.4), bench.D0, a.d1, 2048)
@@ -35,8 +36,15 @@ qd = torch.from_numpy(q32.view(np.int32)).to(dev).reshape(1, -1)
 r = random.Random(2)
 cko = torch.from_numpy(ints_to_limbs([r.randrange(m) for _ in range(1024)], kctx.lm).view(np.int32)).to(dev)
 stream = torch.cuda.current_stream(dev)
-for _ in range(a.reps):
-    st.answer_device(qd, cko, kctx, kctx.lm, stream)
+if a.plan:
+    plan = st.answer_plan(kctx, kctx.lm)
+    plan.qu.copy_(qd)
+    plan.cko.copy_(cko)
+    for _ in range(a.reps):
+        plan.run(a.plan, stream)
+else:
+    for _ in range(a.reps):
+        st.answer_device(qd, cko, kctx, kctx.lm, stream)
 if a.hint:
     pk = z.PaillierPublicKey(m, m.bit_length())
     reg = z.ClientRegistration(pk, b"\x05" * 16, z.client_id_of(pk))
