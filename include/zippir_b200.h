@@ -145,6 +145,18 @@ int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, i
                              int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
                              void* stream);
 
+/* Split group stage (lets the Montgomery work overlap the GEMV):
+ * tz[q][g] = (sum_j 2^(32j) z[c]) mod m_q  -- needs only the compression output;
+ * t[q][g]  = (tz[q][g] + sum_j 2^(32j) (b[q][c] & qmask)) mod m_q -- after the
+ * GEMV; exact because sum_j 2^(32j) b_c < gamma^cap < m (protocol.py:66-78).
+ * Same per-query arrays as zpir_answer_groups_batch; tz and t share t_ld. */
+int zpir_groups_z(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
+                  const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
+                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, void* stream);
+int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
+                       int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
+                       uint32_t* t, int64_t t_ld, int nq, void* stream);
+
 /* ---- slot-decomposed hints and incremental DB update (BASELINE configs[4];
  * the reference rebuilds everything on update, server.py:115-124) ---------
  * Multiexp over an explicit list of exponent rows (row_ids, nullable = 0..rows-1);

@@ -52,6 +52,10 @@ _SIGS = {
     "zpir_pow8_table": ([_p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p], _c_int),
     "zpir_slot_fixed": ([_p, _c_i64, _p, _c_i64, _p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p],
                         _c_int),
+    "zpir_groups_z": ([_p, _c_i64, _c_i64, _c_int, _c_i64, _c_int, _p, _p, _p, _c_int, _p, _p,
+                       _c_i64, _c_int, _p], _c_int),
+    "zpir_groups_finish": ([_p, _p, _c_i64, _c_u32, _c_i64, _c_int, _c_i64, _c_int, _p, _p, _c_i64,
+                            _c_int, _p], _c_int),
     "zpir_rows_differ": ([_p, _p, _c_i64, _c_i64, _p, _p], _c_int),
     "zpir_move_rows": ([_p, _p, _c_i64, _p, _c_i64, _c_int, _p], _c_int),
     "zpir_probe_imad": ([_c_int, _c_int, ctypes.POINTER(ctypes.c_float)], _c_int),

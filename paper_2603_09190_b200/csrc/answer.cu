@@ -128,7 +128,7 @@ struct GroupBatch {
   const uint8_t* fast0s;   // per-query fast0 (nullptr: use fast0)
 };
 
-template <int LPL, int NCH>
+template <int LPL, int NCH, bool WITH_B = true>
 __global__ void __launch_bounds__(128)
 answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict__ b,
                      uint32_t qmask, int64_t d1, int cap, int64_t groups,
@@ -165,7 +165,8 @@ answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict_
   __syncthreads();
   // position sums X_P = b_P + sum_j z_j[P - j], split into lo/hi words
   for (int P = tid; P < NX; P += blockDim.x) {
-    unsigned long long s = (P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
+    unsigned long long s =
+        (WITH_B && P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
     const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
     for (int j = jlo; j <= jhi; ++j) s += zs[j * wz + (P - j)];
     lo[P] = (uint32_t)s;
@@ -216,6 +217,43 @@ answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict_
     big_store<LPL>(out, res, lane);
     for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
   }
+}
+
+// Finish stage: t_g = (tz_g + B_g) mod m with B_g = sum_j 2^(32 j) (b_c & qmask)
+// < gamma^cap < m (capacity bound, protocol.py:66-78), so one addition and one
+// conditional subtraction suffice. tz_g = (sum_j 2^(32j) z_c) mod m comes from
+// answer_groups_kernel<..., WITH_B = false>, which therefore does not wait for
+// the GEMV. One warp per group; per-query strides as in GroupBatch.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+groups_finish_kernel(const uint32_t* __restrict__ tz, const uint32_t* __restrict__ b,
+                     uint32_t qmask, int64_t d1, int cap, int64_t groups,
+                     const uint32_t* __restrict__ mod, uint32_t* __restrict__ t, int64_t t_ld,
+                     GroupBatch bt) {
+  constexpr int LM = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= groups) return;
+  const int64_t q = blockIdx.y;
+  tz += q * groups * t_ld;
+  b += q * bt.bq;
+  t += q * bt.tq;
+  mod += q * bt.mq;
+  const int64_t c0 = g * cap;
+  const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
+  uint32_t n_[LPL], x[LPL], y[LPL];
+  big_load<LPL>(n_, mod, lane);
+  big_load<LPL>(x, tz + g * t_ld, lane);
+#pragma unroll
+  for (int i = 0; i < LPL; ++i) {
+    const int j = lane * LPL + i;
+    y[i] = (j < nrows) ? (b[c0 + j] & qmask) : 0u;
+  }
+  const uint32_t cy = big_add<LPL>(x, y, lane);
+  big_cond_sub<LPL>(x, cy, n_, lane);
+  uint32_t* out = t + g * t_ld;
+  big_store<LPL>(out, x, lane);
+  for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
 }
 
 // K_g = (1 + t_g m) k_g mod m^2, one warp per group, with m^2 context
@@ -314,6 +352,50 @@ static int answer_groups_launch_ex(const uint32_t* z, const uint32_t* b, uint32_
   }
 #undef ZPIR_GROUPS
   return check_launch("answer_groups");
+}
+
+// Group stage without b (tz = (sum_j 2^(32j) z_c) mod m) and the finish stage.
+int groups_z_launch(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
+                    const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
+                    const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, cudaStream_t st) {
+  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
+      nchunks > 3 || 32 * cap >= 32 * lm) {
+    set_error("groups_z: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
+    return kErrInput;
+  }
+  GroupBatch bt{zq, 0, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s};
+  const dim3 grid((unsigned)groups, (unsigned)nq);
+  const size_t zsm = (size_t)cap * (lm + 4) * sizeof(uint32_t);
+#define ZPIR_GZ(NCHV)                                                                          \
+  ZPIR_LPL_DISPATCH(lm / 32, {                                                                 \
+    cudaFuncSetAttribute(answer_groups_kernel<LPL, NCHV, false>,                               \
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)zsm);               \
+    answer_groups_kernel<LPL, NCHV, false><<<grid, 128, zsm, st>>>(                            \
+        z, nullptr, 0u, d1, cap, groups, mods, 0u, rpows, 0, tz, t_ld, bt);                    \
+  })
+  if (nchunks == 2) {
+    ZPIR_GZ(2);
+  } else {
+    ZPIR_GZ(3);
+  }
+#undef ZPIR_GZ
+  return check_launch("groups_z");
+}
+
+int groups_finish_launch(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
+                         int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
+                         uint32_t* t, int64_t t_ld, int nq, cudaStream_t st) {
+  if (lm % 32 || t_ld < lm || cap > lm) {
+    set_error("groups_finish: bad layout");
+    return kErrInput;
+  }
+  GroupBatch bt{0, bq, groups * t_ld, lm, 0, nullptr, nullptr};
+  const dim3 grid((unsigned)ceil_div(groups, 4), (unsigned)nq);
+  ZPIR_LPL_DISPATCH(lm / 32, {
+    groups_finish_kernel<LPL><<<grid, 128, 0, st>>>(tz, b, qmask, d1, cap, groups, mods, t, t_ld,
+                                                    bt);
+  });
+  return check_launch("groups_finish");
 }
 
 // Batched group stage: nq queries sharing d1/cap/lm, per-query moduli.

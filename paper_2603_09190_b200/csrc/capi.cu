@@ -56,6 +56,11 @@ int pow8_table_launch(const uint32_t*, int64_t, int, const uint32_t*, uint32_t, 
                       uint32_t*, cudaStream_t);
 int slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, const int32_t*, int64_t,
                       int, const uint32_t*, uint32_t, const uint32_t*, uint32_t*, cudaStream_t);
+int groups_z_launch(const uint32_t*, int64_t, int64_t, int, int64_t, int, const uint32_t*,
+                    const uint32_t*, const uint32_t*, int, const uint8_t*, uint32_t*, int64_t, int,
+                    cudaStream_t);
+int groups_finish_launch(const uint32_t*, const uint32_t*, int64_t, uint32_t, int64_t, int, int64_t,
+                         int, const uint32_t*, uint32_t*, int64_t, int, cudaStream_t);
 int rows_differ_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
 int move_rows_launch(const uint8_t*, uint8_t*, int64_t, const int32_t*, int64_t, int, cudaStream_t);
 int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
@@ -219,6 +224,20 @@ int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t 
                     uint32_t np, const uint32_t* one_m, uint32_t* W, void* stream) {
   ZPIR_GUARD(slot_fixed_launch(P, n, exps, row_stride, row_ids, rows, limbs, N, np, one_m, W,
                                S(stream)));
+}
+
+int zpir_groups_z(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
+                  const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
+                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, void* stream) {
+  ZPIR_GUARD(groups_z_launch(z, zq, d1, cap, groups, lm, mods, nps, rpows, nchunks, fast0s, tz, t_ld,
+                             nq, S(stream)));
+}
+
+int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
+                       int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
+                       uint32_t* t, int64_t t_ld, int nq, void* stream) {
+  ZPIR_GUARD(groups_finish_launch(tz, b, bq, qmask, d1, cap, groups, lm, mods, t, t_ld, nq,
+                                  S(stream)));
 }
 
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,

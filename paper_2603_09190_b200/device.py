@@ -260,3 +260,19 @@ def slot_fixed(P, n, E, rs, row_ids, rows, kctx, W, stream=None):
               _lib.ptr(row_ids) if row_ids is not None else None, rows, kctx.l2,
               _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_one2), _lib.ptr(W), _s(stream))
     return W
+
+
+def groups_z(z, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, tz, t_ld, stream=None):
+    rows, wz = z.shape[-2], z.shape[-1]
+    nq = 1 if z.dim() == 2 else z.shape[0]
+    _lib.call("zpir_groups_z", _lib.ptr(z), rows * wz, d1, cap, groups, lm, _lib.ptr(d_m),
+              _lib.ptr(d_np), _lib.ptr(d_rpow), nchunks, _lib.ptr(d_f0), _lib.ptr(tz), t_ld, nq,
+              _s(stream))
+    return tz
+
+
+def groups_finish(tz, b, qmask, d1, cap, groups, lm, d_m, t, t_ld, stream=None):
+    nq = 1 if b.dim() == 1 or b.shape[0] == 1 else b.shape[0]
+    _lib.call("zpir_groups_finish", _lib.ptr(tz), _lib.ptr(b), b.shape[-1], qmask, d1, cap, groups,
+              lm, _lib.ptr(d_m), _lib.ptr(t), t_ld, nq, _s(stream))
+    return t

@@ -5,8 +5,9 @@ One plan per (state, thread, key width, output stride). Its input buffers
 -- query planes, compression operand, the two tcgen05 GEMMs, the group
 stage -- is captured once into CUDA graphs and replayed per query:
 
-  full graph     GEMV on (SMs - COMPRESS_CTAS) SMs || compression on a side
-                 stream on COMPRESS_CTAS SMs, joined by the group stage
+  full graph     GEMV on (SMs - COMPRESS_CTAS) SMs || compression + the
+                 Montgomery group stage (tz = Z_g mod m) on a side stream on
+                 COMPRESS_CTAS SMs, joined by the finish (t = tz + B_g mod m)
                  (device-resident throughput; bench `value`)
   gemv graph     query planes + GEMV on all SMs
   compress graph compression operand + compression GEMM (all SMs) + groups
@@ -44,6 +45,7 @@ class AnswerPlan:
         self.bc = torch.empty((device.UMMA_NB[lm], 4 * lay.n), dtype=torch.uint8, device=dev)
         self.z = torch.empty((lay.rows, lm + 4), dtype=torch.int32, device=dev)
         self.t = torch.empty((lay.groups, t_ld), dtype=torch.int32, device=dev)
+        self.tz = torch.empty((lay.groups, t_ld), dtype=torch.int32, device=dev)
         # pinned host mirrors for respond(): written in place, copied async
         self.h_qu = torch.zeros((lay.ld,), dtype=torch.int32).pin_memory()
         self.h_cko = torch.empty((lay.n, lm), dtype=torch.int32).pin_memory()
@@ -88,11 +90,17 @@ class AnswerPlan:
         self.kctx = kctx
         self.key_m = kctx.m
 
-    def _groups(self, stream):
+    def _groups_z(self, stream):
+        """Montgomery part of the group stage; needs only the compression."""
         lay = self.state.layout
-        device.answer_groups_plan(self.z, self.b, lay.qmask, lay.d1, lay.cap, lay.groups,
-                                  self.kctx.lm, self.d_m, self.d_np, self.d_rpow, self.nchunks,
-                                  self.d_f0, self.t, self.t_ld, stream)
+        device.groups_z(self.z, lay.d1, lay.cap, lay.groups, self.kctx.lm, self.d_m, self.d_np,
+                        self.d_rpow, self.nchunks, self.d_f0, self.tz, self.t_ld, stream)
+
+    def _finish(self, stream):
+        """t = (tz + B) mod m once the GEMV's b is complete."""
+        lay = self.state.layout
+        device.groups_finish(self.tz, self.b, lay.qmask, lay.d1, lay.cap, lay.groups,
+                             self.kctx.lm, self.d_m, self.t, self.t_ld, stream)
 
     def _seq(self, which, stream):
         if which == "full":
@@ -100,18 +108,21 @@ class AnswerPlan:
                 self.ev_in.record(stream)
                 self.side.wait_event(self.ev_in)
                 self._compress(self.side, self.ctas)
+                self._groups_z(self.side)      # overlaps the GEMV's tail
                 self.ev_comp.record(self.side)
                 self._gemv(stream, self.sms - self.ctas)
                 stream.wait_event(self.ev_comp)
             else:
                 self._gemv(stream, 0)
                 self._compress(stream, 0)
-            self._groups(stream)
+                self._groups_z(stream)
+            self._finish(stream)
         elif which == "gemv":
             self._gemv(stream, 0)
         elif which == "compress":
             self._compress(stream, 0)
-            self._groups(stream)
+            self._groups_z(stream)
+            self._finish(stream)
         else:
             raise ValueError(which)
 
