@@ -157,6 +157,18 @@ int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32
                        int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
                        uint32_t* t, int64_t t_ld, int nq, void* stream);
 
+/* ---- device ChaCha20 streams (prg.py:23-57), key32/iv16 are HOST byte arrays
+ * (key = SHA-256(seed), iv = domain || 15-byte LE index) --------------------
+ * Public matrix A (protocol.py:91-95): out[r*ld + c] = mask & low32(u64 word
+ * r*cols + c) of the stream. */
+int zpir_chacha_words32(const uint8_t* key32, const uint8_t* iv16, int64_t rows, int64_t cols,
+                        uint32_t* out, int64_t ld, uint32_t mask, void* stream);
+/* ck_r (paillier.py:206-208, protocol.py:285-288): out[k] = Stream(seed, domain,
+ * (query_index << 32) | k).below(bound) for k < n, as `limbs` u32 limbs;
+ * bits = bitlen(bound - 1); bound is a device limb array. */
+int zpir_chacha_below(const uint8_t* key32, uint32_t domain, uint64_t query_index, int64_t n,
+                      const uint32_t* bound, int limbs, int bits, uint32_t* out, void* stream);
+
 /* ---- slot-decomposed hints and incremental DB update (BASELINE configs[4];
  * the reference rebuilds everything on update, server.py:115-124) ---------
  * Multiexp over an explicit list of exponent rows (row_ids, nullable = 0..rows-1);

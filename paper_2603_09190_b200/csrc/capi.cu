@@ -61,6 +61,10 @@ int groups_z_launch(const uint32_t*, int64_t, int64_t, int, int64_t, int, const 
                     cudaStream_t);
 int groups_finish_launch(const uint32_t*, const uint32_t*, int64_t, uint32_t, int64_t, int, int64_t,
                          int, const uint32_t*, uint32_t*, int64_t, int, cudaStream_t);
+int chacha_words32_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, int64_t,
+                          uint32_t, cudaStream_t);
+int chacha_below_launch(const uint8_t*, uint32_t, uint64_t, int64_t, const uint32_t*, int, int,
+                        uint32_t*, cudaStream_t);
 int rows_differ_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
 int move_rows_launch(const uint8_t*, uint8_t*, int64_t, const int32_t*, int64_t, int, cudaStream_t);
 int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
@@ -238,6 +242,17 @@ int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32
                        uint32_t* t, int64_t t_ld, int nq, void* stream) {
   ZPIR_GUARD(groups_finish_launch(tz, b, bq, qmask, d1, cap, groups, lm, mods, t, t_ld, nq,
                                   S(stream)));
+}
+
+int zpir_chacha_words32(const uint8_t* key32, const uint8_t* iv16, int64_t rows, int64_t cols,
+                        uint32_t* out, int64_t ld, uint32_t mask, void* stream) {
+  ZPIR_GUARD(chacha_words32_launch(key32, iv16, rows, cols, out, ld, mask, S(stream)));
+}
+
+int zpir_chacha_below(const uint8_t* key32, uint32_t domain, uint64_t query_index, int64_t n,
+                      const uint32_t* bound, int limbs, int bits, uint32_t* out, void* stream) {
+  ZPIR_GUARD(chacha_below_launch(key32, domain, query_index, n, bound, limbs, bits, out,
+                                 S(stream)));
 }
 
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,

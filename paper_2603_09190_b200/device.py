@@ -276,3 +276,25 @@ def groups_finish(tz, b, qmask, d1, cap, groups, lm, d_m, t, t_ld, stream=None):
     _lib.call("zpir_groups_finish", _lib.ptr(tz), _lib.ptr(b), b.shape[-1], qmask, d1, cap, groups,
               lm, _lib.ptr(d_m), _lib.ptr(t), t_ld, nq, _s(stream))
     return t
+
+
+# ---- device ChaCha20 (prg.py) -------------------------------------------------
+
+def chacha_words32(seed: bytes, domain: int, index: int, rows, cols, out, ld, mask, stream=None):
+    import hashlib
+    key = hashlib.sha256(seed).digest()
+    iv = bytes([domain]) + int(index).to_bytes(15, "little")
+    _lib.call("zpir_chacha_words32", key, iv, rows, cols, _lib.ptr(out), ld, mask, _s(stream))
+    return out
+
+
+def chacha_below(seed: bytes, domain: int, query_index: int, n: int, d_bound, bound: int, limbs,
+                 stream=None):
+    """(n, limbs) int32: Stream(seed, domain, (qi << 32) | k).below(bound)."""
+    import hashlib
+    key = hashlib.sha256(seed).digest()
+    bits = (bound - 1).bit_length()
+    out = torch.empty((n, limbs), dtype=torch.int32, device=d_bound.device)
+    _lib.call("zpir_chacha_below", key, domain, query_index, n, _lib.ptr(d_bound), limbs, bits,
+              _lib.ptr(out), _s(stream))
+    return out

@@ -36,7 +36,7 @@ from .bigint import ints_to_limbs, key_ctx, limbs_to_ints
 from .paillier import PaillierCiphertext, PaillierPublicKey, sample_ciphertext  # noqa: F401
 from .params import Layout, LweParams, ProtocolParams  # noqa: F401
 from .plan import AnswerPlan
-from .prg import Stream, DOM_PUBLIC_MATRIX
+from .prg import DOM_CIPHERTEXT_SAMPLE, DOM_PUBLIC_MATRIX
 
 SEPARATE = "separate"
 COMBINED = "combined"
@@ -165,13 +165,12 @@ class ServerGlobalState:
         dev = self.device = device.require_cuda(device_)
         stream = torch.cuda.current_stream(dev)
         n, d0, d1 = lay.n, lay.d0, lay.d1
-        A32 = Stream(params.a_seed, DOM_PUBLIC_MATRIX).words32(d0 * n).reshape(d0, n)
-        self._A32 = A32
         self._A64 = None
-        A_pad = np.zeros((lay.ld, lay.lda), dtype=np.uint32)
-        A_pad[:d0, :n] = A32
         t0 = time.perf_counter()
-        self.A_dev = device.u32_tensor(A_pad, dev)
+        # public matrix A straight from the seeded stream on the device (device ChaCha20)
+        self.A_dev = torch.zeros((lay.ld, lay.lda), dtype=torch.int32, device=dev)
+        device.chacha_words32(params.a_seed, DOM_PUBLIC_MATRIX, 0, d0, n, self.A_dev, lay.lda,
+                              (lay.q - 1) & 0xFFFFFFFF, stream)
         with warnings.catch_warnings():  # read-only numpy views are only read here
             warnings.simplefilter("ignore", UserWarning)
             db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
@@ -211,7 +210,7 @@ class ServerGlobalState:
         t0 = time.perf_counter()
         new = object.__new__(ServerGlobalState)
         new.__dict__.update(params=params, db=db, basis=self.basis, layout=lay, device=dev,
-                            engine=self.engine, _A32=self._A32, _A64=self._A64, A_dev=self.A_dev,
+                            engine=self.engine, _A64=self._A64, A_dev=self.A_dev,
                             _H_host=None, _H_scaled=None, _lock=threading.Lock(),
                             _tls=threading.local())
         new.db_version = self.db_version + 1 if db_version is None else db_version
@@ -243,9 +242,12 @@ class ServerGlobalState:
 
     @property
     def A(self) -> np.ndarray:
-        if self._A64 is None:
-            self._A64 = self._A32.astype(np.uint64)
-        return self._A64
+        """The (d0, n) public matrix (protocol.py:175-176), host view."""
+        with self._lock:
+            if self._A64 is None:
+                lay = self.layout
+                self._A64 = device.to_host_u32(self.A_dev[: lay.d0, : lay.n]).astype(np.uint64)
+            return self._A64
 
     @property
     def H(self) -> np.ndarray:
@@ -424,9 +426,9 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     dev = state.device
     stream = stream or torch.cuda.current_stream(dev)
     kctx = key_ctx(reg.pk.m, dev)
-    ck_r = [c.c for c in derive_ck_r(reg.pk, reg.seed, query_index, lay.n)]
-    bases = _h2d(ints_to_limbs(ck_r, kctx.l2), dev, "bases", stream).view(torch.int32)
-    bases = bases.reshape(lay.n, kctx.l2)
+    # ck_r[k] = Stream(seed, 1, (qi << 32) | k).below(m^2), sampled on the device
+    bases = device.chacha_below(reg.seed, DOM_CIPHERTEXT_SAMPLE, query_index, lay.n, kctx.d_m2,
+                                kctx.m2, kctx.l2, stream)
     nslot = lay.groups * lay.cap
     W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
     P = device.pow8_table(bases, kctx, stream)
