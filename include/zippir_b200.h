@@ -169,6 +169,13 @@ int zpir_chacha_words32(const uint8_t* key32, const uint8_t* iv16, int64_t rows,
 int zpir_chacha_below(const uint8_t* key32, uint32_t domain, uint64_t query_index, int64_t n,
                       const uint32_t* bound, int limbs, int bits, uint32_t* out, void* stream);
 
+/* Python-int boundary helpers: regroup CPython's 30-bit digits (copied raw by
+ * the host) into 32-bit limbs and back (limbs rows have stride ld). */
+int zpir_digits_to_limbs(const uint32_t* digits, int64_t count, int ndig, uint32_t* limbs, int nl,
+                         void* stream);
+int zpir_limbs_to_digits(const uint32_t* limbs, int64_t count, int nl, int64_t ld,
+                         uint32_t* digits, int ndig, void* stream);
+
 /* ---- slot-decomposed hints and incremental DB update (BASELINE configs[4];
  * the reference rebuilds everything on update, server.py:115-124) ---------
  * Multiexp over an explicit list of exponent rows (row_ids, nullable = 0..rows-1);

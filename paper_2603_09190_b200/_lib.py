@@ -60,6 +60,8 @@ _SIGS = {
                              _p], _c_int),
     "zpir_chacha_below": ([ctypes.c_char_p, _c_u32, ctypes.c_uint64, _c_i64, _p, _c_int, _c_int, _p,
                            _p], _c_int),
+    "zpir_digits_to_limbs": ([_p, _c_i64, _c_int, _p, _c_int, _p], _c_int),
+    "zpir_limbs_to_digits": ([_p, _c_i64, _c_int, _c_i64, _p, _c_int, _p], _c_int),
     "zpir_rows_differ": ([_p, _p, _c_i64, _c_i64, _p, _p], _c_int),
     "zpir_move_rows": ([_p, _p, _c_i64, _p, _c_i64, _c_int, _p], _c_int),
     "zpir_probe_imad": ([_c_int, _c_int, ctypes.POINTER(ctypes.c_float)], _c_int),

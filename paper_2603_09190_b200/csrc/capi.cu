@@ -65,6 +65,8 @@ int chacha_words32_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint
                           uint32_t, cudaStream_t);
 int chacha_below_launch(const uint8_t*, uint32_t, uint64_t, int64_t, const uint32_t*, int, int,
                         uint32_t*, cudaStream_t);
+int digits_to_limbs_launch(const uint32_t*, int64_t, int, uint32_t*, int, cudaStream_t);
+int limbs_to_digits_launch(const uint32_t*, int64_t, int, int64_t, uint32_t*, int, cudaStream_t);
 int rows_differ_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, cudaStream_t);
 int move_rows_launch(const uint8_t*, uint8_t*, int64_t, const int32_t*, int64_t, int, cudaStream_t);
 int build_bc_batch_launch(const uint32_t*, int64_t, int, int, int, uint8_t*, cudaStream_t);
@@ -253,6 +255,16 @@ int zpir_chacha_below(const uint8_t* key32, uint32_t domain, uint64_t query_inde
                       const uint32_t* bound, int limbs, int bits, uint32_t* out, void* stream) {
   ZPIR_GUARD(chacha_below_launch(key32, domain, query_index, n, bound, limbs, bits, out,
                                  S(stream)));
+}
+
+int zpir_digits_to_limbs(const uint32_t* digits, int64_t count, int ndig, uint32_t* limbs, int nl,
+                         void* stream) {
+  ZPIR_GUARD(digits_to_limbs_launch(digits, count, ndig, limbs, nl, S(stream)));
+}
+
+int zpir_limbs_to_digits(const uint32_t* limbs, int64_t count, int nl, int64_t ld,
+                         uint32_t* digits, int ndig, void* stream) {
+  ZPIR_GUARD(limbs_to_digits_launch(limbs, count, nl, ld, digits, ndig, S(stream)));
 }
 
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,

@@ -169,7 +169,94 @@ static PyObject* ints_from(PyObject* self, PyObject* args) {
   return list;
 }
 
+#ifdef ZPIR_FAST_DIGITS
+/* Raw CPython digits: buf[i*ndig .. +ndig) = the 30-bit digits of seq[i]
+ * (zero-padded); the GPU regroups them into 32-bit limbs (zpir_digits_to_limbs). */
+static PyObject* digits_into(PyObject* self, PyObject* args) {
+  PyObject* seq;
+  Py_buffer view;
+  Py_ssize_t ndig;
+  if (!PyArg_ParseTuple(args, "Ow*n", &seq, &view, &ndig)) return NULL;
+  PyObject* fast = PySequence_Fast(seq, "expected a sequence of ints");
+  if (!fast) {
+    PyBuffer_Release(&view);
+    return NULL;
+  }
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
+  if ((size_t)view.len < (size_t)n * ndig * 4) {
+    PyErr_SetString(PyExc_ValueError, "buffer too small");
+    goto fail;
+  }
+  PyObject** items = PySequence_Fast_ITEMS(fast);
+  uint32_t* out = (uint32_t*)view.buf;
+  for (Py_ssize_t i = 0; i < n; ++i) {
+    PyObject* v = items[i];
+    if (!PyLong_Check(v)) {
+      PyErr_SetString(PyExc_TypeError, "expected int");
+      goto fail;
+    }
+    PyLongObject* L = (PyLongObject*)v;
+    const uintptr_t tag = L->long_value.lv_tag;
+    if ((tag & 3) == 2) {
+      PyErr_SetString(PyExc_ValueError, "negative integers are not encodable");
+      goto fail;
+    }
+    const Py_ssize_t nd = (Py_ssize_t)(tag >> 3);
+    if (nd > ndig) {
+      PyErr_SetString(PyExc_ValueError, "integer wider than the limb width");
+      goto fail;
+    }
+    uint32_t* o = out + (size_t)i * ndig;
+    if (nd) memcpy(o, L->long_value.ob_digit, (size_t)nd * 4);
+    if (nd < ndig) memset(o + nd, 0, (size_t)(ndig - nd) * 4);
+  }
+  Py_DECREF(fast);
+  PyBuffer_Release(&view);
+  Py_RETURN_NONE;
+fail:
+  Py_DECREF(fast);
+  PyBuffer_Release(&view);
+  return NULL;
+}
+
+/* count ints from rows of ndig normalised 30-bit digits (zpir_limbs_to_digits). */
+static PyObject* ints_from_digits(PyObject* self, PyObject* args) {
+  Py_buffer view;
+  Py_ssize_t count, ndig;
+  if (!PyArg_ParseTuple(args, "y*nn", &view, &count, &ndig)) return NULL;
+  if ((size_t)view.len < (size_t)count * ndig * 4) {
+    PyBuffer_Release(&view);
+    PyErr_SetString(PyExc_ValueError, "buffer too small");
+    return NULL;
+  }
+  PyObject* list = PyList_New(count);
+  if (!list) {
+    PyBuffer_Release(&view);
+    return NULL;
+  }
+  const uint32_t* p = (const uint32_t*)view.buf;
+  for (Py_ssize_t i = 0; i < count; ++i) {
+    const uint32_t* d = p + (size_t)i * ndig;
+    Py_ssize_t k = ndig;
+    while (k > 0 && d[k - 1] == 0) --k;
+    PyObject* v = k ? (PyObject*)_PyLong_FromDigits(0, k, (digit*)d) : PyLong_FromLong(0);
+    if (!v) {
+      Py_DECREF(list);
+      PyBuffer_Release(&view);
+      return NULL;
+    }
+    PyList_SET_ITEM(list, i, v);
+  }
+  PyBuffer_Release(&view);
+  return list;
+}
+#endif
+
 static PyMethodDef methods[] = {
+#ifdef ZPIR_FAST_DIGITS
+    {"digits_into", digits_into, METH_VARARGS, "ints -> raw 30-bit digits written into a buffer"},
+    {"ints_from_digits", ints_from_digits, METH_VARARGS, "30-bit digit rows -> list of ints"},
+#endif
     {"ints_into", ints_into, METH_VARARGS, "ints -> u32 LE limbs written into a buffer"},
     {"ints_from", ints_from, METH_VARARGS, "u32 LE limbs -> list of ints"},
     {NULL, NULL, 0, NULL}};

@@ -298,3 +298,16 @@ def chacha_below(seed: bytes, domain: int, query_index: int, n: int, d_bound, bo
     _lib.call("zpir_chacha_below", key, domain, query_index, n, _lib.ptr(d_bound), limbs, bits,
               _lib.ptr(out), _s(stream))
     return out
+
+
+def digits_to_limbs(digits, nl, out, stream=None):
+    count, ndig = digits.shape
+    _lib.call("zpir_digits_to_limbs", _lib.ptr(digits), count, ndig, _lib.ptr(out), nl, _s(stream))
+    return out
+
+
+def limbs_to_digits(limbs, nl, digits, stream=None):
+    count, ld = limbs.shape
+    _lib.call("zpir_limbs_to_digits", _lib.ptr(limbs), count, nl, ld, _lib.ptr(digits),
+              digits.shape[1], _s(stream))
+    return digits

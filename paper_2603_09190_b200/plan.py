@@ -51,6 +51,15 @@ class AnswerPlan:
         self.h_cko = torch.empty((lay.n, lm), dtype=torch.int32).pin_memory()
         self.h_t = torch.empty((lay.groups, t_ld), dtype=torch.int32).pin_memory()
         self.h_K = torch.empty((lay.groups, kctx.l2), dtype=torch.int32).pin_memory()
+        # raw CPython 30-bit digits at the API boundary (regrouped on the device)
+        self.ndig_m = -(-32 * lm // 30)
+        self.ndig_2 = -(-32 * kctx.l2 // 30)
+        self.d_ckd = torch.zeros((lay.n, self.ndig_m), dtype=torch.int32, device=dev)
+        self.h_ckd = torch.zeros((lay.n, self.ndig_m), dtype=torch.int32).pin_memory()
+        self.d_td = torch.zeros((lay.groups, self.ndig_m), dtype=torch.int32, device=dev)
+        self.h_td = torch.zeros((lay.groups, self.ndig_m), dtype=torch.int32).pin_memory()
+        self.d_Kd = torch.zeros((lay.groups, self.ndig_2), dtype=torch.int32, device=dev)
+        self.h_Kd = torch.zeros((lay.groups, self.ndig_2), dtype=torch.int32).pin_memory()
         # the client's modulus constants live in plan buffers read by the
         # captured group stage (refreshed by set_key when the client changes)
         self.nchunks = max(2, -(-(lay.cap + lm + 4) // lm))
@@ -123,6 +132,13 @@ class AnswerPlan:
             self._compress(stream, 0)
             self._groups_z(stream)
             self._finish(stream)
+        elif which == "compress_digits":
+            # respond(): ck_o arrives as CPython digits, t leaves as digits
+            device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
+            self._compress(stream, 0)
+            self._groups_z(stream)
+            self._finish(stream)
+            device.limbs_to_digits(self.t, self.kctx.lm, self.d_td, stream)
         else:
             raise ValueError(which)
 

@@ -511,6 +511,13 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
     return res
 
 
+def _digit_conv():
+    """The C extension's raw-digit entry points (CPython 3.12/3.13), or None."""
+    from .bigint import _conv
+    c = _conv()
+    return c if hasattr(c, "digits_into") else None
+
+
 def _stored_device(stored, kctx, dev, stream):
     d = getattr(stored, "dev", None)
     if d is not None and d.device == dev and d.shape[1] == kctx.l2:
@@ -551,21 +558,39 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
         plan.run("gemv", stream)
         if events:
             events[1].record(stream)
-        ints_to_limbs(qmsg.ck_o, kctx.lm, out=plan.h_cko.numpy().view(np.uint32))
-        with torch.cuda.stream(stream):
-            plan.cko.copy_(plan.h_cko, non_blocking=True)
-        plan.run("compress", stream)
+        conv = _digit_conv()
+        if conv is not None:
+            # memcpy of CPython's 30-bit digits; the graph regroups them into limbs
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            with torch.cuda.stream(stream):
+                plan.d_ckd.copy_(plan.h_ckd, non_blocking=True)
+            plan.run("compress_digits", stream)
+        else:
+            ints_to_limbs(qmsg.ck_o, kctx.lm, out=plan.h_cko.numpy().view(np.uint32))
+            with torch.cuda.stream(stream):
+                plan.cko.copy_(plan.h_cko, non_blocking=True)
+            plan.run("compress", stream)
         if events:
             events[2].record(stream)
-        t_dev, h_out = plan.t, plan.h_t
         if mode == COMBINED:
             k_dev = _stored_device(stored, kctx, dev, stream)
-            t_dev = device.combine(plan.t, k_dev, kctx, stream=stream)
-            h_out = plan.h_K
+            K = device.combine(plan.t, k_dev, kctx, stream=stream)
+            if conv is not None:
+                device.limbs_to_digits(K, kctx.l2, plan.d_Kd, stream)
+                src, h_out, nd = plan.d_Kd, plan.h_Kd, plan.ndig_2
+            else:
+                src, h_out, nd = K, plan.h_K, None
+        elif conv is not None:
+            src, h_out, nd = plan.d_td, plan.h_td, plan.ndig_m
+        else:
+            src, h_out, nd = plan.t, plan.h_t, None
         with torch.cuda.stream(stream):
-            h_out.copy_(t_dev, non_blocking=True)
+            h_out.copy_(src, non_blocking=True)
         stream.synchronize()
-        vals = limbs_to_ints(h_out.numpy().view(np.uint32))
+        if nd is not None:
+            vals = conv.ints_from_digits(h_out.numpy(), h_out.shape[0], nd)
+        else:
+            vals = limbs_to_ints(h_out.numpy().view(np.uint32))
     else:
         qu_dev = state._stage_query(qmsg.qu0, stream)
         cko = _h2d(ints_to_limbs(qmsg.ck_o, kctx.lm), dev, "cko", stream).view(torch.int32)
