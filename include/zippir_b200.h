@@ -210,6 +210,9 @@ int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t l
 int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_t* ids,
                    int64_t nrows, int scatter, void* stream);
 
+/* Async pinned-host <-> device copy (kind 0 = H2D, 1 = D2H) on `stream`. */
+int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
+
 /* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
  * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
 int zpir_probe_imad(int blocks, int iters, float* ms);

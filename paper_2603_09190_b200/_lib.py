@@ -64,6 +64,7 @@ _SIGS = {
     "zpir_limbs_to_digits": ([_p, _c_i64, _c_int, _c_i64, _p, _c_int, _p], _c_int),
     "zpir_rows_differ": ([_p, _p, _c_i64, _c_i64, _p, _p], _c_int),
     "zpir_move_rows": ([_p, _p, _c_i64, _p, _c_i64, _c_int, _p], _c_int),
+    "zpir_memcpy_async": ([_p, _p, _c_i64, _c_int, _p], _c_int),
     "zpir_probe_imad": ([_c_int, _c_int, ctypes.POINTER(ctypes.c_float)], _c_int),
 }
 

@@ -277,4 +277,13 @@ int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_
   ZPIR_GUARD(move_rows_launch(src, dst, pitch, ids, nrows, scatter, S(stream)));
 }
 
+// Async copy between pinned host and device memory (kind: 0 = H2D, 1 = D2H)
+// on the caller's stream; lets the API layer skip framework overhead per query.
+int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+  if (cudaMemcpyAsync(dst, src, (size_t)bytes, k, S(stream)) != cudaSuccess)
+    return check_launch("memcpy_async");
+  return kOk;
+}
+
 }  // extern "C"

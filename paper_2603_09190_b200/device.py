@@ -311,3 +311,14 @@ def limbs_to_digits(limbs, nl, digits, stream=None):
     _lib.call("zpir_limbs_to_digits", _lib.ptr(limbs), count, nl, ld, _lib.ptr(digits),
               digits.shape[1], _s(stream))
     return digits
+
+
+def h2d_async(dst, src_pinned, stream):
+    """Raw cudaMemcpyAsync pinned host -> device (same byte size)."""
+    _lib.call("zpir_memcpy_async", _lib.ptr(dst), _lib.ptr(src_pinned),
+              src_pinned.numel() * src_pinned.element_size(), 0, _s(stream))
+
+
+def d2h_async(dst_pinned, src, stream):
+    _lib.call("zpir_memcpy_async", _lib.ptr(dst_pinned), _lib.ptr(src),
+              src.numel() * src.element_size(), 1, _s(stream))

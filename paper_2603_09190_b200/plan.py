@@ -132,6 +132,17 @@ class AnswerPlan:
             self._compress(stream, 0)
             self._groups_z(stream)
             self._finish(stream)
+        elif which == "gemv_part":
+            # respond(): GEMV on the SMs the side stream does not take
+            self._gemv(stream, self.sms - self.ctas if self.ctas > 0 else 0)
+        elif which == "side_digits":
+            # respond(), side stream: ck_o digits -> limbs, compression, Montgomery groups
+            device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
+            self._compress(stream, self.ctas)
+            self._groups_z(stream)
+        elif which == "finish_digits":
+            self._finish(stream)
+            device.limbs_to_digits(self.t, self.kctx.lm, self.d_td, stream)
         elif which == "compress_digits":
             # respond(): ck_o arrives as CPython digits, t leaves as digits
             device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)

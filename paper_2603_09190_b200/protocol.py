@@ -547,28 +547,40 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     plan = state.answer_plan(kctx, t_ld)
     if plan is not None:
         plan.set_key(kctx, stream)
-        # qu -> pinned -> device, GEMV graph; the host converts ck_o meanwhile
+        conv = _digit_conv()
+        # qu -> pinned -> device; GEMV graph on (SMs - COMPRESS_CTAS) SMs
         qu = np.asarray(qmsg.qu0)
         hq = plan.h_qu.numpy().view(np.uint32)
         np.copyto(hq[: lay.d0], qu, casting="unsafe")
-        with torch.cuda.stream(stream):
-            plan.qu.view(-1).copy_(plan.h_qu, non_blocking=True)
+        device.h2d_async(plan.qu, plan.h_qu, stream)
         if events:
             events[0].record(stream)
-        plan.run("gemv", stream)
-        if events:
-            events[1].record(stream)
-        conv = _digit_conv()
-        if conv is not None:
-            # memcpy of CPython's 30-bit digits; the graph regroups them into limbs
+        if conv is not None and plan.ctas > 0:
+            plan.run("gemv_part", stream)
+            if events:
+                events[1].record(stream)
+            # meanwhile: ck_o digits (memcpy) -> side stream graph (compression
+            # + Montgomery group stage on COMPRESS_CTAS SMs, concurrent with the GEMV)
             conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
-            with torch.cuda.stream(stream):
-                plan.d_ckd.copy_(plan.h_ckd, non_blocking=True)
+            side = plan.side
+            side.wait_stream(stream)
+            device.h2d_async(plan.d_ckd, plan.h_ckd, side)
+            plan.run("side_digits", side)
+            stream.wait_stream(side)
+            plan.run("finish_digits", stream)
+        elif conv is not None:
+            plan.run("gemv", stream)
+            if events:
+                events[1].record(stream)
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            device.h2d_async(plan.d_ckd, plan.h_ckd, stream)
             plan.run("compress_digits", stream)
         else:
+            plan.run("gemv", stream)
+            if events:
+                events[1].record(stream)
             ints_to_limbs(qmsg.ck_o, kctx.lm, out=plan.h_cko.numpy().view(np.uint32))
-            with torch.cuda.stream(stream):
-                plan.cko.copy_(plan.h_cko, non_blocking=True)
+            device.h2d_async(plan.cko, plan.h_cko, stream)
             plan.run("compress", stream)
         if events:
             events[2].record(stream)
@@ -584,8 +596,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
             src, h_out, nd = plan.d_td, plan.h_td, plan.ndig_m
         else:
             src, h_out, nd = plan.t, plan.h_t, None
-        with torch.cuda.stream(stream):
-            h_out.copy_(src, non_blocking=True)
+        device.d2h_async(h_out, src, stream)
         stream.synchronize()
         if nd is not None:
             vals = conv.ints_from_digits(h_out.numpy(), h_out.shape[0], nd)
