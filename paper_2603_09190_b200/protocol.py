@@ -556,6 +556,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
         if events:
             events[0].record(stream)
         if conv is not None and plan.ctas > 0:
+            plan.ev_in.record(stream)   # key constants staged; before the GEMV
             plan.run("gemv_part", stream)
             if events:
                 events[1].record(stream)
@@ -563,7 +564,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
             # + Montgomery group stage on COMPRESS_CTAS SMs, concurrent with the GEMV)
             conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
             side = plan.side
-            side.wait_stream(stream)
+            side.wait_event(plan.ev_in)
             device.h2d_async(plan.d_ckd, plan.h_ckd, side)
             plan.run("side_digits", side)
             stream.wait_stream(side)
