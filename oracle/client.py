@@ -148,3 +148,13 @@ def extract(sk: SecretKey, q, p, cap, gamma, d1, t=None, k=None, combined=None):
             phase = (val // gamma ** j) % gamma % q
             out.append((2 * phase + delta) // (2 * delta) % p)
     return out
+
+
+def encrypt(sk: SecretKey, mu: int, rng) -> int:
+    """paillier.py:89-101 (same rng consumption)."""
+    m, m2 = sk.m, sk.m * sk.m
+    while True:
+        r = rng.randrange(1, m)
+        if math.gcd(r, m) == 1:
+            break
+    return (1 + mu * m) * pow(r, m, m2) % m2

@@ -199,3 +199,22 @@ def multiexp(m2: int, bases, exps) -> int:
 def hint_entries(H_scaled, ck_r, m2) -> list:
     """paillier_matmul (paillier.py:196-203) as used by hint() (protocol.py:291-296)."""
     return [multiexp(m2, ck_r, row) for row in H_scaled]
+
+
+# -- compress.py:99-258 (server side) -----------------------------------------
+
+def lwe_compress(m: int, ck, a, b, q) -> int:
+    """trivial_encrypt(b) * multiexp(ck, (q - a_i) mod q) mod m^2 (compress.py:99-105)."""
+    m2 = m * m
+    acc = multiexp(m2, [int(c) for c in ck], [(q - int(x)) % q for x in a])
+    return (1 + (int(b) % m) * m) % m2 * acc % m2
+
+
+def batched_lwe_compress(m: int, ck, cts, gamma: int, q) -> int:
+    """compress.py:213-221 restated literally: x = Enc~(0); x *= lwe_compress(ct_j)^(gamma^j)."""
+    m2 = m * m
+    x = 1
+    for j, (a, b) in enumerate(cts):
+        xj = lwe_compress(m, ck, a, b, q)
+        x = x * pow(xj, gamma ** j, m2) % m2
+    return x
