@@ -88,3 +88,41 @@ def test_incremental_update_bit_exact(golden, name):
     reg.hints[0] = h2
     q = z.QueryMessage(reg.client_id, 0, z.SEPARATE, g.ints("ck_o"), g.arr["qu0"])
     assert z.respond(st2, reg, q).t == z.respond(full, reg, q).t
+
+
+def test_paper_parameters_n1400_3072bit():
+    """The paper's setting (cli.py DEFAULT_PARAMS n=1400,
+    3072-bit) on the reference's c07 desk shape 256x256 (test_acceptance.py:
+    214-217): n % 64 != 0 (CUDA-core hint GEMM), lm = 96 (N = 400 compression
+    GEMM), m^2 of 6144 bits (LPL = 6 Montgomery). Bit-exact vs the oracle and
+    end-to-end retrieval in both modes."""
+    import paper_2603_09190_b200 as z
+    from oracle import ref
+    rng = random.Random(1400)
+    params = z.ProtocolParams(z.LweParams(n=1400, q=1 << 32, p=256, noise_sigma=6.4), 256, 256,
+                              3072)
+    db = np.array([[rng.randrange(256) for _ in range(256)] for _ in range(256)], dtype=np.uint8)
+    st = z.ServerGlobalState(params, db)
+    A = ref.public_matrix(b"\x00" * 16, 256, 1400, 1 << 32)
+    H = ref.global_hint(db, A, 1 << 32)
+    assert np.array_equal(st.H, H)
+    sk, seed = client.setup(3072, rng)
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
+    h = z.hint(st, reg, 0)
+    m2 = sk.m * sk.m
+    ck_r = ref.derive_ck_r(m2, seed, 0, 1400)
+    cap = params.capacity
+    Hs = ref.scale_rows(H, cap, 1 << 32, 256, 1400)
+    assert [c.c for c in h.entries[:2]] == [ref.multiexp(m2, ck_r, Hs[g]) for g in range(2)]
+    reg.hints[0] = h
+    i0 = 77
+    qu0, ck_o, _ = client.query(sk, seed, 1400, 1 << 32, 256, 6.4, 256, i0, 0, rng, A)
+    r = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck_o, qu0))
+    b = ref.db_matvec(db, qu0, 1 << 32)
+    assert r.t == ref.answer_t(H, b, ck_o, sk.m, cap, 1 << 32, 256)
+    assert client.extract(sk, 1 << 32, 256, cap, 1 << 32, 256, t=r.t,
+                          k=[c.c for c in r.k]) == [int(x) for x in db[i0]]
+    rc = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
+    assert client.extract(sk, 1 << 32, 256, cap, 1 << 32, 256,
+                          combined=[c.c for c in rc.k]) == [int(x) for x in db[i0]]
