@@ -200,17 +200,6 @@ def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None):
     return t
 
 
-def answer_groups_plan(z, b, qmask, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, t,
-                       t_ld, stream=None):
-    """One-query group stage whose modulus constants are read from device
-    buffers (so a captured graph serves every client of the same width)."""
-    rows, wz = z.shape
-    _lib.call("zpir_answer_groups_batch", _lib.ptr(z), rows * wz, _lib.ptr(b), b.shape[1], qmask, d1,
-              cap, groups, lm, _lib.ptr(d_m), _lib.ptr(d_np), _lib.ptr(d_rpow), nchunks,
-              _lib.ptr(d_f0), _lib.ptr(t), t_ld, 1, _s(stream))
-    return t
-
-
 # ---- slot-decomposed hints / incremental update ------------------------------
 
 def multiexp_rows(bases, E, row_ids, rows, rs, bs, ls, elimbs, kctx, out, keep_mont, stream=None):
