@@ -143,19 +143,22 @@ int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, i
                              uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
                              const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
                              int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
-                             void* stream);
+                             int stride, void* stream);
 
 /* Split group stage (lets the Montgomery work overlap the GEMV):
  * tz[q][g] = (sum_j 2^(32j) z[c]) mod m_q  -- needs only the compression output;
  * t[q][g]  = (tz[q][g] + sum_j 2^(32j) (b[q][c] & qmask)) mod m_q -- after the
  * GEMV; exact because sum_j 2^(32j) b_c < gamma^cap < m (protocol.py:66-78).
- * Same per-query arrays as zpir_answer_groups_batch; tz and t share t_ld. */
+ * Same per-query arrays as zpir_answer_groups_batch; tz and t share t_ld.
+ * stride = slot stride in 32-bit limbs (gamma = 2^(32 stride): 1 for the
+ * binary-key quarter-delta layout, 2 for the uniform-key one). */
 int zpir_groups_z(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
                   const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
-                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, void* stream);
+                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, int stride,
+                  void* stream);
 int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
                        int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
-                       uint32_t* t, int64_t t_ld, int nq, void* stream);
+                       uint32_t* t, int64_t t_ld, int nq, int stride, void* stream);
 
 /* ---- device ChaCha20 streams (prg.py:23-57), key32/iv16 are HOST byte arrays
  * (key = SHA-256(seed), iv = domain || 15-byte LE index) --------------------
@@ -187,12 +190,23 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
                        const uint32_t* N, uint32_t np, const uint32_t* r2, const uint32_t* one_m,
                        int keep_mont, uint32_t* out, void* workspace, int64_t ws_bytes,
                        void* stream);
-/* k[g] = prod_j W[g*cap + j]^(2^(32 j)) mod N (W in Montgomery form; k canonical)
- * for the groups in group_ids (nullable = all ngroups): the hint entry
+/* k[g] = prod_j W[g*cap + j]^(gamma^j) mod N (W in Montgomery form; k canonical)
+ * for the groups in group_ids (nullable = all ngroups), by Horner in gamma
+ * (gamma = HOST array of ceil(gamma_bits/32) u32 words, gamma_bits <= 256; for
+ * gamma = 2^32 that is 32 squarings per slot): the hint entry
  * k_g = prod_k ck_r[k]^H_scaled[g][k] (paillier.py:134-203) rebuilt from its
  * per-DB-row factors W[c] = prod_k ck_r[k]^H[c][k]. */
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
-                      int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream);
+                      int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
+                      int gamma_bits, uint32_t* out, void* stream);
+/* Group stage for a general batch scale gamma (not 2^32 / 2^64):
+ * t[g] = sum_j (gamma^j mod m) ((b[c] & qmask) + z[c]) mod m, with
+ * ctab[j] = {gamma^j R mod m, gamma^j R^2 mod m} (lm limbs each) and w a
+ * workspace of d1 x lm limbs (protocol.py:219-238, :259-269 generic paths). */
+int zpir_answer_general(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1, int cap,
+                        int64_t groups, int lm, const uint32_t* m, uint32_t np,
+                        const uint32_t* ctab, uint32_t* w, uint32_t* t, int64_t t_ld,
+                        void* stream);
 /* Fixed-base table for 32-bit exponents: P[i*n + k] = bases[k]^(2^(8 i)) in
  * Montgomery form, i < 4. */
 int zpir_pow8_table(const uint32_t* bases, int64_t n, int limbs, const uint32_t* N, uint32_t np,

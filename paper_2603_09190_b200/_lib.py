@@ -45,17 +45,19 @@ _SIGS = {
     "zpir_umma_answer_rows_batch": ([_p, _c_i64, _c_i64, _p, _c_int, _c_int, _c_int, _p, _p],
                                     _c_int),
     "zpir_answer_groups_batch": ([_p, _c_i64, _p, _c_i64, _c_u32, _c_i64, _c_int, _c_i64, _c_int,
-                                  _p, _p, _p, _c_int, _p, _p, _c_i64, _c_int, _p], _c_int),
+                                  _p, _p, _p, _c_int, _p, _p, _c_i64, _c_int, _c_int, _p], _c_int),
     "zpir_multiexp_rows": ([_p, _c_i64, _p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
                             _p, _c_u32, _p, _p, _c_int, _p, _p, _c_i64, _p], _c_int),
-    "zpir_slot_combine": ([_p, _c_int, _p, _c_i64, _c_int, _p, _c_u32, _p, _p], _c_int),
+    "zpir_slot_combine": ([_p, _c_int, _p, _c_i64, _c_int, _p, _c_u32, _p, _c_int, _p, _p], _c_int),
+    "zpir_answer_general": ([_p, _p, _c_u32, _c_i64, _c_int, _c_i64, _c_int, _p, _c_u32, _p, _p, _p,
+                             _c_i64, _p], _c_int),
     "zpir_pow8_table": ([_p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p], _c_int),
     "zpir_slot_fixed": ([_p, _c_i64, _p, _c_i64, _p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p],
                         _c_int),
     "zpir_groups_z": ([_p, _c_i64, _c_i64, _c_int, _c_i64, _c_int, _p, _p, _p, _c_int, _p, _p,
-                       _c_i64, _c_int, _p], _c_int),
+                       _c_i64, _c_int, _c_int, _p], _c_int),
     "zpir_groups_finish": ([_p, _p, _c_i64, _c_u32, _c_i64, _c_int, _c_i64, _c_int, _p, _p, _c_i64,
-                            _c_int, _p], _c_int),
+                            _c_int, _c_int, _p], _c_int),
     "zpir_chacha_words32": ([ctypes.c_char_p, ctypes.c_char_p, _c_i64, _c_i64, _p, _c_i64, _c_u32,
                              _p], _c_int),
     "zpir_chacha_below": ([ctypes.c_char_p, _c_u32, ctypes.c_uint64, _c_i64, _p, _c_int, _c_int, _p,

@@ -96,6 +96,21 @@ class KeyCtx:
         self._dev = dev
         self._lock = threading.Lock()
 
+    def d_gamma_table(self, gamma: int, cap: int):
+        """{gamma^j R mod m, gamma^j R^2 mod m} for j < cap (general-gamma answers)."""
+        key = ("g", gamma, cap)
+        with self._lock:
+            t = self._rpow.get(key)
+            if t is None:
+                m, R = self.m, self.cm.R
+                vals = []
+                g = 1
+                for _ in range(cap):
+                    vals += [g * R % m, g * R * R % m]
+                    g = g * gamma % m
+                t = self._rpow[key] = self._dev(ints_to_limbs(vals, self.lm))
+            return t
+
     def d_rpow(self, nchunks: int):
         with self._lock:
             t = self._rpow.get(nchunks)

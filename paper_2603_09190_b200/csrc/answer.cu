@@ -126,6 +126,7 @@ struct GroupBatch {
   int64_t zq, bq, tq, mq, rq;
   const uint32_t* nps;     // per-query n' (nullptr: use np)
   const uint8_t* fast0s;   // per-query fast0 (nullptr: use fast0)
+  int stride = 1;          // slot stride in 32-bit limbs: gamma = 2^(32 stride)
 };
 
 template <int LPL, int NCH, bool WITH_B = true>
@@ -164,11 +165,13 @@ answer_groups_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict_
   }
   __syncthreads();
   // position sums X_P = b_P + sum_j z_j[P - j], split into lo/hi words
+  const int sd = bt.stride;
   for (int P = tid; P < NX; P += blockDim.x) {
-    unsigned long long s =
-        (WITH_B && P < nrows) ? (unsigned long long)(b[c0 + P] & qmask) : 0ull;
-    const int jlo = max(0, P - wz + 1), jhi = min(nrows - 1, P);
-    for (int j = jlo; j <= jhi; ++j) s += zs[j * wz + (P - j)];
+    unsigned long long s = (WITH_B && P % sd == 0 && P / sd < nrows)
+                               ? (unsigned long long)(b[c0 + P / sd] & qmask)
+                               : 0ull;
+    const int jlo = max(0, (P - wz + sd) / sd), jhi = min(nrows - 1, P / sd);
+    for (int j = jlo; j <= jhi; ++j) s += zs[j * wz + (P - sd * j)];
     lo[P] = (uint32_t)s;
     hi[P + 1] = (uint32_t)(s >> 32);
   }
@@ -247,12 +250,73 @@ groups_finish_kernel(const uint32_t* __restrict__ tz, const uint32_t* __restrict
 #pragma unroll
   for (int i = 0; i < LPL; ++i) {
     const int j = lane * LPL + i;
-    y[i] = (j < nrows) ? (b[c0 + j] & qmask) : 0u;
+    y[i] = (j % bt.stride == 0 && j / bt.stride < nrows) ? (b[c0 + j / bt.stride] & qmask) : 0u;
   }
   const uint32_t cy = big_add<LPL>(x, y, lane);
   big_cond_sub<LPL>(x, cy, n_, lane);
   uint32_t* out = t + g * t_ld;
   big_store<LPL>(out, x, lane);
+  for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
+}
+
+// ---- general gamma (not a power of 2^32): t_g = sum_j (gamma^j mod m)(b_c + z_c)
+// mod m (protocol.py:219-238, :259-269 with the reference's generic loops).
+// rows_weighted: one warp per row c = g*cap + j (< d1): u = z_c + (b_c & qmask)
+// as LM + 4 limbs, w_c = mont(u_lo, gamma^j R mod m) + mont(u_hi, gamma^j R^2
+// mod m) mod m with u = u_lo + R u_hi. ctab[j] = {gamma^j R, gamma^j R^2} mod m.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+rows_weighted_kernel(const uint32_t* __restrict__ z, const uint32_t* __restrict__ b,
+                     uint32_t qmask, int64_t d1, int cap, const uint32_t* __restrict__ mod,
+                     uint32_t np, const uint32_t* __restrict__ ctab, uint32_t* __restrict__ w) {
+  constexpr int LM = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= d1) return;
+  const int j = (int)(c % cap);
+  const uint32_t* zr = z + c * (LM + 4);
+  uint32_t n_[LPL], lo[LPL], hi[LPL], cc[LPL];
+  big_load<LPL>(n_, mod, lane);
+  big_load<LPL>(lo, zr, lane);
+#pragma unroll
+  for (int i = 0; i < LPL; ++i) {
+    const int li = lane * LPL + i;
+    hi[i] = (li < 4) ? zr[LM + li] : 0u;
+    cc[i] = (li == 0) ? (b[c] & qmask) : 0u;
+  }
+  const uint32_t cy = big_add<LPL>(lo, cc, lane);     // lo += b_c, carry into hi
+  big_set_small<LPL>(cc, cy, lane);
+  big_add<LPL>(hi, cc, lane);
+  big_load<LPL>(cc, ctab + (size_t)j * 2 * LM, lane);
+  mont_mul<LPL>(lo, lo, cc, n_, np, lane);
+  big_load<LPL>(cc, ctab + (size_t)j * 2 * LM + LM, lane);
+  mont_mul<LPL>(hi, hi, cc, n_, np, lane);
+  const uint32_t c2 = big_add<LPL>(lo, hi, lane);
+  big_cond_sub<LPL>(lo, c2, n_, lane);
+  big_store<LPL>(w + c * LM, lo, lane);
+}
+
+// t_g = sum_{j < rows of g} w[g*cap + j] mod m, one warp per group.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+group_sum_kernel(const uint32_t* __restrict__ w, int64_t d1, int cap, int64_t groups,
+                 const uint32_t* __restrict__ mod, uint32_t* __restrict__ t, int64_t t_ld) {
+  constexpr int LM = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (g >= groups) return;
+  const int64_t c0 = g * cap;
+  const int nrows = (int)(((int64_t)cap < d1 - c0) ? (int64_t)cap : d1 - c0);
+  uint32_t n_[LPL], acc[LPL], x[LPL];
+  big_load<LPL>(n_, mod, lane);
+  big_set_small<LPL>(acc, 0, lane);
+  for (int j = 0; j < nrows; ++j) {
+    big_load<LPL>(x, w + (c0 + j) * LM, lane);
+    const uint32_t cy = big_add<LPL>(acc, x, lane);
+    big_cond_sub<LPL>(acc, cy, n_, lane);
+  }
+  uint32_t* out = t + g * t_ld;
+  big_store<LPL>(out, acc, lane);
   for (int64_t i = LM + lane; i < t_ld; i += 32) out[i] = 0;
 }
 
@@ -330,7 +394,7 @@ static int answer_groups_launch_ex(const uint32_t* z, const uint32_t* b, uint32_
                                    const uint32_t* mod, uint32_t np, const uint32_t* rpow,
                                    int nchunks, int fast0, uint32_t* t, int64_t t_ld,
                                    cudaStream_t st, int nq, GroupBatch bt) {
-  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
+  if (lm % 32 || nchunks * lm < bt.stride * cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
       nchunks > 3) {
     set_error("answer_groups: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
     return kErrInput;
@@ -357,13 +421,15 @@ static int answer_groups_launch_ex(const uint32_t* z, const uint32_t* b, uint32_
 // Group stage without b (tz = (sum_j 2^(32j) z_c) mod m) and the finish stage.
 int groups_z_launch(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
                     const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
-                    const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, cudaStream_t st) {
-  if (lm % 32 || nchunks * lm < cap + lm + 4 || t_ld < lm || cap <= 0 || nchunks < 2 ||
-      nchunks > 3 || 32 * cap >= 32 * lm) {
-    set_error("groups_z: bad layout (lm=%d cap=%d nchunks=%d)", lm, cap, nchunks);
+                    const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, int stride,
+                    cudaStream_t st) {
+  if (lm % 32 || stride < 1 || nchunks * lm < stride * cap + lm + 4 || t_ld < lm || cap <= 0 ||
+      nchunks < 2 || nchunks > 3 || stride * cap >= lm) {
+    set_error("groups_z: bad layout (lm=%d cap=%d nchunks=%d stride=%d)", lm, cap, nchunks,
+              stride);
     return kErrInput;
   }
-  GroupBatch bt{zq, 0, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s};
+  GroupBatch bt{zq, 0, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s, stride};
   const dim3 grid((unsigned)groups, (unsigned)nq);
   const size_t zsm = (size_t)cap * (lm + 4) * sizeof(uint32_t);
 #define ZPIR_GZ(NCHV)                                                                          \
@@ -384,12 +450,12 @@ int groups_z_launch(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t 
 
 int groups_finish_launch(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
                          int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
-                         uint32_t* t, int64_t t_ld, int nq, cudaStream_t st) {
-  if (lm % 32 || t_ld < lm || cap > lm) {
+                         uint32_t* t, int64_t t_ld, int nq, int stride, cudaStream_t st) {
+  if (lm % 32 || t_ld < lm || stride < 1 || stride * cap > lm) {
     set_error("groups_finish: bad layout");
     return kErrInput;
   }
-  GroupBatch bt{0, bq, groups * t_ld, lm, 0, nullptr, nullptr};
+  GroupBatch bt{0, bq, groups * t_ld, lm, 0, nullptr, nullptr, stride};
   const dim3 grid((unsigned)ceil_div(groups, 4), (unsigned)nq);
   ZPIR_LPL_DISPATCH(lm / 32, {
     groups_finish_kernel<LPL><<<grid, 128, 0, st>>>(tz, b, qmask, d1, cap, groups, mods, t, t_ld,
@@ -403,8 +469,8 @@ int answer_groups_batch_launch(const uint32_t* z, int64_t zq, const uint32_t* b,
                                uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
                                const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
                                int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld,
-                               int nq, cudaStream_t st) {
-  GroupBatch bt{zq, bq, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s};
+                               int nq, int stride, cudaStream_t st) {
+  GroupBatch bt{zq, bq, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s, stride};
   return answer_groups_launch_ex(z, b, qmask, d1, cap, groups, lm, mods, 0, rpows, nchunks, 0, t,
                                  t_ld, st, nq, bt);
 }
@@ -415,6 +481,25 @@ int answer_groups_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, i
                          cudaStream_t st) {
   return answer_groups_launch_ex(z, b, qmask, d1, cap, groups, lm, mod, np, rpow, nchunks, fast0,
                                  t, t_ld, st, 1, GroupBatch{0, 0, 0, 0, 0, nullptr, nullptr});
+}
+
+// General-gamma group stage; w = workspace of d1 x lm limbs.
+int answer_general_launch(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1, int cap,
+                          int64_t groups, int lm, const uint32_t* mod, uint32_t np,
+                          const uint32_t* ctab, uint32_t* w, uint32_t* t, int64_t t_ld,
+                          cudaStream_t st) {
+  if (lm % 32 || t_ld < lm || cap <= 0 || d1 <= 0) {
+    set_error("answer_general: bad layout");
+    return kErrInput;
+  }
+  ZPIR_LPL_DISPATCH(lm / 32, {
+    rows_weighted_kernel<LPL><<<(unsigned)ceil_div(d1, 4), 128, 0, st>>>(z, b, qmask, d1, cap, mod,
+                                                                        np, ctab, w);
+    if (int e = check_launch("rows_weighted")) return e;
+    group_sum_kernel<LPL><<<(unsigned)ceil_div(groups, 4), 128, 0, st>>>(w, d1, cap, groups, mod,
+                                                                        t, t_ld);
+  });
+  return check_launch("group_sum");
 }
 
 int combine_launch(const uint32_t* t, const uint32_t* k, int64_t groups, int l2, const uint32_t* n2,

@@ -51,16 +51,19 @@ int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_
                          int64_t, int64_t, int, int, const uint32_t*, uint32_t, const uint32_t*,
                          const uint32_t*, int, uint32_t*, void*, int64_t, cudaStream_t);
 int slot_combine_launch(const uint32_t*, int, const int32_t*, int64_t, int, const uint32_t*,
-                        uint32_t, uint32_t*, cudaStream_t);
+                        uint32_t, const uint32_t*, int, uint32_t*, cudaStream_t);
+int answer_general_launch(const uint32_t*, const uint32_t*, uint32_t, int64_t, int, int64_t, int,
+                          const uint32_t*, uint32_t, const uint32_t*, uint32_t*, uint32_t*, int64_t,
+                          cudaStream_t);
 int pow8_table_launch(const uint32_t*, int64_t, int, const uint32_t*, uint32_t, const uint32_t*,
                       uint32_t*, cudaStream_t);
 int slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, const int32_t*, int64_t,
                       int, const uint32_t*, uint32_t, const uint32_t*, uint32_t*, cudaStream_t);
 int groups_z_launch(const uint32_t*, int64_t, int64_t, int, int64_t, int, const uint32_t*,
                     const uint32_t*, const uint32_t*, int, const uint8_t*, uint32_t*, int64_t, int,
-                    cudaStream_t);
+                    int, cudaStream_t);
 int groups_finish_launch(const uint32_t*, const uint32_t*, int64_t, uint32_t, int64_t, int, int64_t,
-                         int, const uint32_t*, uint32_t*, int64_t, int, cudaStream_t);
+                         int, const uint32_t*, uint32_t*, int64_t, int, int, cudaStream_t);
 int chacha_words32_launch(const uint8_t*, const uint8_t*, int64_t, int64_t, uint32_t*, int64_t,
                           uint32_t, cudaStream_t);
 int chacha_below_launch(const uint8_t*, uint32_t, uint64_t, int64_t, const uint32_t*, int, int,
@@ -74,7 +77,7 @@ int umma_answer_rows_batch_launch(const uint32_t*, int64_t, int64_t, const uint8
                                   uint32_t*, cudaStream_t);
 int answer_groups_batch_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, uint32_t, int64_t,
                                int, int64_t, int, const uint32_t*, const uint32_t*,
-                               const uint32_t*, int, const uint8_t*, uint32_t*, int64_t, int,
+                               const uint32_t*, int, const uint8_t*, uint32_t*, int64_t, int, int,
                                cudaStream_t);
 
 }  // namespace zpir
@@ -199,9 +202,9 @@ int zpir_answer_groups_batch(const uint32_t* z, int64_t zq, const uint32_t* b, i
                              uint32_t qmask, int64_t d1, int cap, int64_t groups, int lm,
                              const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows,
                              int nchunks, const uint8_t* fast0s, uint32_t* t, int64_t t_ld, int nq,
-                             void* stream) {
+                             int stride, void* stream) {
   ZPIR_GUARD(answer_groups_batch_launch(z, zq, b, bq, qmask, d1, cap, groups, lm, mods, nps, rpows,
-                                        nchunks, fast0s, t, t_ld, nq, S(stream)));
+                                        nchunks, fast0s, t, t_ld, nq, stride, S(stream)));
 }
 
 int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
@@ -216,8 +219,18 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
 }
 
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
-                      int limbs, const uint32_t* N, uint32_t np, uint32_t* out, void* stream) {
-  ZPIR_GUARD(slot_combine_launch(W, cap, group_ids, ngroups, limbs, N, np, out, S(stream)));
+                      int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
+                      int gamma_bits, uint32_t* out, void* stream) {
+  ZPIR_GUARD(slot_combine_launch(W, cap, group_ids, ngroups, limbs, N, np, gamma, gamma_bits, out,
+                                 S(stream)));
+}
+
+int zpir_answer_general(const uint32_t* z, const uint32_t* b, uint32_t qmask, int64_t d1, int cap,
+                        int64_t groups, int lm, const uint32_t* m, uint32_t np,
+                        const uint32_t* ctab, uint32_t* w, uint32_t* t, int64_t t_ld,
+                        void* stream) {
+  ZPIR_GUARD(answer_general_launch(z, b, qmask, d1, cap, groups, lm, m, np, ctab, w, t, t_ld,
+                                   S(stream)));
 }
 
 int zpir_pow8_table(const uint32_t* bases, int64_t n, int limbs, const uint32_t* N, uint32_t np,
@@ -234,15 +247,16 @@ int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t 
 
 int zpir_groups_z(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t groups, int lm,
                   const uint32_t* mods, const uint32_t* nps, const uint32_t* rpows, int nchunks,
-                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, void* stream) {
+                  const uint8_t* fast0s, uint32_t* tz, int64_t t_ld, int nq, int stride,
+                  void* stream) {
   ZPIR_GUARD(groups_z_launch(z, zq, d1, cap, groups, lm, mods, nps, rpows, nchunks, fast0s, tz, t_ld,
-                             nq, S(stream)));
+                             nq, stride, S(stream)));
 }
 
 int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32_t qmask,
                        int64_t d1, int cap, int64_t groups, int lm, const uint32_t* mods,
-                       uint32_t* t, int64_t t_ld, int nq, void* stream) {
-  ZPIR_GUARD(groups_finish_launch(tz, b, bq, qmask, d1, cap, groups, lm, mods, t, t_ld, nq,
+                       uint32_t* t, int64_t t_ld, int nq, int stride, void* stream) {
+  ZPIR_GUARD(groups_finish_launch(tz, b, bq, qmask, d1, cap, groups, lm, mods, t, t_ld, nq, stride,
                                   S(stream)));
 }
 

@@ -169,11 +169,17 @@ combine_windows_kernel(const uint32_t* __restrict__ W, const uint8_t* __restrict
 // Slot-decomposed hint: k_g = prod_j W[g*cap + j]^(2^(32 j)) mod N, with the
 // per-slot products W (Montgomery form) from a 32-bit multiexp per DB row.
 // Horner from the top slot: acc = acc^(2^32) * W_j. One warp per group.
+// Exponent of the Horner step (gamma), up to 256 bits, passed by value.
+struct GammaExp {
+  uint32_t w[8];
+  int nbits;
+};
+
 template <int LPL>
 __global__ void __launch_bounds__(128)
 slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __restrict__ group_ids,
                     int64_t ngroups, const uint32_t* __restrict__ N, uint32_t np,
-                    uint32_t* __restrict__ out) {
+                    uint32_t* __restrict__ out, GammaExp gm) {
   constexpr int L = 32 * LPL;
   const int lane = threadIdx.x & 31;
   const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -183,8 +189,14 @@ slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __re
   big_load<LPL>(n_, N, lane);
   const uint32_t* Wg = W + (size_t)g * cap * L;
   big_load<LPL>(acc, Wg + (size_t)(cap - 1) * L, lane);
+  uint32_t base[LPL];
   for (int j = cap - 2; j >= 0; --j) {
-    for (int s = 0; s < 32; ++s) mont_mul<LPL>(acc, acc, acc, n_, np, lane);
+    // acc = acc^gamma (left-to-right binary; gamma = 2^32 is 32 squarings)
+    big_copy<LPL>(base, acc);
+    for (int bit = gm.nbits - 2; bit >= 0; --bit) {
+      mont_mul<LPL>(acc, acc, acc, n_, np, lane);
+      if ((gm.w[bit >> 5] >> (bit & 31)) & 1u) mont_mul<LPL>(acc, acc, base, n_, np, lane);
+    }
     big_load<LPL>(x, Wg + (size_t)j * L, lane);
     mont_mul<LPL>(acc, acc, x, n_, np, lane);
   }
@@ -413,14 +425,18 @@ int slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t r
 }
 
 int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
-                        int limbs, const uint32_t* N, uint32_t np, uint32_t* out, cudaStream_t st) {
-  if (limbs % 32 || cap <= 0 || ngroups <= 0) {
-    set_error("slot_combine: bad shapes");
+                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
+                        int gamma_bits, uint32_t* out, cudaStream_t st) {
+  if (limbs % 32 || cap <= 0 || ngroups <= 0 || gamma_bits < 1 || gamma_bits > 256) {
+    set_error("slot_combine: bad shapes (gamma_bits=%d)", gamma_bits);
     return kErrInput;
   }
+  GammaExp gm{};
+  for (int i = 0; i < (gamma_bits + 31) / 32; ++i) gm.w[i] = gamma[i];
+  gm.nbits = gamma_bits;
   ZPIR_LPL_DISPATCH2(limbs / 32, {
-    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(W, cap, group_ids,
-                                                                            ngroups, N, np, out);
+    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
+        W, cap, group_ids, ngroups, N, np, out, gm);
   });
   return check_launch("slot_combine");
 }

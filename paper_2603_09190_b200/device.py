@@ -5,6 +5,8 @@ one extern "C" entry point on the caller's current stream. torch is used for
 device memory, streams and events only.
 """
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -183,11 +185,11 @@ def umma_answer_rows_batch(H, bc, lm, stream=None):
     return z
 
 
-def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None):
+def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None, stride=1):
     """z (nq, rows, lm+4), b (nq, rows); per-query Montgomery contexts."""
     nq, rows, wz = z.shape
     lm = kctxs[0].lm
-    nchunks = max(2, -(-(cap + lm + 4) // lm))
+    nchunks = max(2, -(-(stride * cap + lm + 4) // lm))
     dev = z.device
     mods = torch.stack([k.d_m for k in kctxs])
     rpows = torch.stack([k.d_rpow(nchunks) for k in kctxs])
@@ -196,7 +198,7 @@ def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None):
     t = torch.empty((nq, groups, t_ld), dtype=torch.int32, device=dev)
     _lib.call("zpir_answer_groups_batch", _lib.ptr(z), rows * wz, _lib.ptr(b), b.shape[1], qmask, d1,
               cap, groups, lm, _lib.ptr(mods), _lib.ptr(nps), _lib.ptr(rpows), nchunks, _lib.ptr(f0),
-              _lib.ptr(t), t_ld, nq, _s(stream))
+              _lib.ptr(t), t_ld, nq, stride, _s(stream))
     return t
 
 
@@ -214,11 +216,40 @@ def multiexp_rows(bases, E, row_ids, rows, rs, bs, ls, elimbs, kctx, out, keep_m
     return out
 
 
-def slot_combine(W, cap, group_ids, ngroups, kctx, out, stream=None):
+def slot_combine(W, cap, group_ids, ngroups, kctx, out, gamma=1 << 32, stream=None):
+    gw = np.frombuffer(int(gamma).to_bytes(32, "little"), dtype="<u4").copy()
     _lib.call("zpir_slot_combine", _lib.ptr(W), cap,
               _lib.ptr(group_ids) if group_ids is not None else None, ngroups, kctx.l2,
-              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(out), _s(stream))
+              _lib.ptr(kctx.d_m2), kctx.c2.np, gw.ctypes.data_as(ctypes.c_void_p),
+              int(gamma).bit_length(), _lib.ptr(out), _s(stream))
     return out
+
+
+def answer_general(z, b, qmask, d1, cap, groups, kctx, gamma, t_ld, stream=None):
+    """Group stage for a general batch scale gamma (per-row weights)."""
+    lm = kctx.lm
+    ctab = kctx.d_gamma_table(gamma, cap)
+    w = torch.empty((d1, lm), dtype=torch.int32, device=z.device)
+    t = torch.empty((groups, t_ld), dtype=torch.int32, device=z.device)
+    _lib.call("zpir_answer_general", _lib.ptr(z), _lib.ptr(b), qmask, d1, cap, groups, lm,
+              _lib.ptr(kctx.d_m), kctx.cm.np, _lib.ptr(ctab), _lib.ptr(w), _lib.ptr(t), t_ld,
+              _s(stream))
+    return t
+
+
+def answer_groups_strided(z, b, qmask, d1, cap, groups, kctx, t_ld, stride, stream=None):
+    """Positional group stage (gamma = 2^(32 stride)) for one query."""
+    lm = kctx.lm
+    nchunks = max(2, -(-(stride * cap + lm + 4) // lm))
+    rpow = kctx.d_rpow(nchunks)
+    nps = torch.tensor(np.array([kctx.cm.np], dtype=np.uint32).view(np.int32), device=z.device)
+    f0 = torch.tensor([1 if kctx.cm.R < 2 * kctx.m else 0], dtype=torch.uint8, device=z.device)
+    t = torch.empty((groups, t_ld), dtype=torch.int32, device=z.device)
+    rows, wz = z.shape
+    _lib.call("zpir_answer_groups_batch", _lib.ptr(z), rows * wz, _lib.ptr(b), b.shape[-1], qmask,
+              d1, cap, groups, lm, _lib.ptr(kctx.d_m), _lib.ptr(nps), _lib.ptr(rpow), nchunks,
+              _lib.ptr(f0), _lib.ptr(t), t_ld, 1, stride, _s(stream))
+    return t
 
 
 def rows_differ(a, b, stream=None):
@@ -251,19 +282,20 @@ def slot_fixed(P, n, E, rs, row_ids, rows, kctx, W, stream=None):
     return W
 
 
-def groups_z(z, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, tz, t_ld, stream=None):
+def groups_z(z, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, tz, t_ld, stream=None,
+             stride=1):
     rows, wz = z.shape[-2], z.shape[-1]
     nq = 1 if z.dim() == 2 else z.shape[0]
     _lib.call("zpir_groups_z", _lib.ptr(z), rows * wz, d1, cap, groups, lm, _lib.ptr(d_m),
               _lib.ptr(d_np), _lib.ptr(d_rpow), nchunks, _lib.ptr(d_f0), _lib.ptr(tz), t_ld, nq,
-              _s(stream))
+              stride, _s(stream))
     return tz
 
 
-def groups_finish(tz, b, qmask, d1, cap, groups, lm, d_m, t, t_ld, stream=None):
+def groups_finish(tz, b, qmask, d1, cap, groups, lm, d_m, t, t_ld, stream=None, stride=1):
     nq = 1 if b.dim() == 1 or b.shape[0] == 1 else b.shape[0]
     _lib.call("zpir_groups_finish", _lib.ptr(tz), _lib.ptr(b), b.shape[-1], qmask, d1, cap, groups,
-              lm, _lib.ptr(d_m), _lib.ptr(t), t_ld, nq, _s(stream))
+              lm, _lib.ptr(d_m), _lib.ptr(t), t_ld, nq, stride, _s(stream))
     return t
 
 

@@ -10,6 +10,8 @@ from dataclasses import dataclass
 import hashlib
 import math
 
+import numpy as np
+
 from .prg import Stream, DOM_PUBLIC_MATRIX, SEED_BYTES
 
 BINARY = "binary"
@@ -143,12 +145,18 @@ class Layout:
         self.gamma = select_scale(lwe, params.scale_regime)
         self.cap = capacity_of(params)
         self.groups = -(-self.d1 // self.cap)
-        if not (self.q == 1 << 32 and self.gamma == 1 << 32):
+        if self.q & (self.q - 1) or self.q > 1 << 32:
             raise NotImplementedError(
-                "the B200 path implements q = gamma = 2^32 (binary key, quarter-delta "
-                f"batching); got q=2^{self.q.bit_length() - 1}, gamma={self.gamma}. General "
-                "gamma is a planned extension (SURVEY 8f rank 4); there is no CPU fallback")
+                f"the B200 path needs q a power of two <= 2^32 (got q={self.q}); there is no "
+                "CPU fallback")
         self.qmask = (self.q - 1) & 0xFFFFFFFF
+        # slot stride of the positional group fold: gamma = 2^(32 s) (binary key,
+        # quarter-delta: s = 1; uniform key: s = 2); 0 = general gamma
+        self.stride = {1 << 32: 1, 1 << 64: 2}.get(self.gamma, 0)
+        self.gamma_words = np.frombuffer(self.gamma.to_bytes(32, "little"), dtype="<u4").copy() \
+            if self.gamma.bit_length() <= 256 else None
+        if self.gamma_words is None:
+            raise NotImplementedError("batch scale gamma wider than 256 bits")
         # device padding: DB rows (d1) to 128 and to whole groups; K (d0) to 64
         self.rows = _round_up(max(self.d1, self.groups * self.cap), 128)
         self.ld = _round_up(self.d0, 64)

@@ -266,8 +266,8 @@ class ServerGlobalState:
                 h = device.to_host_u32(self.H_dev[: lay.groups * lay.cap])
                 rows = []
                 for g in range(lay.groups):
-                    blk = np.ascontiguousarray(h[g * lay.cap:(g + 1) * lay.cap].astype("<u4").T)
-                    rows.append([int.from_bytes(blk[i].tobytes(), "little") for i in range(lay.n)])
+                    blk = h[g * lay.cap:(g + 1) * lay.cap]
+                    rows.append(_pack_slots(blk, lay))
                 self._H_scaled = rows
             return self._H_scaled
 
@@ -302,7 +302,7 @@ class ServerGlobalState:
         """Group b into d1' packed integers (protocol.py:259-269), host view."""
         lay = self.layout
         arr = np.asarray(b, dtype=np.uint64).astype("<u4")
-        return [int.from_bytes(arr[g * lay.cap:(g + 1) * lay.cap].tobytes(), "little")
+        return [_pack_slots(arr[g * lay.cap:(g + 1) * lay.cap, None], lay)[0]
                 for g in range(lay.groups)]
 
     def _workspace(self, lm):
@@ -329,7 +329,7 @@ class ServerGlobalState:
     def answer_plan(self, kctx, t_ld):
         """Per-thread captured plan for the tcgen05 path, or None."""
         if not (self.engine == "umma" and kctx.lm in device.UMMA_NB
-                and self.layout.qmask == 0xFFFFFFFF):
+                and self.layout.qmask == 0xFFFFFFFF and self.layout.stride == 1):
             return None
         plans = getattr(self._tls, "plans", None)
         if plans is None:
@@ -355,10 +355,23 @@ class ServerGlobalState:
         bc = device.build_bc_batch(cko_dev, lm, stream)
         z = device.umma_answer_rows_batch(self.H_dev, bc, lm, stream)
         t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctxs, t_ld,
-                                       stream)
+                                       stream, stride=lay.stride)
         if events:
             events[2].record(stream)
         return t
+
+    def _group_stage(self, z, b, kctx, t_ld, stream):
+        """t_g = sum_j gamma^j (b_c + z_c) mod m: positional fold for gamma =
+        2^32 / 2^64, per-row weights gamma^j mod m otherwise."""
+        lay = self.layout
+        if lay.stride == 1:
+            return device.answer_groups(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctx, t_ld,
+                                        stream=stream)
+        if lay.stride:
+            return device.answer_groups_strided(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctx,
+                                                t_ld, lay.stride, stream=stream)
+        return device.answer_general(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctx,
+                                     lay.gamma, t_ld, stream=stream)
 
     def answer_device(self, qu_dev, cko_dev, kctx, t_ld, stream, events=None):
         """t (groups x t_ld u32 limbs) for one staged query; all on device.
@@ -397,11 +410,26 @@ class ServerGlobalState:
             if events:
                 events[1].record(stream)
             z = device.answer_rows(self.H_dev, b[0], lay.qmask, cko_dev, lm, stream=stream)
-        t = device.answer_groups(z, b[0], lay.qmask, lay.d1, lay.cap, lay.groups, kctx, t_ld,
-                                 stream=stream)
+        t = self._group_stage(z, b[0], kctx, t_ld, stream)
         if events:
             events[2].record(stream)
         return t
+
+
+def _pack_slots(blk, lay) -> list:
+    """Columns of blk (rows j < cap, u32) as sum_j gamma^j blk[j] (protocol.py:219-238)."""
+    blk = np.asarray(blk, dtype="<u4")
+    if lay.stride:
+        w = np.zeros((blk.shape[1], blk.shape[0] * lay.stride), dtype="<u4")
+        w[:, :: lay.stride] = blk.T
+        return [int.from_bytes(w[i].tobytes(), "little") for i in range(w.shape[0])]
+    out = []
+    for i in range(blk.shape[1]):
+        acc = 0
+        for v in blk[::-1, i]:
+            acc = acc * lay.gamma + int(v)
+        out.append(acc)
+    return out
 
 
 def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
@@ -414,12 +442,12 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups
     (protocol.py:291-296; paillier_matmul / multiexp, paillier.py:134-203).
 
-    Computed through the slot decomposition: with gamma = 2^32,
-    H_scaled[g][k] = sum_j 2^(32j) H[g*cap+j][k], so
-    k_g = prod_j W[g*cap+j]^(2^(32 j)) with W[c] = prod_k ck_r[k]^H[c][k].
+    Computed through the slot decomposition: H_scaled[g][k] = sum_j gamma^j
+    H[g*cap+j][k], so k_g = prod_j W[g*cap+j]^(gamma^j) with
+    W[c] = prod_k ck_r[k]^H[c][k].
     Each W[c] (32-bit exponents) is one fixed-base Pippenger over the table
     P[i][k] = ck_r[k]^(2^(8i)) (255 buckets, 4n digits); the groups are then
-    recombined by Horner (slot_combine). Same group element as the
+    recombined by Horner in gamma (slot_combine). Same group element as the
     reference's windowed multiexp, canonical mod m^2. keep_slots=True keeps W
     and P on the device for refresh_hint."""
     lay = state.layout
@@ -434,7 +462,7 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     P = device.pow8_table(bases, kctx, stream)
     device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
     out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
-    device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, stream)
+    device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, lay.gamma, stream)
     entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
     counters.bump("group_mult", lay.groups * lay.n)
     return ClientHint(query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
@@ -447,7 +475,7 @@ def _refresh_device(state, kctx, old, rows, rid, gid, ngroups, stream):
     k = old.dev.clone()
     if rows:
         device.slot_fixed(old.bases, lay.n, state.H_dev, lay.n, rid, rows, kctx, W, stream)
-        device.slot_combine(W, lay.cap, gid, ngroups, kctx, k, stream)
+        device.slot_combine(W, lay.cap, gid, ngroups, kctx, k, lay.gamma, stream)
     return W, k
 
 
@@ -660,7 +688,7 @@ def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
         kctxs.append(key_ctx(reg.pk.m, dev))
     if not qmsgs:
         return []
-    umma_ok = (state.engine == "umma" and lay.qmask == 0xFFFFFFFF
+    umma_ok = (state.engine == "umma" and lay.qmask == 0xFFFFFFFF and lay.stride > 0
                and all(k.lm == kctxs[0].lm for k in kctxs) and kctxs[0].lm in device.UMMA_NB)
     if not umma_ok:
         return [respond(state, r, q, mode=md, stream=stream)

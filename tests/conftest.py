@@ -73,8 +73,11 @@ class Golden:
         return mod.ProtocolParams(**kw)
 
 
-GPU_CASES = ["desk_reduced", "ragged", "zero_db", "max_db", "tiny"]
-ALL_CASES = ["toy"] + GPU_CASES
+# batch scale gamma != 2^32: toy/standard32 (standard regime, general gamma),
+# uniform_key (gamma = 2^64), q16 (q = gamma = 2^16)
+GAMMA_CASES = ["toy", "uniform_key", "standard32", "q16"]
+GPU_CASES = ["desk_reduced", "ragged", "zero_db", "max_db", "tiny"] + GAMMA_CASES
+ALL_CASES = GPU_CASES
 
 
 @pytest.fixture(scope="session")

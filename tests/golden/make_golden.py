@@ -165,10 +165,28 @@ def prg_cases():
         json.dump(out, f, indent=1)
 
 
+def gamma_cases():
+    """Batch scales other than 2^32 (compress.py:36-43): uniform key with
+    quarter-delta (gamma = q^2 = 2^64), standard regime (gamma = q + n q),
+    and q < 2^32 (gamma = q = 2^16)."""
+    protocol_case("uniform_key", dict(n=32, q=1 << 32, p=256, noise_sigma=6.4,
+                                      key_dist="uniform"), 40, 70, 1024, seed=21)
+    protocol_case("standard32", dict(n=16, q=1 << 32, p=256, noise_sigma=6.4,
+                                     key_dist="binary"), 48, 90, 1024, seed=22,
+                  scale_regime="standard")
+    protocol_case("q16", dict(n=32, q=1 << 16, p=16, noise_sigma=1.0, key_dist="binary"),
+                  64, 100, 1024, seed=23)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-tiny", action="store_true")
+    ap.add_argument("--gamma-only", action="store_true",
+                    help="only the batch-scale cases (gamma != 2^32)")
     args = ap.parse_args()
+    gamma_cases()
+    if args.gamma_only:
+        return
     prg_cases()
     multiexp_cases()
     # reference's toy fixture (tests/test_protocol.py:12-19): standard regime

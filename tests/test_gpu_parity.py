@@ -97,7 +97,7 @@ def test_respond_separate_and_combined(z, golden, name):
                           k=[c.c for c in r.k]) == list(g.arr["record"])
 
 
-@pytest.mark.parametrize("name", ["ragged", "tiny"])
+@pytest.mark.parametrize("name", ["ragged", "tiny", "uniform_key", "standard32"])
 def test_cuda_core_engine_bit_exact(z, golden, name):
     """The CUDA-core engine (IDP4A GEMV, IMAD hint and compression) -- the
     measured alternative to the tcgen05 path -- matches the reference too."""
@@ -259,3 +259,18 @@ def test_respond_batch_bit_exact(z, golden, nq):
     else:
         k = [c.c for c in regs[-1].hints[0].entries]
         assert [c.c for c in got[-1].k] == ref.combined(t, k, sk.m)
+
+
+@pytest.mark.parametrize("name", ["toy", "uniform_key", "standard32", "q16"])
+def test_respond_batch_general_gamma(z, golden, name):
+    """Batch scales other than 2^32 through respond_batch (strided positional
+    fold for gamma = 2^64, per-row weights otherwise) equal the reference."""
+    g = golden(name)
+    st = _state(z, g)
+    reg = _reg(z, g)
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(k) for k in g.ints("k")])
+    qs = [z.QueryMessage(reg.client_id, 0, md, g.ints("ck_o"), g.arr["qu0"])
+          for md in (z.SEPARATE, z.COMBINED, z.SEPARATE)]
+    got = z.respond_batch(st, [reg] * 3, qs)
+    assert got[0].t == g.ints("t") and got[2].t == g.ints("t")
+    assert [c.c for c in got[1].k] == g.ints("K")

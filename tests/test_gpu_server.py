@@ -57,7 +57,7 @@ def test_server_update_and_regenerate():
         srv.close()
 
 
-@pytest.mark.parametrize("name", ["ragged", "tiny"])
+@pytest.mark.parametrize("name", ["ragged", "tiny", "uniform_key", "standard32", "q16"])
 def test_incremental_update_bit_exact(golden, name):
     """updated() + refresh_hint() == full rebuild + full hint, bit for bit."""
     import paper_2603_09190_b200 as z
@@ -74,7 +74,7 @@ def test_incremental_update_bit_exact(golden, name):
     rows = sorted(set(rng.choice(g.d1, size=max(1, g.d1 // 100), replace=False).tolist())
                   | {0, g.d1 - 1})
     for c in rows:
-        db2[:, c] = rng.integers(0, 256, g.d0, dtype=np.uint8)
+        db2[:, c] = rng.integers(0, g.lwe["p"], g.d0, dtype=np.uint8)
     st2, changed = st.updated(db2)
     full = z.ServerGlobalState(params, db2, db_version=1)
     assert st2.db_version == 1

@@ -61,7 +61,8 @@ def test_answer_and_combined(golden, name):
     assert ref.combined(t, g.ints("k"), g.m) == g.ints("K")
 
 
-@pytest.mark.parametrize("name", ["toy", "desk_reduced", "zero_db", "ragged", "max_db"])
+@pytest.mark.parametrize("name", ["toy", "desk_reduced", "zero_db", "ragged", "max_db",
+                                  "uniform_key", "standard32", "q16"])
 def test_hint_entries(golden, name):
     g = golden(name)
     lw = g.lwe
