@@ -19,8 +19,28 @@ _c_int = ctypes.c_int
 _c_u32 = ctypes.c_uint32
 _p = ctypes.c_void_p
 
+class DbParams(ctypes.Structure):
+    """zpir_db_params (include/zippir_db.h)."""
+    _fields_ = [("d0", ctypes.c_int64), ("d1", ctypes.c_int64), ("n", ctypes.c_int64),
+                ("log2q", ctypes.c_int32), ("p", ctypes.c_int32), ("cap", ctypes.c_int32),
+                ("gamma_bits", ctypes.c_int32), ("gamma", ctypes.c_uint32 * 8),
+                ("device", ctypes.c_int32), ("engine", ctypes.c_int32)]
+
+
 _SIGS = {
     "zpir_abi_version": ([], _c_int),
+    # handle-level ABI (include/zippir_db.h), host buffers
+    "zpir_db_create": ([ctypes.POINTER(DbParams), _p, _c_i64, _p, _p, ctypes.POINTER(_p)], _c_int),
+    "zpir_db_destroy": ([_p], _c_int),
+    "zpir_db_info": ([_p, ctypes.POINTER(_c_i64), ctypes.POINTER(_c_i64)], _c_int),
+    "zpir_db_global_hint": ([_p, _p], _c_int),
+    "zpir_db_matvec": ([_p, _p, _c_i64, _p], _c_int),
+    "zpir_db_answer": ([_p, _p, _p, _p, _c_int, _p], _c_int),
+    "zpir_db_answer_combined": ([_p, _p, _p, _p, _c_int, _p, _p], _c_int),
+    "zpir_db_client_hint": ([_p, _p, _c_int, _p, _c_i64, ctypes.c_uint64, _p], _c_int),
+    "zpir_db_update_rows": ([_p, _p, _c_i64, _p], _c_int),
+    "zpir_montmul_batch": ([_p, _p, _c_i64, _p, _c_int, _p, _c_int], _c_int),
+    "zpir_multiexp_batch": ([_p, _c_i64, _p, _c_i64, _c_int, _p, _c_int, _p, _c_int], _c_int),
     "zpir_last_error": ([], ctypes.c_char_p),
     "zpir_transpose_db": ([_p, _c_i64, _c_i64, _c_i64, _p, _c_i64, _c_i64, _p], _c_int),
     "zpir_global_hint": ([_p, _c_i64, _c_i64, _p, _c_i64, _c_i64, _p, _c_u32, _p], _c_int),

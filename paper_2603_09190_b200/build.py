@@ -12,7 +12,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libzpir_b200.so")
-SOURCES = ["capi.cu", "gemv.cu", "hint_gemm.cu", "answer.cu", "multiexp.cu", "umma_gemm.cu", "probe.cu", "chacha.cu", "conv.cu"]
+SOURCES = ["capi.cu", "gemv.cu", "hint_gemm.cu", "answer.cu", "multiexp.cu", "umma_gemm.cu",
+           "probe.cu", "chacha.cu", "conv.cu", "db_handle.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -28,7 +29,8 @@ def needs_build():
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(HERE, "..", "include", "zippir_b200.h"))
+    inc = os.path.join(HERE, "..", "include")
+    deps += [os.path.join(inc, f) for f in os.listdir(inc)]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 

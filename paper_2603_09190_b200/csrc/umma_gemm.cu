@@ -512,7 +512,7 @@ int umma_hint_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t
   return umma_run<256, kLimbRowsNeg>(dbt, rows, ld, ld, aplanes, 4 * n, ld, a, st);
 }
 
-// z[r * wz + i] = limbs of (b[r] & qmask) + sum_k H[r,k] ck_o[k]; bc from build_bc.
+// z[r * wz + i] = limbs of sum_k H[r,k] ck_o[k] (b is added by the group stage); bc from build_bc.
 int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const uint8_t* bc, int nb,
                             const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
                             cudaStream_t st) {

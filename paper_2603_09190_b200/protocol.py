@@ -328,7 +328,7 @@ class ServerGlobalState:
 
     def answer_plan(self, kctx, t_ld):
         """Per-thread captured plan for the tcgen05 path, or None."""
-        if not (self.engine == "umma" and kctx.lm in device.UMMA_NB
+        if not (self.engine == "umma" and kctx.lm in device.UMMA_NB and self.layout.n % 4 == 0
                 and self.layout.qmask == 0xFFFFFFFF and self.layout.stride == 1):
             return None
         plans = getattr(self._tls, "plans", None)
@@ -384,7 +384,7 @@ class ServerGlobalState:
         if events:
             events[0].record(stream)
         if (self.engine == "umma" and lm in device.UMMA_NB and qu_dev.shape[0] == 1
-                and lay.qmask == 0xFFFFFFFF):
+                and lay.qmask == 0xFFFFFFFF and lay.n % 4 == 0):
             w = self._workspace(lm)
             side = w["side"]
             split = COMPRESS_CTAS > 0
@@ -689,6 +689,7 @@ def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
     if not qmsgs:
         return []
     umma_ok = (state.engine == "umma" and lay.qmask == 0xFFFFFFFF and lay.stride > 0
+               and lay.n % 4 == 0
                and all(k.lm == kctxs[0].lm for k in kctxs) and kctxs[0].lm in device.UMMA_NB)
     if not umma_ok:
         return [respond(state, r, q, mode=md, stream=stream)

@@ -41,3 +41,30 @@ def test_status_codes_without_gpu():
         # rows not a multiple of 128
         _lib.call("zpir_gemv", None, 100, 64, None, 1, None, 0xFFFFFFFF, None, None)
     assert b"multiple of 128" in _lib.lib().zpir_last_error()
+
+
+def test_handle_api_validates_before_cuda():
+    """zpir_db_create rejects bad parameters / symbols with status 1 on CPU."""
+    import ctypes
+    import numpy as np
+    import pytest
+    from paper_2603_09190_b200 import _lib
+    _lib.load()
+    prm = _lib.DbParams()
+    prm.d0, prm.d1, prm.n, prm.log2q, prm.p, prm.cap, prm.gamma_bits = 4, 4, 4, 32, 4, 9, 33
+    prm.gamma[1] = 1
+    db = np.full((4, 4), 7, dtype=np.uint8)        # 7 >= p = 4
+    h = ctypes.c_void_p()
+    seed = np.zeros(16, dtype=np.uint8)
+    args = (ctypes.byref(prm), db.ctypes.data_as(ctypes.c_void_p), 4, None,
+            seed.ctypes.data_as(ctypes.c_void_p), ctypes.byref(h))
+    with pytest.raises(ValueError, match="symbol out of range"):
+        _lib.call("zpir_db_create", *args)
+    db[:] = 1
+    prm.gamma_bits = 40                            # inconsistent with gamma
+    with pytest.raises(ValueError, match="gamma_bits"):
+        _lib.call("zpir_db_create", *args)
+    prm.gamma_bits, prm.log2q = 33, 40
+    with pytest.raises(ValueError, match="bad parameters"):
+        _lib.call("zpir_db_create", *args)
+    assert _lib.lib().zpir_db_destroy(None) == 0

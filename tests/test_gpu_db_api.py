@@ -1,0 +1,120 @@
+"""GPU parity through the handle-level C ABI (include/zippir_db.h) with host
+buffers only (numpy in, numpy out; no torch on this path).
+
+Same golden outputs of the unmodified reference as test_gpu_parity.py:
+H, b, t, COMBINED K, hint entries k, the multiexp KATs; plus the row update
+against a fresh build and the oracle for batched matvec.
+"""
+
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, GPU_CASES
+from oracle import client, ref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2603_09190_b200 import _lib, build, dbapi
+    build.build()
+    _lib.load()
+    return dbapi
+
+
+def _params(g):
+    import paper_2603_09190_b200 as z
+    return g.params(z)
+
+
+@pytest.mark.parametrize("name", GPU_CASES)
+def test_handle_api_golden(api, golden, name):
+    g = golden(name)
+    with api.DeviceDatabase(_params(g), g.db) as d:
+        assert d.groups == g.groups
+        H = d.global_hint()
+        if "H" in g.arr:
+            assert np.array_equal(H.astype(np.uint64), g.arr["H"])
+        assert np.array_equal(d.db_matvec(g.arr["qu0"]), g.arr["b"])
+        assert d.answer(g.arr["qu0"], g.ints("ck_o"), g.m) == g.ints("t")
+        assert d.answer_combined(g.arr["qu0"], g.ints("ck_o"), g.m, g.ints("k")) == g.ints("K")
+        assert d.client_hint(g.m, g.seed, 0) == g.ints("k")
+
+
+@pytest.mark.parametrize("name", ["ragged", "standard32", "toy"])
+def test_handle_api_cuda_core_and_explicit_A(api, golden, name):
+    g = golden(name)
+    A = ref.public_matrix(b"\x00" * 16, g.d0, g.lwe["n"], g.lwe["q"])
+    with api.DeviceDatabase(_params(g), g.db, A=A, engine="cuda_core") as d:
+        assert np.array_equal(d.db_matvec(g.arr["qu0"]), g.arr["b"])
+        assert d.answer(g.arr["qu0"], g.ints("ck_o"), g.m) == g.ints("t")
+        assert d.client_hint(g.m, g.seed, 0) == g.ints("k")
+
+
+@pytest.mark.parametrize("name", ["ragged", "uniform_key"])
+def test_handle_api_update_rows(api, golden, name):
+    g = golden(name)
+    params = _params(g)
+    rng = np.random.default_rng(5)
+    cols = np.array(sorted({0, g.d1 - 1, *rng.choice(g.d1, 7, replace=False).tolist()}))
+    vals = rng.integers(0, g.lwe["p"], (cols.size, g.d0), dtype=np.uint8)
+    db2 = np.array(g.db, dtype=np.uint8, copy=True)
+    db2[:, cols] = vals.T
+    with api.DeviceDatabase(params, g.db) as d, api.DeviceDatabase(params, db2) as fresh:
+        d.update_rows(cols, vals)
+        assert np.array_equal(d.global_hint(), fresh.global_hint())
+        qu = g.arr["qu0"]
+        assert np.array_equal(d.db_matvec(qu), ref.db_matvec(db2, qu, g.lwe["q"]))
+        assert d.answer(qu, g.ints("ck_o"), g.m) == fresh.answer(qu, g.ints("ck_o"), g.m)
+        assert d.client_hint(g.m, g.seed, 3) == fresh.client_hint(g.m, g.seed, 3)
+        with pytest.raises(ValueError):
+            d.update_rows([g.d1], vals[:1])
+
+
+def test_handle_api_batched_matvec(api, golden):
+    g = golden("ragged")
+    rng = np.random.default_rng(1)
+    Q = rng.integers(0, 1 << 32, (70, g.d0), dtype=np.uint64)   # 64 + 6: two passes
+    with api.DeviceDatabase(_params(g), g.db) as d:
+        B = d.db_matvec(Q)
+    for v in (0, 33, 63, 64, 69):
+        assert np.array_equal(B[v], ref.db_matvec(g.db, Q[v], 1 << 32)), v
+
+
+def test_handle_api_errors(api, golden):
+    g = golden("q16")                                  # p = 16: symbols 16..255 are invalid
+    bad = np.array(g.db, dtype=np.uint8, copy=True)
+    bad[0, 0] = g.lwe["p"]
+    with pytest.raises(ValueError, match="symbol out of range"):
+        api.DeviceDatabase(_params(g), bad)
+    with pytest.raises(ValueError):
+        api.DeviceDatabase(_params(g), g.db[:, :-1])
+    with api.DeviceDatabase(_params(g), g.db) as d:
+        with pytest.raises(ValueError):
+            d.answer(g.arr["qu0"][:-1], g.ints("ck_o"), g.m)
+        with pytest.raises(ValueError, match="odd"):
+            d.answer(g.arr["qu0"], g.ints("ck_o"), g.m + 1)
+
+
+def test_multiexp_and_montmul_batch_kat(api):
+    with open(os.path.join(GOLDEN, "multiexp_kat.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        m = int(c["m"], 16)
+        bases = [int(x, 16) for x in c["bases"]]
+        exps = [int(x, 16) for x in c["exps"]]
+        got = api.multiexp_batch(bases, [exps, exps[::-1]], m * m)
+        assert got[0] == int(c["result"], 16), (c["bits"], c["tag"])
+        assert got[1] == ref.multiexp(m * m, bases, exps[::-1]), (c["bits"], c["tag"])
+    rng = random.Random(3)
+    for bits in (64, 1024, 2048):          # N = m^2: 128 .. 4096 bits
+        sk = client.keygen(bits, rng)
+        N = sk.m * sk.m
+        a = [rng.randrange(N) for _ in range(50)]
+        b = [rng.randrange(N) for _ in range(50)]
+        assert api.montmul_batch(a, b, N) == [x * y % N for x, y in zip(a, b)]
