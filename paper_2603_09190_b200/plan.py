@@ -140,6 +140,12 @@ class AnswerPlan:
             device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
             self._compress(stream, self.ctas)
             self._groups_z(stream)
+        elif which == "side_limbs":
+            # respond_wire(), side stream: ck_o limbs already staged
+            self._compress(stream, self.ctas)
+            self._groups_z(stream)
+        elif which == "finish":
+            self._finish(stream)
         elif which == "finish_digits":
             self._finish(stream)
             device.limbs_to_digits(self.t, self.kctx.lm, self.d_td, stream)

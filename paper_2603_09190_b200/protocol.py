@@ -655,6 +655,80 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     return out
 
 
+def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_bytes, qu,
+                 stream=None):
+    """respond() on fixed-width wire fields, without Python ints
+    (protocol.py:333-365 + wire.py:141-193).
+
+    ck_bytes: (n, w) uint8 little-endian magnitudes (w <= limb bytes of m,
+    as wire.decode_query returns them); qu: (d0,) integers. Returns the
+    result as (d1', L) u32 limb rows -- t for SEPARATE, K for COMBINED --
+    for wire.field_rows. Same validation and exceptions as respond()."""
+    lay = state.layout
+    ck_bytes = np.asarray(ck_bytes)
+    qu = np.asarray(qu)
+    if ck_bytes.ndim != 2 or ck_bytes.shape[0] != lay.n or qu.shape != (lay.d0,):
+        raise ValueError("query dimensions do not match the parameters")
+    stored = reg.hints.get(query_index)
+    if stored is None or stored.db_version != state.db_version:
+        raise KeyError("no hint for this query index and database version")
+    if mode not in (SEPARATE, COMBINED):
+        raise ValueError("unknown response mode")
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    kctx = key_ctx(reg.pk.m, dev)
+    w = ck_bytes.shape[1]
+    if w > 4 * kctx.lm:
+        raise ValueError("ck_o field wider than the modulus")
+    t_ld = kctx.lm if mode == SEPARATE else kctx.l2
+    plan = state.answer_plan(kctx, t_ld)
+    if plan is None or plan.ctas <= 0:
+        ck = np.zeros((lay.n, 4 * kctx.lm), dtype=np.uint8)
+        ck[:, :w] = ck_bytes
+        q32 = np.zeros(lay.ld, dtype=np.uint32)
+        np.copyto(q32[: lay.d0], qu, casting="unsafe")
+        qd = _h2d(q32, dev, "qu", stream).view(torch.int32).reshape(1, lay.ld)
+        cko = _h2d(ck.view("<u4"), dev, "cko", stream).view(torch.int32).reshape(lay.n, kctx.lm)
+        t_dev = state.answer_device(qd, cko, kctx, t_ld, stream)
+        if mode == COMBINED:
+            t_dev = device.combine(t_dev, _stored_device(stored, kctx, dev, stream), kctx,
+                                   stream=stream)
+        out = _d2h_u32(t_dev, "t", stream)
+    else:
+        plan.set_key(kctx, stream)
+        hq = plan.h_qu.numpy().view(np.uint32)
+        np.copyto(hq[: lay.d0], qu, casting="unsafe")
+        device.h2d_async(plan.qu, plan.h_qu, stream)
+        plan.ev_in.record(stream)
+        plan.run("gemv_part", stream)
+        # meanwhile: ck_o bytes -> pinned limb rows -> side stream compression
+        hc = plan.h_cko.numpy().view(np.uint8).reshape(lay.n, 4 * kctx.lm)
+        if getattr(plan, "_ck_w", None) != w:
+            hc[:] = 0
+            plan._ck_w = w
+        hc[:, :w] = ck_bytes
+        side = plan.side
+        side.wait_event(plan.ev_in)
+        device.h2d_async(plan.cko, plan.h_cko, side)
+        plan.run("side_limbs", side)
+        stream.wait_stream(side)
+        plan.run("finish", stream)
+        if mode == COMBINED:
+            K = device.combine(plan.t, _stored_device(stored, kctx, dev, stream), kctx,
+                               stream=stream)
+            device.d2h_async(plan.h_K, K, stream)
+            h_out = plan.h_K
+        else:
+            device.d2h_async(plan.h_t, plan.t, stream)
+            h_out = plan.h_t
+        stream.synchronize()
+        out = h_out.numpy().view(np.uint32)
+    if mode == COMBINED:
+        counters.bump("add", lay.groups)
+        counters.bump("group_mult", lay.groups)
+    return out
+
+
 MAX_BATCH = 64
 
 

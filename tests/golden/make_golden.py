@@ -165,6 +165,48 @@ def prg_cases():
         json.dump(out, f, indent=1)
 
 
+def wire_cases(names=("desk_reduced", "toy", "q16", "ragged")):
+    """Reference wire bodies (wire.py:128-206) for the golden queries/answers:
+    query bodies (both modes), response bodies, hint request, and a body with
+    non-canonical widths that only the generic decoder accepts."""
+    from zippir import wire
+    from zippir.paillier import PaillierPublicKey
+    for name in names:
+        meta = json.load(open(os.path.join(HERE, f"{name}.json")))
+        arr = np.load(os.path.join(HERE, f"{name}.npz"))
+        ints = lambda k: [int.from_bytes(r.tobytes(), "little") for r in arr[k]]
+        lw = meta["lwe"]
+        kw = dict(lwe=LweParams(**lw), d0=meta["d0"], d1=meta["d1"],
+                  paillier_bits=meta["paillier_bits"], scale_regime=meta["scale_regime"])
+        params = ProtocolParams(**kw)
+        lay = wire.Layout(params.paillier_bits, lw["n"], lw["q"].bit_length() - 1,
+                          params.d0, params.d1_prime)
+        m = int(meta["m"], 16)
+        pk = PaillierPublicKey(m, m.bit_length())
+        cid = client_id_of(pk)
+        qu0 = [int(x) for x in arr["qu0"]]
+        out = dict(
+            params_hash=np.frombuffer(params.params_hash(), np.uint8),
+            client_id=np.frombuffer(cid, np.uint8),
+            hint_request=np.frombuffer(wire.encode_hint_request(
+                lay, m, bytes.fromhex(meta["client_seed"])), np.uint8),
+            query_sep=np.frombuffer(wire.encode_query(lay, cid, 0, 0, ints("ck_o"), qu0), np.uint8),
+            query_comb=np.frombuffer(wire.encode_query(lay, cid, 0, 1, ints("ck_o"), qu0), np.uint8),
+            resp_sep=np.frombuffer(wire.encode_response_separate(lay, 0, ints("t"), ints("k")),
+                                   np.uint8),
+            resp_comb=np.frombuffer(wire.encode_response_combined(lay, 0, ints("K")), np.uint8),
+        )
+        # minimal-width integers: valid for the reference's prefixed decoder
+        from zippir.serial import encode_bigint
+        import struct
+        body = cid + struct.pack("<QB", 0, 0) + b"".join(encode_bigint(v) for v in ints("ck_o")) \
+            + b"".join(encode_bigint(v) for v in qu0)
+        assert wire.decode_query(lay, body)[3] == ints("ck_o")
+        out["query_sep_minimal"] = np.frombuffer(body, np.uint8)
+        np.savez_compressed(os.path.join(HERE, f"wire_{name}.npz"), **out)
+    print("wire fixtures:", names, flush=True)
+
+
 def gamma_cases():
     """Batch scales other than 2^32 (compress.py:36-43): uniform key with
     quarter-delta (gamma = q^2 = 2^64), standard regime (gamma = q + n q),
@@ -181,9 +223,13 @@ def gamma_cases():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-tiny", action="store_true")
+    ap.add_argument("--wire-only", action="store_true", help="only the wire fixtures")
     ap.add_argument("--gamma-only", action="store_true",
                     help="only the batch-scale cases (gamma != 2^32)")
     args = ap.parse_args()
+    if args.wire_only:
+        wire_cases()
+        return
     gamma_cases()
     if args.gamma_only:
         return
@@ -214,6 +260,7 @@ def main():
         protocol_case("tiny", dict(n=1024, q=1 << 32, p=256, noise_sigma=6.4,
                                    key_dist="binary"), d0, d1, 2048, seed=2048,
                       db=db, store_full=False)
+    wire_cases()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,60 @@
+"""PirServer.handle_frame on the GPU: reference-encoded request frames in,
+reply frames byte-identical to the reference encoder's out (fast fixed-width
+path and the generic fallback), plus the error mapping (server.py:128-208)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["desk_reduced", "toy", "q16", "ragged"])
+def test_handle_frame_bytes_match_reference(golden, name):
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import wire
+    from paper_2603_09190_b200.server import PirServer
+    g = golden(name)
+    fx = dict(np.load(os.path.join(GOLDEN, f"wire_{name}.npz")))
+    ph = fx["params_hash"].tobytes()
+    srv = PirServer(g.params(z), g.db)
+    try:
+        pf = lambda t, b: wire.pack_frame(t, ph, b)
+        q = pf(wire.MSG_QUERY, fx["query_sep"].tobytes())[4:]
+        # unknown client -> ERR_STATE
+        r = srv.handle_frame(q)
+        assert r[5] == wire.MSG_ERROR and int.from_bytes(r[38:42], "little") == wire.ERR_STATE
+        assert srv.handle_frame(pf(wire.MSG_HINT_REQUEST, fx["hint_request"].tobytes())[4:]) == \
+            pf(wire.MSG_ACK, b"")
+        srv.wait_for_hints(timeout=120)
+        want_sep = pf(wire.MSG_RESPONSE_SEPARATE, fx["resp_sep"].tobytes())
+        want_comb = pf(wire.MSG_RESPONSE_COMBINED, fx["resp_comb"].tobytes())
+        for _ in range(2):                       # graph capture, then replay
+            assert srv.handle_frame(q) == want_sep
+            assert srv.handle_frame(pf(wire.MSG_QUERY, fx["query_comb"].tobytes())[4:]) == want_comb
+        assert srv.handle_frame(pf(wire.MSG_QUERY, fx["query_sep_minimal"].tobytes())[4:]) == want_sep
+        # a reference Frame-like object works too
+        fr = wire.unpack_frame(q)
+        assert srv.handle_frame(fr) == want_sep
+        # hint transfer: the stored k, then single-use -> ERR_INPUT (ValueError)
+        cid = fx["client_id"].tobytes()
+        ht = pf(wire.MSG_HINT_TRANSFER, cid + (0).to_bytes(8, "little"))[4:]
+        k_body = fx["resp_comb"].tobytes()[:8] + wire.ints_field_rows(
+            g.ints("k"), wire.WireLayout(g.params(z)).m2_bytes).tobytes()
+        assert srv.handle_frame(ht) == pf(wire.MSG_HINT_TRANSFER_REPLY, k_body)
+        r = srv.handle_frame(ht)
+        assert r[5] == wire.MSG_ERROR and int.from_bytes(r[38:42], "little") == wire.ERR_INPUT
+        # wrong parameter hash / unknown type -> ERR_PROTOCOL
+        r = srv.handle_frame(wire.pack_frame(wire.MSG_QUERY, b"\x00" * 32, b"")[4:])
+        assert int.from_bytes(r[38:42], "little") == wire.ERR_PROTOCOL
+        r = srv.handle_frame(pf(77, b"")[4:])
+        assert int.from_bytes(r[38:42], "little") == wire.ERR_PROTOCOL
+        # unfresh query index -> HINT_PENDING
+        far = fx["query_sep"].tobytes()
+        far = far[:32] + (1000).to_bytes(8, "little") + far[40:]
+        assert srv.handle_frame(pf(wire.MSG_QUERY, far)[4:]) == pf(wire.MSG_HINT_PENDING, b"")
+    finally:
+        srv.close()
