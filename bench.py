@@ -54,6 +54,8 @@ def _args():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--no-extra-e2e", action="store_true",
+                    help="skip the wire / C-ABI e2e variants")
     ap.add_argument("--workload", default="1g", choices=["1g", "batch64", "8g", "hint", "update"],
                     help="1g: BASELINE configs[1] (default, the driver's line); batch64: "
                          "configs[3]; 8g: configs[2] (92682^2, strong-scaled over --gpus); "
@@ -363,6 +365,51 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
 
+    # the same answer through the wire front end (PirServer.handle_frame: query
+    # frame bytes in, response frame bytes out) and through the host-buffer
+    # C ABI handle (zpir_db_answer), single GPU only
+    extra_e2e = {}
+    if world == 1 and not args.no_extra_e2e:
+        from paper_2603_09190_b200 import wire
+        from paper_2603_09190_b200.dbapi import DeviceDatabase
+        from paper_2603_09190_b200.server import PirServer
+        srv_w = PirServer(params, None, state=st, hint_workers=1)
+        srv_w.close()                      # no background hint jobs during timing
+        srv_w.registrations[reg.client_id] = reg
+        wl = wire.WireLayout(params)
+        frame = wire.pack_frame(wire.MSG_QUERY, params.params_hash(),
+                                wire.encode_query(wl, reg.client_id, 0, 0, ck_o, qu))[4:]
+        for _ in range(3):
+            rep = srv_w.handle_frame(frame)
+        assert rep[5] == wire.MSG_RESPONSE_SEPARATE, rep[:64]
+        tw = []
+        for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
+            srv_w.handle_frame(frame)
+            tw.append(time.perf_counter() - t1)
+        wire_s = statistics.mean(tw)
+        extra_e2e["e2e_wire"] = {"value": D0 * d1_total / wire_s / 1e9, "unit": "GB/s",
+                                 "ms_per_step": wire_s * 1e3,
+                                 "request_bytes": len(frame), "reply_bytes": len(rep),
+                                 "api": "PirServer.handle_frame (query frame bytes -> response "
+                                        "frame bytes, SEPARATE)"}
+        del srv_w
+        dd = DeviceDatabase(params, db)
+        for _ in range(3):
+            t_h = dd.answer(qu, ck_o, m)
+        assert t_h == z.respond(st, reg, qmsg).t
+        th_ = []
+        for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
+            dd.answer(qu, ck_o, m)
+            th_.append(time.perf_counter() - t1)
+        dd.close()
+        h_s = statistics.mean(th_)
+        extra_e2e["e2e_c_abi"] = {"value": D0 * d1_total / h_s / 1e9, "unit": "GB/s",
+                                  "ms_per_step": h_s * 1e3,
+                                  "api": "zpir_db_answer (include/zippir_db.h): pageable host "
+                                         "buffers, Python ints converted by dbapi.py"}
+
     db_bytes_total = D0 * d1_total
     db_bytes_rank = D0 * (hi - lo)
     value = db_bytes_total / (ms / 1e3) / 1e9
@@ -405,6 +452,7 @@ def run_b200(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond()"},
             "clocks": clk,
+            **extra_e2e,
             "setup_s": setup_s, "hint_s_per_client": hint_s,
             "per_gpu_db_bytes": db_bytes_rank,
         }

@@ -68,7 +68,8 @@ def unpack_frame(data: bytes) -> Frame:
         raise WireError(ERR_PROTOCOL, "short frame")
     if data[0] != WIRE_VERSION:
         raise WireError(ERR_PROTOCOL, f"unsupported wire version {data[0]}")
-    return Frame(data[1], bytes(data[2:34]), data[34:])
+    mv = memoryview(data)
+    return Frame(data[1], bytes(mv[2:34]), mv[34:])   # body: zero-copy view
 
 
 class WireLayout:
@@ -114,16 +115,21 @@ def decode_query(lay: WireLayout, body):
     client_id = bytes(mv[:32])
     qi, mode_b = struct.unpack_from("<QB", mv, 32)
     if len(mv) == lay.query_body and lay.q_bytes <= 4:
-        raw = np.frombuffer(mv, dtype=np.uint8, offset=41)
         cw = 4 + lay.m_bytes
-        ck = raw[: lay.n * cw].reshape(lay.n, cw)
-        qw = 4 + lay.q_bytes
-        qf = raw[lay.n * cw:].reshape(lay.d0, qw)
-        if (np.all(ck[:, :4].view("<u4") == lay.m_bytes)
-                and np.all(qf[:, :4].view("<u4") == lay.q_bytes)):
+        ck = np.frombuffer(mv, dtype=np.uint8, count=lay.n * cw, offset=41).reshape(lay.n, cw)
+        q0 = 41 + lay.n * cw
+        if lay.q_bytes == 4:
+            # (prefix, value) u32 pairs: one strided view, no copy
+            qv = np.frombuffer(mv, dtype="<u4", count=2 * lay.d0, offset=q0)
+            qpre, qu = qv[0::2], qv[1::2]
+        else:
+            qf = np.frombuffer(mv, dtype=np.uint8, offset=q0).reshape(lay.d0, 4 + lay.q_bytes)
+            qpre = qf[:, :4].view("<u4")
             qb = np.zeros((lay.d0, 4), dtype=np.uint8)
             qb[:, : lay.q_bytes] = qf[:, 4:]
-            return client_id, qi, mode_b, ck[:, 4:], qb.view("<u4").reshape(lay.d0)
+            qu = qb.view("<u4").reshape(lay.d0)
+        if (ck[:, :4].view("<u4") == lay.m_bytes).all() and (qpre == lay.q_bytes).all():
+            return client_id, qi, mode_b, ck[:, 4:], qu
     off = 41
     ck_o = []
     for _ in range(lay.n):
@@ -177,12 +183,20 @@ def ints_field_rows(values, width: int) -> np.ndarray:
 
 def encode_response_separate(query_index: int, t_fields: np.ndarray, k_fields: np.ndarray) -> bytes:
     """wire.py:169-173: qi, d1' t fields (m_bytes), d1' k fields (m2_bytes)."""
-    return b"".join((struct.pack("<Q", query_index), t_fields.tobytes(), k_fields.tobytes()))
+    return b"".join((struct.pack("<Q", query_index), t_fields, k_fields))
 
 
 def encode_response_combined(query_index: int, K_fields: np.ndarray) -> bytes:
     """wire.py:190-193 (also the hint transfer reply, wire.py:219-223)."""
-    return struct.pack("<Q", query_index) + K_fields.tobytes()
+    return b"".join((struct.pack("<Q", query_index), K_fields))
+
+
+def pack_reply(msg_type: int, params_hash: bytes, query_index: int, *fields) -> bytes:
+    """pack_frame(msg_type, params_hash, encode_response_*(query_index, *fields))
+    assembled in one pass (no intermediate body copy)."""
+    n = HEADER_BYTES + 8 + sum(f.nbytes for f in fields)
+    return b"".join((struct.pack("<IBB", n, WIRE_VERSION, msg_type), params_hash,
+                     struct.pack("<Q", query_index), *fields))
 
 
 def decode_response(lay: WireLayout, body: bytes, combined: bool):
