@@ -149,6 +149,8 @@ class Layout:
             raise NotImplementedError(
                 f"the B200 path needs q a power of two <= 2^32 (got q={self.q}); there is no "
                 "CPU fallback")
+        if self.p > 256:
+            raise NotImplementedError("the device layout stores one byte per DB symbol (p <= 256)")
         self.qmask = (self.q - 1) & 0xFFFFFFFF
         # slot stride of the positional group fold: gamma = 2^(32 s) (binary key,
         # quarter-delta: s = 1; uniform key: s = 2); 0 = general gamma

@@ -207,6 +207,17 @@ def wire_cases(names=("desk_reduced", "toy", "q16", "ragged")):
     print("wire fixtures:", names, flush=True)
 
 
+def dbfile_cases():
+    """Reference-serialized database files (dbfile.py:24-31)."""
+    from zippir import dbfile
+    arr = np.load(os.path.join(HERE, "desk_reduced.npz"))
+    db = dbfile.DatabaseFile(32, 48, 256, 48, arr["db"].astype(np.int64))
+    dbfile.save(db, os.path.join(HERE, "desk_reduced.zpirdb"))
+    f = dbfile.ingest(bytes(range(80)), 8, 20, p=16)   # two base-16 digits per byte
+    dbfile.save(f, os.path.join(HERE, "ingest_p16.zpirdb"))
+    print("dbfile fixtures", flush=True)
+
+
 def gamma_cases():
     """Batch scales other than 2^32 (compress.py:36-43): uniform key with
     quarter-delta (gamma = q^2 = 2^64), standard regime (gamma = q + n q),
@@ -229,6 +240,7 @@ def main():
     args = ap.parse_args()
     if args.wire_only:
         wire_cases()
+        dbfile_cases()
         return
     gamma_cases()
     if args.gamma_only:
@@ -261,6 +273,7 @@ def main():
                                    key_dist="binary"), d0, d1, 2048, seed=2048,
                       db=db, store_full=False)
     wire_cases()
+    dbfile_cases()
 
 
 if __name__ == "__main__":
