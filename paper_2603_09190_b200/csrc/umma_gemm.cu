@@ -206,12 +206,13 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
 #pragma unroll
           for (int k = 0; k < kBK / 32; ++k) {
             const uint64_t ad = desc_sw128(a0 + k * 32);
-#pragma unroll
-            for (int p = 0; p < (NT + 255) / 256; ++p) {
-              const int np_ = (NT - p * 256) < 256 ? (NT - p * 256) : 256;
-              const uint64_t bd = desc_sw128(b0 + p * 256 * kBK + k * 32);
-              umma_i8(d + p * 256, ad, bd, idesc_u8(kBM, np_), (kb > k0 || k > 0) ? 1u : 0u);
-            }
+            // N > 256: two MMAs of balanced width (multiples of 16), e.g. 144 + 128
+            constexpr int kN0 = NT <= 256 ? NT : ((NT / 2 + 15) / 16) * 16;
+            const uint32_t acc_on = (kb > k0 || k > 0) ? 1u : 0u;
+            umma_i8(d, ad, desc_sw128(b0 + k * 32), idesc_u8(kBM, kN0), acc_on);
+            if constexpr (NT > kN0)
+              umma_i8(d + kN0, ad, desc_sw128(b0 + kN0 * kBK + k * 32),
+                      idesc_u8(kBM, NT - kN0), acc_on);
           }
           umma_commit(&empty[stage]);
           if (++stage == C::kStages) {
@@ -340,6 +341,240 @@ umma_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tbase, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant of the BIGINT (answer compression) GEMM: tcgen05.mma
+// cta_group::2, M = 256 rows per pair tile (128 per CTA, its own TMEM lanes),
+// B split by N halves (each CTA stages NT/2 rows of every k-block: half the
+// per-SM operand feed of the single-CTA kernel, which is feed-bound).
+// Cluster (2,1,1) = one TPC. The leader (rank 0) owns full[] and issues the
+// MMAs; both CTAs' TMA loads signal the leader's full[s]; the leader's
+// commits arrive on empty[] / tfull[] of both CTAs (multicast); both CTAs'
+// epilogues arrive on the leader's tempty[] / oempty.
+template <int NT>
+struct PairCfg {
+  static constexpr int kP0 = NT < 256 ? NT : 256;          // first MMA's N
+  static constexpr int kP1 = NT - kP0;                     // second MMA's N (0 if none)
+  static constexpr int kH0 = kP0 / 2, kH1 = kP1 / 2;       // rows per CTA of each part
+  static constexpr int kABytes = kBM * kBK;
+  static constexpr int kBBytes = (kH0 + kH1) * kBK;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = std::min(12, (200 * 1024) / kStageBytes);
+  static constexpr int kAcc = UmmaCfg<NT>::kAcc;
+  static constexpr int kOv = UmmaCfg<NT>::kOv;
+  static constexpr int kAccOff1 = UmmaCfg<NT>::kAccOff1;
+  static constexpr int kTmemCols = UmmaCfg<NT>::kTmemCols;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+  static_assert(kH0 % 8 == 0 && kH1 % 8 == 0, "B halves must be whole 8-row swizzle atoms");
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+umma_pair_bigint_kernel(const __grid_constant__ CUtensorMap mapA,
+                        const __grid_constant__ CUtensorMap mapB0,
+                        const __grid_constant__ CUtensorMap mapB1, const UmmaArgs args,
+                        int64_t rows) {
+  using C = PairCfg<NT>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kAcc;
+  uint64_t* oempty = tempty + C::kAcc;
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(oempty + 1);
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB0);
+    if (C::kH1) tma_prefetch(&mapB1);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::kAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    mbar_init(oempty, 256);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tbase_smem, C::kTmemCols);
+  tc_fence_before();
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tbase = *tbase_smem;
+
+  // pair work list: units = (pair tile, n) over m_tiles pair tiles of 256 rows
+  UmmaArgs pa = args;
+  const int npairs = (int)(gridDim.x >> 1), pid = (int)(blockIdx.x >> 1);
+  SegIter it;
+  {
+    const int64_t T = (int64_t)pa.m_tiles * pa.n_tiles;
+    it.u = pid * T / npairs;
+    it.u1 = (pid + 1) * T / npairs;
+    it.kb = pa.kblocks;
+    it.split = false;
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      int64_t t;
+      int k0, k1, stage = 0;
+      uint32_t phase = 0;
+      while (it.next(t, k0, k1)) {
+        const int m = (int)(t / pa.n_tiles), n = (int)(t % pa.n_tiles);
+        const int arow = m * 2 * kBM + (int)rank * kBM;
+        for (int kb = k0; kb < k1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+          uint8_t* b = sB + stage * C::kBBytes;
+          tma_load_2d_pair(sA + stage * C::kABytes, &mapA, fb, kb * kBK, arow, pol_a);
+          tma_load_2d_pair(b, &mapB0, fb, kb * kBK, n * NT + (int)rank * C::kH0, pol_b);
+          if (C::kH1)
+            tma_load_2d_pair(b + C::kH0 * kBK, &mapB1, fb, kb * kBK,
+                             n * NT + C::kP0 + (int)rank * C::kH1, pol_b);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader only) ----------------
+      int64_t t;
+      int k0, k1, stage = 0, acc = 0, seg = 0;
+      uint32_t phase = 0, aphase = 0;
+      while (it.next(t, k0, k1)) {
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        if constexpr (C::kOv > 0) {
+          if (seg > 0) mbar_wait(oempty, (uint32_t)((seg - 1) & 1));
+        }
+        tc_fence_after();
+        const uint32_t d = tbase + (uint32_t)(acc * C::kAccOff1);
+        ++seg;
+        for (int kb = k0; kb < k1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b0 = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 32; ++k) {
+            const uint64_t ad = desc_sw128(a0 + k * 32);
+            const uint32_t acc_on = (kb > k0 || k > 0) ? 1u : 0u;
+            umma_i8_pair(d, ad, desc_sw128(b0 + k * 32), idesc_u8(2 * kBM, C::kP0), acc_on);
+            if (C::kP1)
+              umma_i8_pair(d + C::kP0, ad, desc_sw128(b0 + C::kH0 * kBK + k * 32),
+                           idesc_u8(2 * kBM, C::kP1 ? C::kP1 : 16), acc_on);
+          }
+          umma_commit_pair(&empty[stage], 0x3);
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_pair(&tfull[acc], 0x3);
+        if (++acc == C::kAcc) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5 of both CTAs) ----------------
+    const int quarter = warp & 3;
+    const int lrow = quarter * 32 + lane;
+    const uint32_t tempty_l0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_l1 = mapa_shared(smem_u32(&tempty[C::kAcc - 1]), 0);
+    const uint32_t oempty_l = mapa_shared(smem_u32(oempty), 0);
+    int64_t t;
+    int k0, k1, acc = 0;
+    uint32_t aphase = 0;
+    while (it.next(t, k0, k1)) {
+      const int m = (int)(t / pa.n_tiles), n = (int)(t % pa.n_tiles);
+      const int64_t row = (int64_t)m * 2 * kBM + (int64_t)rank * kBM + lrow;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * C::kAccOff1);
+      constexpr int kOvChunks = C::kOv / 16;
+      uint32_t ov[kOvChunks > 0 ? kOvChunks : 1][16];
+      const int first = (acc == 0) ? (NT - C::kOv) : 0;
+      if constexpr (kOvChunks > 0) {
+#pragma unroll
+        for (int q = 0; q < kOvChunks; ++q) tmem_ld16(taddr + first + 16 * q, ov[q]);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive_cluster(oempty_l);
+      }
+      const bool live = row < rows;
+      unsigned long long carry = 0;
+      uint32_t* zr = pa.out + (int64_t)n * pa.zq + row * pa.wz;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += 16) {
+        uint32_t r[16];
+        const bool in_ov = kOvChunks > 0 && c0 >= first && c0 < first + C::kOv;
+        if (in_ov) {
+          const int qi = (c0 - first) >> 4;
+#pragma unroll
+          for (int q = 0; q < (kOvChunks > 0 ? kOvChunks : 1); ++q)
+            if (q == qi)
+#pragma unroll
+              for (int i = 0; i < 16; ++i) r[i] = ov[q][i];
+        } else {
+          tmem_ld16(taddr + c0, r);
+          tmem_wait_ld();
+        }
+        uint32_t limb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const unsigned long long s = (unsigned long long)r[4 * i] +
+                                       ((unsigned long long)r[4 * i + 1] << 8) +
+                                       ((unsigned long long)r[4 * i + 2] << 16) +
+                                       ((unsigned long long)r[4 * i + 3] << 24) + carry;
+          limb[i] = (uint32_t)s;
+          carry = s >> 32;
+        }
+        const int li = c0 / 4;
+        if (live) {
+          if (li + 3 < pa.wz) {
+            *reinterpret_cast<uint4*>(zr + li) = make_uint4(limb[0], limb[1], limb[2], limb[3]);
+          } else {
+            for (int i = 0; i < 4; ++i)
+              if (li + i < pa.wz) zr[li + i] = limb[i];
+          }
+        }
+      }
+      if (live)
+        for (int li = NT / 4; li < pa.wz; ++li) {
+          zr[li] = (uint32_t)carry;
+          carry >>= 32;
+        }
+      tc_fence_before();
+      mbar_arrive_cluster(acc ? tempty_l1 : tempty_l0);
+      if (++acc == C::kAcc) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();   // all MMAs consumed, all TMEM reads done in both CTAs
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, C::kTmemCols);
   }
 }
 
@@ -478,6 +713,57 @@ static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes
   return check_launch("umma_gemm");
 }
 
+// CTA-pair BIGINT GEMM launch: clusters of 2, grid = 2 x pairs.
+template <int NT>
+static int umma_pair_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes,
+                         const uint8_t* B, int64_t brows, int64_t ldb_bytes, UmmaArgs args,
+                         cudaStream_t st, int max_ctas) {
+  using C = PairCfg<NT>;
+  if (rows % kBM || brows % NT) {
+    set_error("umma_pair: rows %% 128 / brows %% NT (rows=%lld brows=%lld NT=%d)",
+              (long long)rows, (long long)brows, NT);
+    return kErrInput;
+  }
+  CUtensorMap ma, mb0, mb1;
+  if (int e = make_map(&ma, A, rows, K, lda_bytes, kBM)) return e;
+  if (int e = make_map(&mb0, B, brows, K, ldb_bytes, C::kH0)) return e;
+  if (int e = make_map(&mb1, B, brows, K, ldb_bytes, C::kH1 ? C::kH1 : C::kH0)) return e;
+  args.m_tiles = (int)ceil_div(rows, 2 * kBM);
+  args.n_tiles = (int)(brows / NT);
+  args.kblocks = (int)ceil_div(K, kBK);
+  args.split = 0;
+  const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
+  const int sms = num_sms();
+  const int cap = (max_ctas > 0 && max_ctas < sms) ? max_ctas : sms;
+  const int pairs = (int)std::min<int64_t>(cap / 2, T);
+  auto kern = umma_pair_bigint_kernel<NT>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * (pairs > 0 ? pairs : 1));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb0, mb1, args, rows) != cudaSuccess)
+    return check_launch("umma_pair_bigint launch");
+  return check_launch("umma_pair_bigint");
+}
+
+static bool use_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZPIR_PAIR");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // b[v * rows + r] = qmask & (DB qu_v)[r] for nvec <= 4 (N = 16) or 64 (N = 256)
 int umma_gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* qplanes,
                      int64_t nvec, uint32_t* out, int ctas, cudaStream_t st) {
@@ -523,6 +809,14 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
   a.qmask = qmask;
   a.wz = wz;
   const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
+  if (use_pair()) {
+    switch (nb) {
+      case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
+      case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
+      case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st, ctas);
+      default: break;
+    }
+  }
   switch (nb) {
     case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
     case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
@@ -561,6 +855,14 @@ int umma_answer_rows_batch_launch(const uint32_t* H, int64_t rows, int64_t n, co
   a.wz = wz;
   a.zq = rows * wz;
   const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
+  if (use_pair()) {
+    switch (nb) {
+      case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st, 0);
+      case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st, 0);
+      case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400LL * nq, 4 * n, a, st, 0);
+      default: break;
+    }
+  }
   switch (nb) {
     case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st);
     case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st);

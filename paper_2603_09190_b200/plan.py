@@ -140,6 +140,20 @@ class AnswerPlan:
             device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
             self._compress(stream, self.ctas)
             self._groups_z(stream)
+        elif which == "e2e_digits":
+            # respond() in one replay: both host->device copies, GEMV || (ck_o
+            # digits -> limbs, compression, Montgomery groups), finish, t as
+            # digits -> pinned host
+            device.h2d_async(self.qu, self.h_qu, stream)
+            self.ev_in.record(stream)
+            self.side.wait_event(self.ev_in)
+            device.h2d_async(self.d_ckd, self.h_ckd, self.side)
+            self._seq("side_digits", self.side)
+            self.ev_comp.record(self.side)
+            self._gemv(stream, self.sms - self.ctas)
+            stream.wait_event(self.ev_comp)
+            self._seq("finish_digits", stream)
+            device.d2h_async(self.h_td, self.d_td, stream)
         elif which == "side_limbs":
             # respond_wire(), side stream: ck_o limbs already staged
             self._compress(stream, self.ctas)

@@ -576,6 +576,15 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     if plan is not None:
         plan.set_key(kctx, stream)
         conv = _digit_conv()
+        if conv is not None and plan.ctas > 0 and mode == SEPARATE and events is None:
+            # one graph replay: copies in, GEMV || compression, finish, copy out
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            hq = plan.h_qu.numpy().view(np.uint32)
+            np.copyto(hq[: lay.d0], np.asarray(qmsg.qu0), casting="unsafe")
+            plan.run("e2e_digits", stream)
+            stream.synchronize()
+            vals = conv.ints_from_digits(plan.h_td.numpy(), plan.h_td.shape[0], plan.ndig_m)
+            return ResponseMessage(SEPARATE, qmsg.query_index, vals, stored.entries)
         # qu -> pinned -> device; GEMV graph on (SMs - COMPRESS_CTAS) SMs
         qu = np.asarray(qmsg.qu0)
         hq = plan.h_qu.numpy().view(np.uint32)
