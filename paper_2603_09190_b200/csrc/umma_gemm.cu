@@ -679,6 +679,15 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return kOk;
 }
 
+static bool tpc_packing() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ZPIR_TPC_PACK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int num_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -709,6 +718,25 @@ static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes
   const int grid = (int)std::min<int64_t>(cap, U);
   auto kern = umma_gemm_kernel<NT, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
+  if (max_ctas > 0 && grid % 2 == 0 && tpc_packing()) {
+    // sharing the GPU with a CTA-pair kernel: occupy whole TPCs (clusters of
+    // 2) so the remaining SMs stay pairable
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, args) != cudaSuccess)
+      return check_launch("umma_gemm cluster launch");
+    return check_launch("umma_gemm");
+  }
   kern<<<grid, kThreads, Cfg::kSmem, st>>>(ma, mb, args);
   return check_launch("umma_gemm");
 }
