@@ -151,3 +151,19 @@ def test_umma_few_ctas_multi_tile(env, lm, ctas):
     planes = device.query_planes(device.u32_tensor(q, dev), 16)
     b = device.to_host_u32(device.umma_gemv(dbt, planes, 1, ctas=ctas))[0]
     assert np.array_equal(b.astype(np.uint64), oracle_c.db_matvec(db, qu))
+
+
+def test_single_cta_compression_variant():
+    """The single-CTA compression GEMM (ZPIR_PAIR=0; the CTA-pair kernel is the
+    default) passes the same kernel checks, in a fresh process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, ZPIR_PAIR="0", ZPIR_TPC_PACK="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_kernels.py"),
+                        "-k", "answer_rows_engines or few_ctas"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout
