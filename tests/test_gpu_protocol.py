@@ -1,0 +1,116 @@
+"""Protocol-level GPU tests mirroring the reference's test_protocol.py
+(tests/test_protocol.py:40-113 there): exhaustive toy retrieval in both
+modes, zero database, update replay (stale hint refused, regenerated hint
+serves), hint determinism per query index -- on the B200 path, with the
+oracle's client restatement manufacturing queries and extracting records."""
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle import client
+
+pytestmark = pytest.mark.gpu
+
+
+def _toy(z, d0=4, d1=4, **kw):
+    args = dict(lwe=z.LweParams(n=4, q=16, p=4, noise_sigma=0.0, key_dist="binary"),
+                d0=d0, d1=d1, paillier_bits=64, scale_regime="standard")
+    args.update(kw)
+    return z.ProtocolParams(**args)
+
+
+def _setup(z, rng, params, db=None):
+    if db is None:
+        db = np.array([[rng.randrange(params.lwe.p) for _ in range(params.d1)]
+                       for _ in range(params.d0)])
+    state = z.ServerGlobalState(params, db)
+    sk, seed = client.setup(params.paillier_bits, rng)
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
+    return db, state, sk, reg
+
+
+def _ask(z, params, state, sk, reg, i0, qi, mode, rng, make_hint=True):
+    lw = params.lwe
+    if make_hint:
+        reg.hints[qi] = z.hint(state, reg, qi)
+    qu0, ck_o, _ = client.query(sk, reg.seed, lw.n, lw.q, lw.p, lw.noise_sigma, params.d0, i0,
+                                qi, rng, state.A)
+    r = z.respond(state, reg, z.QueryMessage(reg.client_id, qi, mode, ck_o, qu0))
+    kw = dict(t=r.t, k=[c.c for c in r.k]) if mode == z.SEPARATE else \
+        dict(combined=[c.c for c in r.k])
+    return client.extract(sk, lw.q, lw.p, params.capacity, params.gamma, params.d1, **kw)
+
+
+@pytest.fixture(scope="module")
+def z():
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import _lib, build
+    build.build()
+    _lib.load()
+    return z
+
+
+def test_end_to_end_exhaustive_toy(z):
+    rng = random.Random(0xC0FFEE)
+    params = _toy(z)
+    db, state, sk, reg = _setup(z, rng, params)
+    for i0 in range(4):
+        mode = z.SEPARATE if i0 % 2 == 0 else z.COMBINED
+        assert _ask(z, params, state, sk, reg, i0, i0, mode, rng) == [int(x) for x in db[i0]]
+
+
+@pytest.mark.parametrize("shape", [(7, 23), (16, 10), (1, 1)])
+def test_end_to_end_toy_shapes(z, shape):
+    """Ragged toy shapes incl. a single record of a single symbol."""
+    rng = random.Random(sum(shape))
+    params = _toy(z, d0=shape[0], d1=shape[1])
+    db, state, sk, reg = _setup(z, rng, params)
+    for i0 in sorted({0, shape[0] - 1, shape[0] // 2}):
+        assert _ask(z, params, state, sk, reg, i0, i0, z.SEPARATE, rng) == \
+            [int(x) for x in db[i0]]
+
+
+def test_zero_database_returns_zero_row(z):
+    rng = random.Random(0xC0FFEE)
+    params = _toy(z)
+    db, state, sk, reg = _setup(z, rng, params, db=np.zeros((4, 4), dtype=np.int64))
+    assert _ask(z, params, state, sk, reg, 2, 0, z.SEPARATE, rng) == [0] * 4
+
+
+def test_database_update_replay(z):
+    rng = random.Random(0xC0FFEE)
+    params = _toy(z)
+    db, state, sk, reg = _setup(z, rng, params)
+    assert _ask(z, params, state, sk, reg, 1, 0, z.SEPARATE, rng) == [int(x) for x in db[1]]
+    db2 = np.array([[rng.randrange(4) for _ in range(4)] for _ in range(4)])
+    state2 = z.ServerGlobalState(params, db2, basis=state.basis, db_version=state.db_version + 1)
+    reg.hints[1] = z.hint(state, reg, 1)                     # stale after the swap
+    lw = params.lwe
+    qu0, ck_o, _ = client.query(sk, reg.seed, lw.n, lw.q, lw.p, 0.0, 4, 3, 1, rng, state2.A)
+    q = z.QueryMessage(reg.client_id, 1, z.SEPARATE, ck_o, qu0)
+    with pytest.raises(KeyError):
+        z.respond(state2, reg, q)
+    reg.hints[1] = z.hint(state2, reg, 1)
+    r = z.respond(state2, reg, q)
+    assert client.extract(sk, lw.q, lw.p, params.capacity, params.gamma, 4, t=r.t,
+                          k=[c.c for c in r.k]) == [int(x) for x in db2[3]]
+    # the incremental path reaches the same state and hint
+    st_inc, changed = state.updated(db2)
+    assert np.array_equal(st_inc.H, state2.H)
+    assert [c.c for c in z.hint(st_inc, reg, 1).entries] == [c.c for c in reg.hints[1].entries]
+
+
+def test_hint_is_deterministic_per_index(z):
+    rng = random.Random(0xC0FFEE)
+    params = _toy(z)
+    db, state, sk, reg = _setup(z, rng, params)
+    h1 = z.hint(state, reg, 5)
+    h2 = z.hint(state, reg, 5)
+    assert [c.c for c in h1.entries] == [c.c for c in h2.entries]
+    h3 = z.hint(state, reg, 6)
+    assert [c.c for c in h1.entries] != [c.c for c in h3.entries]
+    assert [client.decrypt(sk, c.c) for c in h1.entries] == \
+        [client.decrypt(sk, c.c) for c in h2.entries]
