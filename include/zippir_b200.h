@@ -224,6 +224,11 @@ int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t l
 int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_t* ids,
                    int64_t nrows, int scatter, void* stream);
 
+/* Record a cudaEvent_t on `stream`; inside stream capture as an external
+ * event-record node, so timing events around a kernel fire on every replay
+ * of the captured graph (bench.py's in-step roofline). */
+int zpir_event_record(void* event, void* stream);
+
 /* Async pinned-host <-> device copy (kind 0 = H2D, 1 = D2H) on `stream`. */
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 

@@ -293,6 +293,18 @@ int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_
 
 // Async copy between pinned host and device memory (kind: 0 = H2D, 1 = D2H)
 // on the caller's stream; lets the API layer skip framework overhead per query.
+int zpir_event_record(void* event, void* stream) {
+  // external record: inside stream capture this becomes an event-record node
+  // that fires on every graph replay (plain records only order the capture)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(S(stream), &cs) != cudaSuccess) return check_launch("event_record");
+  const unsigned flags = cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+  if (cudaEventRecordWithFlags(reinterpret_cast<cudaEvent_t>(event), S(stream), flags) !=
+      cudaSuccess)
+    return check_launch("event_record");
+  return kOk;
+}
+
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
   const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   if (cudaMemcpyAsync(dst, src, (size_t)bytes, k, S(stream)) != cudaSuccess)

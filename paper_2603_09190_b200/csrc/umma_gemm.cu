@@ -52,6 +52,7 @@ struct UmmaArgs {
   const uint32_t* b;
   int wz;
   int64_t zq;  // BIGINT: per-N-tile (= per query) stride of z
+  int a_keep;  // BIGINT pair kernel: L2 evict_last for the A operand (H)
 };
 
 constexpr int kBM = 128;   // rows per tile (TMEM lanes)
@@ -428,7 +429,11 @@ umma_pair_bigint_kernel(const __grid_constant__ CUtensorMap mapA,
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
-      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      // H (the A operand, 4 bytes x n per DB row) is kept in L2 across
+      // queries when args.a_keep: the concurrent GEMV streams the DB with
+      // evict_first, so H lines survive and the answer reads less HBM
+      const uint64_t pol_a = pa.a_keep ? l2_evict_last() : l2_evict_first();
+      const uint64_t pol_b = l2_evict_last();
       int64_t t;
       int k0, k1, stage = 0;
       uint32_t phase = 0;
@@ -758,6 +763,14 @@ static int umma_pair_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_
   if (int e = make_map(&mb1, B, brows, K, ldb_bytes, C::kH1 ? C::kH1 : C::kH0)) return e;
   args.m_tiles = (int)ceil_div(rows, 2 * kBM);
   args.n_tiles = (int)(brows / NT);
+  {
+    static int keep = -1;
+    if (keep < 0) {
+      const char* e = getenv("ZPIR_H_L2");
+      keep = (e && e[0] == '0') ? 0 : 1;
+    }
+    args.a_keep = keep;
+  }
   args.kblocks = (int)ceil_div(K, kBK);
   args.split = 0;
   const int64_t T = (int64_t)args.m_tiles * args.n_tiles;

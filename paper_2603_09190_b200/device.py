@@ -334,6 +334,11 @@ def limbs_to_digits(limbs, nl, digits, stream=None):
     return digits
 
 
+def event_record(event, stream):
+    """Timing event record that also fires inside replayed CUDA graphs."""
+    _lib.call("zpir_event_record", ctypes.c_void_p(event.cuda_event), _s(stream))
+
+
 def h2d_async(dst, src_pinned, stream):
     """Raw cudaMemcpyAsync pinned host -> device (same byte size)."""
     _lib.call("zpir_memcpy_async", _lib.ptr(dst), _lib.ptr(src_pinned),

@@ -72,6 +72,10 @@ class AnswerPlan:
         self.ev_in = torch.cuda.Event()
         self.ev_comp = torch.cuda.Event()
         self.graphs = {}
+        self.gemv_events = (torch.cuda.Event(enable_timing=True),
+                            torch.cuda.Event(enable_timing=True))
+        for e in self.gemv_events:     # torch creates the cudaEvent_t on first record
+            e.record(torch.cuda.current_stream(dev))
 
     # -- eager pieces (also what gets captured) -----------------------------
 
@@ -112,17 +116,28 @@ class AnswerPlan:
                              self.kctx.lm, self.d_m, self.t, self.t_ld, stream)
 
     def _seq(self, which, stream):
-        if which == "full":
+        if which in ("full", "full_timed"):
+            # full_timed: the same step with timing events around the GEMV
+            # (query planes + GEMV) on the main stream, for the in-step roofline
+            tev = self.gemv_events if which == "full_timed" else None
             if self.ctas > 0:
                 self.ev_in.record(stream)
                 self.side.wait_event(self.ev_in)
                 self._compress(self.side, self.ctas)
                 self._groups_z(self.side)      # overlaps the GEMV's tail
                 self.ev_comp.record(self.side)
+                if tev:
+                    device.event_record(tev[0], stream)
                 self._gemv(stream, self.sms - self.ctas)
+                if tev:
+                    device.event_record(tev[1], stream)
                 stream.wait_event(self.ev_comp)
             else:
+                if tev:
+                    device.event_record(tev[0], stream)
                 self._gemv(stream, 0)
+                if tev:
+                    device.event_record(tev[1], stream)
                 self._compress(stream, 0)
                 self._groups_z(stream)
             self._finish(stream)
