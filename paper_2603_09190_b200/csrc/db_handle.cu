@@ -392,6 +392,39 @@ int hint_rows(zpir_db* h, const uint8_t* dbt_rows, int64_t rows, uint32_t* Hout,
   return zpir_global_hint(dbt_rows, rows, h->ld, h->A.as<uint32_t>(), h->lda, n, Hout, h->qmask, s);
 }
 
+// rows of src_ld device limbs -> rows of dst_limbs host limbs (zero-extended
+// or truncated; callers only truncate zero limbs)
+int d2h_rows(void* dst, int dst_limbs, const void* src, int src_ld, int64_t rows, cudaStream_t s) {
+  const int w = dst_limbs < src_ld ? dst_limbs : src_ld;
+  ZPIR_TRY(cu(cudaMemcpy2DAsync(dst, (size_t)dst_limbs * 4, src, (size_t)src_ld * 4,
+                                (size_t)w * 4, (size_t)rows, cudaMemcpyDeviceToHost, s),
+              "D2H"));
+  ZPIR_TRY(sync(s));
+  if (dst_limbs > w)
+    for (int64_t r = 0; r < rows; ++r)
+      std::memset(static_cast<uint32_t*>(dst) + r * dst_limbs + w, 0,
+                  (size_t)(dst_limbs - w) * 4);
+  return kOk;
+}
+
+// host rows of src_limbs -> device rows of dst_ld limbs (zero-extended; a
+// wider source row must only carry zero limbs beyond dst_ld)
+int h2d_rows(void* dst, int dst_ld, const uint32_t* src, int src_limbs, int64_t rows,
+             cudaStream_t s) {
+  const int w = src_limbs < dst_ld ? src_limbs : dst_ld;
+  for (int64_t r = 0; r < rows; ++r)
+    for (int i = w; i < src_limbs; ++i)
+      if (src[r * src_limbs + i]) {
+        set_error("value wider than the modulus");
+        return kErrInput;
+      }
+  if (w < dst_ld)
+    ZPIR_TRY(cu(cudaMemsetAsync(dst, 0, (size_t)rows * dst_ld * 4, s), "memset"));
+  return cu(cudaMemcpy2DAsync(dst, (size_t)dst_ld * 4, src, (size_t)src_limbs * 4, (size_t)w * 4,
+                              (size_t)rows, cudaMemcpyHostToDevice, s),
+            "H2D");
+}
+
 // qu (d0 u32, host) -> b on the device (w->b), GEMV on `ctas` SMs (0 = all).
 int stage_query_and_gemv(zpir_db* h, Work* w, const uint32_t* qu, int ctas, cudaStream_t s) {
   ZPIR_TRY(cu(cudaMemcpyAsync(w->qu.p, qu, (size_t)h->prm.d0 * 4, cudaMemcpyHostToDevice, s),
@@ -410,9 +443,7 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
   const int lm = k->lm, L = k->L;
   const int64_t n = h->prm.n;
   cudaStream_t s = h->main;
-  ZPIR_TRY(cu(cudaMemcpy2DAsync(w->cko.p, (size_t)lm * 4, cko, (size_t)L * 4, (size_t)L * 4,
-                                (size_t)n, cudaMemcpyHostToDevice, s),
-              "ck_o H2D"));
+  ZPIR_TRY(h2d_rows(w->cko.p, lm, cko, L, n, s));
   const int nb = umma_nb(lm);
   if (h->prm.engine == 0 && nb && n % 4 == 0) {  // TMA rows of 4n bytes: 16-byte pitch
     // compression on kCompressCtas SMs (side stream) || GEMV on the rest
@@ -440,13 +471,6 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
   return zpir_answer_general(w->z.as<uint32_t>(), w->b.as<uint32_t>(), h->qmask, d1, h->prm.cap,
                              h->groups, lm, k->m.as<uint32_t>(), k->np_m, k->ctab.as<uint32_t>(),
                              w->w.as<uint32_t>(), w->t.as<uint32_t>(), t_ld, s);
-}
-
-int d2h_rows(void* dst, int dst_limbs, const void* src, int src_ld, int64_t rows, cudaStream_t s) {
-  ZPIR_TRY(cu(cudaMemcpy2DAsync(dst, (size_t)dst_limbs * 4, src, (size_t)src_ld * 4,
-                                (size_t)dst_limbs * 4, (size_t)rows, cudaMemcpyDeviceToHost, s),
-              "D2H"));
-  return sync(s);
 }
 
 int check_limbs_fit(const Key* k, int L) {
@@ -818,11 +842,7 @@ static int db_answer(zpir_db* h, const uint32_t* qu, const uint32_t* cko, const 
   ZPIR_TRY(answer(h, k, w, qu, cko, t_ld));
   if (!kin) return d2h_rows(out, L, w->t.p, t_ld, h->groups, h->main);
   const int l2 = k->l2;
-  ZPIR_TRY(cu(cudaMemcpy2DAsync(w->k.p, (size_t)l2 * 4, kin, (size_t)2 * L * 4,
-                                (size_t)2 * L * 4 < (size_t)l2 * 4 ? (size_t)2 * L * 4
-                                                                   : (size_t)l2 * 4,
-                                (size_t)h->groups, cudaMemcpyHostToDevice, h->main),
-              "k H2D"));
+  ZPIR_TRY(h2d_rows(w->k.p, l2, kin, 2 * L, h->groups, h->main));
   ZPIR_TRY(zpir_combine(w->t.as<uint32_t>(), w->k.as<uint32_t>(), h->groups, l2,
                         k->m2.as<uint32_t>(), k->np_2, k->r2_2.as<uint32_t>(),
                         k->mr.as<uint32_t>(), w->K.as<uint32_t>(), h->main));

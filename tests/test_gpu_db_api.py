@@ -118,3 +118,36 @@ def test_multiexp_and_montmul_batch_kat(api):
         a = [rng.randrange(N) for _ in range(50)]
         b = [rng.randrange(N) for _ in range(50)]
         assert api.montmul_batch(a, b, N) == [x * y % N for x, y in zip(a, b)]
+
+
+def test_handle_api_mixed_limb_widths(api, golden):
+    """Keys of different widths on one handle, and limb rows wider than the
+    modulus (zero top limbs) in and out: results stay exact."""
+    g = golden("ragged")
+    rng = random.Random(11)
+    with api.DeviceDatabase(_params(g), g.db) as d:
+        H = d.global_hint().astype(np.uint64)
+        qu = g.arr["qu0"]
+        b = ref.db_matvec(g.db, qu, 1 << 32)
+        for bits in (1024, 1000, 950, 1024):
+            m = g.m if bits == 1024 else (rng.getrandbits(bits) | (1 << (bits - 1)) | 1)
+            ck = [rng.randrange(m) for _ in range(g.lwe["n"])]
+            want = ref.answer_t(H, b, ck, m, g.cap, g.gamma, g.d1)
+            assert d.answer(qu, ck, m) == want, bits
+        # explicit wider rows through the raw C ABI: L = 33 limbs for a 1024-bit m
+        import ctypes
+        from paper_2603_09190_b200 import _lib
+        from paper_2603_09190_b200.bigint import ints_to_limbs, limbs_to_ints
+        L = 33
+        ck = g.ints("ck_o")
+        q = np.ascontiguousarray(qu.astype(np.uint32))
+        c = ints_to_limbs(ck, L)
+        mm = ints_to_limbs([g.m], L)
+        t = np.empty((g.groups, L), dtype=np.uint32)
+        vp = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        _lib.call("zpir_db_answer", d._h, vp(q), vp(c), vp(mm), L, vp(t))
+        assert limbs_to_ints(t) == g.ints("t")
+        K = np.empty((g.groups, 2 * L), dtype=np.uint32)
+        kin = ints_to_limbs(g.ints("k"), 2 * L)
+        _lib.call("zpir_db_answer_combined", d._h, vp(q), vp(c), vp(mm), L, vp(kin), vp(K))
+        assert limbs_to_ints(K) == g.ints("K")

@@ -58,3 +58,33 @@ def test_handle_frame_bytes_match_reference(golden, name):
         assert srv.handle_frame(pf(wire.MSG_QUERY, far)[4:]) == pf(wire.MSG_HINT_PENDING, b"")
     finally:
         srv.close()
+
+
+def test_tcp_loopback_round_trip(golden):
+    """A real TCP loopback server (127.0.0.1, as the reference's test_service)."""
+    import socket
+    import struct
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import wire
+    from paper_2603_09190_b200.server import PirServer, serve, _read_exact
+    g = golden("desk_reduced")
+    fx = dict(np.load(os.path.join(GOLDEN, "wire_desk_reduced.npz")))
+    ph = fx["params_hash"].tobytes()
+    pir = PirServer(g.params(z), g.db)
+    srv = serve(pir, "127.0.0.1", 0)
+    try:
+        with socket.create_connection(srv.server_address, timeout=60) as s:
+            def rpc(t, body):
+                s.sendall(wire.pack_frame(t, ph, body))
+                (n,) = struct.unpack("<I", _read_exact(s, 4))
+                return wire.unpack_frame(_read_exact(s, n))
+            assert rpc(wire.MSG_HINT_REQUEST, fx["hint_request"].tobytes()).msg_type == wire.MSG_ACK
+            pir.wait_for_hints(timeout=120)
+            r = rpc(wire.MSG_QUERY, fx["query_sep"].tobytes())
+            assert r.msg_type == wire.MSG_RESPONSE_SEPARATE and bytes(r.body) == fx["resp_sep"].tobytes()
+            r = rpc(wire.MSG_QUERY, fx["query_comb"].tobytes())
+            assert r.msg_type == wire.MSG_RESPONSE_COMBINED and bytes(r.body) == fx["resp_comb"].tobytes()
+    finally:
+        srv.shutdown()
+        srv.server_close()
+        pir.close()

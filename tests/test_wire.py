@@ -84,3 +84,27 @@ def test_frames_and_errors(w, golden):
     assert m == g.m and seed == g.seed
     with pytest.raises(ValueError):
         w.field_rows(np.full((1, 2), 0xFFFFFFFF, dtype=np.uint32), 5)
+
+
+def test_tcp_serve_loop_cpu(w):
+    """The TCP loop frames requests and replies (a stand-in handler; CPU only)."""
+    import socket
+    import struct
+    from paper_2603_09190_b200.server import serve, _read_exact
+
+    class Echo:
+        def handle_frame(self, payload):
+            f = w.unpack_frame(payload)
+            return w.pack_frame(w.MSG_ACK, f.params_hash, bytes(f.body[::-1]))
+
+    srv = serve(Echo(), "127.0.0.1", 0)
+    try:
+        with socket.create_connection(srv.server_address, timeout=10) as s:
+            for body in (b"", b"abc", bytes(range(256)) * 40):
+                s.sendall(w.pack_frame(w.MSG_QUERY, b"\x07" * 32, body))
+                (n,) = struct.unpack("<I", _read_exact(s, 4))
+                f = w.unpack_frame(_read_exact(s, n))
+                assert f.msg_type == w.MSG_ACK and bytes(f.body) == body[::-1]
+    finally:
+        srv.shutdown()
+        srv.server_close()
