@@ -235,6 +235,10 @@ int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void*
 /* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
  * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
 int zpir_probe_imad(int blocks, int iters, float* ms);
+/* Roofline probe: `iters` rounds of 4 tcgen05 kind::i8 MMAs (M = 128, N = n,
+ * K = 32) per CTA from resident smem, blocks CTAs; ops = blocks*iters*4*2*128*n*32.
+ * The int8 tensor rate the compression / hint GEMMs are measured against. */
+int zpir_probe_umma_i8(int blocks, int iters, int n, float* ms);
 
 #ifdef __cplusplus
 }

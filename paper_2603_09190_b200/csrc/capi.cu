@@ -47,6 +47,7 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int umma_probe(int, int, int, float*);
 int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_t*, int64_t, int64_t,
                          int64_t, int64_t, int, int, const uint32_t*, uint32_t, const uint32_t*,
                          const uint32_t*, int, uint32_t*, void*, int64_t, cudaStream_t);
@@ -187,6 +188,10 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
 }
 
 int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(blocks, iters, ms)); }
+
+int zpir_probe_umma_i8(int blocks, int iters, int n, float* ms) {
+  ZPIR_GUARD(umma_probe(blocks, iters, n, ms));
+}
 
 int zpir_build_bc_batch(const uint32_t* cko, int64_t n, int lm, int nb, int nq, uint8_t* bc,
                         void* stream) {
