@@ -127,6 +127,19 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
                           const uint32_t* b, uint32_t qmask, int wz, uint32_t* z, int ctas,
                           void* stream);
 
+/* ---- planar compression (default for lm = 32 / 64) ------------------------
+ * H byte planes: hp[r*4np + a*np + k] = byte a of H[r*n + k], np = n rounded up
+ * to 128 (zero padded); built once per DB version. */
+int zpir_h_planes(const uint32_t* H, int64_t rows, int64_t n, uint8_t* hp, void* stream);
+/* ck_o byte rows for nq queries: bp[q*(4 lm)*np + j*np + k] = byte j of cko[q][k]. */
+int zpir_build_bcp(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp, void* stream);
+/* z[q*rows*wz + r*wz + i] = limbs of sum_k H[r,k] * ck_q[k] (wz = lm + 4), as
+ * zpir_umma_answer_rows, via z = sum_a 2^(8a) sum_j 2^(8j) (Hp_a Bp^T)[r, j]: one
+ * N = 4 lm tcgen05 MMA per 32-byte k-step, four plane passes per tile
+ * (rns.py:163-188 replacement); lm in {32, 64}, n <= 33025. */
+int zpir_umma_answer_rows_planar(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp,
+                                 int lm, int nq, int wz, uint32_t* z, int ctas, void* stream);
+
 /* ---- batched queries (BASELINE configs[3]; no reference counterpart: the
  * reference answers strictly one query at a time, protocol.py:333) ---------
  * nq stacked compression operands (nq x nb x 4n bytes) from nq ck_o limb rows. */

@@ -47,6 +47,10 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int h_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, cudaStream_t);
+int build_bcp_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
+int umma_planar_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int, int, int, uint32_t*,
+                       int, cudaStream_t);
 int umma_probe(int, int, int, float*);
 int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_t*, int64_t, int64_t,
                          int64_t, int64_t, int, int, const uint32_t*, uint32_t, const uint32_t*,
@@ -188,6 +192,19 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
 }
 
 int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(blocks, iters, ms)); }
+
+int zpir_h_planes(const uint32_t* H, int64_t rows, int64_t n, uint8_t* hp, void* stream) {
+  ZPIR_GUARD(h_planes_launch(H, rows, n, hp, S(stream)));
+}
+
+int zpir_build_bcp(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp, void* stream) {
+  ZPIR_GUARD(build_bcp_launch(cko, n, lm, nq, bp, S(stream)));
+}
+
+int zpir_umma_answer_rows_planar(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp,
+                                 int lm, int nq, int wz, uint32_t* z, int ctas, void* stream) {
+  ZPIR_GUARD(umma_planar_launch(hp, rows, n, bp, lm, nq, wz, z, ctas, S(stream)));
+}
 
 int zpir_probe_umma_i8(int blocks, int iters, int n, float* ms) {
   ZPIR_GUARD(umma_probe(blocks, iters, n, ms));

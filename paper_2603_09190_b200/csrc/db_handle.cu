@@ -251,7 +251,7 @@ struct zpir_db {
   int sms = 0;
   cudaStream_t main = nullptr, side = nullptr;
   cudaEvent_t ev_in = nullptr, ev_comp = nullptr;
-  zpir::DevBuf dbt, A, H;
+  zpir::DevBuf dbt, A, H, Hp;  // Hp: H byte planes (planar compression operand)
   std::map<std::string, std::unique_ptr<zpir::Key>> keys;
   std::map<int, std::unique_ptr<zpir::Work>> work;
   std::mutex mu;
@@ -265,6 +265,13 @@ constexpr int kCompressCtas = 40;  // measured SM split
 int umma_nb(int lm) { return lm == 32 ? 144 : lm == 64 ? 272 : lm == 96 ? 400 : 0; }
 
 bool use_umma_gemv(const zpir_db* h) { return h->prm.engine == 0 && h->qmask == 0xffffffffu; }
+
+int64_t planar_np(int64_t n) { return (n + 127) / 128 * 128; }
+
+// planar compression (H byte planes) for lm = 32 / 64 on the tcgen05 engine
+bool planar(const zpir_db* h, int lm) {
+  return h->prm.engine == 0 && (lm == 32 || lm == 64) && h->prm.n <= 33025 && h->Hp.p;
+}
 
 int sync(cudaStream_t s) { return cu(cudaStreamSynchronize(s), "stream synchronize"); }
 
@@ -367,7 +374,10 @@ int get_work(zpir_db* h, int lm, Work** out) {
   ZPIR_TRY(w->planes.alloc((size_t)16 * h->ld));
   ZPIR_TRY(w->b.alloc((size_t)h->rows * 4));
   ZPIR_TRY(w->cko.alloc((size_t)n * lm * 4));
-  if (umma_nb(lm) && n % 4 == 0) ZPIR_TRY(w->bc.alloc((size_t)umma_nb(lm) * 4 * n));
+  if (planar(h, lm))
+    ZPIR_TRY(w->bc.alloc((size_t)4 * lm * planar_np(n)));
+  else if (umma_nb(lm) && n % 4 == 0)
+    ZPIR_TRY(w->bc.alloc((size_t)umma_nb(lm) * 4 * n));
   ZPIR_TRY(w->z.alloc((size_t)h->rows * (lm + 4) * 4));
   ZPIR_TRY(w->t.alloc((size_t)h->groups * l2 * 4));
   ZPIR_TRY(w->k.alloc((size_t)h->groups * l2 * 4));
@@ -449,10 +459,17 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
     // compression on kCompressCtas SMs (side stream) || GEMV on the rest
     ZPIR_TRY(cu(cudaEventRecord(h->ev_in, s), "event"));
     ZPIR_TRY(cu(cudaStreamWaitEvent(h->side, h->ev_in, 0), "event wait"));
-    ZPIR_TRY(zpir_build_bc(w->cko.as<uint32_t>(), n, lm, nb, w->bc.as<uint8_t>(), h->side));
-    ZPIR_TRY(zpir_umma_answer_rows(h->H.as<uint32_t>(), h->rows, n, w->bc.as<uint8_t>(), nb,
-                                   nullptr, h->qmask, lm + 4, w->z.as<uint32_t>(), kCompressCtas,
-                                   h->side));
+    if (planar(h, lm)) {
+      ZPIR_TRY(zpir_build_bcp(w->cko.as<uint32_t>(), n, lm, 1, w->bc.as<uint8_t>(), h->side));
+      ZPIR_TRY(zpir_umma_answer_rows_planar(h->Hp.as<uint8_t>(), h->rows, n, w->bc.as<uint8_t>(),
+                                            lm, 1, lm + 4, w->z.as<uint32_t>(), kCompressCtas,
+                                            h->side));
+    } else {
+      ZPIR_TRY(zpir_build_bc(w->cko.as<uint32_t>(), n, lm, nb, w->bc.as<uint8_t>(), h->side));
+      ZPIR_TRY(zpir_umma_answer_rows(h->H.as<uint32_t>(), h->rows, n, w->bc.as<uint8_t>(), nb,
+                                     nullptr, h->qmask, lm + 4, w->z.as<uint32_t>(),
+                                     kCompressCtas, h->side));
+    }
     ZPIR_TRY(cu(cudaEventRecord(h->ev_comp, h->side), "event"));
     ZPIR_TRY(stage_query_and_gemv(h, w, qu, h->sms - kCompressCtas, s));
     ZPIR_TRY(cu(cudaStreamWaitEvent(s, h->ev_comp, 0), "event wait"));
@@ -560,6 +577,10 @@ int create(const zpir_db_params* prm, const uint8_t* db, int64_t ld_db, const ui
   }
   ZPIR_TRY(h->H.alloc((size_t)h->rows * p.n * 4, false));
   ZPIR_TRY(hint_rows(h.get(), h->dbt.as<uint8_t>(), h->rows, h->H.as<uint32_t>(), s));
+  if (p.engine == 0) {
+    ZPIR_TRY(h->Hp.alloc((size_t)h->rows * 4 * planar_np(p.n), false));
+    ZPIR_TRY(zpir_h_planes(h->H.as<uint32_t>(), h->rows, p.n, h->Hp.as<uint8_t>(), s));
+  }
   ZPIR_TRY(sync(s));
   *out = h.release();
   return kOk;
@@ -687,6 +708,8 @@ int update_rows(zpir_db* h, const int64_t* cols, int64_t count, const uint8_t* v
   ZPIR_TRY(hint_rows(h, part.as<uint8_t>(), rp, Hp.as<uint32_t>(), s));
   ZPIR_TRY(zpir_move_rows(Hp.as<uint8_t>(), h->H.as<uint8_t>(), 4 * n, dids.as<int32_t>(), count,
                           1, s));
+  if (h->Hp.p)
+    ZPIR_TRY(zpir_h_planes(h->H.as<uint32_t>(), h->rows, n, h->Hp.as<uint8_t>(), s));
   return sync(s);
 }
 

@@ -584,6 +584,193 @@ umma_pair_bigint_kernel(const __grid_constant__ CUtensorMap mapA,
 }
 
 // ---------------------------------------------------------------------------
+// Planar BIGINT GEMM (the answer compression, default for lm = 32 / 64):
+//   z_r = sum_a 2^(8a) * sum_j 2^(8j) P_a[r, j],  P_a[r, j] = sum_k Hp[r, a, k] * Bp[j, k]
+// with Hp[r, a, k] = byte a of H[r, k] (byte planes, plane pitch np = n rounded
+// up to 128) and Bp[j, k] = byte j of ck_o[k] (N = 4 lm = 128 / 256 rows). One
+// tile = 4 passes (a = 0..3) of K = np into alternating TMEM buffers; every MMA
+// is a single N = 4 lm instruction (no N = 16 remainder: the tensor pipe spends
+// ~95 cycles on any MMA up to N ~ 144 and ~146 on N = 256, tools/probe_umma.py),
+// 128 MMAs per 128-row tile instead of 256. The epilogue carry-propagates each
+// pass's 4 lm columns and adds them, shifted by 8a bits, into the row's z limbs
+// held in registers. |P_a| <= n * 255^2 < 2^31 for n <= 33025.
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                   const UmmaArgs args, int64_t np) {
+  using C = UmmaCfg<NT>;
+  static_assert(NT % 16 == 0 && NT <= 256 && C::kAcc == 2 && C::kOv == 0, "planar: N <= 256");
+  constexpr int kLimbs = NT / 4;          // limbs of one pass's column block
+  constexpr int kZ = kLimbs + 4;          // z row width (lm + 4)
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kAcc;
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(tempty + C::kAcc + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::kAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tbase_smem, C::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tbase_smem;
+  const int kbp = (int)(np / kBK);        // k-blocks per plane pass
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      SegIter it = seg_range(args);
+      int64_t t;
+      int k0, k1, stage = 0;
+      uint32_t phase = 0;
+      while (it.next(t, k0, k1)) {
+        const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+        for (int a = 0; a < 4; ++a)
+          for (int kb = 0; kb < kbp; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::kStageBytes);
+            tma_load_2d_hint(sA + stage * C::kABytes, &mapA, &full[stage],
+                             (int)(a * np) + kb * kBK, m * kBM, pol_a);
+            tma_load_2d_hint(sB + stage * C::kBBytes, &mapB, &full[stage], kb * kBK, n * NT,
+                             pol_b);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer: one accumulation group per (tile, plane) ----------------
+      SegIter it = seg_range(args);
+      int64_t t;
+      int k0, k1, stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      const uint32_t idesc = idesc_u8(kBM, NT);
+      while (it.next(t, k0, k1)) {
+        for (int a = 0; a < 4; ++a) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + (uint32_t)(acc * C::kAccOff1);
+          for (int kb = 0; kb < kbp; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = desc_sw128(smem_u32(sA + stage * C::kABytes));
+            const uint64_t bd = desc_sw128(smem_u32(sB + stage * C::kBBytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 32; ++k)   // +32 bytes = +2 in the start-address field
+              umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&empty[stage]);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit(&tfull[acc]);
+          if (++acc == C::kAcc) {
+            acc = 0;
+            aphase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5): z row in registers ----------------
+    const int quarter = warp & 3;
+    const int lrow = quarter * 32 + lane;
+    SegIter it = seg_range(args);
+    int64_t t;
+    int k0, k1, acc = 0;
+    uint32_t aphase = 0;
+    while (it.next(t, k0, k1)) {
+      const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+      const int64_t row = (int64_t)m * kBM + lrow;
+      uint32_t z[kZ];
+#pragma unroll
+      for (int i = 0; i < kZ; ++i) z[i] = 0;
+#pragma unroll 1
+      for (int a = 0; a < 4; ++a) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * C::kAccOff1);
+        const uint32_t sh = 8u * (uint32_t)a;
+        unsigned long long carry = 0;   // column carry of this pass
+        uint32_t prev = 0, c2 = 0;       // previous limb (for the shift), carry into z
+#pragma unroll
+        for (int c = 0; c < NT / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16(taddr + 16 * c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned long long sum = (unsigned long long)r[4 * i] +
+                                           ((unsigned long long)r[4 * i + 1] << 8) +
+                                           ((unsigned long long)r[4 * i + 2] << 16) +
+                                           ((unsigned long long)r[4 * i + 3] << 24) + carry;
+            const uint32_t v = (uint32_t)sum;
+            carry = sum >> 32;
+            const uint32_t w = __funnelshift_l(prev, v, sh);
+            const unsigned long long zz = (unsigned long long)z[4 * c + i] + w + c2;
+            z[4 * c + i] = (uint32_t)zz;
+            c2 = (uint32_t)(zz >> 32);
+            prev = v;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        // high limbs: the pass's final carry (< 2^32), then the shifted-out bits
+        {
+          const uint32_t v0 = (uint32_t)carry, v1 = (uint32_t)(carry >> 32);
+          const uint32_t w[4] = {__funnelshift_l(prev, v0, sh), __funnelshift_l(v0, v1, sh),
+                                 __funnelshift_l(v1, 0u, sh), 0u};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned long long zz = (unsigned long long)z[kLimbs + i] + w[i] + c2;
+            z[kLimbs + i] = (uint32_t)zz;
+            c2 = (uint32_t)(zz >> 32);
+          }
+        }
+        if (++acc == C::kAcc) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+      uint32_t* zr = args.out + (int64_t)n * args.zq + row * args.wz;
+#pragma unroll
+      for (int i = 0; i < kZ; i += 4)
+        *reinterpret_cast<uint4*>(zr + i) = make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tbase, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // operand builders
 
 // Bc[b * (4n) + 4k + a] = byte (b - a) of ck_o[k] (0 outside [0, 4 lm)), b < nb.
@@ -912,6 +1099,110 @@ int umma_answer_rows_batch_launch(const uint32_t* H, int64_t rows, int64_t n, co
       set_error("umma_answer_rows_batch: unsupported B width %d", nb);
       return kErrUnsupported;
   }
+}
+
+// Hp[r * 4np + a * np + k] = byte a of H[r * n + k] (zero for k >= n): the
+// compression's A operand, one 128-byte-aligned byte plane per H byte.
+__global__ void __launch_bounds__(256)
+h_planes_kernel(const uint32_t* __restrict__ H, int64_t rows, int64_t n, int64_t np,
+                uint8_t* __restrict__ hp) {
+  const int64_t r = blockIdx.y;
+  const int64_t k4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;  // 4 k per thread
+  if (r >= rows || k4 >= np) return;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};   // w[a] = bytes a of H[r, k4 .. k4+3]
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint32_t h = (k4 + e < n) ? H[r * n + k4 + e] : 0u;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) w[a] |= ((h >> (8 * a)) & 0xffu) << (8 * e);
+  }
+  uint8_t* dst = hp + r * 4 * np + k4;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) *reinterpret_cast<uint32_t*>(dst + a * np) = w[a];
+}
+
+// Bp[q][j * np + k] = byte j of ck_q[k] (j < 4 lm; zero for k >= n)
+__global__ void __launch_bounds__(256)
+build_bcp_kernel(const uint32_t* __restrict__ cko, int64_t n, int lm, int64_t np,
+                 uint8_t* __restrict__ bp) {
+  __shared__ uint32_t tile[32][33];
+  const int64_t q = blockIdx.z;
+  cko += q * n * lm;
+  bp += q * (int64_t)(4 * lm) * np;
+  const int64_t k0 = (int64_t)blockIdx.x * 32;
+  const int l0 = blockIdx.y * 32;   // limb block
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = ty; i < 32; i += 8) {
+    const int64_t k = k0 + i;
+    tile[i][tx] = (k < n && l0 + tx < lm) ? cko[k * lm + l0 + tx] : 0u;
+  }
+  __syncthreads();
+  // thread -> (limb l0 + li, byte e): row j = 4 (l0 + li) + e, 32 consecutive k
+  for (int idx = ty; idx < 32 * 4; idx += 8) {
+    const int li = idx >> 2, e = idx & 3;
+    if (l0 + li >= lm) continue;
+    const int64_t k = k0 + tx;
+    if (k >= np) continue;
+    bp[(int64_t)(4 * (l0 + li) + e) * np + k] = (uint8_t)(tile[tx][li] >> (8 * e));
+  }
+}
+
+int h_planes_launch(const uint32_t* H, int64_t rows, int64_t n, uint8_t* hp, cudaStream_t st) {
+  const int64_t np = ceil_div(n, kBK) * kBK;
+  if (rows <= 0 || rows > 65535 * 64) {
+    set_error("h_planes: bad rows %lld", (long long)rows);
+    return kErrInput;
+  }
+  for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+    const int64_t rr = (rows - r0) < 65535 ? (rows - r0) : 65535;
+    dim3 grid((unsigned)ceil_div(np / 4, 256), (unsigned)rr);
+    h_planes_kernel<<<grid, 256, 0, st>>>(H + r0 * n, rr, n, np, hp + r0 * 4 * np);
+  }
+  return check_launch("h_planes");
+}
+
+int build_bcp_launch(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp, cudaStream_t st) {
+  const int64_t np = ceil_div(n, kBK) * kBK;
+  dim3 grid((unsigned)ceil_div(np, 32), (unsigned)ceil_div(lm, 32), (unsigned)nq);
+  build_bcp_kernel<<<grid, 256, 0, st>>>(cko, n, lm, np, bp);
+  return check_launch("build_bcp");
+}
+
+// z (nq x rows x wz) from the planar operands; lm in {32, 64}.
+int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp, int lm,
+                       int nq, int wz, uint32_t* z, int ctas, cudaStream_t st) {
+  const int64_t np = ceil_div(n, kBK) * kBK;
+  if (wz != lm + 4 || rows % kBM || (lm != 32 && lm != 64) || n > 33025) {
+    set_error("umma_planar: unsupported shape (lm=%d wz=%d rows=%lld n=%lld)", lm, wz,
+              (long long)rows, (long long)n);
+    return kErrUnsupported;
+  }
+  UmmaArgs a{};
+  a.split = 0;
+  a.out = z;
+  a.wz = wz;
+  a.zq = rows * wz;
+  const int NT = 4 * lm;
+  CUtensorMap ma, mb;
+  if (int e = make_map(&ma, hp, rows, 4 * np, 4 * np, kBM)) return e;
+  if (int e = make_map(&mb, bp, (int64_t)NT * nq, np, np, NT)) return e;
+  a.m_tiles = (int)(rows / kBM);
+  a.n_tiles = nq;
+  a.kblocks = (int)(4 * np / kBK);
+  const int64_t T = (int64_t)a.m_tiles * a.n_tiles;
+  const int sms = num_sms();
+  const int cap = (ctas > 0 && ctas < sms) ? ctas : sms;
+  const int grid = (int)std::min<int64_t>(cap, T);
+  if (NT == 256) {
+    auto kern = umma_planar_kernel<256>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, UmmaCfg<256>::kSmem);
+    kern<<<grid, kThreads, UmmaCfg<256>::kSmem, st>>>(ma, mb, a, np);
+  } else {
+    auto kern = umma_planar_kernel<128>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, UmmaCfg<128>::kSmem);
+    kern<<<grid, kThreads, UmmaCfg<128>::kSmem, st>>>(ma, mb, a, np);
+  }
+  return check_launch("umma_planar");
 }
 
 int build_aplanes_launch(const uint32_t* A, int64_t ld, int64_t lda, int64_t n, uint8_t* ap,

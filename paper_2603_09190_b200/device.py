@@ -120,6 +120,40 @@ def multiexp(bases, E, rows, rs, bs, ls, elimbs, kctx, stream=None):
 # ---- tcgen05 (UMMA) engine ----------------------------------------------------
 
 UMMA_NB = {32: 144, 64: 272, 96: 400}
+PLANAR_LM = (32, 64)   # key widths served by the planar compression GEMM
+
+
+def planar_np(n):
+    return -(-n // 128) * 128
+
+
+def h_planes(H, stream=None):
+    """(rows, 4 np) uint8 byte planes of H (the planar compression's A operand)."""
+    rows, n = H.shape
+    hp = torch.empty((rows, 4 * planar_np(n)), dtype=torch.uint8, device=H.device)
+    _lib.call("zpir_h_planes", _lib.ptr(H), rows, n, _lib.ptr(hp), _s(stream))
+    return hp
+
+
+def build_bcp(cko, lm, stream=None, out=None):
+    """cko (n, lm) or (nq, n, lm) int32 -> (nq, 4 lm, np) uint8 ck_o byte rows."""
+    c = cko if cko.dim() == 3 else cko.unsqueeze(0)
+    nq, n, _ = c.shape
+    if out is None:
+        out = torch.empty((nq, 4 * lm, planar_np(n)), dtype=torch.uint8, device=cko.device)
+    _lib.call("zpir_build_bcp", _lib.ptr(c), n, lm, nq, _lib.ptr(out), _s(stream))
+    return out
+
+
+def umma_answer_rows_planar(hp, n, bp, lm, out=None, stream=None, ctas=0):
+    """z (nq, rows, lm + 4) from H planes and ck_o byte rows."""
+    rows = hp.shape[0]
+    nq = bp.shape[0]
+    if out is None:
+        out = torch.empty((nq, rows, lm + 4), dtype=torch.int32, device=hp.device)
+    _lib.call("zpir_umma_answer_rows_planar", _lib.ptr(hp), rows, n, _lib.ptr(bp), lm, nq, lm + 4,
+              _lib.ptr(out), ctas, _s(stream))
+    return out
 
 
 def query_planes(qu_dev, prow, stream=None, planes=None):
@@ -162,7 +196,8 @@ def umma_answer_rows(H, bc, b, qmask, lm, out=None, stream=None, ctas=0):
     rows, n = H.shape
     if out is None:
         out = torch.empty((rows, lm + 4), dtype=torch.int32, device=H.device)
-    _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0], _lib.ptr(b),
+    _lib.call("zpir_umma_answer_rows", _lib.ptr(H), rows, n, _lib.ptr(bc), bc.shape[0],
+              _lib.ptr(b) if b is not None else None,
               qmask, lm + 4, _lib.ptr(out), ctas, _s(stream))
     return out
 

@@ -42,7 +42,7 @@ class AnswerPlan:
         self.cko = torch.zeros((lay.n, lm), dtype=torch.int32, device=dev)
         self.planes = torch.empty((16, lay.ld), dtype=torch.uint8, device=dev)
         self.b = torch.empty((1, lay.rows), dtype=torch.int32, device=dev)
-        self.bc = torch.empty((device.UMMA_NB[lm], 4 * lay.n), dtype=torch.uint8, device=dev)
+        self.bc = torch.empty(state.compress_operand_shape(lm), dtype=torch.uint8, device=dev)
         self.z = torch.empty((lay.rows, lm + 4), dtype=torch.int32, device=dev)
         self.t = torch.empty((lay.groups, t_ld), dtype=torch.int32, device=dev)
         self.tz = torch.empty((lay.groups, t_ld), dtype=torch.int32, device=dev)
@@ -84,10 +84,7 @@ class AnswerPlan:
         device.umma_gemv(self.state.dbt, self.planes, 1, out=self.b, stream=stream, ctas=ctas)
 
     def _compress(self, stream, ctas):
-        st, lm = self.state, self.kctx.lm
-        device.build_bc(self.cko, lm, stream=stream, bc=self.bc)
-        device.umma_answer_rows(st.H_dev, self.bc, self.b[0], st.layout.qmask, lm, out=self.z,
-                                stream=stream, ctas=ctas)
+        self.state.compress_rows(self.cko, self.kctx.lm, stream, out=self.z, ctas=ctas, bc=self.bc)
 
     def set_key(self, kctx, stream):
         """Load a client's modulus constants into the plan buffers (in-stream)."""

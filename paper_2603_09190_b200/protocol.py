@@ -47,6 +47,9 @@ ENGINE = os.environ.get("ZPIR_ENGINE", "umma")
 # SMs given to the compression GEMM while the GEMV streams the DB on the rest
 # (both are HBM-bound; H is ~1/8 of the DB bytes). 0 = run them back to back.
 COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "40"))
+# planar compression GEMM (H byte planes, one N = 4 lm MMA per k-step) for
+# lm = 32 / 64; ZPIR_PLANAR=0 selects the byte-shifted B operand kernels
+PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
 
 
 @dataclass
@@ -183,6 +186,7 @@ class ServerGlobalState:
             self.H_dev = device.umma_global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
         else:
             self.H_dev = device.global_hint(self.dbt, self.A_dev, n, lay.qmask, stream)
+        self.H_planes = device.h_planes(self.H_dev, stream) if self.engine == "umma" else None
         stream.synchronize()
         self.hint_time = time.perf_counter() - t0
         self._H_host = None
@@ -234,6 +238,7 @@ class ServerGlobalState:
                 Hp = device.global_hint(part, self.A_dev, lay.n, lay.qmask, stream)
             device.move_rows(Hp, H, ids, scatter=True, stream=stream)
         new.H_dev = H
+        new.H_planes = device.h_planes(H, stream) if self.engine == "umma" else None
         stream.synchronize()
         new.hint_time = time.perf_counter() - t0
         return new, changed
@@ -321,10 +326,40 @@ class ServerGlobalState:
                 "planes": torch.empty((16, lay.ld), dtype=torch.uint8, device=dev),
                 "b": torch.empty((1, lay.rows), dtype=torch.int32, device=dev),
                 "z": torch.empty((lay.rows, lm + 4), dtype=torch.int32, device=dev),
-                "bc": (torch.empty((device.UMMA_NB[lm], 4 * lay.n), dtype=torch.uint8,
+                "bc": (torch.empty(self.compress_operand_shape(lm), dtype=torch.uint8,
                                    device=dev) if lm in device.UMMA_NB else None),
             }
         return w
+
+    def planar(self, lm) -> bool:
+        """The planar compression GEMM serves this key width."""
+        return (PLANAR and self.engine == "umma" and lm in device.PLANAR_LM
+                and self.H_planes is not None and self.layout.n <= 33025)
+
+    def compress_rows(self, cko, lm, stream, out=None, ctas=0, bc=None):
+        """z (rows x lm+4, or nq x rows x lm+4 for cko of nq queries) on the
+        tensor cores: planar kernel where it applies, else the byte-shifted one."""
+        lay = self.layout
+        batched = cko.dim() == 3
+        if self.planar(lm):
+            bp = device.build_bcp(cko, lm, stream, out=bc)
+            z = out.view(-1, lay.rows, lm + 4) if out is not None else None
+            z = device.umma_answer_rows_planar(self.H_planes, lay.n, bp, lm, out=z, stream=stream,
+                                               ctas=ctas)
+            return z if batched else z[0]
+        if batched:
+            bcs = device.build_bc_batch(cko, lm, stream)
+            return device.umma_answer_rows_batch(self.H_dev, bcs, lm, stream)
+        bcs = device.build_bc(cko, lm, stream=stream, bc=bc)
+        return device.umma_answer_rows(self.H_dev, bcs, None, lay.qmask, lm, out=out, stream=stream,
+                                       ctas=ctas)
+
+    def compress_operand_shape(self, lm):
+        """Shape / dtype of the per-query compression operand buffer."""
+        lay = self.layout
+        if self.planar(lm):
+            return (1, 4 * lm, device.planar_np(lay.n))
+        return (device.UMMA_NB[lm], 4 * lay.n)
 
     def answer_plan(self, kctx, t_ld):
         """Per-thread captured plan for the tcgen05 path, or None."""
@@ -352,8 +387,7 @@ class ServerGlobalState:
         b = device.umma_gemv(self.dbt, planes, nq, stream=stream)
         if events:
             events[1].record(stream)
-        bc = device.build_bc_batch(cko_dev, lm, stream)
-        z = device.umma_answer_rows_batch(self.H_dev, bc, lm, stream)
+        z = self.compress_rows(cko_dev, lm, stream)
         t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctxs, t_ld,
                                        stream, stride=lay.stride)
         if events:
@@ -392,9 +426,8 @@ class ServerGlobalState:
             if split:
                 w["ev_in"].record(stream)
                 side.wait_event(w["ev_in"])
-            bc = device.build_bc(cko_dev, lm, stream=cs, bc=w["bc"])
-            z = device.umma_answer_rows(self.H_dev, bc, w["b"][0], lay.qmask, lm, out=w["z"],
-                                        stream=cs, ctas=COMPRESS_CTAS if split else 0)
+            z = self.compress_rows(cko_dev, lm, cs, out=w["z"], ctas=COMPRESS_CTAS if split else 0,
+                                   bc=w["bc"])
             if split:
                 w["ev_comp"].record(side)
             planes = device.query_planes(qu_dev, 16, stream, planes=w["planes"])

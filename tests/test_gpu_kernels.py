@@ -167,3 +167,33 @@ def test_single_cta_compression_variant():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("lm,n,rows,nq", [(64, 1024, 384, 1), (32, 64, 256, 1), (64, 100, 128, 3),
+                                          (32, 1024, 640, 2), (64, 4096, 128, 1)])
+@pytest.mark.parametrize("ctas", [0, 2])
+def test_planar_compression(env, lm, n, rows, nq, ctas):
+    """Planar compression (H byte planes x ck_o byte rows, 4 plane passes per
+    tile) == CUDA-core rows, incl. n not a multiple of 128 (zero-padded
+    planes), several queries, few persistent CTAs, all-ones extremes."""
+    torch, device = env
+    rng = np.random.default_rng(lm * n + nq)
+    H = rng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
+    H[0] = 0xFFFFFFFF
+    r = random.Random(n + lm)
+    from paper_2603_09190_b200.bigint import ints_to_limbs
+    dev = torch.device("cuda", 0)
+    Hd = device.u32_tensor(H, dev)
+    cks = []
+    for q in range(nq):
+        ck = [r.randrange(1 << (32 * lm)) for _ in range(n)]
+        ck[0] = (1 << (32 * lm)) - 1
+        cks.append(ck)
+    cd = torch.stack([device.u32_tensor(ints_to_limbs(ck, lm), dev) for ck in cks])
+    hp = device.h_planes(Hd)
+    bp = device.build_bcp(cd, lm)
+    z = device.to_host_u32(device.umma_answer_rows_planar(hp, n, bp, lm, ctas=ctas))
+    bd = torch.zeros(rows, dtype=torch.int32, device=dev)
+    for q in range(nq):
+        zr = device.to_host_u32(device.answer_rows(Hd, bd, 0xFFFFFFFF, cd[q].contiguous(), lm))
+        assert np.array_equal(z[q], zr), q
