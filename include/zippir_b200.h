@@ -242,6 +242,13 @@ int zpir_move_rows(const uint8_t* src, uint8_t* dst, int64_t pitch, const int32_
  * of the captured graph (bench.py's in-step roofline). */
 int zpir_event_record(void* event, void* stream);
 
+/* Make `stream` wait for `event`; inside stream capture as an external
+ * event-wait node (the answer's second graph waits for the GEMV graph). */
+int zpir_stream_wait_event(void* stream, void* event);
+/* cudaGraphLaunch of an instantiated graph (cudaGraphExec_t) on `stream`:
+ * the low-overhead replay respond() uses. */
+int zpir_graph_launch(void* graph_exec, void* stream);
+
 /* Async pinned-host <-> device copy (kind 0 = H2D, 1 = D2H) on `stream`. */
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 

@@ -30,6 +30,8 @@ class DbParams(ctypes.Structure):
 _SIGS = {
     "zpir_abi_version": ([], _c_int),
     "zpir_event_record": ([_p, _p], _c_int),
+    "zpir_stream_wait_event": ([_p, _p], _c_int),
+    "zpir_graph_launch": ([_p, _p], _c_int),
     # handle-level ABI (include/zippir_db.h), host buffers
     "zpir_db_create": ([ctypes.POINTER(DbParams), _p, _c_i64, _p, _p, ctypes.POINTER(_p)], _c_int),
     "zpir_db_destroy": ([_p], _c_int),

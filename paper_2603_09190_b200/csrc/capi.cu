@@ -327,6 +327,23 @@ int zpir_event_record(void* event, void* stream) {
   return kOk;
 }
 
+int zpir_stream_wait_event(void* stream, void* event) {
+  // inside stream capture: an external event-wait node (waits, at every
+  // replay, for the event's latest record made outside the graph)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(S(stream), &cs) != cudaSuccess) return check_launch("stream_wait");
+  const unsigned flags = cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0u;
+  if (cudaStreamWaitEvent(S(stream), reinterpret_cast<cudaEvent_t>(event), flags) != cudaSuccess)
+    return check_launch("stream_wait");
+  return kOk;
+}
+
+int zpir_graph_launch(void* graph_exec, void* stream) {
+  if (cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), S(stream)) != cudaSuccess)
+    return check_launch("graph_launch");
+  return kOk;
+}
+
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
   const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
   if (cudaMemcpyAsync(dst, src, (size_t)bytes, k, S(stream)) != cudaSuccess)

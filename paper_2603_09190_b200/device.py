@@ -374,6 +374,15 @@ def event_record(event, stream):
     _lib.call("zpir_event_record", ctypes.c_void_p(event.cuda_event), _s(stream))
 
 
+def stream_wait_event(stream, event):
+    """Stream waits for an event; an external wait node when captured."""
+    _lib.call("zpir_stream_wait_event", _s(stream), ctypes.c_void_p(event.cuda_event))
+
+
+def graph_launch(graph_exec: int, stream):
+    _lib.call("zpir_graph_launch", ctypes.c_void_p(graph_exec), _s(stream))
+
+
 def h2d_async(dst, src_pinned, stream):
     """Raw cudaMemcpyAsync pinned host -> device (same byte size)."""
     _lib.call("zpir_memcpy_async", _lib.ptr(dst), _lib.ptr(src_pinned),

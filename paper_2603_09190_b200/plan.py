@@ -76,6 +76,10 @@ class AnswerPlan:
                             torch.cuda.Event(enable_timing=True))
         for e in self.gemv_events:     # torch creates the cudaEvent_t on first record
             e.record(torch.cuda.current_stream(dev))
+        # respond(): the GEMV graph's completion, recorded outside the graphs
+        self.ev_gemv = torch.cuda.Event()
+        self.ev_gemv.record(torch.cuda.current_stream(dev))
+        self._exec = {}
 
     # -- eager pieces (also what gets captured) -----------------------------
 
@@ -87,9 +91,10 @@ class AnswerPlan:
         self.state.compress_rows(self.cko, self.kctx.lm, stream, out=self.z, ctas=ctas, bc=self.bc)
 
     def set_key(self, kctx, stream):
-        """Load a client's modulus constants into the plan buffers (in-stream)."""
+        """Load a client's modulus constants into the plan buffers (in-stream);
+        True when they changed."""
         if self.key_m == kctx.m:
-            return
+            return False
         import numpy as np
         with torch.cuda.stream(stream):
             self.d_m[0].copy_(kctx.d_m)
@@ -99,6 +104,7 @@ class AnswerPlan:
             self.d_f0.fill_(1 if kctx.cm.R < 2 * kctx.m else 0)
         self.kctx = kctx
         self.key_m = kctx.m
+        return True
 
     def _groups_z(self, stream):
         """Montgomery part of the group stage; needs only the compression."""
@@ -166,6 +172,28 @@ class AnswerPlan:
             stream.wait_event(self.ev_comp)
             self._seq("finish_digits", stream)
             device.d2h_async(self.h_td, self.d_td, stream)
+        elif which == "e2e_g1":
+            # respond(), graph 1 (main stream): qu in, query planes, GEMV
+            device.h2d_async(self.qu, self.h_qu, stream)
+            self._gemv(stream, self.sms - self.ctas)
+        elif which in ("e2e_g2", "e2e_g2t", "w_g2t"):
+            # respond() / respond_wire(), graph 2 (side stream): ck_o in (CPython
+            # digits, or limb rows for the wire path), compression, Montgomery
+            # groups; then (external wait for graph 1) the finish; e2e_g2 also
+            # converts t to digits and copies it out, the others leave t in HBM
+            if which == "w_g2t":
+                device.h2d_async(self.cko, self.h_cko, stream)
+                self._compress(stream, self.ctas)
+                self._groups_z(stream)
+            else:
+                device.h2d_async(self.d_ckd, self.h_ckd, stream)
+                self._seq("side_digits", stream)
+            device.stream_wait_event(stream, self.ev_gemv)
+            if which == "e2e_g2":
+                self._seq("finish_digits", stream)
+                device.d2h_async(self.h_td, self.d_td, stream)
+            else:
+                self._finish(stream)
         elif which == "side_limbs":
             # respond_wire(), side stream: ck_o limbs already staged
             self._compress(stream, self.ctas)
@@ -186,6 +214,17 @@ class AnswerPlan:
             raise ValueError(which)
 
     # -- graph replay ----------------------------------------------------------
+
+    def launch(self, which, stream):
+        """Replay a captured graph with a raw cudaGraphLaunch (no torch stream
+        context); the first call captures it through run()."""
+        ex = self._exec.get(which) if USE_GRAPHS else None
+        if ex is None:
+            self.run(which, stream)
+            if USE_GRAPHS:
+                self._exec[which] = self.graphs[which].raw_cuda_graph_exec()
+            return
+        device.graph_launch(ex, stream)
 
     def run(self, which, stream):
         if self.key_m is None:

@@ -607,17 +607,36 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
     t_ld = kctx.lm if mode == SEPARATE else kctx.l2
     plan = state.answer_plan(kctx, t_ld)
     if plan is not None:
-        plan.set_key(kctx, stream)
+        key_changed = plan.set_key(kctx, stream)
         conv = _digit_conv()
-        if conv is not None and plan.ctas > 0 and mode == SEPARATE and events is None:
-            # one graph replay: copies in, GEMV || compression, finish, copy out
-            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+        if conv is not None and plan.ctas > 0 and events is None:
+            # two raw graph launches: the GEMV graph starts as soon as qu is
+            # staged; ck_o's digits are copied on the host meanwhile, then the
+            # side graph (compression, groups; waits for the GEMV; finish)
             hq = plan.h_qu.numpy().view(np.uint32)
             np.copyto(hq[: lay.d0], np.asarray(qmsg.qu0), casting="unsafe")
-            plan.run("e2e_digits", stream)
-            stream.synchronize()
-            vals = conv.ints_from_digits(plan.h_td.numpy(), plan.h_td.shape[0], plan.ndig_m)
-            return ResponseMessage(SEPARATE, qmsg.query_index, vals, stored.entries)
+            side = plan.side
+            if key_changed:
+                side.wait_stream(stream)     # the new key constants were copied on `stream`
+            plan.launch("e2e_g1", stream)
+            device.event_record(plan.ev_gemv, stream)
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            if mode == SEPARATE:
+                plan.launch("e2e_g2", side)
+                side.synchronize()
+                vals = conv.ints_from_digits(plan.h_td.numpy(), plan.h_td.shape[0], plan.ndig_m)
+                return ResponseMessage(SEPARATE, qmsg.query_index, vals, stored.entries)
+            plan.launch("e2e_g2t", side)
+            k_dev = _stored_device(stored, kctx, dev, side)
+            K = device.combine(plan.t, k_dev, kctx, stream=side)
+            device.limbs_to_digits(K, kctx.l2, plan.d_Kd, side)
+            device.d2h_async(plan.h_Kd, plan.d_Kd, side)
+            side.synchronize()
+            vals = conv.ints_from_digits(plan.h_Kd.numpy(), plan.h_Kd.shape[0], plan.ndig_2)
+            counters.bump("add", lay.groups)
+            counters.bump("group_mult", lay.groups)
+            return ResponseMessage(COMBINED, qmsg.query_index, [],
+                                   [PaillierCiphertext(v) for v in vals])
         # qu -> pinned -> device; GEMV graph on (SMs - COMPRESS_CTAS) SMs
         qu = np.asarray(qmsg.qu0)
         hq = plan.h_qu.numpy().view(np.uint32)
@@ -737,33 +756,29 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
                                    stream=stream)
         out = _d2h_u32(t_dev, "t", stream)
     else:
-        plan.set_key(kctx, stream)
+        side = plan.side
+        if plan.set_key(kctx, stream):
+            side.wait_stream(stream)
         hq = plan.h_qu.numpy().view(np.uint32)
         np.copyto(hq[: lay.d0], qu, casting="unsafe")
-        device.h2d_async(plan.qu, plan.h_qu, stream)
-        plan.ev_in.record(stream)
-        plan.run("gemv_part", stream)
-        # meanwhile: ck_o bytes -> pinned limb rows -> side stream compression
+        plan.launch("e2e_g1", stream)          # qu in, GEMV
+        device.event_record(plan.ev_gemv, stream)
+        # meanwhile: ck_o bytes -> pinned limb rows -> side graph (compression,
+        # groups, then the finish once the GEMV is done)
         hc = plan.h_cko.numpy().view(np.uint8).reshape(lay.n, 4 * kctx.lm)
         if getattr(plan, "_ck_w", None) != w:
             hc[:] = 0
             plan._ck_w = w
         hc[:, :w] = ck_bytes
-        side = plan.side
-        side.wait_event(plan.ev_in)
-        device.h2d_async(plan.cko, plan.h_cko, side)
-        plan.run("side_limbs", side)
-        stream.wait_stream(side)
-        plan.run("finish", stream)
+        plan.launch("w_g2t", side)
         if mode == COMBINED:
-            K = device.combine(plan.t, _stored_device(stored, kctx, dev, stream), kctx,
-                               stream=stream)
-            device.d2h_async(plan.h_K, K, stream)
+            K = device.combine(plan.t, _stored_device(stored, kctx, dev, side), kctx, stream=side)
+            device.d2h_async(plan.h_K, K, side)
             h_out = plan.h_K
         else:
-            device.d2h_async(plan.h_t, plan.t, stream)
+            device.d2h_async(plan.h_t, plan.t, side)
             h_out = plan.h_t
-        stream.synchronize()
+        side.synchronize()
         out = h_out.numpy().view(np.uint32)
     if mode == COMBINED:
         counters.bump("add", lay.groups)
