@@ -252,7 +252,51 @@ static PyObject* ints_from_digits(PyObject* self, PyObject* args) {
 }
 #endif
 
+/* narrow_u32(src, dst, n): dst[i] = (uint32) src[i] for i < n, src a buffer of
+ * 4- or 8-byte unsigned words (the query vector qu0 as numpy uint64 / uint32),
+ * strided or not; the GIL is released for the copy. */
+static PyObject* narrow_u32(PyObject* self, PyObject* args) {
+  PyObject* src_obj;
+  Py_buffer dst;
+  Py_ssize_t n;
+  if (!PyArg_ParseTuple(args, "Ow*n", &src_obj, &dst, &n)) return NULL;
+  Py_buffer src;
+  if (PyObject_GetBuffer(src_obj, &src, PyBUF_STRIDED_RO | PyBUF_FORMAT) < 0) {
+    PyBuffer_Release(&dst);
+    return NULL;
+  }
+  const Py_ssize_t item = src.itemsize;
+  const Py_ssize_t stride = (src.ndim == 1 && src.strides) ? src.strides[0] : item;
+  const Py_ssize_t len = (src.ndim == 1 && src.shape) ? src.shape[0] : src.len / item;
+  if ((item != 4 && item != 8) || src.ndim > 1 || len < n || (size_t)dst.len < (size_t)n * 4) {
+    PyBuffer_Release(&src);
+    PyBuffer_Release(&dst);
+    PyErr_SetString(PyExc_ValueError, "narrow_u32: need a 1-D buffer of 4/8-byte words");
+    return NULL;
+  }
+  uint32_t* out = (uint32_t*)dst.buf;
+  const char* p = (const char*)src.buf;
+  Py_BEGIN_ALLOW_THREADS
+  if (item == 8) {
+    if (stride == 8) {
+      const uint64_t* q = (const uint64_t*)p;
+      for (Py_ssize_t i = 0; i < n; ++i) out[i] = (uint32_t)q[i];
+    } else {
+      for (Py_ssize_t i = 0; i < n; ++i) out[i] = (uint32_t)*(const uint64_t*)(p + i * stride);
+    }
+  } else if (stride == 4) {
+    memcpy(out, p, (size_t)n * 4);
+  } else {
+    for (Py_ssize_t i = 0; i < n; ++i) out[i] = *(const uint32_t*)(p + i * stride);
+  }
+  Py_END_ALLOW_THREADS
+  PyBuffer_Release(&src);
+  PyBuffer_Release(&dst);
+  Py_RETURN_NONE;
+}
+
 static PyMethodDef methods[] = {
+    {"narrow_u32", narrow_u32, METH_VARARGS, "4/8-byte words -> u32 buffer (truncating)"},
 #ifdef ZPIR_FAST_DIGITS
     {"digits_into", digits_into, METH_VARARGS, "ints -> raw 30-bit digits written into a buffer"},
     {"ints_from_digits", ints_from_digits, METH_VARARGS, "30-bit digit rows -> list of ints"},

@@ -20,6 +20,7 @@ warms the TMA-descriptor path). ZPIR_GRAPHS=0 disables capture.
 import os
 import threading
 
+import numpy as np
 import torch
 
 from . import device
@@ -60,6 +61,11 @@ class AnswerPlan:
         self.h_td = torch.zeros((lay.groups, self.ndig_m), dtype=torch.int32).pin_memory()
         self.d_Kd = torch.zeros((lay.groups, self.ndig_2), dtype=torch.int32, device=dev)
         self.h_Kd = torch.zeros((lay.groups, self.ndig_2), dtype=torch.int32).pin_memory()
+        # numpy views of the pinned buffers (made once: respond() is latency-bound)
+        self.np_qu = self.h_qu.numpy().view(np.uint32)
+        self.np_ckd = self.h_ckd.numpy()
+        self.np_td = self.h_td.numpy()
+        self.np_Kd = self.h_Kd.numpy()
         # the client's modulus constants live in plan buffers read by the
         # captured group stage (refreshed by set_key when the client changes)
         self.nchunks = max(2, -(-(lay.cap + lm + 4) // lm))

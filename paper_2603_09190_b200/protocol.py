@@ -613,18 +613,21 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
             # two raw graph launches: the GEMV graph starts as soon as qu is
             # staged; ck_o's digits are copied on the host meanwhile, then the
             # side graph (compression, groups; waits for the GEMV; finish)
-            hq = plan.h_qu.numpy().view(np.uint32)
-            np.copyto(hq[: lay.d0], np.asarray(qmsg.qu0), casting="unsafe")
+            qu = qmsg.qu0
+            if isinstance(qu, np.ndarray) and qu.ndim == 1 and qu.dtype.itemsize in (4, 8):
+                conv.narrow_u32(qu, plan.np_qu, lay.d0)
+            else:
+                np.copyto(plan.np_qu[: lay.d0], np.asarray(qu), casting="unsafe")
             side = plan.side
             if key_changed:
                 side.wait_stream(stream)     # the new key constants were copied on `stream`
             plan.launch("e2e_g1", stream)
             device.event_record(plan.ev_gemv, stream)
-            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            conv.digits_into(qmsg.ck_o, plan.np_ckd, plan.ndig_m)
             if mode == SEPARATE:
                 plan.launch("e2e_g2", side)
                 side.synchronize()
-                vals = conv.ints_from_digits(plan.h_td.numpy(), plan.h_td.shape[0], plan.ndig_m)
+                vals = conv.ints_from_digits(plan.np_td, lay.groups, plan.ndig_m)
                 return ResponseMessage(SEPARATE, qmsg.query_index, vals, stored.entries)
             plan.launch("e2e_g2t", side)
             k_dev = _stored_device(stored, kctx, dev, side)
@@ -632,7 +635,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
             device.limbs_to_digits(K, kctx.l2, plan.d_Kd, side)
             device.d2h_async(plan.h_Kd, plan.d_Kd, side)
             side.synchronize()
-            vals = conv.ints_from_digits(plan.h_Kd.numpy(), plan.h_Kd.shape[0], plan.ndig_2)
+            vals = conv.ints_from_digits(plan.np_Kd, lay.groups, plan.ndig_2)
             counters.bump("add", lay.groups)
             counters.bump("group_mult", lay.groups)
             return ResponseMessage(COMBINED, qmsg.query_index, [],
