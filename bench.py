@@ -339,7 +339,8 @@ def run_b200(args):
     # in the step's graph, read after every replay
     # (steady state: each reading is the last of 20 back-to-back step replays)
     ge0, ge1 = plan.gemv_events
-    in_step = []
+    se0, se1 = plan.side_events
+    in_step, side_step = [], []
     plan.run("full_timed", stream)
     for i in range(12):
         for _ in range(20):
@@ -347,7 +348,10 @@ def run_b200(args):
         stream.synchronize()
         if i >= 2:
             in_step.append(ge0.elapsed_time(ge1))
+            if plan.ctas > 0:
+                side_step.append(se0.elapsed_time(se1))
     gemv_step_ms = statistics.mean(in_step)
+    side_step_ms = statistics.mean(side_step) if side_step else None
     # the GEMV kernel alone (all SMs); and the compression half
     gemv_ms = timed(lambda: plan.run("gemv", stream), args.steps)
     comp_ms = timed(lambda: plan.run("compress", stream), args.steps)
@@ -465,6 +469,7 @@ def run_b200(args):
                                 "achieved_gbs": answer_bytes / (ms / 1e3) / 1e9,
                                 "frac": answer_bytes / (ms / 1e3) / 1e9 / peak,
                                 "gemv_ms": gemv_ms, "compress_plus_groups_ms": comp_ms,
+                                "side_ms_in_step": side_step_ms,
                                 "schedule": f"GEMV on {plan.sms - plan.ctas} SMs || compression on "
                                             f"{plan.ctas} SMs, then group stage; CUDA graph"},
             "e2e": {"value": db_bytes_total / e2e_s / 1e9, "unit": "GB/s",

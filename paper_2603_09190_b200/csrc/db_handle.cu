@@ -260,7 +260,7 @@ struct zpir_db {
 namespace zpir {
 namespace {
 
-constexpr int kCompressCtas = 40;  // measured SM split
+constexpr int kCompressCtas = 36;  // measured SM split
 
 int umma_nb(int lm) { return lm == 32 ? 144 : lm == 64 ? 272 : lm == 96 ? 400 : 0; }
 

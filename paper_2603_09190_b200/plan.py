@@ -80,7 +80,9 @@ class AnswerPlan:
         self.graphs = {}
         self.gemv_events = (torch.cuda.Event(enable_timing=True),
                             torch.cuda.Event(enable_timing=True))
-        for e in self.gemv_events:     # torch creates the cudaEvent_t on first record
+        self.side_events = (torch.cuda.Event(enable_timing=True),
+                            torch.cuda.Event(enable_timing=True))
+        for e in self.gemv_events + self.side_events:   # torch creates the cudaEvent_t on first record
             e.record(torch.cuda.current_stream(dev))
         # respond(): the GEMV graph's completion, recorded outside the graphs
         self.ev_gemv = torch.cuda.Event()
@@ -132,8 +134,12 @@ class AnswerPlan:
             if self.ctas > 0:
                 self.ev_in.record(stream)
                 self.side.wait_event(self.ev_in)
+                if tev:
+                    device.event_record(self.side_events[0], self.side)
                 self._compress(self.side, self.ctas)
                 self._groups_z(self.side)      # overlaps the GEMV's tail
+                if tev:
+                    device.event_record(self.side_events[1], self.side)
                 self.ev_comp.record(self.side)
                 if tev:
                     device.event_record(tev[0], stream)

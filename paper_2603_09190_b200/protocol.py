@@ -46,7 +46,7 @@ COMBINED = "combined"
 ENGINE = os.environ.get("ZPIR_ENGINE", "umma")
 # SMs given to the compression GEMM while the GEMV streams the DB on the rest
 # (both are HBM-bound; H is ~1/8 of the DB bytes). 0 = run them back to back.
-COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "40"))
+COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "36"))
 # planar compression GEMM (H byte planes, one N = 4 lm MMA per k-step) for
 # lm = 32 / 64; ZPIR_PLANAR=0 selects the byte-shifted B operand kernels
 PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
