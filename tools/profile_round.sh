@@ -18,11 +18,14 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 PYTHONPATH=. python tools/profile_answer.py --plan full --reps 3 > $OUT/pa.log 2>&1 && {
   ncu --set full --import-source on --clock-control none -k regex:umma_gemm_kernel -s 2 -c 1 \
     -o $OUT/gemv -f python tools/profile_answer.py --plan full --reps 3 > $OUT/ncu_gemv.log 2>&1
-  ncu --set full --import-source on --clock-control none -k regex:umma_pair_bigint -s 1 -c 1 \
-    -o $OUT/compress -f python tools/profile_answer.py --plan full --reps 3 > $OUT/ncu_comp.log 2>&1
   ncu --set full --import-source on --clock-control none -k regex:answer_groups_kernel -s 1 -c 1 \
     -o $OUT/groups -f python tools/profile_answer.py --plan full --reps 3 > $OUT/ncu_groups.log 2>&1
 }
+# the global hint GEMM (setup): int8 tensor-pipe utilisation
+ncu --set full --import-source on --clock-control none -k regex:umma_gemm_kernel -s 0 -c 1 \
+  -o $OUT/hint_gemm -f python tools/profile_answer.py --plan gemv --reps 1 > $OUT/ncu_hintgemm.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:umma_planar -s 1 -c 1 \
+  -o $OUT/compress_planar -f python tools/profile_answer.py --plan full --reps 3 > $OUT/ncu_planar.log 2>&1
 PYTHONPATH=. python tools/profile_answer.py --hint --reps 1 > $OUT/ph.log 2>&1 && \
   ncu --set full --import-source on --clock-control none -k regex:slot_fixed -s 0 -c 1 \
     -o $OUT/slot_fixed -f python tools/profile_answer.py --hint --reps 1 > $OUT/ncu_slot.log 2>&1
