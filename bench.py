@@ -585,6 +585,26 @@ def run_extra(args):
                "gemv_ms": gemv, "compress_ms": comp,
                "gemv_u8xu32_macs_per_s": ops / 2 / (gemv / 1e3),
                "gemv_hbm_frac": (D0 * D1) / (gemv / 1e3) / 1e9 / peak}
+        # end to end through respond_batch(): 64 QueryMessages with host qu0 /
+        # Python-int ck_o in, 64 ResponseMessages of Python ints out
+        pk = z.PaillierPublicKey(m, m.bit_length())
+        reg = z.ClientRegistration(pk, b"\x05" * 16, z.client_id_of(pk))
+        reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(1)] * params.d1_prime)
+        qms = [z.QueryMessage(reg.client_id, 0, z.SEPARATE,
+                              [r.randrange(m) for _ in range(N_LWE)],
+                              q32[i, :D0].astype(np.uint64)) for i in range(nq)]
+        for _ in range(2):
+            z.respond_batch(st, [reg] * nq, qms)
+        te = []
+        for _ in range(max(3, args.steps // 40)):
+            t1 = time.perf_counter()
+            z.respond_batch(st, [reg] * nq, qms)
+            te.append(time.perf_counter() - t1)
+        e2e_s = statistics.mean(te)
+        out["e2e"] = {"value": nq * D0 * D1 / e2e_s / 1e9, "unit": "GB/s",
+                      "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond_batch()",
+                      "h2d_bytes_per_step": nq * (4 * D0 + 4 * kctx.lm * N_LWE),
+                      "d2h_bytes_per_step": nq * 4 * kctx.lm * params.d1_prime}
     elif args.workload == "update":
         params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
         db = db_slice(0, D1)

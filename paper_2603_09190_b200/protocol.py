@@ -830,37 +830,102 @@ def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
                 for r, q, md in zip(regs, qmsgs, modes)]
     out = []
     lm = kctxs[0].lm
+    conv = _digit_conv()
     for c0 in range(0, len(qmsgs), MAX_BATCH):
         qs = qmsgs[c0:c0 + MAX_BATCH]
         ks = kctxs[c0:c0 + MAX_BATCH]
         nq = len(qs)
-        q32 = np.zeros((nq, lay.ld), dtype=np.uint32)
+        out += _respond_chunk(state, qs, ks, modes[c0:c0 + nq], storeds[c0:c0 + nq], lm, conv,
+                              stream)
+    return out
+
+
+def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
+    """One respond_batch chunk: queries staged straight into pinned buffers
+    (qu0 narrowed, ck_o as raw CPython digits regrouped on the device), one
+    batched answer, all results regrouped to digits on the device and copied
+    out with one synchronisation."""
+    lay = state.layout
+    dev = state.device
+    nq, n = len(qs), lay.n
+    qbuf = _staging.get("qb", nq * lay.ld * 4).numpy().view(np.uint32).reshape(nq, lay.ld)
+    if lay.ld > lay.d0:
+        qbuf[:, lay.d0:] = 0
+    for i, q in enumerate(qs):
+        qu = q.qu0
+        if conv is not None and isinstance(qu, np.ndarray) and qu.ndim == 1 and \
+                qu.dtype.itemsize in (4, 8):
+            conv.narrow_u32(qu, qbuf[i], lay.d0)
+        else:
+            np.copyto(qbuf[i, : lay.d0], np.asarray(qu), casting="unsafe")
+    qd = torch.empty((nq, lay.ld), dtype=torch.int32, device=dev)
+    device.h2d_async(qd, torch.from_numpy(qbuf.view(np.int32)), stream)
+    _staging.mark("qb", stream)
+    cd = torch.empty((nq, n, lm), dtype=torch.int32, device=dev)
+    if conv is not None:
+        ndig = -(-32 * lm // 30)
+        cbuf = _staging.get("cbd", nq * n * ndig * 4).numpy().view(np.int32).reshape(nq * n, ndig)
         for i, q in enumerate(qs):
-            np.copyto(q32[i, : lay.d0], np.asarray(q.qu0), casting="unsafe")
-        qd = _h2d(q32, dev, "qb", stream).view(torch.int32).reshape(nq, lay.ld)
-        cko = np.empty((nq, lay.n, lm), dtype=np.uint32)
+            conv.digits_into(q.ck_o, cbuf[i * n:(i + 1) * n], ndig)
+        dd = torch.empty((nq * n, ndig), dtype=torch.int32, device=dev)
+        device.h2d_async(dd, torch.from_numpy(cbuf), stream)
+        _staging.mark("cbd", stream)
+        device.digits_to_limbs(dd, lm, cd.view(nq * n, lm), stream)
+    else:
+        cko = np.empty((nq, n, lm), dtype=np.uint32)
         for i, q in enumerate(qs):
             ints_to_limbs(q.ck_o, lm, out=cko[i])
-        cd = _h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, lay.n, lm)
-        t = state.answer_batch_device(qd, cd, ks, ks[0].l2, stream)
-        res = []
+        cd.copy_(_h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, n, lm))
+    t = state.answer_batch_device(qd, cd, ks, ks[0].l2, stream)      # (nq, groups, l2)
+    G = lay.groups
+    res = []
+    if conv is not None:
+        nd1, nd2 = -(-32 * lm // 30), -(-32 * ks[0].l2 // 30)
+        td = torch.empty((nq * G, nd1), dtype=torch.int32, device=dev)
+        device.limbs_to_digits(t.view(nq * G, -1), lm, td, stream)
+        outs = [("t", td, nd1)]
+        kd = {}
         for i in range(nq):
-            md = modes[c0 + i]
-            if md == SEPARATE:
-                res.append(t[i, :, :lm])
-            else:
-                k_dev = _stored_device(storeds[c0 + i], ks[i], dev, stream)
-                res.append(device.combine(t[i], k_dev, ks[i], stream=stream))
+            if modes[i] == COMBINED:
+                K = device.combine(t[i], _stored_device(storeds[i], ks[i], dev, stream), ks[i],
+                                   stream=stream)
+                kd[i] = torch.empty((G, nd2), dtype=torch.int32, device=dev)
+                device.limbs_to_digits(K, ks[i].l2, kd[i], stream)
+        hbuf = _staging.get("tb", (nq * G * nd1 + len(kd) * G * nd2) * 4)
+        hv = hbuf.numpy().view(np.int32)
+        device.d2h_async(hbuf[: nq * G * nd1 * 4], td, stream)
+        off = nq * G * nd1
+        koff = {}
+        for i, kt in kd.items():
+            device.d2h_async(hbuf[off * 4:(off + G * nd2) * 4], kt, stream)
+            koff[i] = off
+            off += G * nd2
+        _staging.mark("tb", stream)
+        stream.synchronize()
         for i in range(nq):
-            vals = limbs_to_ints(_d2h_u32(res[i].contiguous(), "tb", stream))
-            md = modes[c0 + i]
-            qi = qs[i].query_index
-            if md == SEPARATE:
-                out.append(ResponseMessage(SEPARATE, qi, vals, storeds[c0 + i].entries))
+            if modes[i] == SEPARATE:
+                seg = hv[i * G * nd1:(i + 1) * G * nd1]
+                res.append(conv.ints_from_digits(seg, G, nd1))
             else:
-                counters.bump("add", lay.groups)
-                counters.bump("group_mult", lay.groups)
-                out.append(ResponseMessage(COMBINED, qi, [], [PaillierCiphertext(v) for v in vals]))
+                seg = hv[koff[i]:koff[i] + G * nd2]
+                res.append(conv.ints_from_digits(seg, G, nd2))
+    else:
+        for i in range(nq):
+            if modes[i] == SEPARATE:
+                r = t[i, :, :lm]
+            else:
+                r = device.combine(t[i], _stored_device(storeds[i], ks[i], dev, stream), ks[i],
+                                   stream=stream)
+            res.append(limbs_to_ints(_d2h_u32(r.contiguous(), "tb", stream)))
+    out = []
+    for i, vals in enumerate(res):
+        qi = qs[i].query_index
+        if modes[i] == SEPARATE:
+            out.append(ResponseMessage(SEPARATE, qi, vals, storeds[i].entries))
+        else:
+            counters.bump("add", lay.groups)
+            counters.bump("group_mult", lay.groups)
+            out.append(ResponseMessage(COMBINED, qi, [], [PaillierCiphertext(v) for v in vals]))
     return out
 
 
