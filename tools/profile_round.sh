@@ -7,7 +7,7 @@ mkdir -p $OUT
 python -c "from paper_2603_09190_b200 import build; build.build()" > $OUT/build.log 2>&1 || exit 1
 python bench.py > $OUT/bench.json 2> $OUT/bench.err
 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err
-for w in batch64 8g hint update; do
+for w in tiny batch64 8g hint update; do
   python bench.py --workload $w --steps 20 --warmup 3 2>> $OUT/workloads.err | tail -1 >> $OUT/workloads.jsonl
 done
 # launch list of the bench command (plain run exited 0 above)
