@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128)
 slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __restrict__ E,
                   int64_t rs, const int32_t* __restrict__ row_ids, int64_t rows,
                   const uint32_t* __restrict__ N, uint32_t np, const uint32_t* __restrict__ one_m,
-                  uint32_t* __restrict__ out) {
+                  uint32_t* __restrict__ out, int S, uint32_t* __restrict__ part) {
   constexpr int L = 32 * LPL;
   extern __shared__ uint32_t smem_u32[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -248,7 +248,13 @@ slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __r
   uint16_t* list = reinterpret_cast<uint16_t*>(off + 256);
   uint32_t n_[LPL];
   big_load<LPL>(n_, N, lane);
-  for (int64_t gi = (int64_t)blockIdx.x * wpb + wid; gi < rows; gi += (int64_t)gridDim.x * wpb) {
+  // S > 1 (few rows): digit range s of the row's 255 buckets per warp,
+  // partial products to part[(gi*S + s)], multiplied together by slot_parts_kernel
+  for (int64_t wi = (int64_t)blockIdx.x * wpb + wid; wi < rows * S;
+       wi += (int64_t)gridDim.x * wpb) {
+    const int64_t gi = wi / S;
+    const int sp = (int)(wi - gi * S);
+    const uint32_t lo = 1u + (uint32_t)(255 * sp / S), hi = (uint32_t)(255 * (sp + 1) / S);
     const int64_t r = row_ids ? (int64_t)row_ids[gi] : gi;
     const uint32_t* er = E + r * rs;
 #pragma unroll
@@ -259,7 +265,7 @@ slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __r
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t d = (w >> (8 * i)) & 0xffu;
-        if (d) atomicAdd(&cnt[d], 1u);
+        if (d >= lo && d <= hi) atomicAdd(&cnt[d], 1u);
       }
     }
     __syncwarp();
@@ -288,13 +294,13 @@ slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __r
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t d = (w >> (8 * i)) & 0xffu;
-        if (d) list[atomicAdd(&off[d], 1u)] = (uint16_t)(i * n + k);
+        if (d >= lo && d <= hi) list[atomicAdd(&off[d], 1u)] = (uint16_t)(i * n + k);
       }
     }
     __syncwarp();
     bool has_run = false, has_tot = false;
     uint32_t run_[LPL], tot[LPL], bkt[LPL], x[LPL];
-    for (int d = 255; d >= 1; --d) {
+    for (int d = (int)hi; d >= (int)lo; --d) {
       const uint32_t cd = cnt[d];
       if (cd) {
         const uint32_t e = off[d], s0 = e - cd;
@@ -314,9 +320,45 @@ slot_fixed_kernel(const uint32_t* __restrict__ P, int64_t n, const uint32_t* __r
       }
     }
     if (!has_tot) big_load<LPL>(tot, one_m, lane);
-    big_store<LPL>(out + r * L, tot, lane);
+    if (S == 1) {
+      big_store<LPL>(out + r * L, tot, lane);
+    } else {
+      // tot = prod_{d in [lo, hi]} B_d^(d - lo + 1); times run^(lo - 1) gives
+      // prod B_d^d over the range (left-to-right binary, lo - 1 < 256)
+      if (has_run && lo > 1) {
+        const uint32_t e = lo - 1;
+        big_copy<LPL>(x, run_);
+        for (int b = 30 - __clz(e); b >= 0; --b) {
+          mont_mul<LPL>(x, x, x, n_, np, lane);
+          if ((e >> b) & 1u) mont_mul<LPL>(x, x, run_, n_, np, lane);
+        }
+        mont_mul<LPL>(tot, tot, x, n_, np, lane);
+      }
+      big_store<LPL>(part + (gi * S + sp) * L, tot, lane);
+    }
     __syncwarp();
   }
+}
+
+// out[row_ids[gi] or gi] = prod_s part[gi*S + s] (Montgomery form), one warp per row.
+template <int LPL>
+__global__ void __launch_bounds__(128)
+slot_parts_kernel(const uint32_t* __restrict__ part, int S, const int32_t* __restrict__ row_ids,
+                  int64_t rows, const uint32_t* __restrict__ N, uint32_t np,
+                  uint32_t* __restrict__ out) {
+  constexpr int L = 32 * LPL;
+  const int lane = threadIdx.x & 31;
+  const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gi >= rows) return;
+  uint32_t n_[LPL], acc[LPL], x[LPL];
+  big_load<LPL>(n_, N, lane);
+  big_load<LPL>(acc, part + gi * S * L, lane);
+  for (int sp = 1; sp < S; ++sp) {
+    big_load<LPL>(x, part + (gi * S + sp) * L, lane);
+    mont_mul<LPL>(acc, acc, x, n_, np, lane);
+  }
+  const int64_t r = row_ids ? (int64_t)row_ids[gi] : gi;
+  big_store<LPL>(out + r * L, acc, lane);
 }
 
 int64_t multiexp_workspace_bytes(int64_t n, int64_t rows, int elimbs, int limbs) {
@@ -414,13 +456,29 @@ int slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t r
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // split each row's buckets over S warps when there are too few rows to fill
+  // the GPU (small DBs, incremental refreshes of a few hundred rows)
+  const int64_t target = (int64_t)sms * 32;
+  int S = 1;
+  while (S < 8 && rows * S < target) S *= 2;
+  uint32_t* part = nullptr;
+  if (S > 1 && cudaMallocAsync(reinterpret_cast<void**>(&part), (size_t)rows * S * limbs * 4, st) !=
+                   cudaSuccess) {
+    cudaGetLastError();
+    S = 1;
+    part = nullptr;
+  }
   ZPIR_LPL_DISPATCH2(limbs / 32, {
     cudaFuncSetAttribute(slot_fixed_kernel<LPL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    const int64_t grid = std::min<int64_t>(ceil_div(rows, 4), (int64_t)sms * 16);
+    const int64_t grid = std::min<int64_t>(ceil_div(rows * S, 4), (int64_t)sms * 16);
     slot_fixed_kernel<LPL><<<(unsigned)grid, 128, smem, st>>>(P, n, E, rs, row_ids, rows, N, np,
-                                                              one_m, W);
+                                                              one_m, W, S, part);
+    if (S > 1)
+      slot_parts_kernel<LPL><<<(unsigned)ceil_div(rows, 4), 128, 0, st>>>(part, S, row_ids, rows,
+                                                                          N, np, W);
   });
+  if (part) cudaFreeAsync(part, st);
   return check_launch("slot_fixed");
 }
 
