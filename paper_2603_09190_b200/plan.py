@@ -38,6 +38,10 @@ class AnswerPlan:
             raise NotImplementedError("plans cover the tcgen05 path (lm 32/64/96, q = 2^32)")
         self.state, self.kctx, self.t_ld = state, kctx, t_ld
         self.ctas = compress_ctas
+        # the host-input graphs start the compression side ~25 us after the
+        # GEMV (ck_o is staged while the GEMV runs), so they give it more SMs
+        self.ctas_e2e = int(os.environ.get("ZPIR_COMPRESS_CTAS_E2E", str(compress_ctas + 8))) \
+            if compress_ctas > 0 else 0
         self.sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.qu = torch.zeros((1, lay.ld), dtype=torch.int32, device=dev)
         self.cko = torch.zeros((lay.n, lm), dtype=torch.int32, device=dev)
@@ -187,7 +191,7 @@ class AnswerPlan:
         elif which == "e2e_g1":
             # respond(), graph 1 (main stream): qu in, query planes, GEMV
             device.h2d_async(self.qu, self.h_qu, stream)
-            self._gemv(stream, self.sms - self.ctas)
+            self._gemv(stream, self.sms - self.ctas_e2e)
         elif which in ("e2e_g2", "e2e_g2t", "w_g2t"):
             # respond() / respond_wire(), graph 2 (side stream): ck_o in (CPython
             # digits, or limb rows for the wire path), compression, Montgomery
@@ -195,11 +199,11 @@ class AnswerPlan:
             # converts t to digits and copies it out, the others leave t in HBM
             if which == "w_g2t":
                 device.h2d_async(self.cko, self.h_cko, stream)
-                self._compress(stream, self.ctas)
-                self._groups_z(stream)
             else:
                 device.h2d_async(self.d_ckd, self.h_ckd, stream)
-                self._seq("side_digits", stream)
+                device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
+            self._compress(stream, self.ctas_e2e)
+            self._groups_z(stream)
             device.stream_wait_event(stream, self.ev_gemv)
             if which == "e2e_g2":
                 self._seq("finish_digits", stream)

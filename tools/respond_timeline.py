@@ -1,5 +1,5 @@
-"""Host/device timeline of one protocol.respond() (plan path) at the 1 GiB config:
-host timestamps of each step and device event times relative to the call entry."""
+"""Host/device timeline of one protocol.respond() (two-graph plan path) at the
+1 GiB config: host timestamps of each step and device events relative to entry."""
 import os
 import random
 import statistics
@@ -33,50 +33,43 @@ for _ in range(5):
 kctx = key_ctx(m, dev)
 plan = st.answer_plan(kctx, kctx.lm)
 s = torch.cuda.current_stream(dev)
+side = plan.side
 conv = protocol._digit_conv()
 lay = st.layout
 E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 rows = []
-for it in range(40):
+for it in range(60):
     H = {}
-    ev = {k: E() for k in ("start", "qu_in", "gemv_end", "side_end", "finish_end", "out")}
+    ev = {k: E() for k in ("start", "g1_end", "g2_end")}
+    for e in ev.values():
+        e.record(s)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ev["start"].record(s)
-    hq = plan.h_qu.numpy().view(np.uint32)
-    np.copyto(hq[: lay.d0], q.qu0, casting="unsafe")
-    H["stage_qu"] = time.perf_counter()
-    device.h2d_async(plan.qu, plan.h_qu, s)
-    ev["qu_in"].record(s)
-    plan.ev_in.record(s)
-    plan.run("gemv_part", s)
-    ev["gemv_end"].record(s)
-    H["gemv_launched"] = time.perf_counter()
-    conv.digits_into(q.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+    device.event_record(ev["start"], s)
+    conv.narrow_u32(q.qu0, plan.np_qu, lay.d0)
+    H["narrow"] = time.perf_counter()
+    plan.launch("e2e_g1", s)
+    device.event_record(plan.ev_gemv, s)
+    device.event_record(ev["g1_end"], s)
+    H["g1_launched"] = time.perf_counter()
+    conv.digits_into(q.ck_o, plan.np_ckd, plan.ndig_m)
     H["digits"] = time.perf_counter()
-    side = plan.side
-    side.wait_event(plan.ev_in)
-    device.h2d_async(plan.d_ckd, plan.h_ckd, side)
-    plan.run("side_digits", side)
-    ev["side_end"].record(side)
-    s.wait_stream(side)
-    plan.run("finish_digits", s)
-    ev["finish_end"].record(s)
-    device.d2h_async(plan.h_td, plan.d_td, s)
-    ev["out"].record(s)
-    H["all_launched"] = time.perf_counter()
-    s.synchronize()
+    plan.launch("e2e_g2", side)
+    device.event_record(ev["g2_end"], side)
+    H["g2_launched"] = time.perf_counter()
+    side.synchronize()
     H["synced"] = time.perf_counter()
-    vals = conv.ints_from_digits(plan.h_td.numpy(), plan.h_td.shape[0], plan.ndig_m)
+    vals = conv.ints_from_digits(plan.np_td, lay.groups, plan.ndig_m)
     H["ints"] = time.perf_counter()
-    if it >= 5:
+    if it >= 10:
         row = {k: (v - t0) * 1e6 for k, v in H.items()}
-        for k in ("qu_in", "gemv_end", "side_end", "finish_end", "out"):
-            row["dev_" + k] = ev["start"].elapsed_time(ev[k]) * 1e3
+        row["dev_g1_end"] = ev["start"].elapsed_time(ev["g1_end"]) * 1e3
+        row["dev_g2_end"] = ev["start"].elapsed_time(ev["g2_end"]) * 1e3
         rows.append(row)
 for k in rows[0]:
-    print(f"{k:18s} {statistics.median(r[k] for r in rows):8.1f} us")
+    print(f"{k:14s} {statistics.median(x[k] for x in rows):8.1f} us")
 t = []
-for _ in range(30):
+for _ in range(50):
     a = time.perf_counter()
     z.respond(st, reg, q)
     t.append((time.perf_counter() - a) * 1e6)
