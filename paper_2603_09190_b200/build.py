@@ -47,7 +47,7 @@ def build_conv(force=False):
     if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
         return out
     tmp = out + ".tmp"
-    subprocess.check_call(["gcc", "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
+    subprocess.check_call(["gcc", "-O3", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"],
                            src, "-o", tmp])
     os.replace(tmp, out)
     return out

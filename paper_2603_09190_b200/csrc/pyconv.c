@@ -279,8 +279,9 @@ static PyObject* narrow_u32(PyObject* self, PyObject* args) {
   Py_BEGIN_ALLOW_THREADS
   if (item == 8) {
     if (stride == 8) {
-      const uint64_t* q = (const uint64_t*)p;
-      for (Py_ssize_t i = 0; i < n; ++i) out[i] = (uint32_t)q[i];
+      const uint64_t* __restrict__ q = (const uint64_t*)p;
+      uint32_t* __restrict__ o = out;
+      for (Py_ssize_t i = 0; i < n; ++i) o[i] = (uint32_t)q[i];
     } else {
       for (Py_ssize_t i = 0; i < n; ++i) out[i] = (uint32_t)*(const uint64_t*)(p + i * stride);
     }
