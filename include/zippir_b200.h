@@ -230,6 +230,14 @@ int zpir_pow8_table(const uint32_t* bases, int64_t n, int limbs, const uint32_t*
 int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t row_stride,
                     const int32_t* row_ids, int64_t rows, int limbs, const uint32_t* N,
                     uint32_t np, const uint32_t* one_m, uint32_t* W, void* stream);
+/* zpir_slot_fixed for rows 0..rows-1 with the Pippenger bucket updates on the
+ * tensor cores (position-major: each position multiplies one bucket per row by
+ * the same P[pos]; Montgomery by a fixed multiplier = three byte-Toeplitz int8
+ * GEMMs); 4096-bit N only (limbs = 128). Nprime = -N^-1 mod 2^4096 (128 limbs).
+ * Transient workspace ~ rows * 130 KB + 4n * 320 KB. */
+int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
+                       int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
+                       const uint32_t* Nprime, uint32_t* W, void* stream);
 /* flags[r] = (row r of a != row r of b), rows of ld bytes. */
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,
                      void* stream);

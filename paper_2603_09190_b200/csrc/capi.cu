@@ -47,6 +47,9 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int tc_slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
+                         const uint32_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*,
+                         cudaStream_t);
 int h_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, cudaStream_t);
 int build_bcp_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int umma_planar_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int, int, int, uint32_t*,
@@ -192,6 +195,16 @@ int zpir_umma_answer_rows(const uint32_t* H, int64_t rows, int64_t n, const uint
 }
 
 int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(blocks, iters, ms)); }
+
+int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
+                       int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
+                       const uint32_t* Nprime, uint32_t* W, void* stream) {
+  if (limbs != 128) {
+    set_error("slot_fixed_tc: the tensor-core path is built for 4096-bit N (limbs=%d)", limbs);
+    return kErrUnsupported;
+  }
+  ZPIR_GUARD(tc_slot_fixed_launch(P, n, E, rs, rows, N, np, one_m, Nprime, W, S(stream)));
+}
 
 int zpir_h_planes(const uint32_t* H, int64_t rows, int64_t n, uint8_t* hp, void* stream) {
   ZPIR_GUARD(h_planes_launch(H, rows, n, hp, S(stream)));

@@ -317,6 +317,14 @@ def slot_fixed(P, n, E, rs, row_ids, rows, kctx, W, stream=None):
     return W
 
 
+def slot_fixed_tc(P, n, E, rs, rows, kctx, W, stream=None):
+    """slot_fixed (all rows) with the bucket updates on the tensor cores."""
+    _lib.call("zpir_slot_fixed_tc", _lib.ptr(P), n, _lib.ptr(E), rs, rows, kctx.l2,
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_one2), _lib.ptr(kctx.d_nprime_full()),
+              _lib.ptr(W), _s(stream))
+    return W
+
+
 def groups_z(z, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, tz, t_ld, stream=None,
              stride=1):
     rows, wz = z.shape[-2], z.shape[-1]

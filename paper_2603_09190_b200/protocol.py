@@ -50,6 +50,8 @@ COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "36"))
 # planar compression GEMM (H byte planes, one N = 4 lm MMA per k-step) for
 # lm = 32 / 64; ZPIR_PLANAR=0 selects the byte-shifted B operand kernels
 PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
+# per-client hints: Pippenger bucket updates on the tensor cores (4096-bit m^2)
+TC_HINT = os.environ.get("ZPIR_TC_HINT", "1") != "0"
 
 
 @dataclass
@@ -493,7 +495,10 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     nslot = lay.groups * lay.cap
     W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
     P = device.pow8_table(bases, kctx, stream)
-    device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
+    if TC_HINT and kctx.l2 == 128 and 4 * lay.n <= 65536:
+        device.slot_fixed_tc(P, lay.n, state.H_dev, lay.n, nslot, kctx, W, stream)
+    else:
+        device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
     out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
     device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, lay.gamma, stream)
     entries = limbs_to_ints(_d2h_u32(out, "hint", stream))

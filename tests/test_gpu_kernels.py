@@ -197,3 +197,33 @@ def test_planar_compression(env, lm, n, rows, nq, ctas):
     for q in range(nq):
         zr = device.to_host_u32(device.answer_rows(Hd, bd, 0xFFFFFFFF, cd[q].contiguous(), lm))
         assert np.array_equal(z[q], zr), q
+
+
+@pytest.mark.parametrize("n,rows", [(64, 300), (256, 129), (32, 128)])
+def test_slot_fixed_tensor_core(env, n, rows):
+    """Tensor-core Pippenger bucket updates (fixed-multiplier Montgomery as three
+    byte-Toeplitz int8 GEMMs) == the IMAD warp path, bit for bit (2048-bit m,
+    4096-bit m^2), incl. zero digits, all-255 rows and a partial last tile."""
+    torch, device = env
+    from oracle import client
+    from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
+    dev = torch.device("cuda", 0)
+    rng = random.Random(n * 7 + rows)
+    sk = client.keygen(2048, random.Random(2048 + n))
+    kctx = key_ctx(sk.m, dev)
+    m2 = kctx.m2
+    bases = device.u32_tensor(ints_to_limbs([rng.randrange(m2) for _ in range(n)], kctx.l2), dev)
+    P = device.pow8_table(bases, kctx)
+    nrng = np.random.default_rng(n + rows)
+    E = nrng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
+    E[0] = 0
+    E[1] = 0xFFFFFFFF
+    E[2, : n // 2] = 0
+    Ed = device.u32_tensor(E, dev)
+    W1 = torch.empty((rows, kctx.l2), dtype=torch.int32, device=dev)
+    W2 = torch.empty_like(W1)
+    device.slot_fixed(P, n, Ed, n, None, rows, kctx, W1)
+    device.slot_fixed_tc(P, n, Ed, n, rows, kctx, W2)
+    a, b = device.to_host_u32(W1), device.to_host_u32(W2)
+    bad = [i for i in range(rows) if not np.array_equal(a[i], b[i])]
+    assert not bad, f"{len(bad)} rows differ, first {bad[:5]}"
