@@ -238,6 +238,19 @@ int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t 
 int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
                        const uint32_t* Nprime, uint32_t* W, void* stream);
+/* zpir_slot_fixed_tc for `clients` independent keys in one launch (the hint
+ * worker's batch; also the incremental refresh): client c's table P[c]
+ * (4n x 128 limbs), N[c] / one_m[c] / Nprime[c] (128 limbs each) and output
+ * rows W[c] are device addresses passed in HOST arrays; np is a host array.
+ * Rows r < rows read exponent row e = row_ids ? row_ids[r] : r and write
+ * W[c][e]. Replaces paillier.multiexp (paillier.py:134-193) as called by
+ * protocol.hint (protocol.py:291-296) for each client of a batch.
+ * Transient workspace: zpir_slot_fixed_tc_workspace(n, rows, clients) bytes. */
+int zpir_slot_fixed_tc_many(int clients, const uint64_t* P, const uint64_t* N, const uint32_t* np,
+                            const uint64_t* one_m, const uint64_t* Nprime, const uint64_t* W,
+                            int64_t n, const uint32_t* E, int64_t rs, const int32_t* row_ids,
+                            int64_t rows, void* stream);
+int64_t zpir_slot_fixed_tc_workspace(int64_t n, int64_t rows, int clients);
 /* flags[r] = (row r of a != row r of b), rows of ld bytes. */
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,
                      void* stream);

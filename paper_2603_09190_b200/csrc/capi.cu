@@ -50,6 +50,11 @@ int imad_probe(int, int, float*);
 int tc_slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
                          const uint32_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*,
                          cudaStream_t);
+int tc_slot_fixed_many_launch(int, const uint32_t* const*, const uint32_t* const*, const uint32_t*,
+                              const uint32_t* const*, const uint32_t* const*, uint32_t* const*,
+                              int64_t, const uint32_t*, int64_t, const int32_t*, int64_t,
+                              cudaStream_t);
+int64_t tc_slot_fixed_workspace(int64_t, int64_t, int);
 int h_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, cudaStream_t);
 int build_bcp_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int umma_planar_launch(const uint8_t*, int64_t, int64_t, const uint8_t*, int, int, int, uint32_t*,
@@ -204,6 +209,25 @@ int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t 
     return kErrUnsupported;
   }
   ZPIR_GUARD(tc_slot_fixed_launch(P, n, E, rs, rows, N, np, one_m, Nprime, W, S(stream)));
+}
+
+int zpir_slot_fixed_tc_many(int clients, const uint64_t* P, const uint64_t* N, const uint32_t* np,
+                            const uint64_t* one_m, const uint64_t* Nprime, const uint64_t* W,
+                            int64_t n, const uint32_t* E, int64_t rs, const int32_t* row_ids,
+                            int64_t rows, void* stream) {
+  if (!P || !N || !np || !one_m || !Nprime || !W) {
+    set_error("slot_fixed_tc_many: null client array");
+    return kErrInput;
+  }
+  ZPIR_GUARD(tc_slot_fixed_many_launch(
+      clients, reinterpret_cast<const uint32_t* const*>(P), reinterpret_cast<const uint32_t* const*>(N),
+      np, reinterpret_cast<const uint32_t* const*>(one_m),
+      reinterpret_cast<const uint32_t* const*>(Nprime), reinterpret_cast<uint32_t* const*>(W), n, E,
+      rs, row_ids, rows, S(stream)));
+}
+
+int64_t zpir_slot_fixed_tc_workspace(int64_t n, int64_t rows, int clients) {
+  return tc_slot_fixed_workspace(n, rows, clients);
 }
 
 int zpir_h_planes(const uint32_t* H, int64_t rows, int64_t n, uint8_t* hp, void* stream) {

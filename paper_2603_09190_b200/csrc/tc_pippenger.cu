@@ -4,22 +4,33 @@
 // W[r] = prod_{pos < 4n} P[pos]^{digit(r, pos)}, digit(r, pos) = byte (pos / n)
 // of H[r][pos % n], P[pos] = ck_r[pos % n]^(2^(8 (pos / n))) (pow8_table, Montgomery
 // form mod N = m^2). Position-major Pippenger: at every position each row
-// multiplies ONE of its 255 buckets by the same P[pos], so a position is a
-// batch "X (rows) times fixed Y mod N" -- three Toeplitz int8 GEMMs:
+// multiplies ONE of its 255 buckets by the same Y = P[pos], so a position is a
+// batch "X (rows) times fixed Y mod N" -- Toeplitz int8 GEMMs:
 //   u = X * Y' mod R          (Y' = Y * N' mod R, N' = -N^-1 mod R, R = 2^4096)
-//   Z = (X * Y + u * N) / R   (< 2N; one conditional subtraction)
-// with a byte-Toeplitz B operand Toep(y)[j][a] = byte_{j-a}(y). Tiles of
-// Toep(y) (256 output columns x 128 K bytes) depend only on delta = c0 - a0, so
-// each multiplier is stored as 6 SW128 tiles (delta = -128 .. 512). One CTA per
-// 128-row tile per position: 30 k-blocks (120 N = 256 MMAs, ~146 cycles each),
-// three TMEM drains with carry chains in registers; X (gathered from the
-// buckets) and u live in shared memory as the MMAs' A operands.
-// The bucket combine (prod_d B_d^d, running sums, per-row operands) stays on
-// the IMAD warp-Montgomery path.
+//   Z = (X * Y + u * N) / R   (< 2N; the conditional subtraction is deferred)
+// with a byte-Toeplitz B operand Toep(y)[j][a] = byte_{delta + j - a}(y).
+//
+// Only 1028 of the 1536 byte columns of u and X*Y + u*N are ever drained from
+// TMEM: S = X*Y + u*N is an exact multiple of R, every column sum is < 2^27,
+// so the carry out of the low half is ceil(low4 / 2^32) with low4 the 4 byte
+// columns 508..511 (the columns below add e < 2^20 to low4 / 2^32 and the total
+// is an integer). Per position and 128-row tile: four 256-column tasks
+//   U0, U1: columns 0..255 / 256..511 of X * Y'        -> u into shared memory
+//   H0:     columns 508..763 of X * Y + u * N           -> carry, Z limbs 0..62
+//   H1:     columns 764..1019                           -> Z limbs 63..126
+// and the three top columns 1020..1022 (12 byte products) on the CUDA cores.
+// 20 k-blocks (80 N = 256 MMAs) per position; the tasks ping-pong two TMEM
+// buffers so the epilogue drains one while the MMA warp fills the other.
+//
+// Several clients (independent keys) run in one launch: blockIdx.y = client,
+// every client with its own Toeplitz tiles, buckets and output rows; rows may be
+// a subset of the exponent rows (row ids), which is the incremental refresh.
+// The bucket combine (prod_d B_d^d, running sums) stays on the IMAD warp path.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "bignum.cuh"
 #include "umma.cuh"
@@ -34,33 +45,51 @@ constexpr int kL = 128;            // limbs of N = m^2 (2048-bit m)
 constexpr int kRows = 128;         // rows per tile (TMEM lanes)
 constexpr int kBK = 128;           // K bytes per k-block
 constexpr int kTile = 256 * kBK;   // one Toeplitz tile: 256 columns x 128 K bytes
-constexpr int kTY = 6;             // tiles per multiplier (delta = -128 .. 512)
-constexpr int kTYp = 4;            // tiles of Y' (columns < 512: delta = -128 .. 256)
+constexpr int kTYp = 4;            // Y' tiles: delta = -128 + 128 t (U0, U1)
+constexpr int kDeltaYp = -128;
+constexpr int kTY = 5;             // Y / N tiles: delta = 124 + 128 t (H0, H1)
+constexpr int kDeltaY = 124;
 constexpr int kStages = 3;
 constexpr int kThreads = 192;
 constexpr int kABytes = kRows * 512;     // one 128 x 512-byte A operand (4 k-blocks)
 constexpr int kSmem = 2 * kABytes + kStages * kTile + 1024 + 1024;
+constexpr int kNSteps = 20;
 
-// The static MMA schedule: (phase, TMEM chunk, A = X (0) / U (1), k-block,
-// B source (0 = Y', 1 = Y, 2 = N), tile index t = 2 cc - ka + 1).
+// The static MMA schedule: task (0 U0, 1 U1, 2 H0, 3 H1; TMEM buffer = task & 1),
+// A operand (0 = X, 1 = u), k-block, B source (0 = Y', 1 = Y, 2 = N), tile t.
 struct Step {
-  int8_t phase, chunk, a, ka, src, t;
+  int8_t task, a, ka, src, t;
 };
-__constant__ Step kSched[30];
-constexpr int kNSteps = 30;
+__constant__ Step kSched[kNSteps];
 
 }  // namespace tcp
 
-// tiles[(c * T + t) * 256 + j][a] = byte_{128 (t - 1) + j - a}(y_c), zero outside [0, 512)
+// Per-client arguments of one batched launch (device copy).
+struct TcClient {
+  const uint32_t* P;        // (npos, 128) Montgomery multipliers
+  const uint32_t* N;        // 128 limbs of N = m^2
+  const uint32_t* one;      // R mod N
+  const uint32_t* Nprime;   // -N^-1 mod R
+  uint32_t* W;              // output rows (Montgomery form), indexed by exponent row
+  uint32_t np;              // -N^-1 mod 2^32
+};
+
+// tiles[((c * npos + p) * T + t) * 256 + j][a] = byte_{delta0 + 128 t + j - a}(y_{c,p}),
+// zero outside [0, 512); y = Y[c][p] (fixed-stride) or the client's N (npos = 1).
 __global__ void __launch_bounds__(256)
-toep_tiles_kernel(const uint32_t* __restrict__ Y, int T, uint8_t* __restrict__ tiles) {
-  const int64_t ct = blockIdx.x;                 // c * T + t
-  const int64_t c = ct / T;
-  const int t = (int)(ct - c * T);
+toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __restrict__ Ybase,
+                  int64_t npos, int T, int delta0, uint8_t* __restrict__ tiles) {
+  const int64_t pt = blockIdx.x;                 // p * T + t
+  const int c = blockIdx.y;
+  const int64_t p = pt / T;
+  const int t = (int)(pt - p * T);
   const int j = threadIdx.x;
-  const uint8_t* y = reinterpret_cast<const uint8_t*>(Y + c * tcp::kL);
-  const int delta = 128 * (t - 1);
-  uint8_t* row = tiles + (ct * 256 + j) * tcp::kBK;
+  const uint32_t* ysrc = which == 0   ? cl[c].P + p * tcp::kL
+                         : which == 1 ? Ybase + ((int64_t)c * npos + p) * tcp::kL
+                                      : cl[c].N;
+  const uint8_t* y = reinterpret_cast<const uint8_t*>(ysrc);
+  const int delta = delta0 + 128 * t;
+  uint8_t* row = tiles + (((int64_t)c * npos * T + pt) * 256 + j) * tcp::kBK;
 #pragma unroll 1
   for (int a0 = 0; a0 < tcp::kBK; a0 += 16) {
     uint32_t w[4];
@@ -79,19 +108,20 @@ toep_tiles_kernel(const uint32_t* __restrict__ Y, int T, uint8_t* __restrict__ t
   }
 }
 
-// out[c] = Y[c] * Np mod 2^4096, one thread per value (product scanning).
+// out[c][p] = P_c[p] * Nprime_c mod 2^4096, one thread per value (product scanning).
 __global__ void __launch_bounds__(128)
-mul_lo_kernel(const uint32_t* __restrict__ Y, int64_t count, const uint32_t* __restrict__ Np,
-              uint32_t* __restrict__ out) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= count) return;
-  const uint32_t* y = Y + c * tcp::kL;
-  uint32_t* o = out + c * tcp::kL;
+mul_lo_kernel(const TcClient* __restrict__ cl, int64_t npos, uint32_t* __restrict__ out) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y;
+  if (p >= npos) return;
+  const uint32_t* y = cl[c].P + p * tcp::kL;
+  const uint32_t* Np = cl[c].Nprime;
+  uint32_t* o = out + ((int64_t)c * npos + p) * tcp::kL;
   unsigned long long lo = 0, hi = 0;  // 128-bit column accumulator (lo, hi)
   for (int k = 0; k < tcp::kL; ++k) {
     for (int i = 0; i <= k; ++i) {
-      const unsigned long long p = (unsigned long long)y[i] * Np[k - i];
-      const unsigned long long s = lo + p;
+      const unsigned long long pr = (unsigned long long)y[i] * Np[k - i];
+      const unsigned long long s = lo + pr;
       hi += (s < lo);
       lo = s;
     }
@@ -101,25 +131,29 @@ mul_lo_kernel(const uint32_t* __restrict__ Y, int64_t count, const uint32_t* __r
   }
 }
 
-__global__ void bucket_fill_kernel(uint32_t* __restrict__ B, int64_t count,
-                                   const uint32_t* __restrict__ one) {
+__global__ void bucket_fill_kernel(const TcClient* __restrict__ cl, uint32_t* __restrict__ B,
+                                   int64_t count) {
+  const int c = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // u32 index
-  if (i < count * tcp::kL) B[i] = one[i % tcp::kL];
+  if (i < count * tcp::kL) B[(int64_t)c * count * tcp::kL + i] = cl[c].one[i % tcp::kL];
 }
 
-// W[r] = prod_d B[r][d]^d (running sums from d = 255 down), Montgomery form.
+// W[row] = prod_d B[r][d]^d (running sums from d = 255 down), Montgomery form.
 // Buckets are stored lazily reduced: flag F[r][d] set means "subtract N (mod R)".
 __global__ void __launch_bounds__(128)
-bucket_combine_kernel(const uint32_t* __restrict__ B, const uint8_t* __restrict__ F, int64_t rows,
-                      const uint32_t* __restrict__ N, uint32_t np, uint32_t* __restrict__ W) {
+bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Ball,
+                      const uint8_t* __restrict__ Fall, int64_t rows, int64_t rows_p,
+                      const int32_t* __restrict__ rid) {
   constexpr int LPL = tcp::kL / 32;
   const int lane = threadIdx.x & 31;
+  const int c = blockIdx.y;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= rows) return;
+  const uint32_t np = cl[c].np;
   uint32_t n_[LPL], run[LPL], tot[LPL], x[LPL];
-  big_load<LPL>(n_, N, lane);
-  const uint32_t* br = B + r * 255 * tcp::kL;
-  const uint8_t* fr = F + r * 255;
+  big_load<LPL>(n_, cl[c].N, lane);
+  const uint32_t* br = Ball + ((int64_t)c * rows_p + r) * 255 * tcp::kL;
+  const uint8_t* fr = Fall + ((int64_t)c * rows_p + r) * 255;
   big_load<LPL>(run, br + 254 * tcp::kL, lane);
   if (fr[254]) big_cond_sub<LPL>(run, 1u, n_, lane);
   big_copy<LPL>(tot, run);
@@ -129,40 +163,55 @@ bucket_combine_kernel(const uint32_t* __restrict__ B, const uint8_t* __restrict_
     mont_mul<LPL>(run, run, x, n_, np, lane);
     mont_mul<LPL>(tot, tot, run, n_, np, lane);
   }
-  big_store<LPL>(W + r * tcp::kL, tot, lane);
+  const int64_t orow = rid ? (int64_t)rid[r] : r;
+  big_store<LPL>(cl[c].W + orow * tcp::kL, tot, lane);
 }
 
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// Carry-propagate 16 TMEM columns (byte positions) into 4 u32 limbs.
-__device__ __forceinline__ void carry4(const uint32_t (&v)[16], unsigned long long& carry,
-                                       uint32_t (&limb)[4]) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const unsigned long long s = (unsigned long long)v[4 * i] +
-                                 ((unsigned long long)v[4 * i + 1] << 8) +
-                                 ((unsigned long long)v[4 * i + 2] << 16) +
-                                 ((unsigned long long)v[4 * i + 3] << 24) + carry;
-    limb[i] = (uint32_t)s;
-    carry = s >> 32;
-  }
+// 32 lanes x 32 bit, 32 consecutive columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
 }
 
-// Pippenger positions pos0..pos1-1 for one 128-row tile per CTA (tiles are
-// independent: a row only touches its own buckets):
+// 64 TMEM columns of this thread's lane -> v[64], ordered after the wait.
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
+  tmem_ld32(taddr, v);
+  tmem_ld32(taddr + 32, v + 32);
+  tmem_wait_ld();
+#pragma unroll
+  for (int i = 0; i < 64; ++i) asm volatile("" : "+r"(v[i]));
+}
+
+// Four byte columns (s32 sums) + carry -> one 32-bit limb.
+__device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long& carry) {
+  const unsigned long long s = (unsigned long long)v[0] + ((unsigned long long)v[1] << 8) +
+                               ((unsigned long long)v[2] << 16) +
+                               ((unsigned long long)v[3] << 24) + carry;
+  carry = s >> 32;
+  return (uint32_t)s;
+}
+
+// Pippenger positions pos0..pos1-1 for one 128-row tile of one client per CTA
+// (tiles are independent: a row only touches its own buckets):
 //   B[r][d - 1] *= P[pos] for d = digit(r, pos) != 0.
-// Per position, six 256-column tasks alternate between two TMEM buffers so
-// the epilogue drains one while the MMA warp fills the other:
-//   U0, U1: columns 0..255 / 256..511 of X * Y'    -> u (mod R) into smem
-//   L0, L1: columns 0..511 of X * Y + u * N        -> carry out of bit 4096
-//   H0, H1: columns 512..1023                       -> Z (< 2N), kept in registers
 __global__ void __launch_bounds__(tcp::kThreads, 1)
 tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant__ CUtensorMap mapY,
-               const __grid_constant__ CUtensorMap mapN, const uint32_t* __restrict__ E,
-               int64_t rs, int64_t n, int pos0, int pos1, int64_t rows, uint32_t* __restrict__ Bk,
-               uint8_t* __restrict__ Fk, const uint32_t* __restrict__ Nlimbs) {
+               const __grid_constant__ CUtensorMap mapN, const TcClient* __restrict__ cl,
+               const uint32_t* __restrict__ E, int64_t rs, const int32_t* __restrict__ rid,
+               int64_t n, int64_t npos, int pos0, int pos1, int64_t rows, int64_t rows_p,
+               uint32_t* __restrict__ Ball, uint8_t* __restrict__ Fall) {
   using namespace tcp;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -173,12 +222,13 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
   uint64_t* full = reinterpret_cast<uint64_t*>(BS + kStages * kTile);
   uint64_t* empty = full + kStages;
   uint64_t* xfull = empty + kStages;
-  uint64_t* uready = xfull + 1;             // [2]: u bytes 0..255 / 256..511 written
-  uint64_t* tfull = uready + 2;             // [2] per TMEM buffer
+  uint64_t* uready = xfull + 1;             // all 512 bytes of u written
+  uint64_t* tfull = uready + 1;             // [2] per TMEM buffer
   uint64_t* tempty = tfull + 2;             // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* sN = tslot + 4;                 // N limbs (512 B)
 
+  const int client = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&mapYp);
@@ -189,14 +239,15 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       mbar_init(&empty[s], 1);
     }
     mbar_init(xfull, 128);
+    mbar_init(uready, 128);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&uready[b], 128);
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128);
     }
     fence_mbar_init();
   }
-  for (int i = threadIdx.x; i < kL; i += blockDim.x) sN[i] = Nlimbs[i];
+  const uint32_t* Ncl = cl[client].N;
+  for (int i = threadIdx.x; i < kL; i += blockDim.x) sN[i] = Ncl[i];
   if (warp == 1) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
@@ -206,8 +257,9 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: the 30 B tiles of every position ----------------
+      // ---------------- TMA producer: the 20 B tiles of every position ----------------
       const uint64_t pol = l2_evict_last();
+      const int64_t cpos = (int64_t)client * npos;
       int stage = 0;
       uint32_t phase = 0;
       for (int pos = pos0; pos < pos1; ++pos)
@@ -217,11 +269,13 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
           mbar_expect_tx(&full[stage], kTile);
           uint8_t* dst = BS + stage * kTile;
           if (st.src == 0)
-            tma_load_2d_hint(dst, &mapYp, &full[stage], 0, (pos * kTYp + st.t) * 256, pol);
+            tma_load_2d_hint(dst, &mapYp, &full[stage], 0, (int)(((cpos + pos) * kTYp + st.t) * 256),
+                             pol);
           else if (st.src == 1)
-            tma_load_2d_hint(dst, &mapY, &full[stage], 0, (pos * kTY + st.t) * 256, pol);
+            tma_load_2d_hint(dst, &mapY, &full[stage], 0, (int)(((cpos + pos) * kTY + st.t) * 256),
+                             pol);
           else
-            tma_load_2d_hint(dst, &mapN, &full[stage], 0, st.t * 256, pol);
+            tma_load_2d_hint(dst, &mapN, &full[stage], 0, (client * kTY + st.t) * 256, pol);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -230,7 +284,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer: tasks 0..5 per position, buffer = task & 1 ----------------
+      // ---------------- MMA issuer: tasks 0..3 per position, buffer = task & 1 ----------------
       const uint32_t idesc = idesc_u8(kRows, 256);
       int stage = 0;
       uint32_t phase = 0, xph = 0;
@@ -241,22 +295,21 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         bool first = true, uwait = false;
         for (int s = 0; s < kNSteps; ++s) {
           const Step st = kSched[s];
-          const int buf = st.phase & 1;
-          if (st.phase != cur) {
+          const int buf = st.task & 1;
+          if (st.task != cur) {
             if (cur >= 0) umma_commit(&tfull[cur & 1]);
             if (used[buf]) {                  // the epilogue has drained this buffer
               mbar_wait(&tempty[buf], eph[buf]);
               eph[buf] ^= 1;
             }
             used[buf] = true;
-            if (st.phase == 0) mbar_wait(xfull, xph);
+            if (st.task == 0) mbar_wait(xfull, xph);
             tc_fence_after();
-            cur = st.phase;
+            cur = st.task;
             first = true;
-            uwait = false;
           }
-          if (st.a && !uwait) {               // u * N: u bytes of this column range ready
-            mbar_wait(&uready[st.phase == 2 ? 0 : 1], xph);
+          if (st.a && !uwait) {               // u * N: all of u written by the epilogue
+            mbar_wait(uready, xph);
             tc_fence_after();
             uwait = true;
           }
@@ -281,92 +334,202 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       }
     }
   } else {
-    // ---------------- epilogue: one row per thread ----------------
+    // ---------------- epilogue: one row per thread (TMEM lane), 4 warps ----------------
     const int quarter = warp & 3;
     const int t = quarter * 32 + lane;          // row within the tile = TMEM lane
     const int64_t r = row0 + t;
+    const int64_t er = r < rows ? (rid ? (int64_t)rid[r] : r) : 0;
+    uint32_t* Bc = Ball + (int64_t)client * rows_p * 255 * kL;
+    uint8_t* Fc = Fall + (int64_t)client * rows_p * 255;
+    const uint32_t* Pc = cl[client].P;
     const uint32_t lanebase = tbase + ((uint32_t)(quarter * 32) << 16);
+    uint32_t nl[4];                             // N limbs 4 lane .. 4 lane + 3 (gather)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nl[i] = sN[4 * lane + i];
+    const uint32_t ntop = sN[kL - 1];
     uint32_t fph[2] = {0, 0};
+    // digit, bucket and flag of this row at position pos (software-pipelined:
+    // the next position's are loaded and its bucket prefetched into L2 while
+    // this position's MMAs run)
+    auto digit_at = [&](int p) -> uint32_t {
+      if (r >= rows) return 0u;
+      const int di = p / (int)n;
+      return (E[er * rs + (p - (int64_t)di * n)] >> (8 * di)) & 0xffu;
+    };
+    uint32_t dg = digit_at(pos0);
+    uint32_t lazy = (dg && Fc[r * 255 + dg - 1]) ? 1u : 0u;
     for (int pos = pos0; pos < pos1; ++pos) {
-      const int dig_i = pos / (int)n;
-      const int64_t dig_k = pos - (int64_t)dig_i * n;
-      uint32_t dg = 0;
-      if (r < rows) dg = (E[r * rs + dig_k] >> (8 * dig_i)) & 0xffu;
       const int64_t bidx = (r * 255) + (dg ? dg - 1 : 0);
-      uint32_t* brow = Bk + bidx * kL;
-      // gather X = B[r][dg - 1] into the SW128 A layout (zero rows for dg == 0);
-      // the previous position's MMAs are complete (its last tfull was waited).
-      // A set flag means the stored value is Z with Z - N still to be taken (mod R).
+      uint32_t* brow = Bc + bidx * kL;
+      const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
+      // ---- gather X = B[r][dg - 1] (zero rows for dg == 0), warp-cooperative
+      // async copies: lane c moves bytes 16c..16c+15 of each of the warp's 32 rows
+      // into the SW128 A layout (zero fill for dg == 0), all in flight at once.
+      // The previous position's MMAs are complete (its last tfull was waited)
+      // and its bucket stores are ordered by the warp barrier.
+      __syncwarp();
       {
-        const bool lazy = dg && Fk[bidx];
-        uint4 v[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c)
-          v[c] = dg ? *reinterpret_cast<const uint4*>(brow + 4 * c) : make_uint4(0u, 0u, 0u, 0u);
-        if (lazy) {
-          uint32_t bw = 0;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            uint32_t* w = reinterpret_cast<uint32_t*>(&v[c]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const unsigned long long dlt = (unsigned long long)w[i] - sN[4 * c + i] - bw;
-              w[i] = (uint32_t)dlt;
-              bw = (uint32_t)(dlt >> 63);
-            }
-          }
+        const int kb = lane >> 3, ch = lane & 7;
+        const uint32_t xa = smem_u32(XA) + kb * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
+        const int64_t rbase = row0 + quarter * 32;
+#pragma unroll 8
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t d_i = __shfl_sync(0xffffffffu, dg, i);
+          const uint32_t* src = Bc + ((rbase + i) * 255 + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
+          const uint32_t dst = xa + i * kBK + ((ch ^ (i & 7)) << 4);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                       "r"(d_i ? 16u : 0u)
+                       : "memory");
         }
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int kb = c >> 3, ch = c & 7;
-          *reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
-              v[c];
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        // lazily reduced buckets: a set flag means the stored value is Z with
+        // Z - N still to be taken (mod R)
+        uint32_t lzm = __ballot_sync(0xffffffffu, lazy != 0);
+        while (lzm) {
+          const int i = __ffs(lzm) - 1;
+          lzm &= lzm - 1;
+          uint8_t* p = XA + kb * (kRows * kBK) + (quarter * 32 + i) * kBK + ((ch ^ (i & 7)) << 4);
+          uint4 w = *reinterpret_cast<const uint4*>(p);
+          uint32_t v[4] = {w.x, w.y, w.z, w.w};
+          big_cond_sub<4>(v, 1u, nl, lane);     // x - N mod R (warp-uniform)
+          *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
         }
       }
       fence_async_smem();
       mbar_arrive(xfull);
+      // next position: digit, flag, and an L2 prefetch of its bucket
+      const uint32_t dg_next = pos + 1 < pos1 ? digit_at(pos + 1) : 0u;
+      uint32_t lazy_next = 0;
+      if (dg_next) {
+        const int64_t nb = r * 255 + dg_next - 1;
+        lazy_next = Fc[nb] ? 1u : 0u;
+        const uint32_t* pb = Bc + nb * kL;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
+      }
+      __syncwarp();
+      // bytes 508..511 of this row's X (k-block 3, chunk 7)
+      const uint32_t xtop =
+          *reinterpret_cast<const uint32_t*>(XA + 3 * (kRows * kBK) + t * kBK + ((7 ^ (t & 7)) << 4) + 12);
+
       unsigned long long carry = 0;
-      uint32_t zb = 0;                        // borrow chain of Z - N, low limbs up
+      uint32_t utop = 0;
+      // ---- U0, U1: u = X * Y' mod R, limbs into the SW128 A layout of u
 #pragma unroll 1
-      for (int task = 0; task < 6; ++task) {
-        const int buf = task & 1;
-        mbar_wait(&tfull[buf], fph[buf]);
-        fph[buf] ^= 1;
+      for (int task = 0; task < 2; ++task) {
+        mbar_wait(&tfull[task], fph[task]);
+        fph[task] ^= 1;
         tc_fence_after();
-        const uint32_t taddr = lanebase + (uint32_t)(buf * 256);
-        if (task == 2) carry = 0;             // the low-column chain of X*Y + u*N starts
-#pragma unroll 2
-        for (int c = 0; c < 16; ++c) {
-          uint32_t v[16], limb[4];
-          tmem_ld16(taddr + 16 * c, v);
-          tmem_wait_ld();
-          carry4(v, carry, limb);
-          if (task < 2) {                     // u bytes -> UA (SW128 A operand)
-            const int cc = task * 16 + c;     // 16-byte chunk of u
+        const uint32_t taddr = lanebase + (uint32_t)(task * 256);
+#pragma unroll 1
+        for (int g = 0; g < 4; ++g) {
+          uint32_t v[64];
+          tmem_ld64(taddr + 64 * g, v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {        // 16-byte chunk of u: 4 limbs
+            uint32_t l[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) l[i] = limb4(v + 16 * j + 4 * i, carry);
+            const int cc = task * 16 + 4 * g + j;
             const int kb = cc >> 3, ch = cc & 7;
             *reinterpret_cast<uint4*>(UA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
-                make_uint4(limb[0], limb[1], limb[2], limb[3]);
-          } else if (task >= 4) {             // Z limbs: unreduced to the bucket, borrow chain
-            const int li = (task - 4) * 64 + 4 * c;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const unsigned long long dlt = (unsigned long long)limb[i] - sN[li + i] - zb;
-              zb = (uint32_t)(dlt >> 63);
-            }
-            if (dg)
-              *reinterpret_cast<uint4*>(brow + li) = make_uint4(limb[0], limb[1], limb[2], limb[3]);
+                make_uint4(l[0], l[1], l[2], l[3]);
+            utop = l[3];
           }
         }
-        if (task < 2) {
+        if (task == 1) {
           fence_async_smem();
-          mbar_arrive(&uready[task]);
+          mbar_arrive(uready);
         }
         tc_fence_before();
-        mbar_arrive(&tempty[buf]);
+        mbar_arrive(&tempty[task]);
       }
-      // Z = z + 2^4096 * carry < 2N: Z >= N iff the top carry is set or Z - N does
-      // not borrow; the subtraction is deferred to the bucket's next reader (flag)
-      if (dg) Fk[bidx] = (carry != 0 || zb == 0) ? 1 : 0;
+      // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
+      uint32_t zb = 0;                        // borrow chain of Z - N, low limbs up
+      uint32_t pend[4];                       // Z limbs awaiting a 16-byte store
+      carry = 0;
+      {
+        mbar_wait(&tfull[0], fph[0]);
+        fph[0] ^= 1;
+        tc_fence_after();
+        const uint32_t taddr = lanebase;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t v[64];
+          tmem_ld64(taddr + 64 * g, v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int slot = 16 * g + k;       // columns 508 + 4 slot ..
+            if (slot == 0) {
+              // low4 = columns 508..511 as one number (< 2^54)
+              const unsigned long long low4 =
+                  (unsigned long long)v[0] + ((unsigned long long)v[1] << 8) +
+                  ((unsigned long long)v[2] << 16) + ((unsigned long long)v[3] << 24);
+              carry = (low4 + 0xffffffffull) >> 32;
+              continue;
+            }
+            const int li = slot - 1;           // Z limb
+            const uint32_t z = limb4(v + 4 * k, carry);
+            const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
+            zb = (uint32_t)(dlt >> 63);
+            pend[li & 3] = z;
+            if ((li & 3) == 3 && dg)
+              *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[0]);
+      }
+      {
+        mbar_wait(&tfull[1], fph[1]);
+        fph[1] ^= 1;
+        tc_fence_after();
+        const uint32_t taddr = lanebase + 256u;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t v[64];
+          tmem_ld64(taddr + 64 * g, v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int li = 63 + 16 * g + k;    // columns 764 + 4 (li - 63) ..
+            const uint32_t z = limb4(v + 4 * k, carry);
+            const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
+            zb = (uint32_t)(dlt >> 63);
+            pend[li & 3] = z;
+            if ((li & 3) == 3 && dg)
+              *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[1]);
+      }
+      // columns 1020..1022 (1023 is empty): bytes 509..511 of X, Y, u, N
+      {
+        const uint32_t x9 = (xtop >> 8) & 0xffu, x10 = (xtop >> 16) & 0xffu, x11 = xtop >> 24;
+        const uint32_t y9 = (ytop >> 8) & 0xffu, y10 = (ytop >> 16) & 0xffu, y11 = ytop >> 24;
+        const uint32_t u9 = (utop >> 8) & 0xffu, u10 = (utop >> 16) & 0xffu, u11 = utop >> 24;
+        const uint32_t n9 = (ntop >> 8) & 0xffu, n10 = (ntop >> 16) & 0xffu, n11 = ntop >> 24;
+        const uint32_t c0 = x9 * y11 + x10 * y10 + x11 * y9 + u9 * n11 + u10 * n10 + u11 * n9;
+        const uint32_t c1 = x10 * y11 + x11 * y10 + u10 * n11 + u11 * n10;
+        const uint32_t c2 = x11 * y11 + u11 * n11;
+        const unsigned long long s = (unsigned long long)c0 + ((unsigned long long)c1 << 8) +
+                                     ((unsigned long long)c2 << 16) + carry;
+        const uint32_t z = (uint32_t)s;
+        const uint32_t top = (uint32_t)(s >> 32);
+        const unsigned long long dlt = (unsigned long long)z - ntop - zb;
+        zb = (uint32_t)(dlt >> 63);
+        pend[3] = z;
+        if (dg) {
+          *reinterpret_cast<uint4*>(brow + kL - 4) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+          // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or Z - N does
+          // not borrow; the subtraction is deferred to the bucket's next reader
+          const uint32_t f = (top != 0 || zb == 0) ? 1u : 0u;
+          Fc[bidx] = (uint8_t)f;
+          if (dg_next == dg) lazy_next = f;     // same bucket again: its new flag
+        }
+      }
+      dg = dg_next;
+      lazy = lazy_next;
     }
   }
   tc_fence_before();
@@ -415,22 +578,24 @@ static int upload_schedule() {
   if (done) return kOk;
   tcp::Step h[tcp::kNSteps];
   int k = 0;
-  // tasks 0, 1 (U0, U1): global 256-column chunks 0, 1 of X * Y'
+  // U0, U1: output columns 256 gc .. of X * Y', tile delta = 256 gc - 128 ka
   for (int gc = 0; gc < 2; ++gc)
     for (int ka = 0; ka < 4; ++ka) {
-      const int t = 2 * gc - ka + 1;
-      if (t >= 0 && t < tcp::kTYp) h[k++] = {(int8_t)gc, (int8_t)(gc & 1), 0, (int8_t)ka, 0, (int8_t)t};
+      const int delta = 256 * gc - 128 * ka;
+      const int t = (delta - tcp::kDeltaYp) / 128;
+      if (delta - 127 < 512 && delta + 255 >= 0 && t >= 0 && t < tcp::kTYp)
+        h[k++] = {(int8_t)gc, 0, (int8_t)ka, 0, (int8_t)t};
     }
-  // tasks 2..5 (L0, L1, H0, H1): chunk gc = task - 2 of X * Y + u * N, the
-  // X * Y k-blocks first (they do not wait for u)
-  for (int gc = 0; gc < 4; ++gc) {
-    const int task = gc + 2;
+  // H0, H1: output columns c0 = 508 / 764 of X * Y + u * N, the X * Y k-blocks
+  // first (they do not wait for u)
+  for (int hh = 0; hh < 2; ++hh) {
+    const int c0 = 508 + 256 * hh;
     for (int a = 0; a < 2; ++a)
       for (int ka = 0; ka < 4; ++ka) {
-        const int t = 2 * gc - ka + 1;
-        if (t < 0 || t >= tcp::kTY) continue;
-        h[k++] = {(int8_t)task, (int8_t)(task & 1), (int8_t)a, (int8_t)ka, (int8_t)(a ? 2 : 1),
-                  (int8_t)t};
+        const int delta = c0 - 128 * ka;
+        if (delta - 127 >= 512) continue;           // window entirely above byte 511
+        const int t = (delta - tcp::kDeltaY) / 128;
+        h[k++] = {(int8_t)(2 + hh), (int8_t)a, (int8_t)ka, (int8_t)(a ? 2 : 1), (int8_t)t};
       }
   }
   if (k != tcp::kNSteps) {
@@ -442,20 +607,33 @@ static int upload_schedule() {
   return kOk;
 }
 
-// W[r] (Montgomery form, 4096-bit N) for rows r < rows of 32-bit exponent rows
-// E[r * rs + k]: the slot_fixed contract, with the bucket updates on tcgen05.
-int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
-                         const uint32_t* N, uint32_t np, const uint32_t* one_m,
-                         const uint32_t* Nprime, uint32_t* W, cudaStream_t st) {
+int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
   using namespace tcp;
   const int64_t npos = 4 * n;
-  if (n <= 0 || rows <= 0 || npos > 65536) {
-    set_error("tc_slot_fixed: bad shapes (n=%lld rows=%lld)", (long long)n, (long long)rows);
+  const int64_t rows_p = ceil_div(rows, kRows) * kRows;
+  return (int64_t)clients * (npos * kL * 4 + npos * (kTY + kTYp) * kTile + kTY * kTile +
+                             rows_p * 255 * (kL * 4 + 1));
+}
+
+// W_c[rid[r] or r] (Montgomery form, 4096-bit N_c) for rows r < rows of 32-bit
+// exponent rows E[(rid[r] or r) * rs + k], for `clients` independent keys in one
+// launch: the slot_fixed contract with the bucket updates on tcgen05.
+int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint32_t* const* N,
+                              const uint32_t* np, const uint32_t* const* one_m,
+                              const uint32_t* const* Nprime, uint32_t* const* W, int64_t n,
+                              const uint32_t* E, int64_t rs, const int32_t* rid, int64_t rows,
+                              cudaStream_t st) {
+  using namespace tcp;
+  const int64_t npos = 4 * n;
+  if (clients <= 0 || clients > 65535 || n <= 0 || rows <= 0 || npos > 65536 ||
+      (int64_t)clients * npos * kTY * 256 >= (1ll << 31)) {
+    set_error("tc_slot_fixed: bad shapes (clients=%d n=%lld rows=%lld)", clients, (long long)n,
+              (long long)rows);
     return kErrInput;
   }
   if (int e = upload_schedule()) return e;
   {
-    // keep the multi-GB workspace in the stream-ordered pool between clients
+    // keep the multi-GB workspace in the stream-ordered pool between calls
     static bool pool_set = false;
     if (!pool_set) {
       int dev = 0;
@@ -468,41 +646,55 @@ int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_
       pool_set = true;
     }
   }
+  const int C = clients;
   const int64_t tiles = ceil_div(rows, kRows);
   const int64_t rows_p = tiles * kRows;
+  std::vector<TcClient> hc(C);
+  for (int c = 0; c < C; ++c) hc[c] = {P[c], N[c], one_m[c], Nprime[c], W[c], np[c]};
+  TcClient* dcl = nullptr;
   uint32_t *Yp = nullptr, *Bk = nullptr;
   uint8_t *tY = nullptr, *tYp = nullptr, *tN = nullptr, *Fk = nullptr;
-  auto fail = [&](const char* what) {
+  auto release = [&]() {
+    if (dcl) cudaFreeAsync(dcl, st);
     if (Yp) cudaFreeAsync(Yp, st);
     if (Bk) cudaFreeAsync(Bk, st);
     if (tY) cudaFreeAsync(tY, st);
     if (tYp) cudaFreeAsync(tYp, st);
     if (tN) cudaFreeAsync(tN, st);
     if (Fk) cudaFreeAsync(Fk, st);
+  };
+  auto fail = [&](const char* what) {
+    release();
     cudaGetLastError();
     set_error("tc_slot_fixed: %s", what);
     return kErrCuda;
   };
-  if (cudaMallocAsync(reinterpret_cast<void**>(&Yp), (size_t)npos * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tY), (size_t)npos * kTY * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tYp), (size_t)npos * kTYp * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tN), (size_t)kTY * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)rows_p * 255 * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)rows_p * 255, st) != cudaSuccess)
+  if (cudaMallocAsync(reinterpret_cast<void**>(&dcl), sizeof(TcClient) * C, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Yp), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tY), (size_t)C * npos * kTY * kTile, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tYp), (size_t)C * npos * kTYp * kTile, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tN), (size_t)C * kTY * kTile, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * 255 * kL * 4, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)C * rows_p * 255, st) != cudaSuccess)
     return fail("workspace allocation");
-  if (cudaMemsetAsync(Fk, 0, (size_t)rows_p * 255, st) != cudaSuccess) return fail("memset");
-  mul_lo_kernel<<<(unsigned)ceil_div(npos, 128), 128, 0, st>>>(P, npos, Nprime, Yp);
-  toep_tiles_kernel<<<(unsigned)(npos * kTY), 256, 0, st>>>(P, kTY, tY);
-  toep_tiles_kernel<<<(unsigned)(npos * kTYp), 256, 0, st>>>(Yp, kTYp, tYp);
-  toep_tiles_kernel<<<(unsigned)kTY, 256, 0, st>>>(N, kTY, tN);
+  // the host vector is read at enqueue time for pageable memory (synchronous copy)
+  if (cudaMemcpyAsync(dcl, hc.data(), sizeof(TcClient) * C, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemsetAsync(Fk, 0, (size_t)C * rows_p * 255, st) != cudaSuccess)
+    return fail("client table / flags");
+  mul_lo_kernel<<<dim3((unsigned)ceil_div(npos, 128), C), 128, 0, st>>>(dcl, npos, Yp);
+  toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 0, nullptr, npos, kTY,
+                                                                     kDeltaY, tY);
+  toep_tiles_kernel<<<dim3((unsigned)(npos * kTYp), C), 256, 0, st>>>(dcl, 1, Yp, npos, kTYp,
+                                                                      kDeltaYp, tYp);
+  toep_tiles_kernel<<<dim3((unsigned)kTY, C), 256, 0, st>>>(dcl, 2, nullptr, 1, kTY, kDeltaY, tN);
   {
     const int64_t cnt = rows_p * 255;
-    bucket_fill_kernel<<<(unsigned)ceil_div(cnt * kL, 256), 256, 0, st>>>(Bk, cnt, one_m);
+    bucket_fill_kernel<<<dim3((unsigned)ceil_div(cnt * kL, 256), C), 256, 0, st>>>(dcl, Bk, cnt);
   }
-  if (int e = check_launch("tc_slot_fixed setup")) return fail("setup kernels");
+  if (check_launch("tc_slot_fixed setup")) return fail("setup kernels");
   CUtensorMap mYp, mY, mN;
-  if (tile_map(&mYp, tYp, npos * kTYp * 256) || tile_map(&mY, tY, npos * kTY * 256) ||
-      tile_map(&mN, tN, (int64_t)kTY * 256))
+  if (tile_map(&mYp, tYp, C * npos * kTYp * 256) || tile_map(&mY, tY, C * npos * kTY * 256) ||
+      tile_map(&mN, tN, (int64_t)C * kTY * 256))
     return fail("tensor maps");
   cudaFuncSetAttribute(tc_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   // one launch walks every position (tiles are independent); chunked so a
@@ -512,21 +704,25 @@ int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_
     const char* e = getenv("ZPIR_TC_CHUNK");
     chunk = e ? std::max<int64_t>(1, atoll(e)) : 1024;
   }
-  for (int64_t p0 = 0; p0 < npos; p0 += chunk) {
-    const int64_t p1 = std::min<int64_t>(npos, p0 + chunk);
-    tc_step_kernel<<<(unsigned)tiles, kThreads, kSmem, st>>>(mYp, mY, mN, E, rs, n, (int)p0,
-                                                             (int)p1, rows, Bk, Fk, N);
+  const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(tiles * C, 2 * 148)));
+  for (int64_t p0 = 0; p0 < npos; p0 += ck) {
+    const int64_t p1 = std::min<int64_t>(npos, p0 + ck);
+    tc_step_kernel<<<dim3((unsigned)tiles, C), kThreads, kSmem, st>>>(
+        mYp, mY, mN, dcl, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk, Fk);
   }
   if (check_launch("tc_step")) return fail("tc_step launch");
-  bucket_combine_kernel<<<(unsigned)ceil_div(rows, 4), 128, 0, st>>>(Bk, Fk, rows, N, np, W);
+  bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, Fk, rows,
+                                                                             rows_p, rid);
   if (check_launch("bucket_combine")) return fail("bucket_combine");
-  cudaFreeAsync(Yp, st);
-  cudaFreeAsync(Bk, st);
-  cudaFreeAsync(tY, st);
-  cudaFreeAsync(tYp, st);
-  cudaFreeAsync(tN, st);
-  cudaFreeAsync(Fk, st);
+  release();
   return check_launch("tc_slot_fixed");
+}
+
+// Single-client form (the original entry point).
+int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
+                         const uint32_t* N, uint32_t np, const uint32_t* one_m,
+                         const uint32_t* Nprime, uint32_t* W, cudaStream_t st) {
+  return tc_slot_fixed_many_launch(1, &P, &N, &np, &one_m, &Nprime, &W, n, E, rs, nullptr, rows, st);
 }
 
 }  // namespace zpir

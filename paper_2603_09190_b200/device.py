@@ -325,6 +325,30 @@ def slot_fixed_tc(P, n, E, rs, rows, kctx, W, stream=None):
     return W
 
 
+def slot_fixed_tc_many(jobs, n, E, rs, rows, rid=None, stream=None):
+    """slot_fixed_tc for several clients in one launch (blockIdx.y = client).
+
+    jobs: [(P, kctx, W)] -- client table P (4n x 128 limbs), its key context and
+    its output rows W (Montgomery form); rows r < rows read exponent row
+    rid[r] (or r) of E and write W[rid[r]] (or W[r])."""
+    import ctypes
+    c = len(jobs)
+    arr = lambda vals: (ctypes.c_uint64 * c)(*vals)  # noqa: E731
+    P = arr([p.data_ptr() for p, _, _ in jobs])
+    N = arr([k.d_m2.data_ptr() for _, k, _ in jobs])
+    one = arr([k.d_one2.data_ptr() for _, k, _ in jobs])
+    npr = arr([k.d_nprime_full().data_ptr() for _, k, _ in jobs])
+    W = arr([w.data_ptr() for _, _, w in jobs])
+    np_ = (ctypes.c_uint32 * c)(*[k.c2.np for _, k, _ in jobs])
+    _lib.call("zpir_slot_fixed_tc_many", c, P, N, np_, one, npr, W, n, _lib.ptr(E), rs,
+              _lib.ptr(rid) if rid is not None else None, rows, _s(stream))
+    return [w for _, _, w in jobs]
+
+
+def slot_fixed_tc_workspace(n, rows, clients):
+    return _lib.lib().zpir_slot_fixed_tc_workspace(n, rows, clients)
+
+
 def groups_z(z, d1, cap, groups, lm, d_m, d_np, d_rpow, nchunks, d_f0, tz, t_ld, stream=None,
              stride=1):
     rows, wz = z.shape[-2], z.shape[-1]

@@ -52,6 +52,10 @@ COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "36"))
 PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
 # per-client hints: Pippenger bucket updates on the tensor cores (4096-bit m^2)
 TC_HINT = os.environ.get("ZPIR_TC_HINT", "1") != "0"
+# transient workspace cap of one tensor-core hint launch (tiles + buckets)
+TC_WS_BYTES = float(os.environ.get("ZPIR_TC_WS_GB", "24")) * 2**30
+# refreshes with at least this many (changed row x client) pairs use the tensor cores
+TC_REFRESH_MIN = int(os.environ.get("ZPIR_TC_REFRESH_MIN", "256"))
 
 
 @dataclass
@@ -472,6 +476,18 @@ def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
     return [sample_ciphertext(pk, seed, (query_index << 32) | i) for i in range(n)]
 
 
+def _tc_eligible(state, kctx) -> bool:
+    return TC_HINT and kctx.l2 == 128 and 4 * state.layout.n <= 65536
+
+
+def _tc_batches(state, items, rows):
+    """Split tensor-core jobs into launches whose transient workspace stays
+    under ZPIR_TC_WS_GB (default 24 GB; at least one client per launch)."""
+    per = device.slot_fixed_tc_workspace(state.layout.n, rows, 1)
+    k = max(1, int(TC_WS_BYTES // max(per, 1)))
+    return [items[i:i + k] for i in range(0, len(items), k)]
+
+
 def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
          keep_slots: bool = False) -> ClientHint:
     """k_g = prod_k ck_r[k]^{H_scaled[g][k]} mod m^2 for all d1' groups
@@ -481,30 +497,50 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     H[g*cap+j][k], so k_g = prod_j W[g*cap+j]^(gamma^j) with
     W[c] = prod_k ck_r[k]^H[c][k].
     Each W[c] (32-bit exponents) is one fixed-base Pippenger over the table
-    P[i][k] = ck_r[k]^(2^(8i)) (255 buckets, 4n digits); the groups are then
-    recombined by Horner in gamma (slot_combine). Same group element as the
-    reference's windowed multiexp, canonical mod m^2. keep_slots=True keeps W
-    and P on the device for refresh_hint."""
+    P[i][k] = ck_r[k]^(2^(8i)) (255 buckets, 4n digits) -- for 4096-bit m^2
+    with the bucket updates on the tensor cores (tc_pippenger.cu); the groups
+    are then recombined by Horner in gamma (slot_combine). Same group element
+    as the reference's windowed multiexp, canonical mod m^2. keep_slots=True
+    keeps W and P on the device for refresh_hint."""
+    return hints(state, [(reg, query_index)], stream=stream, keep_slots=keep_slots)[0]
+
+
+def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False) -> list:
+    """hint() for several (registration, query index) jobs: the tensor-core
+    Pippenger runs all of them in one launch (blockIdx.y = client), so the
+    row tiles of a batch fill whole waves of SMs (the hint worker's batch;
+    SURVEY.md section 8f rank 1). Returns one ClientHint per job, in order."""
     lay = state.layout
     dev = state.device
     stream = stream or torch.cuda.current_stream(dev)
-    kctx = key_ctx(reg.pk.m, dev)
-    # ck_r[k] = Stream(seed, 1, (qi << 32) | k).below(m^2), sampled on the device
-    bases = device.chacha_below(reg.seed, DOM_CIPHERTEXT_SAMPLE, query_index, lay.n, kctx.d_m2,
-                                kctx.m2, kctx.l2, stream)
     nslot = lay.groups * lay.cap
-    W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
-    P = device.pow8_table(bases, kctx, stream)
-    if TC_HINT and kctx.l2 == 128 and 4 * lay.n <= 65536:
-        device.slot_fixed_tc(P, lay.n, state.H_dev, lay.n, nslot, kctx, W, stream)
-    else:
-        device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
-    out = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
-    device.slot_combine(W, lay.cap, None, lay.groups, kctx, out, lay.gamma, stream)
-    entries = limbs_to_ints(_d2h_u32(out, "hint", stream))
-    counters.bump("group_mult", lay.groups * lay.n)
-    return ClientHint(query_index, state.db_version, [PaillierCiphertext(e) for e in entries],
-                      dev=out, slots=W if keep_slots else None, bases=P if keep_slots else None)
+    prep = []
+    for reg, qi in jobs:
+        kctx = key_ctx(reg.pk.m, dev)
+        # ck_r[k] = Stream(seed, 1, (qi << 32) | k).below(m^2), sampled on the device
+        bases = device.chacha_below(reg.seed, DOM_CIPHERTEXT_SAMPLE, qi, lay.n, kctx.d_m2,
+                                    kctx.m2, kctx.l2, stream)
+        P = device.pow8_table(bases, kctx, stream)
+        W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
+        prep.append((P, kctx, W))
+    tc = [j for j in prep if _tc_eligible(state, j[1])]
+    for batch in (_tc_batches(state, tc, nslot) if tc else []):
+        device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, nslot, stream=stream)
+    out = []
+    for (reg, qi), (P, kctx, W) in zip(jobs, prep):
+        if not _tc_eligible(state, kctx):
+            device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
+        k = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
+        device.slot_combine(W, lay.cap, None, lay.groups, kctx, k, lay.gamma, stream)
+        out.append(k)
+    res = []
+    for (reg, qi), (P, kctx, W), k in zip(jobs, prep, out):
+        entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
+        counters.bump("group_mult", lay.groups * lay.n)
+        res.append(ClientHint(qi, state.db_version, [PaillierCiphertext(e) for e in entries],
+                              dev=k, slots=W if keep_slots else None,
+                              bases=P if keep_slots else None))
+    return res
 
 
 def _refresh_device(state, kctx, old, rows, rid, gid, ngroups, stream):
@@ -544,30 +580,48 @@ def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
 
 def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
                   nstreams: int = 8) -> list:
-    """refresh_hint for many (registration, hint) pairs at once: the clients'
-    kernels are spread over `nstreams` CUDA streams so that small refreshes
-    (a few hundred rows each) fill the GPU together."""
+    """refresh_hint for many (registration, hint) pairs at once. With enough
+    work (changed rows x clients >= ZPIR_TC_REFRESH_MIN, default 256) and
+    4096-bit m^2 the changed rows' W of all clients are recomputed by one
+    tensor-core launch (row ids, one grid row per client); otherwise the IMAD
+    kernels of each client are spread over `nstreams` CUDA streams so that
+    small refreshes fill the GPU together."""
     for _, old in pairs:
         if old.slots is None or old.bases is None:
             raise ValueError("refresh_hint needs a hint computed with keep_slots=True")
     dev = state.device
+    lay = state.layout
     main = stream or torch.cuda.current_stream(dev)
     rows, rid, gid, ng = _changed_ids(state, changed_rows)
-    streams = [main] if len(pairs) == 1 else [torch.cuda.Stream(dev)
-                                              for _ in range(min(nstreams, len(pairs)))]
-    ev = torch.cuda.Event()
-    ev.record(main)
-    outs = []
-    for i, (reg, old) in enumerate(pairs):
-        st = streams[i % len(streams)]
-        if st is not main:
-            st.wait_event(ev)
-        kctx = key_ctx(reg.pk.m, dev)
-        with torch.cuda.stream(st):
-            outs.append(_refresh_device(state, kctx, old, rows, rid, gid, ng, st))
-    for st in streams:
-        if st is not main:
-            main.wait_stream(st)
+    kctxs = [key_ctx(reg.pk.m, dev) for reg, _ in pairs]
+    use_tc = rows > 0 and rows * len(pairs) >= TC_REFRESH_MIN and \
+        all(_tc_eligible(state, k) for k in kctxs)
+    if use_tc:
+        outs = []
+        jobs = []
+        for (reg, old), kctx in zip(pairs, kctxs):
+            W = old.slots.clone()
+            outs.append((W, old.dev.clone()))
+            jobs.append((old.bases, kctx, W))
+        for batch in _tc_batches(state, jobs, rows):
+            device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, rows, rid=rid, stream=main)
+        for (W, k), kctx in zip(outs, kctxs):
+            device.slot_combine(W, lay.cap, gid, ng, kctx, k, lay.gamma, main)
+    else:
+        streams = [main] if len(pairs) == 1 else [torch.cuda.Stream(dev)
+                                                  for _ in range(min(nstreams, len(pairs)))]
+        ev = torch.cuda.Event()
+        ev.record(main)
+        outs = []
+        for i, ((reg, old), kctx) in enumerate(zip(pairs, kctxs)):
+            st = streams[i % len(streams)]
+            if st is not main:
+                st.wait_event(ev)
+            with torch.cuda.stream(st):
+                outs.append(_refresh_device(state, kctx, old, rows, rid, gid, ng, st))
+        for st in streams:
+            if st is not main:
+                main.wait_stream(st)
     res = []
     for (reg, old), (W, k) in zip(pairs, outs):
         entries = limbs_to_ints(_d2h_u32(k, "hint", main))

@@ -227,3 +227,71 @@ def test_slot_fixed_tensor_core(env, n, rows):
     a, b = device.to_host_u32(W1), device.to_host_u32(W2)
     bad = [i for i in range(rows) if not np.array_equal(a[i], b[i])]
     assert not bad, f"{len(bad)} rows differ, first {bad[:5]}"
+
+
+@pytest.mark.parametrize("m", [(1 << 2048) - 1 - 2 * 12345, (1 << 2047) + 1, None])
+def test_slot_fixed_tensor_core_moduli(env, m):
+    """The column-508 carry shortcut and the deferred subtraction hold for any
+    odd 2048-bit m: m^2 just below R = 2^4096 (Z < 2N exceeds R), m^2 just above
+    2^4094 (N < R/2), and a random keygen modulus; every digit value 1..255
+    appears, buckets are hit back to back (equal digits at consecutive positions)."""
+    torch, device = env
+    from oracle import client
+    from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
+    dev = torch.device("cuda", 0)
+    if m is None:
+        m = client.keygen(2048, random.Random(77)).m
+    rng = random.Random(m % 1000)
+    n, rows = 32, 260
+    kctx = key_ctx(m, dev)
+    m2 = kctx.m2
+    bases = [m2 - 1 - rng.randrange(1000) for _ in range(n // 2)] + \
+        [rng.randrange(m2) for _ in range(n - n // 2)]
+    P = device.pow8_table(device.u32_tensor(ints_to_limbs(bases, kctx.l2), dev), kctx)
+    nrng = np.random.default_rng(5)
+    E = nrng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
+    E[3] = 0x01010101 * 7                       # one bucket, every position
+    E[4, :] = np.arange(n, dtype=np.uint32) * 0x01010101 % 256 * 0x01010101
+    E[5] = 0xFFFFFFFF
+    Ed = device.u32_tensor(E, dev)
+    W1 = torch.empty((rows, kctx.l2), dtype=torch.int32, device=dev)
+    W2 = torch.empty_like(W1)
+    device.slot_fixed(P, n, Ed, n, None, rows, kctx, W1)
+    device.slot_fixed_tc(P, n, Ed, n, rows, kctx, W2)
+    a, b = device.to_host_u32(W1), device.to_host_u32(W2)
+    bad = [i for i in range(rows) if not np.array_equal(a[i], b[i])]
+    assert not bad, f"{len(bad)} rows differ, first {bad[:5]}"
+
+
+def test_slot_fixed_tensor_core_many_clients_row_ids(env):
+    """One tensor-core launch for three clients (different keys and tables),
+    on a row-id subset of the exponent rows (the incremental refresh): every
+    client's rows equal its own IMAD slot_fixed; rows outside the subset are
+    left untouched."""
+    torch, device = env
+    from oracle import client
+    from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
+    dev = torch.device("cuda", 0)
+    n, nrow = 64, 400
+    nrng = np.random.default_rng(31)
+    E = nrng.integers(0, 1 << 32, (nrow, n), dtype=np.uint64).astype(np.uint32)
+    Ed = device.u32_tensor(E, dev)
+    rid_h = np.sort(nrng.choice(nrow, size=150, replace=False)).astype(np.int32)
+    rid = torch.from_numpy(rid_h).to(dev)
+    jobs, refs = [], []
+    for c in range(3):
+        rng = random.Random(900 + c)
+        kctx = key_ctx(client.keygen(2048, rng).m, dev)
+        bases = device.u32_tensor(ints_to_limbs([rng.randrange(kctx.m2) for _ in range(n)],
+                                                kctx.l2), dev)
+        P = device.pow8_table(bases, kctx)
+        W_ref = torch.zeros((nrow, kctx.l2), dtype=torch.int32, device=dev)
+        device.slot_fixed(P, n, Ed, n, rid, len(rid_h), kctx, W_ref)
+        W = torch.zeros_like(W_ref)
+        jobs.append((P, kctx, W))
+        refs.append(W_ref)
+    device.slot_fixed_tc_many(jobs, n, Ed, n, len(rid_h), rid=rid)
+    for (_, _, W), W_ref in zip(jobs, refs):
+        a, b = device.to_host_u32(W_ref), device.to_host_u32(W)
+        assert np.array_equal(a, b)
+        assert not b[np.setdiff1d(np.arange(nrow), rid_h)].any()

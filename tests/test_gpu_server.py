@@ -126,3 +126,35 @@ def test_paper_parameters_n1400_3072bit():
     rc = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
     assert client.extract(sk, 1 << 32, 256, cap, 1 << 32, 256,
                           combined=[c.c for c in rc.k]) == [int(x) for x in db[i0]]
+
+
+def test_batched_hints_and_tensor_core_refresh(golden, monkeypatch):
+    """hints() for several clients in one tensor-core launch == hint() per
+    client; a refresh of two clients through the batched tensor-core path
+    (row ids) == full hints on the rebuilt state (BASELINE configs[0] shape,
+    2048-bit keys)."""
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import protocol
+    g = golden("tiny")
+    params = g.params(z)
+    st = z.ServerGlobalState(params, g.db)
+    regs = []
+    for i in range(2):
+        sk, seed = client.setup(2048, random.Random(50 + i))
+        pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+        regs.append(z.ClientRegistration(pk, seed, z.client_id_of(pk)))
+    hs = z.hints(st, [(regs[0], 0), (regs[1], 3)], keep_slots=True)
+    assert [c.c for c in hs[0].entries] == [c.c for c in z.hint(st, regs[0], 0).entries]
+    assert [c.c for c in hs[1].entries] == [c.c for c in z.hint(st, regs[1], 3).entries]
+    rng = np.random.default_rng(4)
+    db2 = np.array(g.db, dtype=np.uint8, copy=True)
+    rows = sorted(rng.choice(g.d1, size=40, replace=False).tolist())
+    for c in rows:
+        db2[:, c] = rng.integers(0, 256, g.d0, dtype=np.uint8)
+    st2, changed = st.updated(db2)
+    monkeypatch.setattr(protocol, "TC_REFRESH_MIN", 1)
+    ref_pairs = list(zip(regs, hs))
+    out = z.refresh_hints(st2, ref_pairs, changed)
+    full = z.ServerGlobalState(params, db2, db_version=1)
+    for reg, h, qi in zip(regs, out, (0, 3)):
+        assert [c.c for c in h.entries] == [c.c for c in z.hint(full, reg, qi).entries]
