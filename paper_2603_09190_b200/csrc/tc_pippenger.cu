@@ -74,8 +74,38 @@ struct TcClient {
   uint32_t np;              // -N^-1 mod 2^32
 };
 
+// Radix of the exponent digits: D digits per 32-bit exponent word, digit i
+// = bits off[i] .. off[i] + width[i] - 1; nb = 2^max(width) - 1 buckets per row.
+// Fewer, wider digits mean fewer positions (tensor-core work, 4n at D = 4) but
+// more buckets to combine on the IMAD path (2 nb Montgomery products per row).
+struct DigitSpec {
+  int D, nb;
+  int off[8], width[8];
+};
+
+// Pd[c][i * n + k] = base_k^(2^off[i]) (Montgomery form), base_k = P_c[k] (the
+// first block of the client's pow8 table): one warp per base, squarings only.
+__global__ void __launch_bounds__(128)
+powtab_kernel(const TcClient* __restrict__ cl, int64_t n, DigitSpec ds, uint32_t* __restrict__ Pd) {
+  constexpr int LPL = tcp::kL / 32;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.y;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (k >= n) return;
+  uint32_t n_[LPL], a[LPL];
+  big_load<LPL>(n_, cl[c].N, lane);
+  big_load<LPL>(a, cl[c].P + k * tcp::kL, lane);
+  const uint32_t np = cl[c].np;
+  uint32_t* out = Pd + (int64_t)c * ds.D * n * tcp::kL;
+  int cur = 0;
+  for (int i = 0; i < ds.D; ++i) {
+    for (; cur < ds.off[i]; ++cur) mont_mul<LPL>(a, a, a, n_, np, lane);
+    big_store<LPL>(out + ((int64_t)i * n + k) * tcp::kL, a, lane);
+  }
+}
+
 // tiles[((c * npos + p) * T + t) * 256 + j][a] = byte_{delta0 + 128 t + j - a}(y_{c,p}),
-// zero outside [0, 512); y = Y[c][p] (fixed-stride) or the client's N (npos = 1).
+// zero outside [0, 512); y = Y[c][p] (which = 1, fixed stride) or the client's N.
 __global__ void __launch_bounds__(256)
 toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __restrict__ Ybase,
                   int64_t npos, int T, int delta0, uint8_t* __restrict__ tiles) {
@@ -84,9 +114,7 @@ toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __
   const int64_t p = pt / T;
   const int t = (int)(pt - p * T);
   const int j = threadIdx.x;
-  const uint32_t* ysrc = which == 0   ? cl[c].P + p * tcp::kL
-                         : which == 1 ? Ybase + ((int64_t)c * npos + p) * tcp::kL
-                                      : cl[c].N;
+  const uint32_t* ysrc = which == 1 ? Ybase + ((int64_t)c * npos + p) * tcp::kL : cl[c].N;
   const uint8_t* y = reinterpret_cast<const uint8_t*>(ysrc);
   const int delta = delta0 + 128 * t;
   uint8_t* row = tiles + (((int64_t)c * npos * T + pt) * 256 + j) * tcp::kBK;
@@ -108,13 +136,14 @@ toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __
   }
 }
 
-// out[c][p] = P_c[p] * Nprime_c mod 2^4096, one thread per value (product scanning).
+// out[c][p] = Pd_c[p] * Nprime_c mod 2^4096, one thread per value (product scanning).
 __global__ void __launch_bounds__(128)
-mul_lo_kernel(const TcClient* __restrict__ cl, int64_t npos, uint32_t* __restrict__ out) {
+mul_lo_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Pd, int64_t npos,
+              uint32_t* __restrict__ out) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int c = blockIdx.y;
   if (p >= npos) return;
-  const uint32_t* y = cl[c].P + p * tcp::kL;
+  const uint32_t* y = Pd + ((int64_t)c * npos + p) * tcp::kL;
   const uint32_t* Np = cl[c].Nprime;
   uint32_t* o = out + ((int64_t)c * npos + p) * tcp::kL;
   unsigned long long lo = 0, hi = 0;  // 128-bit column accumulator (lo, hi)
@@ -138,11 +167,11 @@ __global__ void bucket_fill_kernel(const TcClient* __restrict__ cl, uint32_t* __
   if (i < count * tcp::kL) B[(int64_t)c * count * tcp::kL + i] = cl[c].one[i % tcp::kL];
 }
 
-// W[row] = prod_d B[r][d]^d (running sums from d = 255 down), Montgomery form.
+// W[row] = prod_d B[r][d]^d (running sums from d = nb down), Montgomery form.
 // Buckets are stored lazily reduced: flag F[r][d] set means "subtract N (mod R)".
 __global__ void __launch_bounds__(128)
 bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Ball,
-                      const uint8_t* __restrict__ Fall, int64_t rows, int64_t rows_p,
+                      const uint8_t* __restrict__ Fall, int nb, int64_t rows, int64_t rows_p,
                       const int32_t* __restrict__ rid) {
   constexpr int LPL = tcp::kL / 32;
   const int lane = threadIdx.x & 31;
@@ -152,12 +181,12 @@ bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restric
   const uint32_t np = cl[c].np;
   uint32_t n_[LPL], run[LPL], tot[LPL], x[LPL];
   big_load<LPL>(n_, cl[c].N, lane);
-  const uint32_t* br = Ball + ((int64_t)c * rows_p + r) * 255 * tcp::kL;
-  const uint8_t* fr = Fall + ((int64_t)c * rows_p + r) * 255;
-  big_load<LPL>(run, br + 254 * tcp::kL, lane);
-  if (fr[254]) big_cond_sub<LPL>(run, 1u, n_, lane);
+  const uint32_t* br = Ball + ((int64_t)c * rows_p + r) * nb * tcp::kL;
+  const uint8_t* fr = Fall + ((int64_t)c * rows_p + r) * nb;
+  big_load<LPL>(run, br + (nb - 1) * tcp::kL, lane);
+  if (fr[nb - 1]) big_cond_sub<LPL>(run, 1u, n_, lane);
   big_copy<LPL>(tot, run);
-  for (int d = 254; d >= 1; --d) {
+  for (int d = nb - 1; d >= 1; --d) {
     big_load<LPL>(x, br + (d - 1) * tcp::kL, lane);
     if (fr[d - 1]) big_cond_sub<LPL>(x, 1u, n_, lane);
     mont_mul<LPL>(run, run, x, n_, np, lane);
@@ -209,6 +238,7 @@ __device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long&
 __global__ void __launch_bounds__(tcp::kThreads, 1)
 tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant__ CUtensorMap mapY,
                const __grid_constant__ CUtensorMap mapN, const TcClient* __restrict__ cl,
+               const uint32_t* __restrict__ Pd, const __grid_constant__ DigitSpec ds,
                const uint32_t* __restrict__ E, int64_t rs, const int32_t* __restrict__ rid,
                int64_t n, int64_t npos, int pos0, int pos1, int64_t rows, int64_t rows_p,
                uint32_t* __restrict__ Ball, uint8_t* __restrict__ Fall) {
@@ -339,9 +369,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     const int t = quarter * 32 + lane;          // row within the tile = TMEM lane
     const int64_t r = row0 + t;
     const int64_t er = r < rows ? (rid ? (int64_t)rid[r] : r) : 0;
-    uint32_t* Bc = Ball + (int64_t)client * rows_p * 255 * kL;
-    uint8_t* Fc = Fall + (int64_t)client * rows_p * 255;
-    const uint32_t* Pc = cl[client].P;
+    const int nb = ds.nb;
+    uint32_t* Bc = Ball + (int64_t)client * rows_p * nb * kL;
+    uint8_t* Fc = Fall + (int64_t)client * rows_p * nb;
+    const uint32_t* Pc = Pd + (int64_t)client * npos * kL;
     const uint32_t lanebase = tbase + ((uint32_t)(quarter * 32) << 16);
     uint32_t nl[4];                             // N limbs 4 lane .. 4 lane + 3 (gather)
 #pragma unroll
@@ -354,12 +385,12 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     auto digit_at = [&](int p) -> uint32_t {
       if (r >= rows) return 0u;
       const int di = p / (int)n;
-      return (E[er * rs + (p - (int64_t)di * n)] >> (8 * di)) & 0xffu;
+      return (E[er * rs + (p - (int64_t)di * n)] >> ds.off[di]) & ((1u << ds.width[di]) - 1u);
     };
     uint32_t dg = digit_at(pos0);
-    uint32_t lazy = (dg && Fc[r * 255 + dg - 1]) ? 1u : 0u;
+    uint32_t lazy = (dg && Fc[r * nb + dg - 1]) ? 1u : 0u;
     for (int pos = pos0; pos < pos1; ++pos) {
-      const int64_t bidx = (r * 255) + (dg ? dg - 1 : 0);
+      const int64_t bidx = (r * nb) + (dg ? dg - 1 : 0);
       uint32_t* brow = Bc + bidx * kL;
       const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
       // ---- gather X = B[r][dg - 1] (zero rows for dg == 0), warp-cooperative
@@ -375,7 +406,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
 #pragma unroll 8
         for (int i = 0; i < 32; ++i) {
           const uint32_t d_i = __shfl_sync(0xffffffffu, dg, i);
-          const uint32_t* src = Bc + ((rbase + i) * 255 + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
+          const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
           const uint32_t dst = xa + i * kBK + ((ch ^ (i & 7)) << 4);
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                        "r"(d_i ? 16u : 0u)
@@ -401,9 +432,9 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       const uint32_t dg_next = pos + 1 < pos1 ? digit_at(pos + 1) : 0u;
       uint32_t lazy_next = 0;
       if (dg_next) {
-        const int64_t nb = r * 255 + dg_next - 1;
-        lazy_next = Fc[nb] ? 1u : 0u;
-        const uint32_t* pb = Bc + nb * kL;
+        const int64_t nbi = r * nb + dg_next - 1;
+        lazy_next = Fc[nbi] ? 1u : 0u;
+        const uint32_t* pb = Bc + nbi * kL;
 #pragma unroll
         for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
       }
@@ -607,24 +638,51 @@ static int upload_schedule() {
   return kOk;
 }
 
+// Digits per 32-bit exponent word: ZPIR_TC_DIGITS (4..8, default 6 -> widths
+// 6,6,5,5,5,5 and 63 buckets per row); balanced widths, wider digits first.
+static DigitSpec digit_spec() {
+  static int D = -1;
+  if (D < 0) {
+    const char* e = getenv("ZPIR_TC_DIGITS");
+    D = e ? std::min(8, std::max(4, atoi(e))) : 6;
+  }
+  DigitSpec ds{};
+  ds.D = D;
+  int off = 0, maxw = 0;
+  for (int i = 0; i < D; ++i) {
+    const int w = 32 / D + (i < 32 % D ? 1 : 0);
+    ds.off[i] = off;
+    ds.width[i] = w;
+    off += w;
+    maxw = std::max(maxw, w);
+  }
+  ds.nb = (1 << maxw) - 1;
+  return ds;
+}
+
 int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
   using namespace tcp;
-  const int64_t npos = 4 * n;
+  const DigitSpec ds = digit_spec();
+  const int64_t npos = ds.D * n;
   const int64_t rows_p = ceil_div(rows, kRows) * kRows;
-  return (int64_t)clients * (npos * kL * 4 + npos * (kTY + kTYp) * kTile + kTY * kTile +
-                             rows_p * 255 * (kL * 4 + 1));
+  return (int64_t)clients * (2 * npos * kL * 4 + npos * (kTY + kTYp) * kTile + kTY * kTile +
+                             rows_p * ds.nb * (kL * 4 + 1));
 }
 
 // W_c[rid[r] or r] (Montgomery form, 4096-bit N_c) for rows r < rows of 32-bit
 // exponent rows E[(rid[r] or r) * rs + k], for `clients` independent keys in one
-// launch: the slot_fixed contract with the bucket updates on tcgen05.
+// launch: the slot_fixed contract (P_c = the client's pow8 table, of which the
+// first n entries -- the Montgomery bases -- are read) with the bucket updates
+// on tcgen05.
 int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint32_t* const* N,
                               const uint32_t* np, const uint32_t* const* one_m,
                               const uint32_t* const* Nprime, uint32_t* const* W, int64_t n,
                               const uint32_t* E, int64_t rs, const int32_t* rid, int64_t rows,
                               cudaStream_t st) {
   using namespace tcp;
-  const int64_t npos = 4 * n;
+  const DigitSpec ds = digit_spec();
+  const int nb = ds.nb;
+  const int64_t npos = ds.D * n;
   if (clients <= 0 || clients > 65535 || n <= 0 || rows <= 0 || npos > 65536 ||
       (int64_t)clients * npos * kTY * 256 >= (1ll << 31)) {
     set_error("tc_slot_fixed: bad shapes (clients=%d n=%lld rows=%lld)", clients, (long long)n,
@@ -652,10 +710,11 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   std::vector<TcClient> hc(C);
   for (int c = 0; c < C; ++c) hc[c] = {P[c], N[c], one_m[c], Nprime[c], W[c], np[c]};
   TcClient* dcl = nullptr;
-  uint32_t *Yp = nullptr, *Bk = nullptr;
+  uint32_t *Pd = nullptr, *Yp = nullptr, *Bk = nullptr;
   uint8_t *tY = nullptr, *tYp = nullptr, *tN = nullptr, *Fk = nullptr;
   auto release = [&]() {
     if (dcl) cudaFreeAsync(dcl, st);
+    if (Pd) cudaFreeAsync(Pd, st);
     if (Yp) cudaFreeAsync(Yp, st);
     if (Bk) cudaFreeAsync(Bk, st);
     if (tY) cudaFreeAsync(tY, st);
@@ -670,25 +729,27 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
     return kErrCuda;
   };
   if (cudaMallocAsync(reinterpret_cast<void**>(&dcl), sizeof(TcClient) * C, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Pd), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Yp), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&tY), (size_t)C * npos * kTY * kTile, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&tYp), (size_t)C * npos * kTYp * kTile, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&tN), (size_t)C * kTY * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * 255 * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)C * rows_p * 255, st) != cudaSuccess)
+      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * nb * kL * 4, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)C * rows_p * nb, st) != cudaSuccess)
     return fail("workspace allocation");
   // the host vector is read at enqueue time for pageable memory (synchronous copy)
   if (cudaMemcpyAsync(dcl, hc.data(), sizeof(TcClient) * C, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemsetAsync(Fk, 0, (size_t)C * rows_p * 255, st) != cudaSuccess)
+      cudaMemsetAsync(Fk, 0, (size_t)C * rows_p * nb, st) != cudaSuccess)
     return fail("client table / flags");
-  mul_lo_kernel<<<dim3((unsigned)ceil_div(npos, 128), C), 128, 0, st>>>(dcl, npos, Yp);
-  toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 0, nullptr, npos, kTY,
+  powtab_kernel<<<dim3((unsigned)ceil_div(n, 4), C), 128, 0, st>>>(dcl, n, ds, Pd);
+  mul_lo_kernel<<<dim3((unsigned)ceil_div(npos, 128), C), 128, 0, st>>>(dcl, Pd, npos, Yp);
+  toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 1, Pd, npos, kTY,
                                                                      kDeltaY, tY);
   toep_tiles_kernel<<<dim3((unsigned)(npos * kTYp), C), 256, 0, st>>>(dcl, 1, Yp, npos, kTYp,
                                                                       kDeltaYp, tYp);
   toep_tiles_kernel<<<dim3((unsigned)kTY, C), 256, 0, st>>>(dcl, 2, nullptr, 1, kTY, kDeltaY, tN);
   {
-    const int64_t cnt = rows_p * 255;
+    const int64_t cnt = rows_p * nb;
     bucket_fill_kernel<<<dim3((unsigned)ceil_div(cnt * kL, 256), C), 256, 0, st>>>(dcl, Bk, cnt);
   }
   if (check_launch("tc_slot_fixed setup")) return fail("setup kernels");
@@ -708,10 +769,10 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   for (int64_t p0 = 0; p0 < npos; p0 += ck) {
     const int64_t p1 = std::min<int64_t>(npos, p0 + ck);
     tc_step_kernel<<<dim3((unsigned)tiles, C), kThreads, kSmem, st>>>(
-        mYp, mY, mN, dcl, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk, Fk);
+        mYp, mY, mN, dcl, Pd, ds, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk, Fk);
   }
   if (check_launch("tc_step")) return fail("tc_step launch");
-  bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, Fk, rows,
+  bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, Fk, nb, rows,
                                                                              rows_p, rid);
   if (check_launch("bucket_combine")) return fail("bucket_combine");
   release();

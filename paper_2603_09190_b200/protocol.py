@@ -54,8 +54,10 @@ PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
 TC_HINT = os.environ.get("ZPIR_TC_HINT", "1") != "0"
 # transient workspace cap of one tensor-core hint launch (tiles + buckets)
 TC_WS_BYTES = float(os.environ.get("ZPIR_TC_WS_GB", "24")) * 2**30
-# refreshes with at least this many (changed row x client) pairs use the tensor cores
-TC_REFRESH_MIN = int(os.environ.get("ZPIR_TC_REFRESH_MIN", "256"))
+# refreshes of at least this many changed DB rows use the tensor cores (a tensor-core
+# launch costs ~D*n positions of fixed latency and ~2 GB of Toeplitz tiles per
+# client whatever the row count; the IMAD kernels cost ~0.05 ms per row and client)
+TC_REFRESH_MIN_ROWS = int(os.environ.get("ZPIR_TC_REFRESH_MIN_ROWS", "2048"))
 
 
 @dataclass
@@ -526,13 +528,25 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
     tc = [j for j in prep if _tc_eligible(state, j[1])]
     for batch in (_tc_batches(state, tc, nslot) if tc else []):
         device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, nslot, stream=stream)
+    # the per-client group recombination (slot_combine: one warp per group, a
+    # 32 * cap-deep Horner chain) is latency bound for one client; several
+    # clients' run side by side on a small stream pool
+    side = [stream] if len(jobs) == 1 else [torch.cuda.Stream(dev) for _ in range(min(4, len(jobs)))]
+    ev = torch.cuda.Event()
+    ev.record(stream)
     out = []
-    for (reg, qi), (P, kctx, W) in zip(jobs, prep):
+    for i, ((reg, qi), (P, kctx, W)) in enumerate(zip(jobs, prep)):
+        st = side[i % len(side)]
+        if st is not stream:
+            st.wait_event(ev)
         if not _tc_eligible(state, kctx):
-            device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, stream)
+            device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, st)
         k = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
-        device.slot_combine(W, lay.cap, None, lay.groups, kctx, k, lay.gamma, stream)
+        device.slot_combine(W, lay.cap, None, lay.groups, kctx, k, lay.gamma, st)
         out.append(k)
+    for st in side:
+        if st is not stream:
+            stream.wait_stream(st)
     res = []
     for (reg, qi), (P, kctx, W), k in zip(jobs, prep, out):
         entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
@@ -580,8 +594,8 @@ def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
 
 def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
                   nstreams: int = 8) -> list:
-    """refresh_hint for many (registration, hint) pairs at once. With enough
-    work (changed rows x clients >= ZPIR_TC_REFRESH_MIN, default 256) and
+    """refresh_hint for many (registration, hint) pairs at once. For large
+    updates (>= ZPIR_TC_REFRESH_MIN_ROWS changed rows, default 2048) and
     4096-bit m^2 the changed rows' W of all clients are recomputed by one
     tensor-core launch (row ids, one grid row per client); otherwise the IMAD
     kernels of each client are spread over `nstreams` CUDA streams so that
@@ -594,8 +608,7 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
     main = stream or torch.cuda.current_stream(dev)
     rows, rid, gid, ng = _changed_ids(state, changed_rows)
     kctxs = [key_ctx(reg.pk.m, dev) for reg, _ in pairs]
-    use_tc = rows > 0 and rows * len(pairs) >= TC_REFRESH_MIN and \
-        all(_tc_eligible(state, k) for k in kctxs)
+    use_tc = rows >= TC_REFRESH_MIN_ROWS and all(_tc_eligible(state, k) for k in kctxs)
     if use_tc:
         outs = []
         jobs = []

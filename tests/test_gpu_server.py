@@ -152,7 +152,7 @@ def test_batched_hints_and_tensor_core_refresh(golden, monkeypatch):
     for c in rows:
         db2[:, c] = rng.integers(0, 256, g.d0, dtype=np.uint8)
     st2, changed = st.updated(db2)
-    monkeypatch.setattr(protocol, "TC_REFRESH_MIN", 1)
+    monkeypatch.setattr(protocol, "TC_REFRESH_MIN_ROWS", 1)
     ref_pairs = list(zip(regs, hs))
     out = z.refresh_hints(st2, ref_pairs, changed)
     full = z.ServerGlobalState(params, db2, db_version=1)
