@@ -239,8 +239,11 @@ def run_reference(args):
         "value": v, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 3),
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8xu32 / 2048-bit", "data": "synthetic",
-        "config": {"workload": "1 GiB DB (32768 x 32768 u8), n=1024, q=2^32, 2048-bit Paillier, "
-                               "single query (sampled rows)", "d0": D0, "d1": D1},
+        "config": {"workload": "BASELINE configs[1]: 1 GiB DB per GPU (32768 x 32768 u8), "
+                               "n=1024, q=2^32, 2048-bit Paillier, single query, SEPARATE",
+                   "d0": D0, "d1": D1, "groups": -(-D1 // CAP),
+                   "parallelism": "host CPU (reference arm, rank 0 only)",
+                   "l2": "n/a (CPU)", "sampled_rows_per_step": rows},
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -58,6 +58,8 @@ TC_WS_BYTES = float(os.environ.get("ZPIR_TC_WS_GB", "24")) * 2**30
 # launch costs ~D*n positions of fixed latency and ~2 GB of Toeplitz tiles per
 # client whatever the row count; the IMAD kernels cost ~0.05 ms per row and client)
 TC_REFRESH_MIN_ROWS = int(os.environ.get("ZPIR_TC_REFRESH_MIN_ROWS", "2048"))
+# full hints: tensor cores when the batch has at least this many exponent rows in total
+TC_MIN_ROWS = int(os.environ.get("ZPIR_TC_MIN_ROWS", "2048"))
 
 
 @dataclass
@@ -525,9 +527,14 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
         P = device.pow8_table(bases, kctx, stream)
         W = torch.empty((nslot, kctx.l2), dtype=torch.int32, device=dev)
         prep.append((P, kctx, W))
+    # the tensor-core launch costs ~D*n positions of fixed latency per wave of row
+    # tiles; below ~TC_MIN_ROWS rows in the whole batch the IMAD kernel is faster
     tc = [j for j in prep if _tc_eligible(state, j[1])]
+    if nslot * len(tc) < TC_MIN_ROWS:
+        tc = []
     for batch in (_tc_batches(state, tc, nslot) if tc else []):
         device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, nslot, stream=stream)
+    tc_ids = {id(j[2]) for j in tc}
     # the per-client group recombination (slot_combine: one warp per group, a
     # 32 * cap-deep Horner chain) is latency bound for one client; several
     # clients' run side by side on a small stream pool
@@ -539,7 +546,7 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
         st = side[i % len(side)]
         if st is not stream:
             st.wait_event(ev)
-        if not _tc_eligible(state, kctx):
+        if id(W) not in tc_ids:
             device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, st)
         k = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
         device.slot_combine(W, lay.cap, None, lay.groups, kctx, k, lay.gamma, st)
