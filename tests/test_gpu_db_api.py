@@ -151,3 +151,23 @@ def test_handle_api_mixed_limb_widths(api, golden):
         kin = ints_to_limbs(g.ints("k"), 2 * L)
         _lib.call("zpir_db_answer_combined", d._h, vp(q), vp(c), vp(mm), L, vp(kin), vp(K))
         assert limbs_to_ints(K) == g.ints("K")
+
+
+def test_handle_api_tensor_core_hint(api, monkeypatch):
+    """zpir_db_client_hint on a DB with >= 2048 exponent rows takes the
+    tensor-core Pippenger (full Montgomery inverse computed on the host by
+    Newton iteration); its entries equal the Python API's IMAD path."""
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import protocol
+    rng = random.Random(2048)
+    d0, d1, n = 128, 2100, 64
+    params = z.ProtocolParams(z.LweParams(n=n, q=1 << 32, p=256, noise_sigma=6.4), d0, d1, 2048)
+    db = np.frombuffer(np.random.default_rng(3).bytes(d0 * d1), dtype=np.uint8).reshape(d0, d1)
+    sk, seed = client.setup(2048, rng)
+    with api.DeviceDatabase(params, db) as d:
+        k_tc = d.client_hint(sk.m, seed, 2)
+    monkeypatch.setattr(protocol, "TC_MIN_ROWS", 1 << 30)        # IMAD slot_fixed
+    st = z.ServerGlobalState(params, db)
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
+    assert k_tc == [c.c for c in z.hint(st, reg, 2).entries]
