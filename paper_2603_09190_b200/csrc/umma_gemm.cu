@@ -770,6 +770,206 @@ umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   }
 }
 
+// Planar BIGINT GEMM on CTA pairs (cta_group::2): the umma_planar_kernel
+// contract with M = 256 rows per pair tile (128 per CTA, each CTA's own TMEM
+// lanes) and the ck_o byte rows (B, N = 4 lm) split by N halves, so each SM
+// stages its own 16 KB of H planes and HALF of the B k-block per MMA group:
+// 32 KB instead of 48 KB per 4 MMAs of L2->SM traffic (the single-CTA kernel
+// is L2-throughput bound when many queries are compressed at once). Both
+// CTAs' TMA loads complete on the leader's full barrier; the leader's commits
+// multicast to both CTAs; both epilogues arrive on the leader's tempty.
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1)
+umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
+                        const __grid_constant__ CUtensorMap mapB, const UmmaArgs args,
+                        int64_t np, int64_t rows) {
+  using C = PairCfg<NT>;
+  static_assert(C::kP1 == 0 && C::kAcc == 2 && C::kOv == 0, "planar pair: N <= 256");
+  constexpr int kLimbs = NT / 4;
+  constexpr int kZ = kLimbs + 4;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + C::kAcc;
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(tempty + C::kAcc + 1);
+
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&mapA);
+    tma_prefetch(&mapB);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::kAcc; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 256);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc_pair(tbase_smem, C::kTmemCols);
+  tc_fence_before();
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tbase = *tbase_smem;
+  const int kbp = (int)(np / kBK);        // k-blocks per plane pass
+
+  // pair work list: units = (pair tile of 256 rows, query)
+  const int npairs = (int)(gridDim.x >> 1), pid = (int)(blockIdx.x >> 1);
+  SegIter it;
+  {
+    const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
+    it.u = pid * T / npairs;
+    it.u1 = (pid + 1) * T / npairs;
+    it.kb = args.kblocks;
+    it.split = false;
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs) ----------------
+      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      int64_t t;
+      int k0, k1, stage = 0;
+      uint32_t phase = 0;
+      while (it.next(t, k0, k1)) {
+        const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+        const int arow = m * 2 * kBM + (int)rank * kBM;
+        for (int a = 0; a < 4; ++a)
+          for (int kb = 0; kb < kbp; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+            if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
+            tma_load_2d_pair(sA + stage * C::kABytes, &mapA, fb, (int)(a * np) + kb * kBK, arow,
+                             pol_a);
+            tma_load_2d_pair(sB + stage * C::kBBytes, &mapB, fb, kb * kBK,
+                             n * NT + (int)rank * C::kH0, pol_b);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (leader): one group per (pair tile, plane) ----------------
+      int64_t t;
+      int k0, k1, stage = 0, acc = 0;
+      uint32_t phase = 0, aphase = 0;
+      const uint32_t idesc = idesc_u8(2 * kBM, NT);
+      while (it.next(t, k0, k1)) {
+        for (int a = 0; a < 4; ++a) {
+          mbar_wait(&tempty[acc], aphase ^ 1);
+          tc_fence_after();
+          const uint32_t d = tbase + (uint32_t)(acc * C::kAccOff1);
+          for (int kb = 0; kb < kbp; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint64_t ad = desc_sw128(smem_u32(sA + stage * C::kABytes));
+            const uint64_t bd = desc_sw128(smem_u32(sB + stage * C::kBBytes));
+#pragma unroll
+            for (int k = 0; k < kBK / 32; ++k)
+              umma_i8_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit_pair(&empty[stage], 0x3);
+            if (++stage == C::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          umma_commit_pair(&tfull[acc], 0x3);
+          if (++acc == C::kAcc) {
+            acc = 0;
+            aphase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5 of both CTAs): z row in registers ----------------
+    const int quarter = warp & 3;
+    const int lrow = quarter * 32 + lane;
+    const uint32_t tempty_l[2] = {mapa_shared(smem_u32(&tempty[0]), 0),
+                                  mapa_shared(smem_u32(&tempty[1]), 0)};
+    int64_t t;
+    int k0, k1, acc = 0;
+    uint32_t aphase = 0;
+    while (it.next(t, k0, k1)) {
+      const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+      const int64_t row = (int64_t)m * 2 * kBM + (int64_t)rank * kBM + lrow;
+      uint32_t z[kZ];
+#pragma unroll
+      for (int i = 0; i < kZ; ++i) z[i] = 0;
+#pragma unroll 1
+      for (int a = 0; a < 4; ++a) {
+        mbar_wait(&tfull[acc], aphase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * C::kAccOff1);
+        const uint32_t sh = 8u * (uint32_t)a;
+        unsigned long long carry = 0;
+        uint32_t prev = 0, c2 = 0;
+#pragma unroll
+        for (int c = 0; c < NT / 16; ++c) {
+          uint32_t r[16];
+          tmem_ld16(taddr + 16 * c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned long long sum = (unsigned long long)r[4 * i] +
+                                           ((unsigned long long)r[4 * i + 1] << 8) +
+                                           ((unsigned long long)r[4 * i + 2] << 16) +
+                                           ((unsigned long long)r[4 * i + 3] << 24) + carry;
+            const uint32_t v = (uint32_t)sum;
+            carry = sum >> 32;
+            const uint32_t w = __funnelshift_l(prev, v, sh);
+            const unsigned long long zz = (unsigned long long)z[4 * c + i] + w + c2;
+            z[4 * c + i] = (uint32_t)zz;
+            c2 = (uint32_t)(zz >> 32);
+            prev = v;
+          }
+        }
+        tc_fence_before();
+        mbar_arrive_cluster(tempty_l[acc]);
+        {
+          const uint32_t v0 = (uint32_t)carry, v1 = (uint32_t)(carry >> 32);
+          const uint32_t w[4] = {__funnelshift_l(prev, v0, sh), __funnelshift_l(v0, v1, sh),
+                                 __funnelshift_l(v1, 0u, sh), 0u};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const unsigned long long zz = (unsigned long long)z[kLimbs + i] + w[i] + c2;
+            z[kLimbs + i] = (uint32_t)zz;
+            c2 = (uint32_t)(zz >> 32);
+          }
+        }
+        if (++acc == C::kAcc) {
+          acc = 0;
+          aphase ^= 1;
+        }
+      }
+      if (row < rows) {
+        uint32_t* zr = args.out + (int64_t)n * args.zq + row * args.wz;
+#pragma unroll
+        for (int i = 0; i < kZ; i += 4)
+          *reinterpret_cast<uint4*>(zr + i) = make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();   // all MMAs consumed, all TMEM reads done in both CTAs
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tbase, C::kTmemCols);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // operand builders
 
@@ -1168,6 +1368,20 @@ int build_bcp_launch(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp
   return check_launch("build_bcp");
 }
 
+// CTA-pair planar kernel: ZPIR_PLANAR_PAIR = 0 never, 1 always, default from
+// ZPIR_PLANAR_PAIR_MINQ queries per launch (default 2: batches)
+static bool use_planar_pair(int nq) {
+  static int mode = -2, minq = 2;
+  if (mode == -2) {
+    const char* e = getenv("ZPIR_PLANAR_PAIR");
+    mode = e ? (e[0] == '0' ? 0 : 1) : -1;
+    const char* q = getenv("ZPIR_PLANAR_PAIR_MINQ");
+    if (q) minq = atoi(q);
+  }
+  if (mode >= 0) return mode == 1;
+  return nq >= minq;
+}
+
 // z (nq x rows x wz) from the planar operands; lm in {32, 64}.
 int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp, int lm,
                        int nq, int wz, uint32_t* z, int ctas, cudaStream_t st) {
@@ -1193,6 +1407,38 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
   const int sms = num_sms();
   const int cap = (ctas > 0 && ctas < sms) ? ctas : sms;
   const int grid = (int)std::min<int64_t>(cap, T);
+  if (use_planar_pair(nq) && cap >= 2) {
+    CUtensorMap mbp;
+    if (int e = make_map(&mbp, bp, (int64_t)NT * nq, np, np, NT / 2)) return e;
+    a.m_tiles = (int)ceil_div(rows, 2 * kBM);
+    const int64_t Tp = (int64_t)a.m_tiles * a.n_tiles;
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(cap / 2, Tp));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e;
+    if (NT == 256) {
+      auto kern = umma_planar_pair_kernel<256>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256>::kSmem);
+      cfg.dynamicSmemBytes = PairCfg<256>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows);
+    } else {
+      auto kern = umma_planar_pair_kernel<128>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<128>::kSmem);
+      cfg.dynamicSmemBytes = PairCfg<128>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows);
+    }
+    if (e != cudaSuccess) return check_launch("umma_planar_pair launch");
+    return check_launch("umma_planar_pair");
+  }
   if (NT == 256) {
     auto kern = umma_planar_kernel<256>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, UmmaCfg<256>::kSmem);
