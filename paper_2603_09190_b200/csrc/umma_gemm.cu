@@ -637,7 +637,10 @@ umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      // batches: every H tile is re-read once per query by the same CTA (pair),
+      // so H stays in L2 (the working set is ~1 MB per pair tile in flight)
+      const uint64_t pol_a = args.a_keep ? l2_evict_last() : l2_evict_first();
+      const uint64_t pol_b = l2_evict_last();
       SegIter it = seg_range(args);
       int64_t t;
       int k0, k1, stage = 0;
@@ -835,7 +838,10 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
-      const uint64_t pol_a = l2_evict_first(), pol_b = l2_evict_last();
+      // batches: every H tile is re-read once per query by the same CTA (pair),
+      // so H stays in L2 (the working set is ~1 MB per pair tile in flight)
+      const uint64_t pol_a = args.a_keep ? l2_evict_last() : l2_evict_first();
+      const uint64_t pol_b = l2_evict_last();
       int64_t t;
       int k0, k1, stage = 0;
       uint32_t phase = 0;
@@ -1396,6 +1402,7 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
   a.out = z;
   a.wz = wz;
   a.zq = rows * wz;
+  a.a_keep = nq > 1 ? 1 : 0;
   const int NT = 4 * lm;
   CUtensorMap ma, mb;
   if (int e = make_map(&ma, hp, rows, 4 * np, 4 * np, kBM)) return e;
