@@ -56,9 +56,10 @@ constexpr int kSmem = 2 * kABytes + kStages * kTile + 1024 + 1024;
 constexpr int kNSteps = 20;
 
 // The static MMA schedule: task (0 U0, 1 U1, 2 H0, 3 H1; TMEM buffer = task & 1),
-// A operand (0 = X, 1 = u), k-block, B source (0 = Y', 1 = Y, 2 = N), tile t.
+// A operand (0 = X, 1 = u), k-block, B source (0 = Y', 1 = Y, 2 = N), tile t,
+// issue segment: 0 U0, 1 U1, 2 H0 X*Y, 3 H1 X*Y (then X is free), 4 H0 u*N, 5 H1 u*N.
 struct Step {
-  int8_t task, a, ka, src, t;
+  int8_t task, a, ka, src, t, seg;
 };
 __constant__ Step kSched[kNSteps];
 
@@ -255,7 +256,8 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
   uint64_t* uready = xfull + 1;             // all 512 bytes of u written
   uint64_t* tfull = uready + 1;             // [2] per TMEM buffer
   uint64_t* tempty = tfull + 2;             // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xfree = tempty + 2;             // every MMA reading X of this position done
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(xfree + 2);
   uint32_t* sN = tslot + 4;                 // N limbs (512 B)
 
   const int client = blockIdx.y;
@@ -274,6 +276,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128);
     }
+    mbar_init(xfree, 1);
     fence_mbar_init();
   }
   const uint32_t* Ncl = cl[client].N;
@@ -314,34 +317,48 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer: tasks 0..3 per position, buffer = task & 1 ----------------
+      // ---------------- MMA issuer: six segments per position, buffer = task & 1 ----------------
       const uint32_t idesc = idesc_u8(kRows, 256);
       int stage = 0;
       uint32_t phase = 0, xph = 0;
       uint32_t eph[2] = {0, 0};
-      bool used[2] = {false, false};
+      bool used0 = false, used1 = false;
       for (int pos = pos0; pos < pos1; ++pos) {
         int cur = -1;
-        bool first = true, uwait = false;
+        bool first = true;
         for (int s = 0; s < kNSteps; ++s) {
           const Step st = kSched[s];
           const int buf = st.task & 1;
-          if (st.task != cur) {
-            if (cur >= 0) umma_commit(&tfull[cur & 1]);
-            if (used[buf]) {                  // the epilogue has drained this buffer
-              mbar_wait(&tempty[buf], eph[buf]);
-              eph[buf] ^= 1;
+          if (st.seg != cur) {
+            if (cur == 0) umma_commit(&tfull[0]);          // U0 -> epilogue
+            else if (cur == 1) umma_commit(&tfull[1]);     // U1
+            else if (cur == 3) umma_commit(xfree);         // X no longer read
+            else if (cur == 4) umma_commit(&tfull[0]);     // H0
+            switch (st.seg) {
+              case 0:                                      // buffer 0 after H0(pos-1) drained
+                if (used0) { mbar_wait(&tempty[0], eph[0]); eph[0] ^= 1; }
+                used0 = true;
+                mbar_wait(xfull, xph);
+                break;
+              case 1:                                      // buffer 1 after H1(pos-1) drained
+                if (used1) { mbar_wait(&tempty[1], eph[1]); eph[1] ^= 1; }
+                used1 = true;
+                break;
+              case 2:                                      // U0 drained
+                mbar_wait(&tempty[0], eph[0]); eph[0] ^= 1;
+                break;
+              case 3:                                      // U1 drained
+                mbar_wait(&tempty[1], eph[1]); eph[1] ^= 1;
+                break;
+              case 4:                                      // all of u written
+                mbar_wait(uready, xph);
+                break;
+              default:
+                break;
             }
-            used[buf] = true;
-            if (st.task == 0) mbar_wait(xfull, xph);
             tc_fence_after();
-            cur = st.task;
-            first = true;
-          }
-          if (st.a && !uwait) {               // u * N: all of u written by the epilogue
-            mbar_wait(uready, xph);
-            tc_fence_after();
-            uwait = true;
+            cur = st.seg;
+            first = cur <= 3;                              // u * N accumulates onto X * Y
           }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -359,7 +376,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             phase ^= 1;
           }
         }
-        umma_commit(&tfull[cur & 1]);
+        umma_commit(&tfull[1]);                            // H1
         xph ^= 1;
       }
     }
@@ -378,70 +395,78 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
 #pragma unroll
     for (int i = 0; i < 4; ++i) nl[i] = sN[4 * lane + i];
     const uint32_t ntop = sN[kL - 1];
-    uint32_t fph[2] = {0, 0};
-    // digit, bucket and flag of this row at position pos (software-pipelined:
-    // the next position's are loaded and its bucket prefetched into L2 while
-    // this position's MMAs run)
+    uint32_t fph[2] = {0, 0}, xfph = 0;
+    const int kbl = lane >> 3, chl = lane & 7;  // this lane's 16-byte chunk of a row
+    const uint32_t xa_l = smem_u32(XA) + kbl * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
+    const int64_t rbase = row0 + quarter * 32;
     auto digit_at = [&](int p) -> uint32_t {
       if (r >= rows) return 0u;
       const int di = p / (int)n;
       return (E[er * rs + (p - (int64_t)di * n)] >> ds.off[di]) & ((1u << ds.width[di]) - 1u);
     };
-    uint32_t dg = digit_at(pos0);
-    uint32_t lazy = (dg && Fc[r * nb + dg - 1]) ? 1u : 0u;
-    for (int pos = pos0; pos < pos1; ++pos) {
-      const int64_t bidx = (r * nb) + (dg ? dg - 1 : 0);
-      uint32_t* brow = Bc + bidx * kL;
-      const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
-      // ---- gather X = B[r][dg - 1] (zero rows for dg == 0), warp-cooperative
-      // async copies: lane c moves bytes 16c..16c+15 of each of the warp's 32 rows
-      // into the SW128 A layout (zero fill for dg == 0), all in flight at once.
-      // The previous position's MMAs are complete (its last tfull was waited)
-      // and its bucket stores are ordered by the warp barrier.
-      __syncwarp();
-      {
-        const int kb = lane >> 3, ch = lane & 7;
-        const uint32_t xa = smem_u32(XA) + kb * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
-        const int64_t rbase = row0 + quarter * 32;
+    // X rows of the warp from their buckets, warp-cooperative async copies: lane
+    // c moves bytes 16c..16c+15 of each of the warp's 32 rows into the SW128 A
+    // layout (zero fill for digit 0); rows with `skip` set are written by their
+    // own thread instead (bucket updated at this very position).
+    auto gather_issue = [&](uint32_t dgv, uint32_t skip) {
+      const uint32_t sk = __ballot_sync(0xffffffffu, skip != 0);
 #pragma unroll 8
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t d_i = __shfl_sync(0xffffffffu, dg, i);
-          const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
-          const uint32_t dst = xa + i * kBK + ((ch ^ (i & 7)) << 4);
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                       "r"(d_i ? 16u : 0u)
-                       : "memory");
-        }
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        // lazily reduced buckets: a set flag means the stored value is Z with
-        // Z - N still to be taken (mod R)
-        uint32_t lzm = __ballot_sync(0xffffffffu, lazy != 0);
-        while (lzm) {
-          const int i = __ffs(lzm) - 1;
-          lzm &= lzm - 1;
-          uint8_t* p = XA + kb * (kRows * kBK) + (quarter * 32 + i) * kBK + ((ch ^ (i & 7)) << 4);
-          uint4 w = *reinterpret_cast<const uint4*>(p);
-          uint32_t v[4] = {w.x, w.y, w.z, w.w};
-          big_cond_sub<4>(v, 1u, nl, lane);     // x - N mod R (warp-uniform)
-          *reinterpret_cast<uint4*>(p) = make_uint4(v[0], v[1], v[2], v[3]);
-        }
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t d_i = __shfl_sync(0xffffffffu, dgv, i);
+        if ((sk >> i) & 1u) continue;
+        const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
+        const uint32_t dst = xa_l + i * kBK + ((chl ^ (i & 7)) << 4);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                     "r"(d_i ? 16u : 0u)
+                     : "memory");
+      }
+    };
+    // copies landed; lazily reduced buckets: a set flag means the stored value
+    // is Z with Z - N still to be taken (mod R)
+    auto gather_finish = [&](uint32_t lz) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncwarp();
+      uint32_t lzm = __ballot_sync(0xffffffffu, lz != 0);
+      while (lzm) {
+        const int i = __ffs(lzm) - 1;
+        lzm &= lzm - 1;
+        uint8_t* q = XA + kbl * (kRows * kBK) + (quarter * 32 + i) * kBK + ((chl ^ (i & 7)) << 4);
+        uint4 w = *reinterpret_cast<const uint4*>(q);
+        uint32_t v[4] = {w.x, w.y, w.z, w.w};
+        big_cond_sub<4>(v, 1u, nl, lane);       // x - N mod R (warp-uniform)
+        *reinterpret_cast<uint4*>(q) = make_uint4(v[0], v[1], v[2], v[3]);
       }
       fence_async_smem();
       mbar_arrive(xfull);
-      // next position: digit, flag, and an L2 prefetch of its bucket
-      const uint32_t dg_next = pos + 1 < pos1 ? digit_at(pos + 1) : 0u;
-      uint32_t lazy_next = 0;
-      if (dg_next) {
-        const int64_t nbi = r * nb + dg_next - 1;
-        lazy_next = Fc[nbi] ? 1u : 0u;
-        const uint32_t* pb = Bc + nbi * kL;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
-      }
       __syncwarp();
-      // bytes 508..511 of this row's X (k-block 3, chunk 7)
-      const uint32_t xtop =
-          *reinterpret_cast<const uint32_t*>(XA + 3 * (kRows * kBK) + t * kBK + ((7 ^ (t & 7)) << 4) + 12);
+    };
+    // bytes 508..511 of this row's X (k-block 3, chunk 7)
+    const uint32_t* xtop_p =
+        reinterpret_cast<const uint32_t*>(XA + 3 * (kRows * kBK) + t * kBK + ((7 ^ (t & 7)) << 4) + 12);
+    auto prefetch_bucket = [&](uint32_t d) {
+      if (!d) return;
+      const uint32_t* pb = Bc + (r * nb + d - 1) * kL;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
+    };
+
+    // prologue: X of the first position
+    uint32_t dg = digit_at(pos0);
+    gather_issue(dg, 0u);
+    gather_finish((dg && Fc[r * nb + dg - 1]) ? 1u : 0u);
+    uint32_t xtop = *xtop_p;
+    uint32_t dg_n = pos0 + 1 < pos1 ? digit_at(pos0 + 1) : 0u;
+    prefetch_bucket(dg_n);
+
+    for (int pos = pos0; pos < pos1; ++pos) {
+      const bool last = pos + 1 >= pos1;
+      const int64_t bidx = (r * nb) + (dg ? dg - 1 : 0);
+      uint32_t* brow = Bc + bidx * kL;
+      const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
+      // the next position's bucket is this position's (digit repeats): its X is
+      // this position's Z, written into the A layout by this thread below
+      const uint32_t conflict = (!last && dg && dg_n == dg) ? 1u : 0u;
+      const uint32_t lazy_n = (!last && dg_n && !conflict && Fc[r * nb + dg_n - 1]) ? 1u : 0u;
 
       unsigned long long carry = 0;
       uint32_t utop = 0;
@@ -475,9 +500,25 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         tc_fence_before();
         mbar_arrive(&tempty[task]);
       }
+      // ---- the next position's gather, once no MMA reads X any more; it lands
+      // while H0 / H1 are computed and drained
+      if (!last) {
+        mbar_wait(xfree, xfph);
+        xfph ^= 1;
+        gather_issue(dg_n, conflict);
+      }
       // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
       uint32_t zb = 0;                        // borrow chain of Z - N, low limbs up
       uint32_t pend[4];                       // Z limbs awaiting a 16-byte store
+      auto emit = [&](int li) {               // limbs li-3..li complete
+        if (dg)
+          *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+        if (conflict) {
+          const int cc = (li - 3) >> 2, kb = cc >> 3, ch = cc & 7;
+          *reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
+              make_uint4(pend[0], pend[1], pend[2], pend[3]);
+        }
+      };
       carry = 0;
       {
         mbar_wait(&tfull[0], fph[0]);
@@ -504,8 +545,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
             zb = (uint32_t)(dlt >> 63);
             pend[li & 3] = z;
-            if ((li & 3) == 3 && dg)
-              *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+            if ((li & 3) == 3) emit(li);
           }
         }
         tc_fence_before();
@@ -527,8 +567,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
             zb = (uint32_t)(dlt >> 63);
             pend[li & 3] = z;
-            if ((li & 3) == 3 && dg)
-              *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+            if ((li & 3) == 3) emit(li);
           }
         }
         tc_fence_before();
@@ -550,17 +589,37 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         const unsigned long long dlt = (unsigned long long)z - ntop - zb;
         zb = (uint32_t)(dlt >> 63);
         pend[3] = z;
-        if (dg) {
-          *reinterpret_cast<uint4*>(brow + kL - 4) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
-          // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or Z - N does
-          // not borrow; the subtraction is deferred to the bucket's next reader
-          const uint32_t f = (top != 0 || zb == 0) ? 1u : 0u;
-          Fc[bidx] = (uint8_t)f;
-          if (dg_next == dg) lazy_next = f;     // same bucket again: its new flag
+        emit(kL - 1);
+        // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or Z - N does
+        // not borrow; the bucket keeps Z and a flag (the subtraction is deferred
+        // to its next reader), the forwarded X is reduced right here
+        const uint32_t f = (top != 0 || zb == 0) ? 1u : 0u;
+        if (dg) Fc[bidx] = (uint8_t)f;
+        if (conflict && f) {
+          uint32_t bw = 0;
+#pragma unroll 1
+          for (int cc = 0; cc < 32; ++cc) {
+            const int kb = cc >> 3, ch = cc & 7;
+            uint4* q = reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4));
+            uint4 w = *q;
+            uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const unsigned long long d = (unsigned long long)v[i] - sN[4 * cc + i] - bw;
+              v[i] = (uint32_t)d;
+              bw = (uint32_t)(d >> 63);
+            }
+            *q = make_uint4(v[0], v[1], v[2], v[3]);
+          }
         }
       }
-      dg = dg_next;
-      lazy = lazy_next;
+      if (!last) {
+        gather_finish(lazy_n);                  // + xfull for the next position
+        xtop = *xtop_p;
+        dg = dg_n;
+        dg_n = pos + 2 < pos1 ? digit_at(pos + 2) : 0u;
+        prefetch_bucket(dg_n);
+      }
     }
   }
   tc_fence_before();
@@ -615,20 +674,22 @@ static int upload_schedule() {
       const int delta = 256 * gc - 128 * ka;
       const int t = (delta - tcp::kDeltaYp) / 128;
       if (delta - 127 < 512 && delta + 255 >= 0 && t >= 0 && t < tcp::kTYp)
-        h[k++] = {(int8_t)gc, 0, (int8_t)ka, 0, (int8_t)t};
+        h[k++] = {(int8_t)gc, 0, (int8_t)ka, 0, (int8_t)t, (int8_t)gc};
     }
-  // H0, H1: output columns c0 = 508 / 764 of X * Y + u * N, the X * Y k-blocks
-  // first (they do not wait for u)
-  for (int hh = 0; hh < 2; ++hh) {
-    const int c0 = 508 + 256 * hh;
-    for (int a = 0; a < 2; ++a)
+  // H0, H1 (output columns c0 = 508 / 764 of X * Y + u * N): both X * Y parts
+  // first (after them X is no longer read: the next position's gather may
+  // start), then both u * N parts (they wait for u)
+  for (int a = 0; a < 2; ++a)
+    for (int hh = 0; hh < 2; ++hh) {
+      const int c0 = 508 + 256 * hh;
       for (int ka = 0; ka < 4; ++ka) {
         const int delta = c0 - 128 * ka;
         if (delta - 127 >= 512) continue;           // window entirely above byte 511
         const int t = (delta - tcp::kDeltaY) / 128;
-        h[k++] = {(int8_t)(2 + hh), (int8_t)a, (int8_t)ka, (int8_t)(a ? 2 : 1), (int8_t)t};
+        h[k++] = {(int8_t)(2 + hh), (int8_t)a, (int8_t)ka, (int8_t)(a ? 2 : 1), (int8_t)t,
+                  (int8_t)(2 + 2 * a + hh)};
       }
-  }
+    }
   if (k != tcp::kNSteps) {
     set_error("tc_pippenger: schedule has %d steps", k);
     return kErrCuda;
