@@ -224,6 +224,40 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
   for (int i = 0; i < 64; ++i) asm volatile("" : "+r"(v[i]));
 }
 
+// Wait for this thread's outstanding TMEM loads, ordered after `dep` (the
+// last value computed from the previous batch) so the compiler keeps that
+// work ahead of the wait.
+__device__ __forceinline__ void tmem_wait_after(unsigned long long dep) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::"l"(dep) : "memory");
+}
+__device__ __forceinline__ void regs_ready(uint32_t (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(v[i]));
+}
+
+// Drain 256 TMEM columns of this thread's lane in eight 32-column batches,
+// double-buffered: batch g + 1 is in flight while batch g is processed.
+// f(g, v) consumes columns 32 g .. 32 g + 31; it updates `carry`, which also
+// orders the next wait after the processing.
+template <class F>
+__device__ __forceinline__ void drain256(uint32_t taddr, unsigned long long& carry, F&& f) {
+  uint32_t va[32], vb[32];
+  tmem_ld32(taddr, va);
+  tmem_wait_after(carry);
+  regs_ready(va);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    uint32_t (&cur)[32] = (g & 1) ? vb : va;
+    uint32_t (&nxt)[32] = (g & 1) ? va : vb;
+    if (g < 7) tmem_ld32(taddr + 32 * (g + 1), nxt);
+    f(g, cur);
+    if (g < 7) {
+      tmem_wait_after(carry);
+      regs_ready(nxt);
+    }
+  }
+}
+
 // Four byte columns (s32 sums) + carry -> one 32-bit limb.
 __device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long& carry) {
   const unsigned long long s = (unsigned long long)v[0] + ((unsigned long long)v[1] << 8) +
@@ -394,7 +428,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     uint32_t nl[4];                             // N limbs 4 lane .. 4 lane + 3 (gather)
 #pragma unroll
     for (int i = 0; i < 4; ++i) nl[i] = sN[4 * lane + i];
-    const uint32_t ntop = sN[kL - 1];
+    const uint32_t ntop = sN[kL - 1], n126 = sN[kL - 2];
     uint32_t fph[2] = {0, 0}, xfph = 0;
     const int kbl = lane >> 3, chl = lane & 7;  // this lane's 16-byte chunk of a row
     const uint32_t xa_l = smem_u32(XA) + kbl * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
@@ -477,22 +511,19 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         fph[task] ^= 1;
         tc_fence_after();
         const uint32_t taddr = lanebase + (uint32_t)(task * 256);
-#pragma unroll 1
-        for (int g = 0; g < 4; ++g) {
-          uint32_t v[64];
-          tmem_ld64(taddr + 64 * g, v);
+        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {        // 16-byte chunk of u: 4 limbs
+          for (int j = 0; j < 2; ++j) {        // 16-byte chunk of u: 4 limbs
             uint32_t l[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) l[i] = limb4(v + 16 * j + 4 * i, carry);
-            const int cc = task * 16 + 4 * g + j;
+            const int cc = task * 16 + 2 * g + j;
             const int kb = cc >> 3, ch = cc & 7;
             *reinterpret_cast<uint4*>(UA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
                 make_uint4(l[0], l[1], l[2], l[3]);
             utop = l[3];
           }
-        }
+        });
         if (task == 1) {
           fence_async_smem();
           mbar_arrive(uready);
@@ -508,7 +539,6 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         gather_issue(dg_n, conflict);
       }
       // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
-      uint32_t zb = 0;                        // borrow chain of Z - N, low limbs up
       uint32_t pend[4];                       // Z limbs awaiting a 16-byte store
       auto emit = [&](int li) {               // limbs li-3..li complete
         if (dg)
@@ -525,13 +555,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         fph[0] ^= 1;
         tc_fence_after();
         const uint32_t taddr = lanebase;
+        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t v[64];
-          tmem_ld64(taddr + 64 * g, v);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int slot = 16 * g + k;       // columns 508 + 4 slot ..
+          for (int k = 0; k < 8; ++k) {
+            const int slot = 8 * g + k;        // columns 508 + 4 slot ..
             if (slot == 0) {
               // low4 = columns 508..511 as one number (< 2^54)
               const unsigned long long low4 =
@@ -541,13 +568,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
               continue;
             }
             const int li = slot - 1;           // Z limb
-            const uint32_t z = limb4(v + 4 * k, carry);
-            const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
-            zb = (uint32_t)(dlt >> 63);
-            pend[li & 3] = z;
+            pend[li & 3] = limb4(v + 4 * k, carry);
             if ((li & 3) == 3) emit(li);
           }
-        }
+        });
         tc_fence_before();
         mbar_arrive(&tempty[0]);
       }
@@ -556,20 +580,14 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         fph[1] ^= 1;
         tc_fence_after();
         const uint32_t taddr = lanebase + 256u;
+        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t v[64];
-          tmem_ld64(taddr + 64 * g, v);
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int li = 63 + 16 * g + k;    // columns 764 + 4 (li - 63) ..
-            const uint32_t z = limb4(v + 4 * k, carry);
-            const unsigned long long dlt = (unsigned long long)z - sN[li] - zb;
-            zb = (uint32_t)(dlt >> 63);
-            pend[li & 3] = z;
+          for (int k = 0; k < 8; ++k) {
+            const int li = 63 + 8 * g + k;     // columns 764 + 4 (li - 63) ..
+            pend[li & 3] = limb4(v + 4 * k, carry);
             if ((li & 3) == 3) emit(li);
           }
-        }
+        });
         tc_fence_before();
         mbar_arrive(&tempty[1]);
       }
@@ -586,14 +604,35 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
                                      ((unsigned long long)c2 << 16) + carry;
         const uint32_t z = (uint32_t)s;
         const uint32_t top = (uint32_t)(s >> 32);
-        const unsigned long long dlt = (unsigned long long)z - ntop - zb;
-        zb = (uint32_t)(dlt >> 63);
         pend[3] = z;
         emit(kL - 1);
-        // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or Z - N does
-        // not borrow; the bucket keeps Z and a flag (the subtraction is deferred
-        // to its next reader), the forwarded X is reduced right here
-        const uint32_t f = (top != 0 || zb == 0) ? 1u : 0u;
+        // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or z >= N,
+        // decided by the top two limbs unless both equal N's (then by all of
+        // them, read back). The bucket keeps Z and a flag (the subtraction is
+        // deferred to its next reader); the forwarded X is reduced right here.
+        uint32_t f;
+        if (top) {
+          f = 1u;
+        } else if (pend[3] != ntop || pend[2] != n126) {
+          f = (pend[3] > ntop || (pend[3] == ntop && pend[2] > n126)) ? 1u : 0u;
+        } else {
+          f = 1u;                                // z == N so far: equal counts as >=
+          const uint32_t* zs = conflict ? nullptr : brow;
+          for (int li = kL - 3; li >= 0; --li) {
+            uint32_t zl;
+            if (zs) {
+              zl = zs[li];
+            } else {
+              const int cc = li >> 2, kb = cc >> 3, ch = cc & 7;
+              zl = reinterpret_cast<const uint32_t*>(
+                  XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4))[li & 3];
+            }
+            if (zl != sN[li]) {
+              f = zl > sN[li] ? 1u : 0u;
+              break;
+            }
+          }
+        }
         if (dg) Fc[bidx] = (uint8_t)f;
         if (conflict && f) {
           uint32_t bw = 0;
