@@ -761,8 +761,12 @@ umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
       }
       uint32_t* zr = args.out + (int64_t)n * args.zq + row * args.wz;
 #pragma unroll
-      for (int i = 0; i < kZ; i += 4)
-        *reinterpret_cast<uint4*>(zr + i) = make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]);
+      for (int i = 0; i < kZ; i += 4) {
+        if (args.a_keep)   // batches: stream z past L2 so the H tiles stay resident
+          __stcs(reinterpret_cast<uint4*>(zr + i), make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]));
+        else
+          *reinterpret_cast<uint4*>(zr + i) = make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]);
+      }
     }
   }
   tc_fence_before();
@@ -964,7 +968,7 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
         uint32_t* zr = args.out + (int64_t)n * args.zq + row * args.wz;
 #pragma unroll
         for (int i = 0; i < kZ; i += 4)
-          *reinterpret_cast<uint4*>(zr + i) = make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]);
+          __stcs(reinterpret_cast<uint4*>(zr + i), make_uint4(z[i], z[i + 1], z[i + 2], z[i + 3]));
       }
     }
   }
