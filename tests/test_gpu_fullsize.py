@@ -8,7 +8,8 @@ checked through size-independent properties and sampled oracle values
   in both modes decodes to the requested DB row, all 32768 entries;
 * b = DB qu mod 2^32 equals the C oracle GEMV, and is linear in qu;
 * H = -DB A mod 2^32 equals the C oracle on sampled DB rows;
-* t on sampled groups equals the reference formula (oracle/ref.answer_t).
+* t on sampled groups equals the reference formula (oracle/ref.answer_t);
+* BASELINE configs[2] (8 GiB, 92682^2) on one GPU: b and sampled t groups.
 """
 
 import random
@@ -85,3 +86,41 @@ def test_fullsize_retrieval_and_sampled_groups(full):
     rc = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
     got = client.extract(sk, Q, 256, cap, Q, D, combined=[c.c for c in rc.k])
     assert got == [int(x) for x in db[i0]]
+
+
+def test_fullsize_8gib_gemv_and_sampled_groups():
+    """BASELINE configs[2] on one GPU: 92682 x 92682 (8 GiB, d0 > 2^16 so the
+    byte-plane sums wrap s32 many times): b equals the C oracle GEMV, t on
+    sampled groups (incl. the partial last group) equals the reference formula."""
+    import os
+    import torch
+    import paper_2603_09190_b200 as z
+    d = 92682
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    except (ValueError, OSError):
+        mem = 0
+    if mem and mem < 48 * 2**30:
+        pytest.skip("needs ~48 GB of host memory")
+    db = np.frombuffer(np.random.default_rng(92682).bytes(d * d), dtype=np.uint8).reshape(d, d)
+    params = z.ProtocolParams(z.LweParams(N, Q, 256, 6.4), d, d, 2048)
+    st = z.ServerGlobalState(params, db)
+    qu = np.random.default_rng(2).integers(0, Q, d, dtype=np.uint64)
+    b = st.db_matvec(qu)
+    assert np.array_equal(b, oracle_c.db_matvec(db, qu))
+    sk = client.keygen(2048, random.Random(8))
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, b"\x08" * 16, z.client_id_of(pk))
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(1)] * params.d1_prime)
+    r = random.Random(9)
+    ck_o = [r.randrange(sk.m) for _ in range(N)]
+    t = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck_o, qu)).t
+    cap = params.capacity
+    A = ref.public_matrix(b"\x00" * 16, d, N, Q)
+    for g in (0, 777, params.d1_prime - 1):
+        lo, hi = g * cap, min((g + 1) * cap, d)
+        Hg = oracle_c.hint_cols(db, A, list(range(lo, hi)))
+        want = ref.answer_t(Hg, b[lo:hi], ck_o, sk.m, cap, Q, hi - lo)
+        assert t[g] == want[0], g
+    del st
+    torch.cuda.empty_cache()
