@@ -124,3 +124,20 @@ def test_fullsize_8gib_gemv_and_sampled_groups():
         assert t[g] == want[0], g
     del st
     torch.cuda.empty_cache()
+
+
+def test_fullsize_batch_equals_single(full):
+    """BASELINE configs[3] shape (queries batched on the N = 256 GEMV and the
+    CTA-pair planar compression) at 1 GiB: every query's t equals respond()."""
+    z, params, db, st = full
+    sk = client.keygen(2048, random.Random(64))
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, b"\x40" * 16, z.client_id_of(pk))
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(1)] * params.d1_prime)
+    rng = np.random.default_rng(64)
+    r = random.Random(65)
+    qms = [z.QueryMessage(reg.client_id, 0, z.SEPARATE, [r.randrange(sk.m) for _ in range(N)],
+                          rng.integers(0, Q, D, dtype=np.uint64)) for _ in range(6)]
+    outs = z.respond_batch(st, [reg] * len(qms), qms)
+    for q, o in zip(qms, outs):
+        assert o.t == z.respond(st, reg, q).t
