@@ -215,15 +215,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
       : "r"(taddr));
 }
 
-// 64 TMEM columns of this thread's lane -> v[64], ordered after the wait.
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t (&v)[64]) {
-  tmem_ld32(taddr, v);
-  tmem_ld32(taddr + 32, v + 32);
-  tmem_wait_ld();
-#pragma unroll
-  for (int i = 0; i < 64; ++i) asm volatile("" : "+r"(v[i]));
-}
-
 // Wait for this thread's outstanding TMEM loads, ordered after `dep` (the
 // last value computed from the previous batch) so the compiler keeps that
 // work ahead of the wait.
@@ -539,7 +530,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         gather_issue(dg_n, conflict);
       }
       // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
-      uint32_t pend[4];                       // Z limbs awaiting a 16-byte store
+      uint32_t pend[4] = {0u, 0u, 0u, 0u};      // Z limbs awaiting a 16-byte store
       auto emit = [&](int li) {               // limbs li-3..li complete
         if (dg)
           *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
