@@ -64,7 +64,7 @@ def build(verbose=False, force=False):
         obj = os.path.join(HERE, "build", src.replace(".cu", ".o"))
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-I", os.path.join(HERE, "..", "include"), "-c", os.path.join(CSRC, src),
-               "-o", obj]
+               "-o", obj, *os.environ.get("ZPIR_NVCC_EXTRA", "").split()]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
