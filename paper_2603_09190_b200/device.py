@@ -6,6 +6,7 @@ device memory, streams and events only.
 """
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -220,16 +221,37 @@ def umma_answer_rows_batch(H, bc, lm, stream=None):
     return z
 
 
+_KEY_TABLES = {}
+_KEY_TABLES_LOCK = threading.Lock()
+
+
+def _key_tables(kctxs, nchunks, dev):
+    """Per-query modulus tables of a batch (stacked moduli, R^k tables, -m^-1
+    mod 2^32, R < 2m flags) on the device, cached per key sequence: building
+    them from host lists would synchronise the stream on every batch."""
+    key = (tuple(id(k) for k in kctxs), nchunks, str(dev))
+    with _KEY_TABLES_LOCK:
+        ent = _KEY_TABLES.get(key)
+        if ent is None:
+            if len(_KEY_TABLES) > 256:
+                _KEY_TABLES.clear()
+            mods = torch.stack([k.d_m for k in kctxs])
+            rpows = torch.stack([k.d_rpow(nchunks) for k in kctxs])
+            nps = torch.tensor(np.array([k.cm.np for k in kctxs], dtype=np.uint32).view(np.int32),
+                               device=dev)
+            f0 = torch.tensor([1 if k.cm.R < 2 * k.m else 0 for k in kctxs], dtype=torch.uint8,
+                              device=dev)
+            ent = _KEY_TABLES[key] = (mods, rpows, nps, f0, list(kctxs))
+        return ent[:4]
+
+
 def answer_groups_batch(z, b, qmask, d1, cap, groups, kctxs, t_ld, stream=None, stride=1):
     """z (nq, rows, lm+4), b (nq, rows); per-query Montgomery contexts."""
     nq, rows, wz = z.shape
     lm = kctxs[0].lm
     nchunks = max(2, -(-(stride * cap + lm + 4) // lm))
     dev = z.device
-    mods = torch.stack([k.d_m for k in kctxs])
-    rpows = torch.stack([k.d_rpow(nchunks) for k in kctxs])
-    nps = torch.tensor(np.array([k.cm.np for k in kctxs], dtype=np.uint32).view(np.int32), device=dev)
-    f0 = torch.tensor([1 if k.cm.R < 2 * k.m else 0 for k in kctxs], dtype=torch.uint8, device=dev)
+    mods, rpows, nps, f0 = _key_tables(kctxs, nchunks, dev)
     t = torch.empty((nq, groups, t_ld), dtype=torch.int32, device=dev)
     _lib.call("zpir_answer_groups_batch", _lib.ptr(z), rows * wz, _lib.ptr(b), b.shape[1], qmask, d1,
               cap, groups, lm, _lib.ptr(mods), _lib.ptr(nps), _lib.ptr(rpows), nchunks, _lib.ptr(f0),

@@ -388,21 +388,28 @@ class ServerGlobalState:
     def answer_batch_device(self, qu_dev, cko_dev, kctxs, t_ld, stream, events=None):
         """t (nq x groups x t_ld) for nq <= 64 staged queries (tcgen05 path):
         one N = 4*nq GEMV over the DB, one compression launch, one group launch."""
-        lay = self.layout
-        nq = qu_dev.shape[0]
-        lm = kctxs[0].lm
         if events:
             events[0].record(stream)
-        planes = device.query_planes(qu_dev, 16 if nq <= 4 else 256, stream)
-        b = device.umma_gemv(self.dbt, planes, nq, stream=stream)
+        b = self.gemv_batch_device(qu_dev, stream)
         if events:
             events[1].record(stream)
-        z = self.compress_rows(cko_dev, lm, stream)
-        t = device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctxs, t_ld,
-                                       stream, stride=lay.stride)
+        t = self.compress_groups_batch(cko_dev, b, kctxs, t_ld, stream)
         if events:
             events[2].record(stream)
         return t
+
+    def gemv_batch_device(self, qu_dev, stream):
+        """b (nq x rows) = DB qu_v mod q for nq <= 64 staged queries: one pass over the DB."""
+        nq = qu_dev.shape[0]
+        planes = device.query_planes(qu_dev, 16 if nq <= 4 else 256, stream)
+        return device.umma_gemv(self.dbt, planes, nq, stream=stream)
+
+    def compress_groups_batch(self, cko_dev, b, kctxs, t_ld, stream):
+        """t (nq x groups x t_ld) from the queries' ck_o limbs and their GEMV rows b."""
+        lay = self.layout
+        z = self.compress_rows(cko_dev, kctxs[0].lm, stream)
+        return device.answer_groups_batch(z, b, lay.qmask, lay.d1, lay.cap, lay.groups, kctxs,
+                                          t_ld, stream, stride=lay.stride)
 
     def _group_stage(self, z, b, kctx, t_ld, stream):
         """t_g = sum_j gamma^j (b_c + z_c) mod m: positional fold for gamma =
@@ -869,6 +876,8 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
 
 
 MAX_BATCH = 64
+# respond_batch: queries per compression / copy-out sub-batch (host work overlaps the device)
+BATCH_SUB = int(os.environ.get("ZPIR_BATCH_SUB", "16"))
 
 
 def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
@@ -922,8 +931,14 @@ def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
 def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
     """One respond_batch chunk: queries staged straight into pinned buffers
     (qu0 narrowed, ck_o as raw CPython digits regrouped on the device), one
-    batched answer, all results regrouped to digits on the device and copied
-    out with one synchronisation."""
+    batched answer, results regrouped to digits on the device and copied out.
+
+    With the C extension the host work is pipelined against the device: the
+    GEMV (all queries, one pass over the DB) starts as soon as every qu0 is
+    staged; the compression, group stage and copy-out then run in sub-batches
+    of BATCH_SUB queries, so the host stages the next sub-batch's ck_o digits
+    and turns the previous sub-batch's result digits into Python ints while
+    the device works."""
     lay = state.layout
     dev = state.device
     nq, n = len(qs), lay.n
@@ -940,55 +955,13 @@ def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
     qd = torch.empty((nq, lay.ld), dtype=torch.int32, device=dev)
     device.h2d_async(qd, torch.from_numpy(qbuf.view(np.int32)), stream)
     _staging.mark("qb", stream)
-    cd = torch.empty((nq, n, lm), dtype=torch.int32, device=dev)
-    if conv is not None:
-        ndig = -(-32 * lm // 30)
-        cbuf = _staging.get("cbd", nq * n * ndig * 4).numpy().view(np.int32).reshape(nq * n, ndig)
-        for i, q in enumerate(qs):
-            conv.digits_into(q.ck_o, cbuf[i * n:(i + 1) * n], ndig)
-        dd = torch.empty((nq * n, ndig), dtype=torch.int32, device=dev)
-        device.h2d_async(dd, torch.from_numpy(cbuf), stream)
-        _staging.mark("cbd", stream)
-        device.digits_to_limbs(dd, lm, cd.view(nq * n, lm), stream)
-    else:
+    if conv is None:
         cko = np.empty((nq, n, lm), dtype=np.uint32)
         for i, q in enumerate(qs):
             ints_to_limbs(q.ck_o, lm, out=cko[i])
-        cd.copy_(_h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, n, lm))
-    t = state.answer_batch_device(qd, cd, ks, ks[0].l2, stream)      # (nq, groups, l2)
-    G = lay.groups
-    res = []
-    if conv is not None:
-        nd1, nd2 = -(-32 * lm // 30), -(-32 * ks[0].l2 // 30)
-        td = torch.empty((nq * G, nd1), dtype=torch.int32, device=dev)
-        device.limbs_to_digits(t.view(nq * G, -1), lm, td, stream)
-        outs = [("t", td, nd1)]
-        kd = {}
-        for i in range(nq):
-            if modes[i] == COMBINED:
-                K = device.combine(t[i], _stored_device(storeds[i], ks[i], dev, stream), ks[i],
-                                   stream=stream)
-                kd[i] = torch.empty((G, nd2), dtype=torch.int32, device=dev)
-                device.limbs_to_digits(K, ks[i].l2, kd[i], stream)
-        hbuf = _staging.get("tb", (nq * G * nd1 + len(kd) * G * nd2) * 4)
-        hv = hbuf.numpy().view(np.int32)
-        device.d2h_async(hbuf[: nq * G * nd1 * 4], td, stream)
-        off = nq * G * nd1
-        koff = {}
-        for i, kt in kd.items():
-            device.d2h_async(hbuf[off * 4:(off + G * nd2) * 4], kt, stream)
-            koff[i] = off
-            off += G * nd2
-        _staging.mark("tb", stream)
-        stream.synchronize()
-        for i in range(nq):
-            if modes[i] == SEPARATE:
-                seg = hv[i * G * nd1:(i + 1) * G * nd1]
-                res.append(conv.ints_from_digits(seg, G, nd1))
-            else:
-                seg = hv[koff[i]:koff[i] + G * nd2]
-                res.append(conv.ints_from_digits(seg, G, nd2))
-    else:
+        cd = _h2d(cko, dev, "cb", stream).view(torch.int32).reshape(nq, n, lm)
+        t = state.answer_batch_device(qd, cd, ks, ks[0].l2, stream)      # (nq, groups, l2)
+        res = []
         for i in range(nq):
             if modes[i] == SEPARATE:
                 r = t[i, :, :lm]
@@ -996,6 +969,66 @@ def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
                 r = device.combine(t[i], _stored_device(storeds[i], ks[i], dev, stream), ks[i],
                                    stream=stream)
             res.append(limbs_to_ints(_d2h_u32(r.contiguous(), "tb", stream)))
+        return _batch_messages(state, qs, modes, storeds, res)
+
+    G = lay.groups
+    l2 = ks[0].l2
+    nd1, nd2 = -(-32 * lm // 30), -(-32 * l2 // 30)
+    b = state.gemv_batch_device(qd, stream)                          # (nq, rows)
+    cbuf = _staging.get("cbd", nq * n * nd1 * 4).numpy().view(np.int32).reshape(nq * n, nd1)
+    ncomb = sum(1 for md in modes if md == COMBINED)
+    hbuf = _staging.get("tb", (nq * G * nd1 + ncomb * G * nd2) * 4)
+    hv = hbuf.numpy().view(np.int32)
+    res = [None] * nq
+    pending = []
+    koff, off = {}, nq * G * nd1
+
+    def drain(item):
+        ev, lo, hi = item
+        ev.synchronize()
+        for i in range(lo, hi):
+            if modes[i] == SEPARATE:
+                res[i] = conv.ints_from_digits(hv[i * G * nd1:(i + 1) * G * nd1], G, nd1)
+            else:
+                res[i] = conv.ints_from_digits(hv[koff[i]:koff[i] + G * nd2], G, nd2)
+
+    sub = max(1, BATCH_SUB)
+    for lo in range(0, nq, sub):
+        hi = min(nq, lo + sub)
+        m = hi - lo
+        for i in range(lo, hi):
+            conv.digits_into(qs[i].ck_o, cbuf[i * n:(i + 1) * n], nd1)
+        dd = torch.empty((m * n, nd1), dtype=torch.int32, device=dev)
+        device.h2d_async(dd, torch.from_numpy(cbuf[lo * n:hi * n]), stream)
+        cd = torch.empty((m, n, lm), dtype=torch.int32, device=dev)
+        device.digits_to_limbs(dd, lm, cd.view(m * n, lm), stream)
+        t = state.compress_groups_batch(cd, b[lo:hi], ks[lo:hi], l2, stream)   # (m, G, l2)
+        td = torch.empty((m * G, nd1), dtype=torch.int32, device=dev)
+        device.limbs_to_digits(t.view(m * G, -1), lm, td, stream)
+        device.d2h_async(hbuf[lo * G * nd1 * 4:hi * G * nd1 * 4], td, stream)
+        for i in range(lo, hi):
+            if modes[i] == COMBINED:
+                K = device.combine(t[i - lo], _stored_device(storeds[i], ks[i], dev, stream),
+                                   ks[i], stream=stream)
+                kd = torch.empty((G, nd2), dtype=torch.int32, device=dev)
+                device.limbs_to_digits(K, ks[i].l2, kd, stream)
+                device.d2h_async(hbuf[off * 4:(off + G * nd2) * 4], kd, stream)
+                koff[i] = off
+                off += G * nd2
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        if pending:
+            drain(pending.pop())
+        pending.append((ev, lo, hi))
+    _staging.mark("cbd", stream)
+    _staging.mark("tb", stream)
+    while pending:
+        drain(pending.pop())
+    return _batch_messages(state, qs, modes, storeds, res)
+
+
+def _batch_messages(state, qs, modes, storeds, res):
+    lay = state.layout
     out = []
     for i, vals in enumerate(res):
         qi = qs[i].query_index
