@@ -507,12 +507,14 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     Computed through the slot decomposition: H_scaled[g][k] = sum_j gamma^j
     H[g*cap+j][k], so k_g = prod_j W[g*cap+j]^(gamma^j) with
     W[c] = prod_k ck_r[k]^H[c][k].
-    Each W[c] (32-bit exponents) is one fixed-base Pippenger over the table
-    P[i][k] = ck_r[k]^(2^(8i)) (255 buckets, 4n digits) -- for 4096-bit m^2
-    with the bucket updates on the tensor cores (tc_pippenger.cu); the groups
-    are then recombined by Horner in gamma (slot_combine). Same group element
-    as the reference's windowed multiexp, canonical mod m^2. keep_slots=True
-    keeps W and P on the device for refresh_hint."""
+    Each W[c] (32-bit exponents) is one fixed-base Pippenger over a table of
+    powers of ck_r[k]: on the IMAD path (slot_fixed) 8-bit digits, 255
+    buckets, P[i][k] = ck_r[k]^(2^(8i)); for 4096-bit m^2 and enough rows the
+    bucket updates run on the tensor cores instead (tc_pippenger.cu: D digits
+    per word, default 6 -> 63 buckets). The groups are then recombined by
+    Horner in gamma (slot_combine). Same group element as the reference's
+    windowed multiexp, canonical mod m^2. keep_slots=True keeps W and the
+    8-bit table P on the device for refresh_hint."""
     return hints(state, [(reg, query_index)], stream=stream, keep_slots=keep_slots)[0]
 
 
