@@ -1,11 +1,13 @@
 // Per-client hint on the tensor cores: the Pippenger bucket updates of
 // slot_fixed (multiexp.cu) as Montgomery multiplications by a FIXED multiplier.
 //
-// W[r] = prod_{pos < 4n} P[pos]^{digit(r, pos)}, digit(r, pos) = byte (pos / n)
-// of H[r][pos % n], P[pos] = ck_r[pos % n]^(2^(8 (pos / n))) (pow8_table, Montgomery
-// form mod N = m^2). Position-major Pippenger: at every position each row
-// multiplies ONE of its 255 buckets by the same Y = P[pos], so a position is a
-// batch "X (rows) times fixed Y mod N" -- Toeplitz int8 GEMMs:
+// W[r] = prod_{pos < D n} P[pos]^{digit(r, pos)}: every 32-bit exponent word
+// H[r][k] is cut into D digits (DigitSpec, default D = 6: widths 6,6,5,5,5,5),
+// pos = i n + k, digit(r, pos) = digit i of H[r][k] and P[pos] = ck_r[k]^(2^off_i)
+// (powtab_kernel, Montgomery form mod N = m^2). Position-major Pippenger: at
+// every position each row multiplies ONE of its 2^w - 1 buckets by the same
+// Y = P[pos], so a position is a batch "X (rows) times fixed Y mod N" --
+// Toeplitz int8 GEMMs:
 //   u = X * Y' mod R          (Y' = Y * N' mod R, N' = -N^-1 mod R, R = 2^4096)
 //   Z = (X * Y + u * N) / R   (< 2N; the conditional subtraction is deferred)
 // with a byte-Toeplitz B operand Toep(y)[j][a] = byte_{delta + j - a}(y).
@@ -20,7 +22,10 @@
 //   H1:     columns 764..1019                           -> Z limbs 63..126
 // and the three top columns 1020..1022 (12 byte products) on the CUDA cores.
 // 20 k-blocks (80 N = 256 MMAs) per position; the tasks ping-pong two TMEM
-// buffers so the epilogue drains one while the MMA warp fills the other.
+// buffers so the epilogue drains one while the MMA warp fills the other. The
+// X * Y parts of H0 and H1 are issued before the u * N parts, so the next
+// position's bucket gather (cp.async) overlaps the H drains; a row whose digit
+// repeats gets its next X forwarded from Z by its own thread.
 //
 // Several clients (independent keys) run in one launch: blockIdx.y = client,
 // every client with its own Toeplitz tiles, buckets and output rows; rows may be
