@@ -234,7 +234,10 @@ int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t 
  * tensor cores (position-major: each position multiplies one bucket per row by
  * the same P[pos]; Montgomery by a fixed multiplier = three byte-Toeplitz int8
  * GEMMs); 4096-bit N only (limbs = 128). Nprime = -N^-1 mod 2^4096 (128 limbs).
- * Transient workspace ~ rows * 130 KB + 4n * 320 KB. */
+ * P is the pow8 table of zpir_pow8_table (only its first n entries, the
+ * Montgomery bases, are read). Transient workspace:
+ * zpir_slot_fixed_tc_workspace(n, rows, 1) bytes (~32 KB per row + ~1.8 GB per
+ * client at n = 1024). */
 int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
                        const uint32_t* Nprime, uint32_t* W, void* stream);
