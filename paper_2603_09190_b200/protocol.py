@@ -23,6 +23,7 @@ raises.
 
 from dataclasses import dataclass, field
 import hashlib
+import logging
 import os
 import threading
 import time
@@ -31,12 +32,14 @@ import warnings
 import numpy as np
 import torch
 
-from . import counters, device
+from . import _lib, counters, device
 from .bigint import ints_to_limbs, key_ctx, limbs_to_ints
 from .paillier import PaillierCiphertext, PaillierPublicKey, sample_ciphertext  # noqa: F401
 from .params import Layout, LweParams, ProtocolParams  # noqa: F401
 from .plan import AnswerPlan
 from .prg import DOM_CIPHERTEXT_SAMPLE, DOM_PUBLIC_MATRIX
+
+log = logging.getLogger(__name__)
 
 SEPARATE = "separate"
 COMBINED = "combined"
@@ -541,9 +544,14 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
     tc = [j for j in prep if _tc_eligible(state, j[1])]
     if nslot * len(tc) < TC_MIN_ROWS:
         tc = []
+    tc_ids = set()
     for batch in (_tc_batches(state, tc, nslot) if tc else []):
-        device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, nslot, stream=stream)
-    tc_ids = {id(j[2]) for j in tc}
+        try:
+            device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, nslot, stream=stream)
+        except _lib.ZpirError as e:      # e.g. no room for the workspace: IMAD kernels below
+            log.warning("tensor-core hint batch of %d fell back to IMAD: %s", len(batch), e)
+            continue
+        tc_ids.update(id(j[2]) for j in batch)
     # the per-client group recombination (slot_combine: one warp per group, a
     # 32 * cap-deep Horner chain) is latency bound for one client; several
     # clients' run side by side on a small stream pool
@@ -633,7 +641,13 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
             outs.append((W, old.dev.clone()))
             jobs.append((old.bases, kctx, W))
         for batch in _tc_batches(state, jobs, rows):
-            device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, rows, rid=rid, stream=main)
+            try:
+                device.slot_fixed_tc_many(batch, lay.n, state.H_dev, lay.n, rows, rid=rid,
+                                          stream=main)
+            except _lib.ZpirError as e:  # e.g. no room for the workspace: IMAD kernels
+                log.warning("tensor-core refresh of %d fell back to IMAD: %s", len(batch), e)
+                for P, kctx, W in batch:
+                    device.slot_fixed(P, lay.n, state.H_dev, lay.n, rid, rows, kctx, W, main)
         for (W, k), kctx in zip(outs, kctxs):
             device.slot_combine(W, lay.cap, gid, ng, kctx, k, lay.gamma, main)
     else:
