@@ -185,6 +185,11 @@ def _traffic():
 
 def cpu_baseline(m, repeats=7):
     from oracle import ref_port
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count())
+    except Exception:
+        pass
     rows = CPU_SAMPLE_ROWS
     db = db_slice(0, D1)[:, :rows].copy()
     from paper_2603_09190_b200.prg import Stream, DOM_PUBLIC_MATRIX
@@ -213,6 +218,12 @@ def run_reference(args):
     rank, world, _ = _dist_env()
     if rank != 0:
         return
+    # all host threads for the CPU reference arm (torchrun sets OMP_NUM_THREADS=1)
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(os.cpu_count())
+    except Exception:
+        pass
     m = paillier_modulus(BITS, 2048)
     from oracle import ref_port
     rows = CPU_SAMPLE_ROWS
