@@ -158,3 +158,26 @@ def test_batched_hints_and_tensor_core_refresh(golden, monkeypatch):
     full = z.ServerGlobalState(params, db2, db_version=1)
     for reg, h, qi in zip(regs, out, (0, 3)):
         assert [c.c for c in h.entries] == [c.c for c in z.hint(full, reg, qi).entries]
+
+
+def test_tensor_core_hint_failure_falls_back_to_imad(golden, monkeypatch):
+    """A tensor-core launch that cannot run (e.g. its workspace does not fit)
+    falls back to the IMAD kernels for that batch: same entries."""
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import _lib, device, protocol
+    g = golden("tiny")
+    st = z.ServerGlobalState(g.params(z), g.db)
+    regs = []
+    for i in range(2):
+        sk, seed = client.setup(2048, random.Random(70 + i))
+        pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+        regs.append(z.ClientRegistration(pk, seed, z.client_id_of(pk)))
+    want = [[c.c for c in z.hint(st, r, 0).entries] for r in regs]     # IMAD (< 2048 rows)
+
+    def boom(*a, **k):
+        raise _lib.ZpirError("simulated workspace failure")
+
+    monkeypatch.setattr(device, "slot_fixed_tc_many", boom)
+    monkeypatch.setattr(protocol, "TC_MIN_ROWS", 1)                       # would take the TC path
+    got = [[c.c for c in h.entries] for h in z.hints(st, [(r, 0) for r in regs])]
+    assert got == want
