@@ -114,3 +114,35 @@ def test_hint_is_deterministic_per_index(z):
     assert [c.c for c in h1.entries] != [c.c for c in h3.entries]
     assert [client.decrypt(sk, c.c) for c in h1.entries] == \
         [client.decrypt(sk, c.c) for c in h2.entries]
+
+
+@pytest.mark.parametrize("bits", [1024, 4096])
+def test_end_to_end_other_key_sizes(z, bits):
+    """Paillier moduli other than the headline's 2048 bits through the whole
+    protocol on the device: 1024-bit m (m^2 = 2048 bits, 2 limbs per lane) and
+    4096-bit m (m^2 = 8192 bits, 8 limbs per lane; compression on the CUDA-core
+    rows kernel): hint, respond in both modes and the client's extraction
+    return the requested DB row; t equals the oracle formula."""
+    import random
+    from oracle import client, ref
+    rng = random.Random(bits)
+    d0, d1, n = 256, 200, 128
+    params = z.ProtocolParams(z.LweParams(n=n, q=1 << 32, p=256, noise_sigma=6.4), d0, d1, bits)
+    db = np.array([[rng.randrange(256) for _ in range(d1)] for _ in range(d0)], dtype=np.uint8)
+    st = z.ServerGlobalState(params, db)
+    sk, seed = client.setup(bits, rng)
+    pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+    reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
+    reg.hints[0] = z.hint(st, reg, 0)
+    A = ref.public_matrix(b"\x00" * 16, d0, n, 1 << 32)
+    i0 = 101
+    qu0, ck_o, _ = client.query(sk, seed, n, 1 << 32, 256, 6.4, d0, i0, 0, rng, A)
+    cap = params.capacity
+    r = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck_o, qu0))
+    H = ref.global_hint(db, A, 1 << 32)
+    assert r.t == ref.answer_t(H, ref.db_matvec(db, qu0, 1 << 32), ck_o, sk.m, cap, 1 << 32, d1)
+    got = client.extract(sk, 1 << 32, 256, cap, 1 << 32, d1, t=r.t, k=[c.c for c in r.k])
+    assert got == [int(x) for x in db[i0]]
+    rc = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
+    got = client.extract(sk, 1 << 32, 256, cap, 1 << 32, d1, combined=[c.c for c in rc.k])
+    assert got == [int(x) for x in db[i0]]
