@@ -23,6 +23,11 @@ import threading
 import numpy as np
 import torch
 
+# respond()'s host-input graphs read qu from and write t's digits to pinned,
+# device-mapped host buffers directly (no copy nodes); ZPIR_E2E_ZEROCOPY=0 copies
+ZERO_COPY = os.environ.get("ZPIR_E2E_ZEROCOPY", "1") != "0"
+ZERO_COPY_CK = os.environ.get("ZPIR_E2E_ZEROCOPY_CK", "1") != "0"
+
 from . import device
 
 USE_GRAPHS = os.environ.get("ZPIR_GRAPHS", "1") != "0"
@@ -189,9 +194,15 @@ class AnswerPlan:
             self._seq("finish_digits", stream)
             device.d2h_async(self.h_td, self.d_td, stream)
         elif which == "e2e_g1":
-            # respond(), graph 1 (main stream): qu in, query planes, GEMV
-            device.h2d_async(self.qu, self.h_qu, stream)
-            self._gemv(stream, self.sms - self.ctas_e2e)
+            # respond(), graph 1 (main stream): query planes read straight from
+            # the pinned (device-mapped) host qu -- no copy node -- then the GEMV
+            if ZERO_COPY:
+                device.query_planes(self.h_qu.view(1, -1), 16, stream, planes=self.planes)
+                device.umma_gemv(self.state.dbt, self.planes, 1, out=self.b, stream=stream,
+                                 ctas=self.sms - self.ctas_e2e)
+            else:
+                device.h2d_async(self.qu, self.h_qu, stream)
+                self._gemv(stream, self.sms - self.ctas_e2e)
         elif which in ("e2e_g2", "e2e_g2t", "w_g2t"):
             # respond() / respond_wire(), graph 2 (side stream): ck_o in (CPython
             # digits, or limb rows for the wire path), compression, Montgomery
@@ -199,6 +210,8 @@ class AnswerPlan:
             # converts t to digits and copies it out, the others leave t in HBM
             if which == "w_g2t":
                 device.h2d_async(self.cko, self.h_cko, stream)
+            elif ZERO_COPY and ZERO_COPY_CK:     # digits read from pinned host memory
+                device.digits_to_limbs(self.h_ckd, self.kctx.lm, self.cko, stream)
             else:
                 device.h2d_async(self.d_ckd, self.h_ckd, stream)
                 device.digits_to_limbs(self.d_ckd, self.kctx.lm, self.cko, stream)
@@ -206,8 +219,14 @@ class AnswerPlan:
             self._groups_z(stream)
             device.stream_wait_event(stream, self.ev_gemv)
             if which == "e2e_g2":
-                self._seq("finish_digits", stream)
-                device.d2h_async(self.h_td, self.d_td, stream)
+                # t's digits written by the kernel straight into the pinned
+                # (device-mapped) host buffer: no copy node at the tail
+                self._finish(stream)
+                if ZERO_COPY:
+                    device.limbs_to_digits(self.t, self.kctx.lm, self.h_td, stream)
+                else:
+                    device.limbs_to_digits(self.t, self.kctx.lm, self.d_td, stream)
+                    device.d2h_async(self.h_td, self.d_td, stream)
             else:
                 self._finish(stream)
         elif which == "side_limbs":
