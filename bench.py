@@ -437,12 +437,31 @@ def run_b200(args):
             t1 = time.perf_counter()
             dd.answer(qu, ck_o, m)
             th_.append(time.perf_counter() - t1)
+        # the bare C call a C / cgo / JNI caller makes: limb arrays already in
+        # (pageable) host memory, t's limbs written back to host memory
+        from paper_2603_09190_b200 import _lib
+        from paper_2603_09190_b200.dbapi import _vp
+        q_l, c_l, m_l, L_l = dd._query(qu, ck_o, m)
+        t_l = np.empty((dd.groups, L_l), dtype=np.uint32)
+        tc_ = []
+        for i in range(3 + args.e2e_steps):
+            t1 = time.perf_counter()
+            _lib.call("zpir_db_answer", dd._h, _vp(q_l), _vp(c_l), _vp(m_l), L_l, _vp(t_l))
+            if i >= 3:
+                tc_.append(time.perf_counter() - t1)
+        from paper_2603_09190_b200.bigint import limbs_to_ints
+        assert limbs_to_ints(t_l) == t_h
         dd.close()
         h_s = statistics.mean(th_)
+        c_s = statistics.mean(tc_)
         extra_e2e["e2e_c_abi"] = {"value": D0 * d1_total / h_s / 1e9, "unit": "GB/s",
                                   "ms_per_step": h_s * 1e3,
                                   "api": "zpir_db_answer (include/zippir_db.h): pageable host "
-                                         "buffers, Python ints converted by dbapi.py"}
+                                         "buffers, Python ints converted by dbapi.py",
+                                  "call_only": {"value": D0 * d1_total / c_s / 1e9,
+                                                "ms_per_step": c_s * 1e3,
+                                                "api": "the bare zpir_db_answer call on host "
+                                                       "limb arrays (no Python int conversion)"}}
 
     db_bytes_total = D0 * d1_total
     db_bytes_rank = D0 * (hi - lo)

@@ -266,8 +266,35 @@ struct Key {
 };
 
 // Per key-width workspace of the online answer.
+// Pinned host staging: the handle's per-query copies run asynchronously from
+// here instead of through the driver's pageable bounce path (which blocks the
+// host until each source is staged and so delays the next launch).
+struct HostBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  HostBuf() = default;
+  HostBuf(const HostBuf&) = delete;
+  HostBuf& operator=(const HostBuf&) = delete;
+  ~HostBuf() { if (p) cudaFreeHost(p); }
+  int alloc(size_t n) {
+    if (p && bytes >= n) return kOk;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    if (cudaHostAlloc(&p, n ? n : 16, cudaHostAllocDefault) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("pinned host allocation of %zu bytes failed", n);
+      return kErrCuda;
+    }
+    bytes = n;
+    return kOk;
+  }
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
 struct Work {
   DevBuf qu, planes, b, cko, bc, z, t, k, K, w, gemv_ws;
+  HostBuf h_qu, h_cko, h_out;  // staging of one query's qu / ck_o and its result rows
 };
 
 }  // namespace
@@ -418,6 +445,9 @@ int get_work(zpir_db* h, int lm, Work** out) {
   ZPIR_TRY(w->K.alloc((size_t)h->groups * l2 * 4));
   ZPIR_TRY(w->gemv_ws.alloc((size_t)zpir_gemv_workspace_bytes(h->ld, 1)));
   if (h->stride == 0) ZPIR_TRY(w->w.alloc((size_t)h->prm.d1 * lm * 4));
+  ZPIR_TRY(w->h_qu.alloc((size_t)h->prm.d0 * 4));
+  ZPIR_TRY(w->h_cko.alloc((size_t)n * lm * 4));
+  ZPIR_TRY(w->h_out.alloc((size_t)h->groups * l2 * 4));
   *out = w.get();
   h->work.emplace(lm, std::move(w));
   return kOk;
@@ -469,9 +499,61 @@ int h2d_rows(void* dst, int dst_ld, const uint32_t* src, int src_limbs, int64_t 
             "H2D");
 }
 
-// qu (d0 u32, host) -> b on the device (w->b), GEMV on `ctas` SMs (0 = all).
+// a host row wider than dst_ld limbs must only carry zero limbs beyond it
+int rows_fit(const uint32_t* src, int src_limbs, int dst_ld, int64_t rows) {
+  for (int64_t r = 0; r < rows; ++r)
+    for (int i = dst_ld; i < src_limbs; ++i)
+      if (src[r * src_limbs + i]) {
+        set_error("value wider than the modulus");
+        return kErrInput;
+      }
+  return kOk;
+}
+
+// host rows of src_limbs -> pinned stage (dst_ld limbs, zero-extended) -> device,
+// asynchronously on s (the stage is free again once s passes the copy; every
+// handle call ends with a synchronize). Widths are checked by rows_fit first.
+int h2d_rows_staged(void* dst, int dst_ld, const uint32_t* src, int src_limbs, int64_t rows,
+                    HostBuf& stage, cudaStream_t s) {
+  const int w = src_limbs < dst_ld ? src_limbs : dst_ld;
+  uint32_t* st = stage.as<uint32_t>();
+  if (w == dst_ld && src_limbs == dst_ld) {
+    std::memcpy(st, src, (size_t)rows * dst_ld * 4);
+  } else {
+    for (int64_t r = 0; r < rows; ++r) {
+      std::memcpy(st + r * dst_ld, src + r * src_limbs, (size_t)w * 4);
+      if (w < dst_ld) std::memset(st + r * dst_ld + w, 0, (size_t)(dst_ld - w) * 4);
+    }
+  }
+  return cu(cudaMemcpyAsync(dst, st, (size_t)rows * dst_ld * 4, cudaMemcpyHostToDevice, s),
+            "H2D");
+}
+
+// device rows (src_ld limbs) -> pinned stage -> host rows of dst_limbs (zero-extended)
+int d2h_rows_staged(void* dst, int dst_limbs, const void* src, int src_ld, int64_t rows,
+                    HostBuf& stage, cudaStream_t s) {
+  uint32_t* st = stage.as<uint32_t>();
+  ZPIR_TRY(cu(cudaMemcpyAsync(st, src, (size_t)rows * src_ld * 4, cudaMemcpyDeviceToHost, s),
+              "D2H"));
+  ZPIR_TRY(sync(s));
+  const int w = dst_limbs < src_ld ? dst_limbs : src_ld;
+  uint32_t* d = static_cast<uint32_t*>(dst);
+  if (w == src_ld && dst_limbs == src_ld) {
+    std::memcpy(d, st, (size_t)rows * src_ld * 4);
+    return kOk;
+  }
+  for (int64_t r = 0; r < rows; ++r) {
+    std::memcpy(d + r * dst_limbs, st + r * src_ld, (size_t)w * 4);
+    if (dst_limbs > w) std::memset(d + r * dst_limbs + w, 0, (size_t)(dst_limbs - w) * 4);
+  }
+  return kOk;
+}
+
+// qu (d0 u32, host) -> pinned stage -> b on the device (w->b), GEMV on `ctas` SMs (0 = all).
 int stage_query_and_gemv(zpir_db* h, Work* w, const uint32_t* qu, int ctas, cudaStream_t s) {
-  ZPIR_TRY(cu(cudaMemcpyAsync(w->qu.p, qu, (size_t)h->prm.d0 * 4, cudaMemcpyHostToDevice, s),
+  std::memcpy(w->h_qu.p, qu, (size_t)h->prm.d0 * 4);
+  ZPIR_TRY(cu(cudaMemcpyAsync(w->qu.p, w->h_qu.p, (size_t)h->prm.d0 * 4, cudaMemcpyHostToDevice,
+                              s),
               "query H2D"));
   if (use_umma_gemv(h)) {
     ZPIR_TRY(zpir_query_planes(w->qu.as<uint32_t>(), h->ld, 1, w->planes.as<uint8_t>(), 16, s));
@@ -487,12 +569,15 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
   const int lm = k->lm, L = k->L;
   const int64_t n = h->prm.n;
   cudaStream_t s = h->main;
-  ZPIR_TRY(h2d_rows(w->cko.p, lm, cko, L, n, s));
+  ZPIR_TRY(rows_fit(cko, L, lm, n));
   const int nb = umma_nb(lm);
   if (h->prm.engine == 0 && nb && n % 4 == 0) {  // TMA rows of 4n bytes: 16-byte pitch
-    // compression on kCompressCtas SMs (side stream) || GEMV on the rest
+    // qu first: the GEMV (on SMs - kCompressCtas) runs while ck_o is staged on
+    // the host; then the compression on kCompressCtas SMs (side stream)
     ZPIR_TRY(cu(cudaEventRecord(h->ev_in, s), "event"));
+    ZPIR_TRY(stage_query_and_gemv(h, w, qu, h->sms - kCompressCtas, s));
     ZPIR_TRY(cu(cudaStreamWaitEvent(h->side, h->ev_in, 0), "event wait"));
+    ZPIR_TRY(h2d_rows_staged(w->cko.p, lm, cko, L, n, w->h_cko, h->side));
     if (planar(h, lm)) {
       ZPIR_TRY(zpir_build_bcp(w->cko.as<uint32_t>(), n, lm, 1, w->bc.as<uint8_t>(), h->side));
       ZPIR_TRY(zpir_umma_answer_rows_planar(h->Hp.as<uint8_t>(), h->rows, n, w->bc.as<uint8_t>(),
@@ -505,9 +590,9 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
                                      kCompressCtas, h->side));
     }
     ZPIR_TRY(cu(cudaEventRecord(h->ev_comp, h->side), "event"));
-    ZPIR_TRY(stage_query_and_gemv(h, w, qu, h->sms - kCompressCtas, s));
     ZPIR_TRY(cu(cudaStreamWaitEvent(s, h->ev_comp, 0), "event wait"));
   } else {
+    ZPIR_TRY(h2d_rows_staged(w->cko.p, lm, cko, L, n, w->h_cko, s));
     ZPIR_TRY(stage_query_and_gemv(h, w, qu, 0, s));
     ZPIR_TRY(zpir_answer_rows(h->H.as<uint32_t>(), h->rows, n, nullptr, h->qmask,
                               w->cko.as<uint32_t>(), lm, w->z.as<uint32_t>(), s));
@@ -902,13 +987,13 @@ static int db_answer(zpir_db* h, const uint32_t* qu, const uint32_t* cko, const 
   ZPIR_TRY(get_work(h, k->lm, &w));
   const int t_ld = kin ? k->l2 : k->lm;
   ZPIR_TRY(answer(h, k, w, qu, cko, t_ld));
-  if (!kin) return d2h_rows(out, L, w->t.p, t_ld, h->groups, h->main);
+  if (!kin) return d2h_rows_staged(out, L, w->t.p, t_ld, h->groups, w->h_out, h->main);
   const int l2 = k->l2;
   ZPIR_TRY(h2d_rows(w->k.p, l2, kin, 2 * L, h->groups, h->main));
   ZPIR_TRY(zpir_combine(w->t.as<uint32_t>(), w->k.as<uint32_t>(), h->groups, l2,
                         k->m2.as<uint32_t>(), k->np_2, k->r2_2.as<uint32_t>(),
                         k->mr.as<uint32_t>(), w->K.as<uint32_t>(), h->main));
-  return d2h_rows(out, 2 * L, w->K.p, l2, h->groups, h->main);
+  return d2h_rows_staged(out, 2 * L, w->K.p, l2, h->groups, w->h_out, h->main);
 }
 
 int zpir_db_answer(zpir_db* h, const uint32_t* qu, const uint32_t* ck_o, const uint32_t* m, int L,

@@ -114,7 +114,11 @@ class DeviceDatabase:
         if q.shape != (lay.d0,) or len(ck_o) != lay.n:
             raise ValueError("query dimensions do not match the parameters")
         L = _limbs(int(m).bit_length())
-        return q, ints_to_limbs([int(c) for c in ck_o], L), ints_to_limbs([int(m)], L), L
+        try:   # Python ints (the reference's QueryMessage.ck_o) convert in C directly
+            c = ints_to_limbs(ck_o, L)
+        except TypeError:   # other integer types (numpy scalars, ...)
+            c = ints_to_limbs([int(v) for v in ck_o], L)
+        return q, c, ints_to_limbs([int(m)], L), L
 
     def answer(self, qu, ck_o, m) -> list:
         """SEPARATE answer t (d1' ints < m)."""

@@ -1,3 +1,7 @@
-# usage: bash tools/_gpu_one.sh <pytest args...>
-python -c "from paper_2603_09190_b200 import build; build.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 1200 python -m pytest -q -x "$@" 2>&1 | tail -40
+#!/bin/bash
+# One focused GPU check: build, the handle-ABI parity tests, one bench line.
+mkdir -p gpurun_out/one
+python -c "from paper_2603_09190_b200 import build; build.build()" > gpurun_out/one/build.log 2>&1 || { tail gpurun_out/one/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_gpu_db_api.py -q -x -m gpu 2>&1 | tail -4
+timeout 600 python bench.py > gpurun_out/one/bench.json 2> gpurun_out/one/bench.err; echo "bench rc=$?"
+python -c "import json; d=json.load(open('gpurun_out/one/bench.json')); print(d['ms_per_step'], d['e2e']['ms_per_step'], d['e2e_c_abi'], d['clocks'])"
