@@ -1,7 +1,9 @@
 #!/bin/bash
-# One focused GPU check: build, the handle-ABI parity tests, one bench line.
+# One focused GPU check: build, the batch parity tests, batch64 workload A/B on host threads.
 mkdir -p gpurun_out/one
 python -c "from paper_2603_09190_b200 import build; build.build()" > gpurun_out/one/build.log 2>&1 || { tail gpurun_out/one/build.log; exit 1; }
-timeout 900 python -m pytest tests/test_gpu_db_api.py -q -x -m gpu 2>&1 | tail -4
-timeout 600 python bench.py > gpurun_out/one/bench.json 2> gpurun_out/one/bench.err; echo "bench rc=$?"
-python -c "import json; d=json.load(open('gpurun_out/one/bench.json')); print(d['ms_per_step'], d['e2e']['ms_per_step'], d['e2e_c_abi'], d['clocks'])"
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -x -m gpu -k "batch" 2>&1 | tail -3
+for t in 1 8 1 8; do
+  ZPIR_HOST_THREADS=$t timeout 600 python bench.py --workload batch64 --steps 20 --warmup 3 2> gpurun_out/one/b64_$t.err | tail -1 > gpurun_out/one/b64_$t.json
+  echo "threads=$t"; python -c "import json; d=json.load(open('gpurun_out/one/b64_$t.json')); print(d['ms_per_step'], d.get('e2e'))"
+done
