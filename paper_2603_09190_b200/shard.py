@@ -34,6 +34,25 @@ def shard_params(params, rows: int):
     return dataclasses.replace(params, d1=rows)
 
 
+_GATHER_BUFS = {}
+
+
+def _gather_buffers(t_local, gmax, L, world, group):
+    """The zero-padded send slice and the receive buffer of gather_groups,
+    kept per (device, stream, shape, group): a rank's slice length never
+    changes for fixed bounds, so the padding rows stay zero and a step costs
+    one copy + the all_gather (no allocation or memset launches)."""
+    dev = t_local.device
+    sid = torch.cuda.current_stream(dev).stream_id if dev.type == "cuda" else 0
+    key = (str(dev), sid, t_local.dtype, gmax, L, world, id(group), t_local.shape[0])
+    bufs = _GATHER_BUFS.get(key)
+    if bufs is None:
+        bufs = (torch.zeros((gmax, L), dtype=t_local.dtype, device=dev),
+                torch.empty((world * gmax, L), dtype=t_local.dtype, device=dev))
+        _GATHER_BUFS[key] = bufs
+    return bufs
+
+
 def gather_groups(t_local: torch.Tensor, bounds, rank: int, group=None) -> torch.Tensor:
     """Assemble the full (G, L) answer on every rank from per-rank (g_i, L)
     slices with one all_gather_into_tensor (equal-size padded slices)."""
@@ -41,9 +60,8 @@ def gather_groups(t_local: torch.Tensor, bounds, rank: int, group=None) -> torch
     world = len(bounds)
     gmax = max(b[3] - b[2] for b in bounds)
     L = t_local.shape[1]
-    pad = torch.zeros((gmax, L), dtype=t_local.dtype, device=t_local.device)
+    pad, full = _gather_buffers(t_local, gmax, L, world, group)
     pad[: t_local.shape[0]] = t_local
-    full = torch.empty((world * gmax, L), dtype=t_local.dtype, device=t_local.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(full, pad, group=group)
     else:  # gloo (CPU tests of the multi-rank host logic)
