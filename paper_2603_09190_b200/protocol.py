@@ -27,7 +27,6 @@ import logging
 import os
 import threading
 import time
-import warnings
 
 import numpy as np
 import torch
@@ -162,6 +161,25 @@ def _d2h_u32(t: torch.Tensor, key, stream) -> np.ndarray:
     return pinned.numpy().view(np.uint32).reshape(t.shape).copy()
 
 
+def _host_symbol_check(db: np.ndarray, p: int) -> bool:
+    """The reference's range check `db.max() >= p -> ValueError`
+    (protocol.py:168-169) without a host pass over a u8 database's bytes:
+    every u8 symbol is < 256, so for p >= 256 the check always passes, and for
+    p < 256 it runs on the device after the upload (_device_symbol_check).
+    Other dtypes are checked here, before the cast to u8. Returns True when
+    the device check is still due."""
+    if db.dtype == np.uint8:
+        return p < 256
+    if int(db.max(initial=0)) >= p:
+        raise ValueError("database symbol out of range")
+    return False
+
+
+def _device_symbol_check(db_dev: torch.Tensor, p: int) -> None:
+    if db_dev.numel() and int(db_dev.max().item()) >= p:
+        raise ValueError("database symbol out of range")
+
+
 class ServerGlobalState:
     """Database-derived state, immutable between update_database calls."""
 
@@ -171,8 +189,7 @@ class ServerGlobalState:
         db = np.asarray(db)
         if db.shape != (params.d0, params.d1):
             raise ValueError("database shape mismatch")
-        if int(db.max(initial=0)) >= lwe.p:
-            raise ValueError("database symbol out of range")
+        dev_check = _host_symbol_check(db, lwe.p)
         self.params = params
         self.db = db
         self.db_version = db_version
@@ -187,9 +204,9 @@ class ServerGlobalState:
         self.A_dev = torch.zeros((lay.ld, lay.lda), dtype=torch.int32, device=dev)
         device.chacha_words32(params.a_seed, DOM_PUBLIC_MATRIX, 0, d0, n, self.A_dev, lay.lda,
                               (lay.q - 1) & 0xFFFFFFFF, stream)
-        with warnings.catch_warnings():  # read-only numpy views are only read here
-            warnings.simplefilter("ignore", UserWarning)
-            db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+        db_dev = device.upload_bytes(db, dev, stream)
+        if dev_check:
+            _device_symbol_check(db_dev, lwe.p)
         self.dbt = device.transpose_db(db_dev, d0, d1, lay.rows, lay.ld, stream)
         del db_dev
         self.engine = engine or ENGINE
@@ -219,8 +236,7 @@ class ServerGlobalState:
         db = np.asarray(db)
         if db.shape != (params.d0, params.d1):
             raise ValueError("database shape mismatch")
-        if int(db.max(initial=0)) >= params.lwe.p:
-            raise ValueError("database symbol out of range")
+        dev_check = _host_symbol_check(db, params.lwe.p)
         lay = self.layout
         dev = self.device
         stream = torch.cuda.current_stream(dev)
@@ -231,9 +247,9 @@ class ServerGlobalState:
                             _H_host=None, _H_scaled=None, _lock=threading.Lock(),
                             _tls=threading.local())
         new.db_version = self.db_version + 1 if db_version is None else db_version
-        with warnings.catch_warnings():
-            warnings.simplefilter("ignore", UserWarning)
-            db_dev = torch.from_numpy(np.ascontiguousarray(db, dtype=np.uint8)).to(dev)
+        db_dev = device.upload_bytes(db, dev, stream)
+        if dev_check:
+            _device_symbol_check(db_dev, params.lwe.p)
         new.dbt = device.transpose_db(db_dev, lay.d0, lay.d1, lay.rows, lay.ld, stream)
         del db_dev
         flags = device.rows_differ(new.dbt, self.dbt, stream)

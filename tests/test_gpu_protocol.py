@@ -146,3 +146,34 @@ def test_end_to_end_other_key_sizes(z, bits):
     rc = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
     got = client.extract(sk, 1 << 32, 256, cap, 1 << 32, d1, combined=[c.c for c in rc.k])
     assert got == [int(x) for x in db[i0]]
+
+
+@pytest.mark.parametrize("dtype", [np.uint8, np.int64, np.uint16])
+def test_symbol_range_check(z, dtype):
+    """db.max() >= p raises ValueError (protocol.py:168-169), for u8 databases
+    on the device, for wider dtypes on the host -- in the constructor and in
+    the incremental update -- and in-range databases of any dtype build the
+    same state."""
+    import torch
+    params = _toy(z, d0=5, d1=7)                        # p = 4
+    rng = random.Random(5)
+    db = np.array([[rng.randrange(4) for _ in range(7)] for _ in range(5)], dtype=dtype)
+    st = z.ServerGlobalState(params, db)
+    ref = z.ServerGlobalState(params, db.astype(np.uint8))
+    assert torch.equal(st.H_dev, ref.H_dev)
+    bad = db.copy()
+    bad[4, 6] = 4
+    with pytest.raises(ValueError, match="symbol out of range"):
+        z.ServerGlobalState(params, bad)
+    with pytest.raises(ValueError, match="symbol out of range"):
+        st.updated(bad)
+    if dtype != np.uint8:
+        bad[4, 6] = 260                                 # would wrap to 4 as u8
+        with pytest.raises(ValueError, match="symbol out of range"):
+            z.ServerGlobalState(params, bad)
+    # p = 256: every u8 symbol is in range, no pass over the bytes needed
+    p256 = _toy(z, d0=5, d1=7, lwe=z.LweParams(n=4, q=1 << 32, p=256, noise_sigma=0.0,
+                                                 key_dist="binary"))
+    full = np.full((5, 7), 255, dtype=np.uint8)
+    st2, changed = z.ServerGlobalState(p256, full * 0).updated(full)
+    assert list(changed) == list(range(7))
