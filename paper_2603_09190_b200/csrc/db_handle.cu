@@ -11,6 +11,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/zippir_b200.h"
@@ -499,6 +500,56 @@ int h2d_rows(void* dst, int dst_ld, const uint32_t* src, int src_limbs, int64_t 
             "H2D");
 }
 
+// Bulk host -> device copy of a database (~1 GiB): pageable copies go through the
+// driver's single-threaded bounce buffer (~11 GB/s on the B200 hosts). Here 64 MB
+// chunks are copied into two pinned stages by up to 8 host threads while the
+// previous stage's DMA runs (28-39 GB/s, tools/upload_probe.py for the Python twin,
+// device.upload_bytes). The stages are process-wide, allocated on first use.
+int upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  constexpr size_t kChunk = size_t(64) << 20;
+  if (bytes < (size_t(16) << 20))
+    return cu(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+  struct Stages {
+    HostBuf buf[2];
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  static std::mutex mu;
+  static auto* per_device = new std::map<int, Stages*>();  // never freed (no teardown-order issue)
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  ZPIR_TRY(cu(cudaGetDevice(&dev), "cudaGetDevice"));
+  Stages*& sg = (*per_device)[dev];
+  if (!sg) sg = new Stages();
+  HostBuf* stage = sg->buf;
+  cudaEvent_t* ev = sg->ev;
+  for (int k = 0; k < 2; ++k) {
+    ZPIR_TRY(stage[k].alloc(kChunk));
+    if (!ev[k]) ZPIR_TRY(cu(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event"));
+  }
+  unsigned hc = std::thread::hardware_concurrency();
+  const int nt = hc == 0 ? 4 : (hc > 8 ? 8 : (int)hc);
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+    const int k = (int)(i & 1);
+    const size_t n = bytes - off < kChunk ? bytes - off : kChunk;
+    ZPIR_TRY(cu(cudaEventSynchronize(ev[k]), "event synchronize"));  // stage k is free
+    char* st = stage[k].as<char>();
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) {
+      const size_t a = n * t / nt, b = n * (t + 1) / nt;
+      th.emplace_back([=] { std::memcpy(st + a, in + off + a, b - a); });
+    }
+    std::memcpy(st, in + off, n / nt);
+    for (auto& x : th) x.join();
+    ZPIR_TRY(cu(cudaMemcpyAsync(out + off, st, n, cudaMemcpyHostToDevice, s), "db H2D"));
+    ZPIR_TRY(cu(cudaEventRecord(ev[k], s), "event"));
+  }
+  // the stages are reused by the next upload (any handle, any stream)
+  for (int k = 0; k < 2; ++k) ZPIR_TRY(cu(cudaEventSynchronize(ev[k]), "event synchronize"));
+  return kOk;
+}
+
 // a host row wider than dst_ld limbs must only carry zero limbs beyond it
 int rows_fit(const uint32_t* src, int src_limbs, int dst_ld, int64_t rows) {
   for (int64_t r = 0; r < rows; ++r)
@@ -636,12 +687,14 @@ int create(const zpir_db_params* prm, const uint8_t* db, int64_t ld_db, const ui
     set_error("zpir_db_create: need A or a_seed");
     return kErrInput;
   }
-  for (int64_t i = 0; i < p.d0; ++i)
-    for (int64_t c = 0; c < p.d1; ++c)
-      if (db[i * ld_db + c] >= (uint32_t)p.p) {
-        set_error("database symbol out of range");
-        return kErrInput;
-      }
+  // protocol.py:168-169; every u8 symbol is < 256, so for p >= 256 there is nothing to check
+  if (p.p < 256)
+    for (int64_t i = 0; i < p.d0; ++i)
+      for (int64_t c = 0; c < p.d1; ++c)
+        if (db[i * ld_db + c] >= (uint32_t)p.p) {
+          set_error("database symbol out of range");
+          return kErrInput;
+        }
   auto h = std::make_unique<zpir_db>();
   h->prm = p;
   h->qmask = p.log2q == 32 ? 0xffffffffu : ((1u << p.log2q) - 1u);
@@ -687,8 +740,7 @@ int create(const zpir_db_params* prm, const uint8_t* db, int64_t ld_db, const ui
   {
     DevBuf raw;
     ZPIR_TRY(raw.alloc((size_t)p.d0 * ld_db, false));
-    ZPIR_TRY(cu(cudaMemcpyAsync(raw.p, db, (size_t)p.d0 * ld_db, cudaMemcpyHostToDevice, s),
-                "db H2D"));
+    ZPIR_TRY(upload_staged(raw.p, db, (size_t)p.d0 * ld_db, s));
     ZPIR_TRY(h->dbt.alloc((size_t)h->rows * h->ld, false));
     ZPIR_TRY(zpir_transpose_db(raw.as<uint8_t>(), p.d0, p.d1, ld_db, h->dbt.as<uint8_t>(),
                                h->rows, h->ld, s));

@@ -28,3 +28,18 @@ for threads in ("0", "4", "8", "16", "0", "8"):
     print(f"threads={threads}: upload 1 GiB {min(ts) * 1e3:.1f} ms (median "
           f"{sorted(ts)[len(ts) // 2] * 1e3:.1f}) = {a.nbytes / min(ts) / 1e9:.1f} GB/s", flush=True)
     del out
+
+# the handle C ABI (zpir_db_create: staged upload + transpose + A + H)
+import paper_2603_09190_b200 as z  # noqa: E402
+from paper_2603_09190_b200.dbapi import DeviceDatabase  # noqa: E402
+
+params = z.ProtocolParams(z.LweParams(1024, 1 << 32, 256, 6.4), 32768, 32768, 2048)
+for _ in range(3):
+    t = time.perf_counter()
+    d = DeviceDatabase(params, a)
+    print(f"zpir_db_create 1 GiB: {(time.perf_counter() - t) * 1e3:.1f} ms", flush=True)
+    d.close()
+t = time.perf_counter()
+st = z.ServerGlobalState(params, a)
+torch.cuda.synchronize()
+print(f"ServerGlobalState 1 GiB: {(time.perf_counter() - t) * 1e3:.1f} ms", flush=True)
