@@ -483,9 +483,12 @@ def upload_bytes(a: np.ndarray, dev, stream) -> torch.Tensor:
     flat = a.reshape(-1)
     o = out.view(-1)
     with _UPLOAD_LOCK:
-        if _UPLOAD_POOL is None or _UPLOAD_POOL._max_workers != nthreads:
+        if _UPLOAD_POOL is None or _UPLOAD_POOL[0] != nthreads:
             from concurrent.futures import ThreadPoolExecutor
-            _UPLOAD_POOL = ThreadPoolExecutor(nthreads, thread_name_prefix="zpir-upload")
+            if _UPLOAD_POOL is not None:
+                _UPLOAD_POOL[1].shutdown(wait=False)
+            _UPLOAD_POOL = (nthreads, ThreadPoolExecutor(nthreads, thread_name_prefix="zpir-upload"))
+        pool = _UPLOAD_POOL[1]
         key = str(dev)
         if key not in _UPLOAD_STAGES:
             _UPLOAD_STAGES[key] = [
@@ -498,7 +501,7 @@ def upload_bytes(a: np.ndarray, dev, stream) -> torch.Tensor:
             n = min(_UPLOAD_CHUNK, flat.size - off)
             st = buf.numpy()
             cuts = [n * t // nthreads for t in range(nthreads + 1)]
-            list(_UPLOAD_POOL.map(
+            list(pool.map(
                 lambda t: np.copyto(st[cuts[t]:cuts[t + 1]], flat[off + cuts[t]:off + cuts[t + 1]]),
                 range(nthreads)))
             with torch.cuda.stream(stream):
