@@ -171,3 +171,63 @@ def test_handle_api_tensor_core_hint(api, monkeypatch):
     pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
     reg = z.ClientRegistration(pk, seed, z.client_id_of(pk))
     assert k_tc == [c.c for c in z.hint(st, reg, 2).entries]
+
+
+def test_handle_api_concurrent_threads(api, golden):
+    """The handle ABI from several threads at once (ctypes drops the GIL):
+    calls on one handle serialise on its lock and share its pinned staging;
+    two handles (and their creation, which shares the process-wide upload
+    stages) run side by side. Every answer stays bit-exact."""
+    import threading
+    import paper_2603_09190_b200 as z
+    g = golden("tiny")                                 # BASELINE configs[0]
+    qu, ck, m = g.arr["qu0"], g.ints("ck_o"), g.m
+    t_want, K_want, k_want = g.ints("t"), g.ints("K"), g.ints("k")
+    errors = []
+    handles = []
+    lock = threading.Lock()
+    # a DB above the staged-upload threshold (16 MiB), created from two threads
+    big_p = z.ProtocolParams(z.LweParams(1024, 1 << 32, 256, 6.4), 4096, 4160, 2048)
+    big = np.frombuffer(np.random.default_rng(3).bytes(4096 * 4160), np.uint8).reshape(4096, 4160)
+    big_q = np.random.default_rng(4).integers(0, 1 << 32, 4096, dtype=np.uint64)
+    big_b = ref.db_matvec(big, big_q, 1 << 32)
+
+    def create(prm, db, into):
+        try:
+            d = api.DeviceDatabase(prm, db)
+            with lock:
+                into.append(d)
+        except Exception as e:
+            errors.append(e)
+
+    bigs = []
+    th = [threading.Thread(target=create, args=a) for a in
+          [(big_p, big, bigs), (big_p, big, bigs), (_params(g), g.db, handles),
+           (_params(g), g.db, handles)]]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors and len(handles) == 2 and len(bigs) == 2, errors[:1]
+    for d in bigs:
+        assert np.array_equal(d.db_matvec(big_q), big_b)
+        d.close()
+
+    def work(d, i):
+        try:
+            for _ in range(4):
+                if i % 2:
+                    assert d.answer_combined(qu, ck, m, k_want) == K_want
+                else:
+                    assert d.answer(qu, ck, m) == t_want
+        except Exception as e:
+            errors.append(e)
+
+    th = [threading.Thread(target=work, args=(handles[i % 2], i)) for i in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for d in handles:
+        d.close()
+    assert not errors, errors[:1]
