@@ -313,3 +313,22 @@ def test_slot_fixed_tensor_core_many_clients_row_ids(env):
         a, b = device.to_host_u32(W_ref), device.to_host_u32(W)
         assert np.array_equal(a, b)
         assert not b[np.setdiff1d(np.arange(nrow), rid_h)].any()
+
+
+@pytest.mark.parametrize("shape,view", [((4097, 4099), None), (((64 << 20) + 1,), None),
+                                        ((11000, 12289), "cols")])
+def test_upload_bytes_staged(env, shape, view):
+    """device.upload_bytes (pinned stages, threaded host copies) == the plain
+    torch copy, at sizes straddling the 16 MiB threshold and the 64 MiB chunk,
+    for contiguous and strided (column-sliced) arrays."""
+    torch, device = env
+    dev = torch.device("cuda", 0)
+    a = np.frombuffer(np.random.default_rng(len(shape)).bytes(int(np.prod(shape))),
+                      np.uint8).reshape(shape)
+    if view == "cols":
+        a = a[:, 7:-5]
+    stream = torch.cuda.current_stream(dev)
+    out = device.upload_bytes(a, dev, stream)
+    torch.cuda.synchronize()
+    assert out.shape == a.shape
+    assert torch.equal(out.cpu(), torch.from_numpy(np.array(a)))   # writable copy
