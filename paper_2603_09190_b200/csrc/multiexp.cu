@@ -21,6 +21,7 @@
 // H_scaled[g][k] are H[g*cap + j][k] (protocol.py:223-230); no H_scaled is
 // ever materialised.
 #include <algorithm>
+#include <cstdlib>
 
 #include "bignum.cuh"
 
@@ -175,12 +176,13 @@ struct GammaExp {
   int nbits;
 };
 
-template <int LPL>
+template <int LPL, bool UNR>
 __global__ void __launch_bounds__(128)
 slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __restrict__ group_ids,
                     int64_t ngroups, const uint32_t* __restrict__ N, uint32_t np,
                     uint32_t* __restrict__ out, GammaExp gm) {
   constexpr int L = 32 * LPL;
+#define MM(...) (UNR ? mont_mul_unrolled<LPL>(__VA_ARGS__) : mont_mul<LPL>(__VA_ARGS__))
   const int lane = threadIdx.x & 31;
   const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gi >= ngroups) return;
@@ -194,16 +196,17 @@ slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __re
     // acc = acc^gamma (left-to-right binary; gamma = 2^32 is 32 squarings)
     big_copy<LPL>(base, acc);
     for (int bit = gm.nbits - 2; bit >= 0; --bit) {
-      mont_mul<LPL>(acc, acc, acc, n_, np, lane);
-      if ((gm.w[bit >> 5] >> (bit & 31)) & 1u) mont_mul<LPL>(acc, acc, base, n_, np, lane);
+      MM(acc, acc, acc, n_, np, lane);
+      if ((gm.w[bit >> 5] >> (bit & 31)) & 1u) MM(acc, acc, base, n_, np, lane);
     }
     big_load<LPL>(x, Wg + (size_t)j * L, lane);
-    mont_mul<LPL>(acc, acc, x, n_, np, lane);
+    MM(acc, acc, x, n_, np, lane);
   }
   big_set_small<LPL>(x, 1, lane);
-  mont_mul<LPL>(acc, acc, x, n_, np, lane);  // leave Montgomery form
+  MM(acc, acc, x, n_, np, lane);  // leave Montgomery form
   big_store<LPL>(out + g * L, acc, lane);
 }
+#undef MM
 
 // ---- fixed-base slot multiexp (w = 8) -------------------------------------
 // P[i][k] = ck_k^(2^(8 i)) in Montgomery form (i < 4), one warp per base.
@@ -492,9 +495,21 @@ int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, in
   GammaExp gm{};
   for (int i = 0; i < (gamma_bits + 31) / 32; ++i) gm.w[i] = gamma[i];
   gm.nbits = gamma_bits;
+  // latency-bound (one warp per group, few groups): the unrolled CIOS is
+  // 17.4 -> 15.1 ms for one client at 1 GiB (tools/slot_probe.py, bit-identical);
+  // ZPIR_SLOT_UNROLL=0 selects the rolled loop
+  static int unr = -1;
+  if (unr < 0) {
+    const char* e = getenv("ZPIR_SLOT_UNROLL");
+    unr = e ? atoi(e) : 1;
+  }
   ZPIR_LPL_DISPATCH2(limbs / 32, {
-    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
-        W, cap, group_ids, ngroups, N, np, out, gm);
+    if (unr)
+      slot_combine_kernel<LPL, true><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
+          W, cap, group_ids, ngroups, N, np, out, gm);
+    else
+      slot_combine_kernel<LPL, false><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
+          W, cap, group_ids, ngroups, N, np, out, gm);
   });
   return check_launch("slot_combine");
 }
