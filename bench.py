@@ -53,6 +53,10 @@ def _args():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-rows", type=int, default=0,
+                    help="reference arm: serve only this many DB rows (0 = the whole config)")
+    ap.add_argument("--no-single-thread", action="store_true",
+                    help="reference arm: skip the single-thread figure")
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-extra-e2e", action="store_true",
                     help="skip the wire / C-ABI e2e variants")
@@ -181,24 +185,48 @@ def _traffic():
         return None
 
 
-# -- CPU baseline (reference algorithm port; rank 0 only) --------------------
+def _config(world):
+    """The workload description, identical in both arms (driver same_config)."""
+    return {"workload": "BASELINE configs[1]: 1 GiB DB per GPU (32768 x 32768 u8), "
+                        "n=1024, q=2^32, 2048-bit Paillier, single query, SEPARATE",
+            "d0": D0, "d1": D1 * world, "groups": -(-(D1 * world) // CAP), "n": N_LWE,
+            "paillier_bits": BITS, "queries_per_step": 1,
+            "l2": "no flush: the DB (1 GiB per GPU) exceeds L2 (126 MB) and the host LLC"}
 
-def cpu_baseline(m, repeats=7):
-    from oracle import ref_port
+
+def _threads(n):
     try:
         from threadpoolctl import threadpool_limits
-        threadpool_limits(os.cpu_count())
+        threadpool_limits(n)
     except Exception:
         pass
-    rows = CPU_SAMPLE_ROWS
-    db = db_slice(0, D1)[:, :rows].copy()
-    from paper_2603_09190_b200.prg import Stream, DOM_PUBLIC_MATRIX
-    A = Stream(b"\x00" * 16, DOM_PUBLIC_MATRIX).words32(D0 * N_LWE).reshape(D0, N_LWE)
-    st = ref_port.PortState(db, A, CAP)
+
+
+def _cpu_query(m):
     rng = np.random.default_rng(11)
     qu = rng.integers(0, 1 << 32, D0, dtype=np.uint64)
     r = random.Random(12)
-    ck_o = [r.randrange(m) for _ in range(N_LWE)]
+    return qu, [r.randrange(m) for _ in range(N_LWE)]
+
+
+def _port_state(rows, d0=D0, seed_rank=0):
+    """The reference's ServerGlobalState built its own way (oracle/ref_port.py:
+    float64 GEMMs for H, H_scaled, 240-prime residues, the centered float64
+    DB copy) over DB rows [0, rows); A from oracle/ref's ChaCha20."""
+    from oracle import ref, ref_port
+    db = db_slice(seed_rank, D1)[:, :rows] if d0 == D0 else None
+    db = np.ascontiguousarray(db)
+    A = ref.public_matrix(b"\x00" * 16, d0, N_LWE, 1 << 32)
+    return ref_port.PortState(db, A, CAP)
+
+
+def cpu_baseline(m, repeats=7):
+    """Bounded sample beside the B200 line: the reference algorithm on
+    CPU_SAMPLE_ROWS of the 32768 DB rows, all host cores."""
+    _threads(os.cpu_count())
+    rows = CPU_SAMPLE_ROWS
+    st = _port_state(rows)
+    qu, ck_o = _cpu_query(m)
     times = []
     for _ in range(repeats):
         t0 = time.perf_counter()
@@ -215,50 +243,116 @@ def cpu_baseline(m, repeats=7):
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU algorithm for respond()
+    (oracle/ref_port.py, bit-exact with the reference's goldens) on the
+    B200 arm's config, all host cores; exactly --warmup untimed and --steps
+    timed respond()s. At N = 1 the whole configs[1] DB (32768 x 32768) is
+    served; at N > 1 (N GiB) a 1 GiB row slice is timed and the metric is
+    per DB byte of that slice. Then the same respond() single-threaded
+    (OPENBLAS_NUM_THREADS = 1, the paper's methodology)."""
     rank, world, _ = _dist_env()
     if rank != 0:
         return
-    # all host threads for the CPU reference arm (torchrun sets OMP_NUM_THREADS=1)
-    try:
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(os.cpu_count())
-    except Exception:
-        pass
+    _threads(os.cpu_count())
     m = paillier_modulus(BITS, 2048)
-    from oracle import ref_port
-    rows = CPU_SAMPLE_ROWS
-    db = db_slice(0, D1)[:, :rows].copy()
-    from paper_2603_09190_b200.prg import Stream, DOM_PUBLIC_MATRIX
-    A = Stream(b"\x00" * 16, DOM_PUBLIC_MATRIX).words32(D0 * N_LWE).reshape(D0, N_LWE)
-    st = ref_port.PortState(db, A, CAP)
-    rng = np.random.default_rng(11)
-    qu = rng.integers(0, 1 << 32, D0, dtype=np.uint64)
-    r = random.Random(12)
-    ck_o = [r.randrange(m) for _ in range(N_LWE)]
-    steps = max(1, min(args.steps, 50))
-    for _ in range(min(args.warmup, 3)):
-        st.respond_t(qu, ck_o, m)
+    rows = args.ref_rows or D1
     t0 = time.perf_counter()
-    for _ in range(steps):
+    st = _port_state(rows)
+    setup_s = time.perf_counter() - t0
+    qu, ck_o = _cpu_query(m)
+    for _ in range(args.warmup):
         st.respond_t(qu, ck_o, m)
-    dt = (time.perf_counter() - t0) / steps
+    times = []
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        st.respond_t(qu, ck_o, m)
+        times.append(time.perf_counter() - t1)
+    dt = statistics.mean(times)
     v = D0 * rows / dt / 1e9
-    sample = (f"{rows} of {D1} DB rows ({rows // CAP} groups) x d0={D0} per step; reference "
-              "algorithm port (oracle/ref_port.py: float64 BLAS GEMV + 240-prime RNS)")
+    one = None
+    if not args.no_single_thread:
+        _threads(1)
+        t1s = []
+        for _ in range(2):
+            t1 = time.perf_counter()
+            st.respond_t(qu, ck_o, m)
+            t1s.append(time.perf_counter() - t1)
+        _threads(os.cpu_count())
+        one = {"value": D0 * rows / min(t1s) / 1e9, "unit": "GB/s", "cores": 1,
+               "ms_per_step": min(t1s) * 1e3, "note": "OPENBLAS_NUM_THREADS=1, best of 2"}
+    whole = rows == D1 * world
+    sample = (f"{'all' if whole else rows} of {D1 * world} DB rows x d0={D0} per step, "
+              f"n={N_LWE}, {BITS}-bit m: the reference's respond() algorithm (oracle/ref_port.py: "
+              "centered float64 BLAS GEMV + 240x27-bit-prime RNS matvec + Garner + scaled_b), "
+              f"{os.cpu_count()} host threads")
     print(json.dumps({
         "impl": "reference", "metric": "online server throughput (DB GB/s per query)",
-        "value": v, "unit": "GB/s", "n_gpus": world, "steps": steps, "warmup": min(args.warmup, 3),
+        "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8xu32 / 2048-bit", "data": "synthetic",
-        "config": {"workload": "BASELINE configs[1]: 1 GiB DB per GPU (32768 x 32768 u8), "
-                               "n=1024, q=2^32, 2048-bit Paillier, single query, SEPARATE",
-                   "d0": D0, "d1": D1, "groups": -(-D1 // CAP),
-                   "parallelism": "host CPU (reference arm, rank 0 only)",
-                   "l2": "n/a (CPU)", "sampled_rows_per_step": rows},
+        "vs_baseline": None, "dtype": "u8xu32 mod 2^32 / 2048-bit (float64-exact + RNS on CPU)",
+        "data": "synthetic (seeded uniform u8 DB, uniform qu0 / ck_o, seeded Paillier modulus)",
+        "config": _config(world),
         "cpu_baseline": {"value": v, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "single_thread": one, "setup_s": setup_s,
+        "ms_per_step_median": statistics.median(times) * 1e3,
+        "cpu_model": _cpu_model(),
     }), flush=True)
+
+
+def cpu_hint_baseline(db, m, nentries=None):
+    """Reference-equivalent hint cost on the host: the reference's windowed
+    multiexp (paillier.py:134-193) restated over libgmp (oracle/c, the
+    library gmpy2 wraps) on `nentries` real 1 GiB hint entries (exponents from
+    the oracle's H of the first groups, ck_r from the oracle's ChaCha20),
+    one entry per host thread in parallel; extrapolated x d1' per client and
+    x 256 clients as the reference's bench.py:183-190 does."""
+    from oracle import c as oc, ref
+    threads = os.cpu_count()
+    nentries = nentries or threads
+    A = ref.public_matrix(b"\x00" * 16, D0, N_LWE, 1 << 32)
+    H = oc.hint_rows(db, A, 0, nentries * CAP)
+    E = oc.scaled_exponents(H, CAP)
+    m2 = m * m
+    ck_r = ref.derive_ck_r(m2, b"\x05" * 16, 0, N_LWE)
+    t0 = time.perf_counter()
+    oc.multiexp_rows(ck_r, E, m2)
+    wall = time.perf_counter() - t0
+    per_entry_core = wall * min(threads, nentries) / nentries     # one core, one entry
+    groups = -(-D1 // CAP)
+    per_client = per_entry_core * groups / threads
+    return {"value": per_client, "unit": "s per client (all host cores)", "cores": threads,
+            "kind": "port",
+            "sample": f"{nentries} hint entries (groups 0..{nentries - 1}, 1024 exponents of "
+                      f"2016 bits, 4096-bit m^2) by the reference's w=6 windowed multiexp over "
+                      f"libgmp, {threads} threads; {per_entry_core:.2f} s per entry per core, "
+                      f"x {groups} entries per client / {threads} cores",
+            "per_entry_core_s": per_entry_core, "clients_256_s": 256 * per_client}
+
+
+def cpu_rebuild_baseline(db, rows=CPU_SAMPLE_ROWS):
+    """The reference's full state rebuild (ServerGlobalState.__init__:
+    float64 H GEMMs, H_scaled, residues, centered DB copy) on a row sample,
+    extrapolated linearly to all 32768 rows."""
+    _threads(os.cpu_count())
+    from oracle import ref, ref_port
+    A = ref.public_matrix(b"\x00" * 16, D0, N_LWE, 1 << 32)
+    part = np.ascontiguousarray(db[:, :rows])
+    t0 = time.perf_counter()
+    ref_port.PortState(part, A, CAP)
+    dt = time.perf_counter() - t0
+    return dt * D1 / rows, f"{rows} of {D1} DB rows, x{D1 / rows:.2f}"
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # -- B200 path -----------------------------------------------------------------
@@ -483,11 +577,7 @@ def run_b200(args):
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8xu32 mod 2^32 / 2048-bit Montgomery",
             "data": "synthetic (seeded uniform u8 DB, uniform qu0 / ck_o, seeded Paillier modulus)",
-            "config": {"workload": "BASELINE configs[1]: 1 GiB DB per GPU (32768 x 32768 u8), "
-                                   "n=1024, q=2^32, 2048-bit Paillier, single query, SEPARATE",
-                       "d0": D0, "d1": d1_total, "groups": params.d1_prime,
-                       "parallelism": f"db-row shards x{world}",
-                       "l2": "no flush: DB (1 GiB/GPU) > L2 (126 MB)"},
+            "config": _config(world), "parallelism": f"db-row shards x{world}",
             "gpu_launches": 6 * args.steps,   # qplanes, GEMV, build_bc, compression, groups_z, finish
             "roofline": {"bound": "hbm",
                          "kernel": "umma_gemm_kernel<16,0> (tcgen05 GEMV + query planes) inside the "
@@ -557,6 +647,8 @@ def run_extra(args):
         t0 = time.perf_counter()
         srv = ShardedServer(params, db[:, lo:hi], rank, world)
         setup = time.perf_counter() - t0
+        cpu_part = (np.ascontiguousarray(db[:, :CPU_SAMPLE_ROWS])
+                    if rank == 0 and not args.no_cpu_baseline else None)
         del db
         st = srv.state
         plan = st.answer_plan(kctx, kctx.lm)
@@ -601,6 +693,27 @@ def run_extra(args):
                "metric": "online server throughput (DB GB/s per query)",
                "value": d * d / (ms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": ms,
                "per_gpu_hbm_frac": (d * (hi - lo)) / (ms / 1e3) / 1e9 / peak, "setup_s": setup}
+        if cpu_part is not None:
+            # the chunked restatement of the reference's respond (d0 = 92682 is
+            # past its float64 bound; ref_port.PortState chunks d0 by 32768)
+            from oracle import ref, ref_port
+            _threads(os.cpu_count())
+            A = ref.public_matrix(b"\x00" * 16, d, N_LWE, 1 << 32)
+            pst = ref_port.PortState(cpu_part, A, CAP)
+            rq = np.random.default_rng(13).integers(0, 1 << 32, d, dtype=np.uint64)
+            rr = random.Random(14)
+            ck = [rr.randrange(m) for _ in range(N_LWE)]
+            ts = []
+            for _ in range(5):
+                t1 = time.perf_counter()
+                pst.respond_t(rq, ck, m)
+                ts.append(time.perf_counter() - t1)
+            out["cpu_baseline"] = {
+                "value": d * CPU_SAMPLE_ROWS / min(ts) / 1e9, "unit": "GB/s",
+                "cores": os.cpu_count(), "kind": "port",
+                "sample": f"{CPU_SAMPLE_ROWS} of {d} DB rows x d0={d}: the reference's respond "
+                          "algorithm chunked over d0 (3 float64 GEMV chunks of <= 32768 records, "
+                          "summed mod 2^32; RNS matvec + Garner), best of 5"}
     elif args.workload == "batch64":
         params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
         st = z.ServerGlobalState(params, db_slice(0, D1))
@@ -660,114 +773,123 @@ def run_extra(args):
                       "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond_batch()",
                       "h2d_bytes_per_step": nq * (4 * D0 + 4 * kctx.lm * N_LWE),
                       "d2h_bytes_per_step": nq * 4 * kctx.lm * params.d1_prime}
-    elif args.workload == "update":
+        if not args.no_cpu_baseline:
+            # the reference has no batch path: 64 sequential respond()s
+            # (protocol.py:333-365), here on a row sample
+            _threads(os.cpu_count())
+            pst = _port_state(CPU_SAMPLE_ROWS)
+            rq = np.random.default_rng(15)
+            qs_cpu = [(rq.integers(0, 1 << 32, D0, dtype=np.uint64),
+                       [r.randrange(m) for _ in range(N_LWE)]) for _ in range(nq)]
+            pst.respond_t(*qs_cpu[0], m)
+            t1 = time.perf_counter()
+            for qu_c, ck_c in qs_cpu:
+                pst.respond_t(qu_c, ck_c, m)
+            dt = time.perf_counter() - t1
+            out["cpu_baseline"] = {
+                "value": nq * D0 * CPU_SAMPLE_ROWS / dt / 1e9, "unit": "GB/s",
+                "cores": os.cpu_count(), "kind": "port",
+                "sample": f"64 sequential respond()s (the reference's algorithm, no batch path) on "
+                          f"{CPU_SAMPLE_ROWS} of {D1} DB rows x d0={D0}; {dt:.2f} s"}
+    elif args.workload in ("update", "hint"):
+        # BASELINE configs[4]: global H, then compressed hints for 256 client
+        # keys (the hint worker's batches of 16), then (update) 1% of the DB
+        # rows re-drawn from a seed, the incremental state and the refresh of
+        # all 256 hints -- every client measured, nothing extrapolated
         params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
         db = db_slice(0, D1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
         st = z.ServerGlobalState(params, db)
-        nclients = 16
+        setup = time.perf_counter() - t0
+        nclients, batch = 256, 16
         regs = []
         for j in range(nclients):
             mj = paillier_modulus(BITS, 3000 + j)
             pk = z.PaillierPublicKey(mj, mj.bit_length())
-            regs.append(z.ClientRegistration(pk, bytes([j]) * 16, z.client_id_of(pk)))
-        z.hints(st, [(reg, 0) for reg in regs[:8]])      # warm-up (memory pool, kernels)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        hints = z.hints(st, [(reg, 0) for reg in regs], keep_slots=True)
-        torch.cuda.synchronize()
-        t_full = [(time.perf_counter() - t1) / nclients]
-        # update 1% of DB rows (DB = db^T rows = db columns), re-drawn from a seed
-        rng = np.random.default_rng(77)
-        rows = np.sort(rng.choice(D1, size=D1 // 100, replace=False))
-        db2 = db.copy()
-        db2[:, rows] = rng.integers(0, 256, (D0, rows.size), dtype=np.uint8)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        st2, changed = st.updated(db2)
-        torch.cuda.synchronize()
-        t_state = time.perf_counter() - t1
-        t1 = time.perf_counter()
-        z.refresh_hint(st2, regs[0], hints[0], changed)
-        torch.cuda.synchronize()
-        t_one = time.perf_counter() - t1
-        t1 = time.perf_counter()
-        z.refresh_hints(st2, list(zip(regs, hints)), changed)
-        torch.cuda.synchronize()
-        r = (time.perf_counter() - t1) / nclients
-        # the full rebuild timed the same way as updated(): wall clock around the call
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        z.ServerGlobalState(params, db2, db_version=1)
-        torch.cuda.synchronize()
-        full_rebuild = time.perf_counter() - t1
-        f = statistics.median(t_full)
-        out = {"workload": "BASELINE configs[4] update: 1 GiB DB, 1% of DB rows (328) re-drawn, "
-                           "incremental state + hint refresh (slot-decomposed hints)",
-               "n_gpus": 1, "changed_rows": int(changed.size),
-               "state_update_s": t_state, "state_full_rebuild_gpu_s": full_rebuild,
-               "hint_full_s_per_client": f, "hint_refresh_s_per_client": r,
-               "hint_refresh_single_client_s": t_one,
-               "refresh_speedup": f / r, "clients_sampled": nclients,
-               "extrapolated_256_clients_refresh_s": 256 * r,
-               "extrapolated_256_clients_full_regen_s": 256 * f}
-    elif args.workload == "hint":
-        params = z.ProtocolParams(z.LweParams(N_LWE, 1 << 32, 256, 6.4), D0, D1, BITS)
-        t0 = time.perf_counter()
-        st = z.ServerGlobalState(params, db_slice(0, D1))
-        setup = time.perf_counter() - t0
-        nclients = 2
-        times = []
-        # warm-up: first use grows the stream-ordered memory pool (tensor-core
-        # workspace) and loads the kernels; not part of the timing
-        mw = paillier_modulus(BITS, 2999)
-        pkw = z.PaillierPublicKey(mw, mw.bit_length())
-        z.hints(st, [(z.ClientRegistration(pkw, b"\xff" * 16, z.client_id_of(pkw)), 0)] * 8)
+            regs.append(z.ClientRegistration(pk, j.to_bytes(2, "little") * 8, z.client_id_of(pk)))
+        keep = args.workload == "update"
+        z.hints(st, [(reg, 0) for reg in regs[:batch]], keep_slots=keep)   # warm-up (pool, kernels)
         torch.cuda.synchronize()
         clocks = ClockSampler(0)
         clocks.start()
-        for j in range(nclients):
-            mj = paillier_modulus(BITS, 3000 + j)
-            pk = z.PaillierPublicKey(mj, mj.bit_length())
-            reg = z.ClientRegistration(pk, bytes([j]) * 16, z.client_id_of(pk))
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            z.hint(st, reg, 0)
-            torch.cuda.synchronize()
-            times.append(time.perf_counter() - t1)
-        single = statistics.median(times)
-        # the hint worker's batch: 16 clients through protocol.hints (one
-        # tensor-core launch per workspace-sized group of clients)
-        nbatch = 16
-        jobs = []
-        for j in range(nbatch):
-            mj = paillier_modulus(BITS, 4000 + j)
-            pk = z.PaillierPublicKey(mj, mj.bit_length())
-            jobs.append((z.ClientRegistration(pk, bytes([j]) * 16, z.client_id_of(pk)), 0))
-        torch.cuda.synchronize()
         t1 = time.perf_counter()
-        z.hints(st, jobs)
+        hints = []
+        for c0 in range(0, nclients, batch):
+            hints += z.hints(st, [(reg, 0) for reg in regs[c0:c0 + batch]], keep_slots=keep)
         torch.cuda.synchronize()
-        times = [(time.perf_counter() - t1) / nbatch]
-        nclients = nbatch
-        clk = clocks.stop()
-        per = statistics.median(times)
+        t_all = time.perf_counter() - t1
+        t1 = time.perf_counter()
+        z.hint(st, regs[0], 0)
+        torch.cuda.synchronize()
+        single = time.perf_counter() - t1
         ref_mulmods = 361620 * params.d1_prime
         imad = None
         try:
             imad = json.load(open(os.path.join(ROOT, "profiles", "imad_peak.json")))["imad_per_s"]
         except Exception:
             pass
-        out = {"workload": "BASELINE configs[4]: global H = DB A (1 GiB, n=1024) + per-client "
-                           "compressed hint (521 entries, 2048-bit)", "n_gpus": 1,
+        per = t_all / nclients
+        out = {"workload": "BASELINE configs[4]: global H = DB A (1 GiB, n=1024) + compressed hints "
+                           "(521 entries, 2048-bit) for 256 client keys"
+                           + (", then 1% of DB rows re-drawn + incremental state + refresh of all "
+                              "256 hints" if keep else ""),
+               "n_gpus": 1, "metric": "compressed hints per second (256 clients)",
+               "value": nclients / t_all, "unit": "clients/s", "higher_is_better": True,
                "global_hint_s": st.hint_time, "setup_s": setup,
-               "hint_s_per_client": per, "clients_sampled": nclients,
-               "hint_single_client_s": single, "clocks": clk,
-               "schedule": "protocol.hints: 16 clients, tensor-core Pippenger launches of "
-                           "up to ZPIR_TC_WS_GB of workspace each",
-               "extrapolated_256_clients_s": 256 * per,
+               "hints_256_clients_s": t_all, "hint_s_per_client": per,
+               "hint_single_client_s": single,
+               "schedule": f"protocol.hints in batches of {batch} clients (the hint worker's batch), "
+                           "tensor-core Pippenger",
                "reference_equivalent_mulmods_per_s": ref_mulmods / per,
                "imad_peak_per_s": imad,
                "imad_util_reference_equivalent": (ref_mulmods / per * 65792 / imad) if imad else None}
+        if keep:
+            rng = np.random.default_rng(77)
+            rows = np.sort(rng.choice(D1, size=D1 // 100, replace=False))
+            db2 = db.copy()
+            db2[:, rows] = rng.integers(0, 256, (D0, rows.size), dtype=np.uint8)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            st2, changed = st.updated(db2)
+            torch.cuda.synchronize()
+            t_state = time.perf_counter() - t1
+            t1 = time.perf_counter()
+            new = []
+            for c0 in range(0, nclients, batch):
+                new += z.refresh_hints(st2, list(zip(regs[c0:c0 + batch], hints[c0:c0 + batch])),
+                                       changed)
+            torch.cuda.synchronize()
+            t_ref = time.perf_counter() - t1
+            # spot check: two refreshed hints equal full hints on the updated state
+            for i in (0, nclients - 1):
+                full = z.hint(st2, regs[i], 0)
+                assert [c.c for c in full.entries] == [c.c for c in new[i].entries]
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            z.ServerGlobalState(params, db2, db_version=1)
+            torch.cuda.synchronize()
+            full_rebuild = time.perf_counter() - t1
+            out.update({"changed_rows": int(changed.size), "state_update_s": t_state,
+                        "state_full_rebuild_gpu_s": full_rebuild,
+                        "refresh_256_clients_s": t_ref,
+                        "hint_refresh_s_per_client": t_ref / nclients,
+                        "refresh_speedup": t_all / t_ref,
+                        "metric": "seconds to update 1% of rows and refresh 256 hints",
+                        "value": t_state + t_ref, "unit": "s", "higher_is_better": False})
+        out["clocks"] = clocks.stop()
+        if not args.no_cpu_baseline:
+            hb = cpu_hint_baseline(db, m)
+            out["cpu_baseline"] = {k: hb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            out["cpu_baseline"]["clients_256_s"] = hb["clients_256_s"]
+            if keep:
+                rb, rs = cpu_rebuild_baseline(db)
+                out["cpu_baseline_update"] = {
+                    "value": rb + hb["clients_256_s"], "unit": "s", "cores": os.cpu_count(),
+                    "kind": "port",
+                    "sample": f"reference full rebuild (ServerGlobalState.__init__ restated: "
+                              f"{rs}) = {rb:.1f} s + every hint regenerated (server.py:115-124): "
+                              f"256 x {hb['value']:.1f} s (multiexp sample above)"}
     elif args.workload == "tiny":
         # BASELINE configs[0]: the reference's CPU-runnable case, end to end on
         # the device: global hint, one client's compressed hint, one answer

@@ -129,7 +129,16 @@ class Basis:
 
 
 class PortState:
-    """Server state built the reference's way for db (d0, d1) uint8."""
+    """Server state built the reference's way for db (d0, d1) uint8.
+
+    For d0 <= 32768 this is exactly the reference's fast path (the float64
+    exactness bound d0 * 128 * 2^31 <= 2^53, protocol.py:177-179). Beyond it
+    (BASELINE configs[2], d0 = 92682, where the reference falls to its
+    Python triple loops, protocol.py:209-217 / :253-257) the same float64
+    GEMMs / GEMV run over d0 chunks of <= 32768 records and the chunk results
+    are summed mod 2^32 -- the "chunked restatement" of SURVEY 8c."""
+
+    CHUNK = 32768
 
     def __init__(self, db, A, cap, basis=None):
         db = np.asarray(db)
@@ -137,14 +146,17 @@ class PortState:
         self.cap = cap
         self.groups = -(-self.d1 // cap)
         self.basis = basis or Basis()
-        dbt = db.astype(np.float64).T
         Ai = np.asarray(A, dtype=np.int64)
-        glo = (dbt @ (Ai & 0xFFFF).astype(np.float64)).astype(np.int64)
-        ghi = (dbt @ (Ai >> 16).astype(np.float64)).astype(np.int64)
         mask = (1 << 32) - 1
-        h = (np.mod(glo, 1 << 32) + (np.mod(ghi, 1 << 16) << 16)) & mask
+        h = np.zeros((self.d1, Ai.shape[1]), dtype=np.int64)
+        for s0 in range(0, self.d0, self.CHUNK):
+            s1 = min(self.d0, s0 + self.CHUNK)
+            dbt = db[s0:s1].astype(np.float64).T
+            glo = (dbt @ (Ai[s0:s1] & 0xFFFF).astype(np.float64)).astype(np.int64)
+            ghi = (dbt @ (Ai[s0:s1] >> 16).astype(np.float64)).astype(np.int64)
+            h = (h + np.mod(glo, 1 << 32) + (np.mod(ghi, 1 << 16) << 16)) & mask
+            del dbt, glo, ghi
         self.H = ((1 << 32) - h) & mask
-        del dbt, glo, ghi
         n = self.H.shape[1]
         scaled = []
         for g in range(self.groups):
@@ -153,15 +165,23 @@ class PortState:
         flat = [x for row in scaled for x in row]
         res = self.basis.to_rns(flat)
         self.H_rns = np.ascontiguousarray(res.T.reshape(self.basis.count, self.groups, n))
-        self._dbt_c = (db.astype(np.float64) - 128.0).T.copy()
-        self._colsum_c = (db.astype(np.int64) - 128).sum(axis=0)
+        self._chunks = []
+        for s0 in range(0, self.d0, self.CHUNK):
+            s1 = min(self.d0, s0 + self.CHUNK)
+            part = db[s0:s1]
+            self._chunks.append((s0, s1, (part.astype(np.float64) - 128.0).T.copy(),
+                                 (part.astype(np.int64) - 128).sum(axis=0)))
 
     def db_matvec(self, qu):
-        quf = qu.astype(np.float64) - float(1 << 31)
-        s = (self._dbt_c @ quf).astype(np.int64)
-        sum_quc = int(qu.astype(np.uint64).sum()) - self.d0 * (1 << 31)
-        total = s + (self._colsum_c << 31) + (128 * sum_quc + self.d0 * 128 * (1 << 31))
-        return np.mod(total, 1 << 32).astype(np.uint64)
+        total = np.zeros(self.d1, dtype=np.int64)
+        for s0, s1, dbt_c, colsum_c in self._chunks:
+            q = qu[s0:s1]
+            quf = q.astype(np.float64) - float(1 << 31)
+            s = (dbt_c @ quf).astype(np.int64)
+            sum_quc = int(q.astype(np.uint64).sum()) - (s1 - s0) * (1 << 31)
+            part = s + (colsum_c << 31) + (128 * sum_quc + (s1 - s0) * 128 * (1 << 31))
+            total = np.mod(total + np.mod(part, 1 << 32), 1 << 32)
+        return total.astype(np.uint64)
 
     def rns_matvec(self, v, m):
         b = self.basis
