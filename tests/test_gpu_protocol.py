@@ -177,3 +177,91 @@ def test_symbol_range_check(z, dtype):
     full = np.full((5, 7), 255, dtype=np.uint8)
     st2, changed = z.ServerGlobalState(p256, full * 0).updated(full)
     assert list(changed) == list(range(7))
+
+
+def test_combined_op_profile_through_caller_counters(z, monkeypatch):
+    """test_protocol.py:147-155 through the drop-in: a caller measuring its own
+    `zippir.counters` (here a freshly written minimal module -- the reference
+    package does not travel to the GPU box) around respond(COMBINED) sees
+    exactly d1' additions and 0 modexp / scalar_mul."""
+    import sys
+    import types
+    from paper_2603_09190_b200 import counters
+    tally = {k: 0 for k in counters.NAMES}
+    mod = types.ModuleType("zippir.counters")
+
+    def bump(name, amount=1):
+        tally[name] += amount
+    mod.bump = bump
+    monkeypatch.setitem(sys.modules, "zippir.counters", mod)
+    rng = random.Random(147)
+    params = _toy(z, d0=6, d1=9)
+    db, state, sk, reg = _setup(z, rng, params)
+    reg.hints[0] = z.hint(state, reg, 0)
+    lw = params.lwe
+    qu0, ck_o, _ = client.query(sk, reg.seed, lw.n, lw.q, lw.p, lw.noise_sigma, params.d0, 2, 0,
+                                rng, state.A)
+    before = dict(tally)
+    r = z.respond(state, reg, z.QueryMessage(reg.client_id, 0, z.COMBINED, ck_o, qu0))
+    delta = {k: tally[k] - before[k] for k in tally}
+    assert delta["add"] == params.d1_prime
+    assert delta["modexp"] == 0 and delta["scalar_mul"] == 0
+    got = client.extract(sk, lw.q, lw.p, params.capacity, params.gamma, params.d1,
+                         combined=[c.c for c in r.k])
+    assert got == [int(x) for x in db[2]]
+
+
+def test_pirserver_store_dir_delegation(z, tmp_path, monkeypatch):
+    """PirServer(params, db, store_dir) as the reference calls it: the path opens
+    zippir.hintstore.HintStore (here a minimal in-memory stand-in registered under
+    that name); registrations and generated hints are saved, and a second server
+    on the same store_dir restores them."""
+    import sys
+    import types
+    from paper_2603_09190_b200.server import PirServer
+    saved = {"regs": {}, "hints": {}}
+
+    class HintStore:
+        def __init__(self, root):
+            self.root = root
+
+        def save_registration(self, cid, pk, seed):
+            saved["regs"][(self.root, cid)] = (pk, seed)
+
+        def load_registrations(self):
+            for (root, cid), (pk, seed) in saved["regs"].items():
+                if root == self.root:
+                    yield cid, pk, seed
+
+        def save_hint(self, cid, qi, version, entries):
+            saved["hints"][(self.root, cid, qi, version)] = list(entries)
+
+        def load_hints(self, cid, version):
+            return {qi: e for (root, c, qi, v), e in saved["hints"].items()
+                    if root == self.root and c == cid and v == version}
+
+        def purge_stale(self, cid, version):
+            pass
+    mod = types.ModuleType("zippir.hintstore")
+    mod.HintStore = HintStore
+    monkeypatch.setitem(sys.modules, "zippir.hintstore", mod)
+    rng = random.Random(30)
+    params = _toy(z, d0=4, d1=8)
+    db = np.array([[rng.randrange(params.lwe.p) for _ in range(params.d1)]
+                   for _ in range(params.d0)])
+    d = str(tmp_path / "store")
+    srv = PirServer(params, db, d)
+    try:
+        sk, seed = client.setup(params.paillier_bits, rng)
+        pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
+        cid = srv.register(pk, seed)
+        srv.wait_for_hints(timeout=120)
+        entries = [c.c for c in srv.registrations[cid].hints[0].entries]
+    finally:
+        srv.close()
+    assert saved["regs"][(d, cid)][1] == seed
+    srv2 = PirServer(params, db, d)
+    try:
+        assert [c.c for c in srv2.registrations[cid].hints[0].entries] == entries
+    finally:
+        srv2.close()
