@@ -856,9 +856,33 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
         raise KeyError("no hint for this query index and database version")
     if mode not in (SEPARATE, COMBINED):
         raise ValueError("unknown response mode")
+    out = _wire_rows(state, reg.pk.m, mode, ck_bytes, qu, stored, stream)
+    if mode == COMBINED:
+        counters.bump("add", lay.groups)
+        counters.bump("group_mult", lay.groups)
+    return out
+
+
+def answer_wire(state: ServerGlobalState, m: int, ck_bytes, qu, stream=None,
+                on_device: bool = False):
+    """t (d1' x lm u32 limb rows) of one query on fixed-width wire fields,
+    without a stored-hint check: the per-shard answer of a row-sharded server
+    (shard.py), whose hints live on the answering rank. on_device=True
+    returns the device rows (int32 view, valid until the next answer on this
+    thread) instead of a host copy."""
+    lay = state.layout
+    ck_bytes = np.asarray(ck_bytes)
+    qu = np.asarray(qu)
+    if ck_bytes.ndim != 2 or ck_bytes.shape[0] != lay.n or qu.shape != (lay.d0,):
+        raise ValueError("query dimensions do not match the parameters")
+    return _wire_rows(state, m, SEPARATE, ck_bytes, qu, None, stream, on_device)
+
+
+def _wire_rows(state, m, mode, ck_bytes, qu, stored, stream, on_device=False):
+    lay = state.layout
     dev = state.device
     stream = stream or torch.cuda.current_stream(dev)
-    kctx = key_ctx(reg.pk.m, dev)
+    kctx = key_ctx(m, dev)
     w = ck_bytes.shape[1]
     if w > 4 * kctx.lm:
         raise ValueError("ck_o field wider than the modulus")
@@ -875,6 +899,9 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
         if mode == COMBINED:
             t_dev = device.combine(t_dev, _stored_device(stored, kctx, dev, stream), kctx,
                                    stream=stream)
+        if on_device:
+            stream.synchronize()
+            return t_dev[: lay.groups]
         out = _d2h_u32(t_dev, "t", stream)
     else:
         side = plan.side
@@ -892,6 +919,9 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
             plan._ck_w = w
         hc[:, :w] = ck_bytes
         plan.launch("w_g2t", side)
+        if on_device:
+            side.synchronize()
+            return plan.t[: lay.groups]
         if mode == COMBINED:
             K = device.combine(plan.t, _stored_device(stored, kctx, dev, side), kctx, stream=side)
             device.d2h_async(plan.h_K, K, side)
@@ -901,9 +931,6 @@ def respond_wire(state: ServerGlobalState, reg, query_index: int, mode: str, ck_
             h_out = plan.h_t
         side.synchronize()
         out = h_out.numpy().view(np.uint32)
-    if mode == COMBINED:
-        counters.bump("add", lay.groups)
-        counters.bump("group_mult", lay.groups)
     return out
 
 

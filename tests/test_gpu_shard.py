@@ -81,3 +81,17 @@ def test_two_shards_on_device_match_single_process():
         p.join(timeout=120)
     assert ok
     assert all(p.exitcode == 0 for p in procs)
+
+
+def test_sharded_pirserver_full_api_on_device():
+    """ShardedPirServer with the real rank-local device path (DeviceShard: the
+    shard's ServerGlobalState, tensor-core / IMAD hints, respond on the
+    device) on two ranks sharing this box's GPU, gloo command channels:
+    register -> hint worker -> answer() and handle_frame() in both modes ->
+    update_database (1% of the rows, incremental per shard) -> regenerated
+    hints -> answers, all bit-exact against the single-process oracle and
+    decoding to the requested record (tests/test_shard_server_gloo.py's
+    driver with DeviceShard instead of the CPU oracle)."""
+    from test_shard_server_gloo import run_two_ranks
+    run_two_ranks(dict(d0=512, d1=700, n=64, bits=1024, sigma=1.0, local="device",
+                       rows=[0, 5, 63, 64, 699, 350, 351]), timeout=600)
