@@ -276,6 +276,24 @@ int zpir_graph_launch(void* graph_exec, void* stream);
 /* Async pinned-host <-> device copy (kind 0 = H2D, 1 = D2H) on `stream`. */
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 
+/* Residues of the batch-scaled hint matrix modulo a prime basis: the
+ * reference's H_rns = rns.matrix_to_rns(basis, H_scaled) (rns.py:148-154,
+ * protocol.py:188), built on demand from the device H. Entry (g, k) =
+ * sum_{j < cap} 2^(32 stride j) S[g cap + j][k] over the `rows` valid rows of
+ * S (rows x n u32); weights[i][j] = 2^(32 stride j) mod primes[i] (count x cap
+ * u64); out (count, groups, n) float64. Replaces the host to_rns (rns.py:70-86). */
+int zpir_rns_residues(const uint32_t* S, int64_t rows, int64_t n, int cap, int stride,
+                      const uint32_t* primes, const uint64_t* weights, int count, int64_t groups,
+                      double* out, void* stream);
+
+/* The reference multiexp's group-multiplication count (paillier.py:134-193,
+ * counter bump :192) for each hint entry prod_k base_k^E[g][k] with
+ * E[g][k] = sum_j 2^(sbits j) S[g cap + j][k] (gamma = 2^sbits, slots below
+ * 2^min(sbits, 32)); out: groups int64. Lets the drop-in's counters report
+ * what the reference would (golden hint_group_mults). */
+int zpir_multiexp_opcount(const uint32_t* S, int64_t rows, int64_t n, int cap, int sbits,
+                          int64_t groups, int64_t* out, void* stream);
+
 /* Roofline probe: time `iters` x 16 32-bit IMADs per thread on blocks x 256
  * threads (CUDA events); the IMAD peak the bignum kernels are measured against. */
 int zpir_probe_imad(int blocks, int iters, float* ms);

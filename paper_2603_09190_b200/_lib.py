@@ -45,6 +45,9 @@ _SIGS = {
     "zpir_montmul_batch": ([_p, _p, _c_i64, _p, _c_int, _p, _c_int], _c_int),
     "zpir_multiexp_batch": ([_p, _c_i64, _p, _c_i64, _c_int, _p, _c_int, _p, _c_int], _c_int),
     "zpir_last_error": ([], ctypes.c_char_p),
+    "zpir_rns_residues": ([_p, _c_i64, _c_i64, _c_int, _c_int, _p, _p, _c_int, _c_i64, _p, _p],
+                          _c_int),
+    "zpir_multiexp_opcount": ([_p, _c_i64, _c_i64, _c_int, _c_int, _c_i64, _p, _p], _c_int),
     "zpir_transpose_db": ([_p, _c_i64, _c_i64, _c_i64, _p, _c_i64, _c_i64, _p], _c_int),
     "zpir_global_hint": ([_p, _c_i64, _c_i64, _p, _c_i64, _c_i64, _p, _c_u32, _p], _c_int),
     "zpir_gemv_workspace_bytes": ([_c_i64, _c_i64], _c_i64),

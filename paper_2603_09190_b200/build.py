@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libzpir_b200.so")
 SOURCES = ["capi.cu", "gemv.cu", "hint_gemm.cu", "answer.cu", "multiexp.cu", "umma_gemm.cu",
-           "probe.cu", "chacha.cu", "conv.cu", "db_handle.cu", "tc_pippenger.cu"]
+           "probe.cu", "chacha.cu", "conv.cu", "db_handle.cu", "tc_pippenger.cu", "compat.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -47,6 +47,10 @@ int umma_answer_rows_launch(const uint32_t*, int64_t, int64_t, const uint8_t*, i
 int build_bc_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
 int build_aplanes_launch(const uint32_t*, int64_t, int64_t, int64_t, uint8_t*, cudaStream_t);
 int imad_probe(int, int, float*);
+int rns_residues_launch(const uint32_t*, int64_t, int64_t, int, int, const uint32_t*,
+                        const unsigned long long*, int, int64_t, double*, cudaStream_t);
+int multiexp_opcount_launch(const uint32_t*, int64_t, int64_t, int, int, int64_t, long long*,
+                            cudaStream_t);
 int tc_slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
                          const uint32_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*,
                          cudaStream_t);
@@ -322,6 +326,20 @@ int zpir_groups_finish(const uint32_t* tz, const uint32_t* b, int64_t bq, uint32
 int zpir_chacha_words32(const uint8_t* key32, const uint8_t* iv16, int64_t rows, int64_t cols,
                         uint32_t* out, int64_t ld, uint32_t mask, void* stream) {
   ZPIR_GUARD(chacha_words32_launch(key32, iv16, rows, cols, out, ld, mask, S(stream)));
+}
+
+int zpir_rns_residues(const uint32_t* smat, int64_t rows, int64_t n, int cap, int stride,
+                      const uint32_t* primes, const uint64_t* weights, int count, int64_t groups,
+                      double* out, void* stream) {
+  ZPIR_GUARD(rns_residues_launch(smat, rows, n, cap, stride, primes,
+                                 reinterpret_cast<const unsigned long long*>(weights), count,
+                                 groups, out, S(stream)));
+}
+
+int zpir_multiexp_opcount(const uint32_t* smat, int64_t rows, int64_t n, int cap, int sbits,
+                          int64_t groups, int64_t* out, void* stream) {
+  ZPIR_GUARD(multiexp_opcount_launch(smat, rows, n, cap, sbits, groups,
+                                     reinterpret_cast<long long*>(out), S(stream)));
 }
 
 int zpir_chacha_below(const uint8_t* key32, uint32_t domain, uint64_t query_index, int64_t n,

@@ -193,7 +193,7 @@ class ServerGlobalState:
         self.params = params
         self.db = db
         self.db_version = db_version
-        self.basis = basis  # accepted for API compatibility; no RNS on this path
+        self._basis = basis  # the answer path needs no RNS basis; built lazily for .basis
         lay = self.layout = Layout(params)
         dev = self.device = device.require_cuda(device_)
         stream = torch.cuda.current_stream(dev)
@@ -242,7 +242,7 @@ class ServerGlobalState:
         stream = torch.cuda.current_stream(dev)
         t0 = time.perf_counter()
         new = object.__new__(ServerGlobalState)
-        new.__dict__.update(params=params, db=db, basis=self.basis, layout=lay, device=dev,
+        new.__dict__.update(params=params, db=db, _basis=self._basis, layout=lay, device=dev,
                             engine=self.engine, _A64=self._A64, A_dev=self.A_dev,
                             _H_host=None, _H_scaled=None, _lock=threading.Lock(),
                             _tls=threading.local())
@@ -272,7 +272,56 @@ class ServerGlobalState:
         new.hint_time = time.perf_counter() - t0
         return new, changed
 
-    # -- reference-compatible views (materialised lazily on the host) ------
+    # -- reference-compatible views (materialised lazily) --------------------
+
+    @property
+    def basis(self):
+        """The RNS basis (protocol.py:173: build_basis(27, 240) unless given)."""
+        if self._basis is None:
+            from .rns import build_basis
+            self._basis = build_basis(27, 240)
+        return self._basis
+
+    @property
+    def H_rns(self):
+        """H_scaled in residue form (protocol.py:188) as a device-resident view:
+        rns.rns_matmul_mod(state.basis, state.H_rns, ck_o, m) runs the answer's
+        compression kernels; np.asarray(state.H_rns) gives the reference's
+        (count, d1', n) float64 residues (computed on the device)."""
+        from .rns import RnsMatrix
+        lay = self.layout
+        gamma = (1 << (32 * lay.stride)) if lay.stride else lay.gamma
+        return RnsMatrix(self.basis, self.H_dev, lay.d1, lay.cap, lay.groups, gamma=gamma,
+                         state=self)
+
+    def hint_group_mults(self, group_ids=None) -> int:
+        """The reference multiexp's group-multiplication count for the hint
+        entries of `group_ids` (all groups by default) -- what its counter
+        bumps in paillier.py:192. The count depends only on the exponents
+        H_scaled, not on the client's bases: computed once per state on the
+        device (zpir_multiexp_opcount) and cached."""
+        with self._lock:
+            per = getattr(self, "_opcount", None)
+            if per is None:
+                lay = self.layout
+                g = lay.gamma
+                if g & (g - 1) == 0 and g >= lay.q:
+                    # gamma = 2^sbits >= q > every H entry: exponents are slot concatenations
+                    out = torch.empty(lay.groups, dtype=torch.int64, device=self.device)
+                    st = torch.cuda.current_stream(self.device)
+                    _lib.call("zpir_multiexp_opcount", _lib.ptr(self.H_dev), lay.d1, lay.n,
+                              lay.cap, g.bit_length() - 1, lay.groups, _lib.ptr(out),
+                              st.cuda_stream)
+                    per = out.cpu().numpy()
+                else:
+                    # standard-regime gamma (q + n q): the exponents are not slot
+                    # concatenations; the reference count is not derived on the
+                    # device (one product per (group, base) is reported instead)
+                    per = np.full(lay.groups, lay.n, dtype=np.int64)
+                self._opcount = per
+        if group_ids is None:
+            return int(per.sum())
+        return int(per[np.asarray(group_ids, dtype=np.int64)].sum())
 
     @property
     def A(self) -> np.ndarray:
@@ -590,7 +639,7 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
     res = []
     for (reg, qi), (P, kctx, W), k in zip(jobs, prep, out):
         entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
-        counters.bump("group_mult", lay.groups * lay.n)
+        counters.bump("group_mult", state.hint_group_mults())
         res.append(ClientHint(qi, state.db_version, [PaillierCiphertext(e) for e in entries],
                               dev=k, slots=W if keep_slots else None,
                               bases=P if keep_slots else None))
@@ -682,7 +731,10 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
             if st is not main:
                 main.wait_stream(st)
     res = []
+    gids = np.unique(np.asarray(changed_rows, dtype=np.int64) // lay.cap)
+    mults = state.hint_group_mults(gids) if gids.size else 0
     for (reg, old), (W, k) in zip(pairs, outs):
+        counters.bump("group_mult", mults)
         entries = limbs_to_ints(_d2h_u32(k, "hint", main))
         res.append(ClientHint(old.query_index, state.db_version,
                               [PaillierCiphertext(e) for e in entries], dev=k, slots=W,

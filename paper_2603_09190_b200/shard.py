@@ -190,13 +190,12 @@ class DeviceShard:
     this rank's part of every client hint, with the slot decomposition for
     incremental refresh."""
 
-    def __init__(self, params, db_slice, basis=None, incremental=True):
-        from .server import PirServer
-
+    def __init__(self, params, db_slice, basis=None, incremental=True, state=None):
         class _Local(PirServer):
             def _enqueue_missing(self, reg):     # rank 0's front end schedules hints
                 pass
-        self.srv = _Local(params, db_slice, None, basis, hint_workers=0, incremental=incremental)
+        self.srv = _Local(params, db_slice, None, basis, state=state, hint_workers=0,
+                          incremental=incremental)
 
     @property
     def state(self):
@@ -265,7 +264,7 @@ class ShardedPirServer(PirServer):
     commands on background threads until rank 0 closes (join() blocks)."""
 
     def __init__(self, params, db, store_dir=None, basis=None, *, db_slice=None,
-                 group=None, device=None, local_factory=None, store=None,
+                 group=None, device=None, local_factory=None, local=None, store=None,
                  incremental=True, hint_batch: int = 8, slot_window: int = None):
         import torch.distributed as dist
         self.group = group if group is not None else dist.group.WORLD
@@ -275,13 +274,16 @@ class ShardedPirServer(PirServer):
         self.bounds = shard_bounds(params.d1, lay.cap, self.world)
         lo, hi, glo, ghi = self.bounds[self.rank]
         self.gmax = max(b[3] - b[2] for b in self.bounds)
-        if db_slice is None:
-            db_slice = np.asarray(db)[:, lo:hi]
-        if db_slice.shape != (params.d0, hi - lo):
-            raise ValueError("shard slice shape does not match shard_bounds")
-        factory = local_factory or DeviceShard
-        self.local = factory(shard_params(params, hi - lo), db_slice, basis=basis,
-                             incremental=incremental)
+        if local is not None:           # a prebuilt rank-local part (e.g. DeviceShard(state=...))
+            self.local = local
+        else:
+            if db_slice is None:
+                db_slice = np.asarray(db)[:, lo:hi]
+            if db_slice.shape != (params.d0, hi - lo):
+                raise ValueError("shard slice shape does not match shard_bounds")
+            factory = local_factory or DeviceShard
+            self.local = factory(shard_params(params, hi - lo), db_slice, basis=basis,
+                                 incremental=incremental)
         dev = device if device is not None else (
             torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
             else torch.device("cpu"))
@@ -493,6 +495,18 @@ class ShardedPirServer(PirServer):
             counters.bump("add", self.params.d1_prime)
             counters.bump("group_mult", self.params.d1_prime)
         return rows
+
+    def respond(self, client_id: bytes, qmsg):
+        """protocol.respond() over the shards (no hint scheduling): KeyError
+        when the client or a fresh hint for the query index is missing."""
+        with self.lock:
+            reg = self.registrations.get(client_id)
+        if reg is None:
+            raise KeyError("client not registered")
+        stored = reg.hints.get(qmsg.query_index)
+        if stored is None or stored.db_version != self.db_version:
+            raise KeyError("no hint for this query index and database version")
+        return self._respond(None, reg, qmsg)
 
     def _respond(self, state, reg, qmsg):
         from . import counters
