@@ -55,6 +55,9 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-rows", type=int, default=0,
                     help="reference arm: serve only this many DB rows (0 = the whole config)")
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="process-group backend for N > 1 (gloo only to exercise the multi-rank "
+                         "code path with several ranks on one GPU; never for numbers)")
     ap.add_argument("--no-single-thread", action="store_true",
                     help="reference arm: skip the single-thread figure")
     ap.add_argument("--e2e-steps", type=int, default=50)
@@ -360,12 +363,16 @@ def _cpu_model():
 def run_b200(args):
     import torch
     rank, world, local = _dist_env()
+    local %= max(1, torch.cuda.device_count())     # (gloo code-path runs: ranks share a GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     import paper_2603_09190_b200 as z
     from paper_2603_09190_b200 import _lib, build as zb
     from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
@@ -471,24 +478,42 @@ def run_b200(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, gemv_ms, comp_ms, gemv_step_ms = t.tolist()
 
-    # e2e through the public API (host buffers, H2D/D2H inside)
+    # e2e through the public API (host buffers, H2D/D2H inside). N > 1: the
+    # sharded server -- rank 0 receives the query, broadcasts qu0 + ck_o, every
+    # rank answers its shard, the t rows are gathered to rank 0 (shard.py)
     qmsg = z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck_o, qu)
-    for _ in range(3):
-        z.respond(st, reg, qmsg)
-    e2e_times = []
-    for _ in range(args.e2e_steps):
-        if world > 1:
-            dist.barrier()
-        t1 = time.perf_counter()
-        resp = z.respond(st, reg, qmsg)
-        if world > 1:
-            tl = torch.from_numpy(ints_to_limbs(resp.t, kctx.lm).view(np.int32)).to(dev)
-            from paper_2603_09190_b200.shard import gather_groups
-            full = gather_groups(tl, bounds, rank)
-            full.cpu()
-        e2e_times.append(time.perf_counter() - t1)
-    e2e_s = statistics.mean(e2e_times)
-    if world > 1:
+    api = "paper_2603_09190_b200.respond()"
+    if world == 1:
+        for _ in range(3):
+            z.respond(st, reg, qmsg)
+        e2e_times = []
+        for _ in range(args.e2e_steps):
+            t1 = time.perf_counter()
+            z.respond(st, reg, qmsg)
+            e2e_times.append(time.perf_counter() - t1)
+        e2e_s = statistics.mean(e2e_times)
+    else:
+        from paper_2603_09190_b200.shard import DeviceShard, ShardedPirServer
+        from paper_2603_09190_b200.shard import shard_params
+        api = "ShardedPirServer.respond() on rank 0 (broadcast, per-shard answer, NCCL gather)"
+        local = DeviceShard(shard_params(params, hi - lo), None, state=st)
+        sps = ShardedPirServer(params, None, local=local, hint_batch=1)
+        if rank == 0:
+            cid = sps.register(pk, reg.seed)
+            sps.wait_for_hints(timeout=600)
+            for _ in range(3):
+                sps.respond(cid, qmsg)
+            e2e_times = []
+            for _ in range(args.e2e_steps):
+                t1 = time.perf_counter()
+                sps.respond(cid, qmsg)
+                e2e_times.append(time.perf_counter() - t1)
+            e2e_s = statistics.mean(e2e_times)
+            sps.close()
+        else:
+            sps.join()
+            sps.close()
+            e2e_s = 0.0
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = t.item()
@@ -599,7 +624,7 @@ def run_b200(args):
                                             f"{plan.ctas} SMs, then group stage; CUDA graph"},
             "e2e": {"value": db_bytes_total / e2e_s / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond()"},
+                    "ms_per_step": e2e_s * 1e3, "api": api},
             "clocks": clk,
             **extra_e2e,
             "setup_s": setup_s, "hint_s_per_client": hint_s,

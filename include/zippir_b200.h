@@ -273,6 +273,11 @@ int zpir_stream_wait_event(void* stream, void* event);
  * the low-overhead replay respond() uses. */
 int zpir_graph_launch(void* graph_exec, void* stream);
 
+/* The device address of pinned host memory (cudaHostGetDevicePointer); the
+ * zero-copy answer graphs pass host buffers to kernels only where it equals
+ * the host address (UVA), else they take the copy-node path. */
+int zpir_host_device_pointer(void* host, void** dev);
+
 /* Async pinned-host <-> device copy (kind 0 = H2D, 1 = D2H) on `stream`. */
 int zpir_memcpy_async(void* dst, const void* src, int64_t bytes, int kind, void* stream);
 

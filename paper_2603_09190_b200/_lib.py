@@ -45,6 +45,7 @@ _SIGS = {
     "zpir_montmul_batch": ([_p, _p, _c_i64, _p, _c_int, _p, _c_int], _c_int),
     "zpir_multiexp_batch": ([_p, _c_i64, _p, _c_i64, _c_int, _p, _c_int, _p, _c_int], _c_int),
     "zpir_last_error": ([], ctypes.c_char_p),
+    "zpir_host_device_pointer": ([_p, ctypes.POINTER(_p)], _c_int),
     "zpir_rns_residues": ([_p, _c_i64, _c_i64, _c_int, _c_int, _p, _p, _c_int, _c_i64, _p, _p],
                           _c_int),
     "zpir_multiexp_opcount": ([_p, _c_i64, _c_i64, _c_int, _c_int, _c_i64, _p, _p], _c_int),

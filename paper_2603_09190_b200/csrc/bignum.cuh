@@ -186,8 +186,11 @@ __device__ __forceinline__ void mac_row(uint32_t (&t)[LPL], uint32_t& s0, uint32
 }
 
 // r = a * b * R^-1 mod N, canonical. Requires a < R, b < N (then T < 2N).
-// r may alias a or b.
-template <int LPL>
+// r may alias a or b. UNR unrolls the limb-broadcast loop: 1 for the
+// IMAD-throughput-bound kernels; 4 for latency-bound callers with few warps per
+// SM (slot_combine's 2016-deep Horner chain per group), so the independent
+// a-limb broadcasts of later steps overlap the u-chain.
+template <int LPL, int UNR = 1>
 __device__ __forceinline__ void mont_mul(uint32_t (&r)[LPL], const uint32_t (&a)[LPL],
                                          const uint32_t (&b)[LPL], const uint32_t (&n)[LPL],
                                          uint32_t np, int lane) {
@@ -195,57 +198,7 @@ __device__ __forceinline__ void mont_mul(uint32_t (&r)[LPL], const uint32_t (&a)
 #pragma unroll
   for (int i = 0; i < LPL; ++i) t[i] = 0;
   uint32_t s0 = 0, s1 = 0;
-#pragma unroll 1
-  for (int src = 0; src < 32; ++src) {
-#pragma unroll
-    for (int rr = 0; rr < LPL; ++rr) {
-      const uint32_t ai = __shfl_sync(ZPIR_FULL, a[rr], src);
-      mac_row(t, s0, s1, ai, b);
-      const uint32_t u = __shfl_sync(ZPIR_FULL, t[0] * np, 0);
-      mac_row(t, s0, s1, u, n);
-      uint32_t nx = __shfl_down_sync(ZPIR_FULL, t[0], 1);
-      nx = (lane == 31) ? 0u : nx;
-#pragma unroll
-      for (int k = 0; k < LPL - 1; ++k) t[k] = t[k + 1];
-      const uint64_t z = (uint64_t)nx + s0;
-      t[LPL - 1] = (uint32_t)z;
-      s0 = s1 + (uint32_t)(z >> 32);
-      s1 = 0;
-    }
-  }
-  // resolve the pending spills: lane l owes s0 to lane l+1's lowest limb
-  uint32_t sp = __shfl_up_sync(ZPIR_FULL, s0, 1);
-  sp = (lane == 0) ? 0u : sp;
-  uint64_t c = sp;
-#pragma unroll
-  for (int i = 0; i < LPL; ++i) {
-    c += t[i];
-    t[i] = (uint32_t)c;
-    c >>= 32;
-  }
-  const bool g = c != 0;
-  const bool p = lane_all(t, 0xffffffffu);
-  uint32_t cout;
-  const uint32_t cin = lane_carry_in(g, p, lane, &cout);
-  lane_inc(t, cin);
-  const uint32_t top = __shfl_sync(ZPIR_FULL, s0, 31) + cout;
-  big_cond_sub(t, top, n, lane);
-#pragma unroll
-  for (int i = 0; i < LPL; ++i) r[i] = t[i];
-}
-
-// mont_mul with the limb-broadcast loop unrolled 4x: for latency-bound callers
-// with few warps per SM (slot_combine's 2016-deep Horner chain per group), so
-// the independent a-limb broadcasts of later steps overlap the u-chain.
-template <int LPL>
-__device__ __forceinline__ void mont_mul_unrolled(uint32_t (&r)[LPL], const uint32_t (&a)[LPL],
-                                         const uint32_t (&b)[LPL], const uint32_t (&n)[LPL],
-                                         uint32_t np, int lane) {
-  uint32_t t[LPL];
-#pragma unroll
-  for (int i = 0; i < LPL; ++i) t[i] = 0;
-  uint32_t s0 = 0, s1 = 0;
-#pragma unroll 4
+#pragma unroll UNR
   for (int src = 0; src < 32; ++src) {
 #pragma unroll
     for (int rr = 0; rr < LPL; ++rr) {

@@ -328,6 +328,20 @@ int zpir_chacha_words32(const uint8_t* key32, const uint8_t* iv16, int64_t rows,
   ZPIR_GUARD(chacha_words32_launch(key32, iv16, rows, cols, out, ld, mask, S(stream)));
 }
 
+int zpir_host_device_pointer(void* host, void** dev) {
+  if (!host || !dev) {
+    set_error("zpir_host_device_pointer: null argument");
+    return kErrInput;
+  }
+  const cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
 int zpir_rns_residues(const uint32_t* smat, int64_t rows, int64_t n, int cap, int stride,
                       const uint32_t* primes, const uint64_t* weights, int count, int64_t groups,
                       double* out, void* stream) {

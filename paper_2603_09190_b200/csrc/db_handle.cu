@@ -272,30 +272,44 @@ struct Key {
 // host until each source is staged and so delays the next launch).
 struct HostBuf {
   void* p = nullptr;
+  void* dev = nullptr;   // device alias of a mapped buffer (kernels read / write it in place)
   size_t bytes = 0;
   HostBuf() = default;
   HostBuf(const HostBuf&) = delete;
   HostBuf& operator=(const HostBuf&) = delete;
   ~HostBuf() { if (p) cudaFreeHost(p); }
-  int alloc(size_t n) {
-    if (p && bytes >= n) return kOk;
+  int alloc(size_t n, bool mapped = false) {
+    if (p && bytes >= n && (!mapped || dev)) return kOk;
     if (p) cudaFreeHost(p);
-    p = nullptr;
+    p = dev = nullptr;
     bytes = 0;
-    if (cudaHostAlloc(&p, n ? n : 16, cudaHostAllocDefault) != cudaSuccess) {
+    if (cudaHostAlloc(&p, n ? n : 16, mapped ? cudaHostAllocMapped : cudaHostAllocDefault) !=
+        cudaSuccess) {
       cudaGetLastError();
       set_error("pinned host allocation of %zu bytes failed", n);
       return kErrCuda;
     }
     bytes = n;
+    std::memset(p, 0, n);
+    // the device address of the mapping (cudaHostGetDevicePointer: valid also
+    // where host and device pointers differ)
+    if (mapped && cudaHostGetDevicePointer(&dev, p, 0) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("cudaHostGetDevicePointer failed");
+      return kErrCuda;
+    }
     return kOk;
   }
   template <class T> T* as() const { return static_cast<T*>(p); }
+  template <class T> T* dev_as() const { return static_cast<T*>(dev); }
 };
 
 struct Work {
-  DevBuf qu, planes, b, cko, bc, z, t, k, K, w, gemv_ws;
+  DevBuf qu, planes, b, cko, bc, z, t, tz, k, K, w, gemv_ws;
   HostBuf h_qu, h_cko, h_out;  // staging of one query's qu / ck_o and its result rows
+  HostBuf m_qu, m_cko;         // mapped: read in place by the query-planes / operand kernels
+  cudaEvent_t ev_gemv = nullptr;
+  ~Work() { if (ev_gemv) cudaEventDestroy(ev_gemv); }
 };
 
 }  // namespace
@@ -318,7 +332,8 @@ struct zpir_db {
 namespace zpir {
 namespace {
 
-constexpr int kCompressCtas = 36;  // measured SM split
+constexpr int kCompressCtas = 36;     // measured SM split
+constexpr int kCompressCtasE2E = 44;  // host-input answers: the compression starts later
 
 int umma_nb(int lm) { return lm == 32 ? 144 : lm == 64 ? 272 : lm == 96 ? 400 : 0; }
 
@@ -446,9 +461,13 @@ int get_work(zpir_db* h, int lm, Work** out) {
   ZPIR_TRY(w->K.alloc((size_t)h->groups * l2 * 4));
   ZPIR_TRY(w->gemv_ws.alloc((size_t)zpir_gemv_workspace_bytes(h->ld, 1)));
   if (h->stride == 0) ZPIR_TRY(w->w.alloc((size_t)h->prm.d1 * lm * 4));
+  ZPIR_TRY(w->tz.alloc((size_t)h->groups * l2 * 4));
   ZPIR_TRY(w->h_qu.alloc((size_t)h->prm.d0 * 4));
   ZPIR_TRY(w->h_cko.alloc((size_t)n * lm * 4));
   ZPIR_TRY(w->h_out.alloc((size_t)h->groups * l2 * 4));
+  ZPIR_TRY(w->m_qu.alloc((size_t)h->ld * 4, true));      // tail beyond d0 stays zero
+  ZPIR_TRY(w->m_cko.alloc((size_t)n * lm * 4, true));
+  ZPIR_TRY(cu(cudaEventCreateWithFlags(&w->ev_gemv, cudaEventDisableTiming), "event"));
   *out = w.get();
   h->work.emplace(lm, std::move(w));
   return kOk;
@@ -535,13 +554,23 @@ int upload_staged(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     const size_t n = bytes - off < kChunk ? bytes - off : kChunk;
     ZPIR_TRY(cu(cudaEventSynchronize(ev[k]), "event synchronize"));  // stage k is free
     char* st = stage[k].as<char>();
-    std::vector<std::thread> th;
-    for (int t = 1; t < nt; ++t) {
-      const size_t a = n * t / nt, b = n * (t + 1) / nt;
-      th.emplace_back([=] { std::memcpy(st + a, in + off + a, b - a); });
+    {
+      // the helper threads are joined by the guard on every exit path (a
+      // throwing emplace_back must not destroy joinable threads)
+      struct Joiner {
+        std::vector<std::thread> th;
+        ~Joiner() {
+          for (auto& x : th)
+            if (x.joinable()) x.join();
+        }
+      } jn;
+      jn.th.reserve(nt);
+      for (int t = 1; t < nt; ++t) {
+        const size_t a = n * t / nt, b = n * (t + 1) / nt;
+        jn.th.emplace_back([=] { std::memcpy(st + a, in + off + a, b - a); });
+      }
+      std::memcpy(st, in + off, n / nt);
     }
-    std::memcpy(st, in + off, n / nt);
-    for (auto& x : th) x.join();
     ZPIR_TRY(cu(cudaMemcpyAsync(out + off, st, n, cudaMemcpyHostToDevice, s), "db H2D"));
     ZPIR_TRY(cu(cudaEventRecord(ev[k], s), "event"));
   }
@@ -615,31 +644,85 @@ int stage_query_and_gemv(zpir_db* h, Work* w, const uint32_t* qu, int ctas, cuda
                    w->b.as<uint32_t>(), h->qmask, w->gemv_ws.p, s);
 }
 
-// The answer t (groups x t_ld limbs) into w->t; returns with work queued on main.
-int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko, int t_ld) {
+// host rows of src_limbs -> rows of dst_ld limbs in host memory (zero-extended;
+// widths checked by rows_fit first)
+void rows_into(uint32_t* dst, int dst_ld, const uint32_t* src, int src_limbs, int64_t rows) {
+  const int w = src_limbs < dst_ld ? src_limbs : dst_ld;
+  if (w == dst_ld && src_limbs == dst_ld) {
+    std::memcpy(dst, src, (size_t)rows * dst_ld * 4);
+    return;
+  }
+  for (int64_t r = 0; r < rows; ++r) {
+    std::memcpy(dst + r * dst_ld, src + r * src_limbs, (size_t)w * 4);
+    if (w < dst_ld) std::memset(dst + r * dst_ld + w, 0, (size_t)(dst_ld - w) * 4);
+  }
+}
+
+// The answer t (groups x t_ld limbs) into w->t; *res is set to the stream the
+// result is complete on (work still queued).
+//
+// tcgen05 path, as respond()'s host-input plan (protocol.py / plan.py):
+//   main : query planes (reading qu in place from mapped pinned memory) ->
+//          GEMV on SMs - kCompressCtasE2E
+//   host : ck_o rows copied into mapped pinned memory while the GEMV runs
+//   side : compression operand (reading ck_o in place) -> compression GEMM on
+//          kCompressCtasE2E SMs -> Montgomery group stage tz = Z_g mod m ->
+//          (wait for the GEMV) -> finish t = tz + B_g mod m
+int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko, int t_ld,
+           cudaStream_t* res) {
   const int lm = k->lm, L = k->L;
   const int64_t n = h->prm.n;
+  const int64_t d1 = h->prm.d1;
   cudaStream_t s = h->main;
+  *res = s;
   ZPIR_TRY(rows_fit(cko, L, lm, n));
   const int nb = umma_nb(lm);
-  if (h->prm.engine == 0 && nb && n % 4 == 0) {  // TMA rows of 4n bytes: 16-byte pitch
-    // qu first: the GEMV (on SMs - kCompressCtas) runs while ck_o is staged on
-    // the host; then the compression on kCompressCtas SMs (side stream)
+  if (h->prm.engine == 0 && nb && n % 4 == 0 && use_umma_gemv(h)) {
+    const bool split = h->stride && h->stride * h->prm.cap < lm && k->nchunks <= 3;
+    const int ctas = kCompressCtasE2E;
+    std::memcpy(w->m_qu.p, qu, (size_t)h->prm.d0 * 4);
+    ZPIR_TRY(cu(cudaEventRecord(h->ev_in, s), "event"));
+    ZPIR_TRY(zpir_query_planes(w->m_qu.dev_as<uint32_t>(), h->ld, 1, w->planes.as<uint8_t>(), 16,
+                               s));
+    ZPIR_TRY(zpir_umma_gemv(h->dbt.as<uint8_t>(), h->rows, h->ld, w->planes.as<uint8_t>(), 1,
+                            w->b.as<uint32_t>(), h->sms - ctas, s));
+    ZPIR_TRY(cu(cudaEventRecord(w->ev_gemv, s), "event"));
+    rows_into(w->m_cko.as<uint32_t>(), lm, cko, L, n);        // overlaps the GEMV
+    cudaStream_t c = h->side;
+    ZPIR_TRY(cu(cudaStreamWaitEvent(c, h->ev_in, 0), "event wait"));
+    const uint32_t* ck_dev = w->m_cko.dev_as<uint32_t>();
+    if (planar(h, lm)) {
+      ZPIR_TRY(zpir_build_bcp(ck_dev, n, lm, 1, w->bc.as<uint8_t>(), c));
+      ZPIR_TRY(zpir_umma_answer_rows_planar(h->Hp.as<uint8_t>(), h->rows, n, w->bc.as<uint8_t>(),
+                                            lm, 1, lm + 4, w->z.as<uint32_t>(), ctas, c));
+    } else {
+      ZPIR_TRY(zpir_build_bc(ck_dev, n, lm, nb, w->bc.as<uint8_t>(), c));
+      ZPIR_TRY(zpir_umma_answer_rows(h->H.as<uint32_t>(), h->rows, n, w->bc.as<uint8_t>(), nb,
+                                     nullptr, h->qmask, lm + 4, w->z.as<uint32_t>(), ctas, c));
+    }
+    if (split) {
+      ZPIR_TRY(zpir_groups_z(w->z.as<uint32_t>(), 0, d1, h->prm.cap, h->groups, lm,
+                             k->m.as<uint32_t>(), k->npd.as<uint32_t>(), k->rpow.as<uint32_t>(),
+                             k->nchunks, k->f0.as<uint8_t>(), w->tz.as<uint32_t>(), t_ld, 1,
+                             h->stride, c));
+      ZPIR_TRY(cu(cudaStreamWaitEvent(c, w->ev_gemv, 0), "event wait"));
+      ZPIR_TRY(zpir_groups_finish(w->tz.as<uint32_t>(), w->b.as<uint32_t>(), 0, h->qmask, d1,
+                                  h->prm.cap, h->groups, lm, k->m.as<uint32_t>(),
+                                  w->t.as<uint32_t>(), t_ld, 1, h->stride, c));
+      *res = c;
+      return kOk;
+    }
+    ZPIR_TRY(cu(cudaEventRecord(h->ev_comp, c), "event"));
+    ZPIR_TRY(cu(cudaStreamWaitEvent(s, h->ev_comp, 0), "event wait"));
+  } else if (h->prm.engine == 0 && nb && n % 4 == 0) {
     ZPIR_TRY(cu(cudaEventRecord(h->ev_in, s), "event"));
     ZPIR_TRY(stage_query_and_gemv(h, w, qu, h->sms - kCompressCtas, s));
     ZPIR_TRY(cu(cudaStreamWaitEvent(h->side, h->ev_in, 0), "event wait"));
     ZPIR_TRY(h2d_rows_staged(w->cko.p, lm, cko, L, n, w->h_cko, h->side));
-    if (planar(h, lm)) {
-      ZPIR_TRY(zpir_build_bcp(w->cko.as<uint32_t>(), n, lm, 1, w->bc.as<uint8_t>(), h->side));
-      ZPIR_TRY(zpir_umma_answer_rows_planar(h->Hp.as<uint8_t>(), h->rows, n, w->bc.as<uint8_t>(),
-                                            lm, 1, lm + 4, w->z.as<uint32_t>(), kCompressCtas,
-                                            h->side));
-    } else {
-      ZPIR_TRY(zpir_build_bc(w->cko.as<uint32_t>(), n, lm, nb, w->bc.as<uint8_t>(), h->side));
-      ZPIR_TRY(zpir_umma_answer_rows(h->H.as<uint32_t>(), h->rows, n, w->bc.as<uint8_t>(), nb,
-                                     nullptr, h->qmask, lm + 4, w->z.as<uint32_t>(),
-                                     kCompressCtas, h->side));
-    }
+    ZPIR_TRY(zpir_build_bc(w->cko.as<uint32_t>(), n, lm, nb, w->bc.as<uint8_t>(), h->side));
+    ZPIR_TRY(zpir_umma_answer_rows(h->H.as<uint32_t>(), h->rows, n, w->bc.as<uint8_t>(), nb,
+                                   nullptr, h->qmask, lm + 4, w->z.as<uint32_t>(), kCompressCtas,
+                                   h->side));
     ZPIR_TRY(cu(cudaEventRecord(h->ev_comp, h->side), "event"));
     ZPIR_TRY(cu(cudaStreamWaitEvent(s, h->ev_comp, 0), "event wait"));
   } else {
@@ -648,7 +731,6 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
     ZPIR_TRY(zpir_answer_rows(h->H.as<uint32_t>(), h->rows, n, nullptr, h->qmask,
                               w->cko.as<uint32_t>(), lm, w->z.as<uint32_t>(), s));
   }
-  const int64_t d1 = h->prm.d1;
   if (h->stride)
     return zpir_answer_groups_batch(w->z.as<uint32_t>(), 0, w->b.as<uint32_t>(), 0, h->qmask, d1,
                                     h->prm.cap, h->groups, lm, k->m.as<uint32_t>(),
@@ -1038,14 +1120,15 @@ static int db_answer(zpir_db* h, const uint32_t* qu, const uint32_t* cko, const 
   Work* w;
   ZPIR_TRY(get_work(h, k->lm, &w));
   const int t_ld = kin ? k->l2 : k->lm;
-  ZPIR_TRY(answer(h, k, w, qu, cko, t_ld));
-  if (!kin) return d2h_rows_staged(out, L, w->t.p, t_ld, h->groups, w->h_out, h->main);
+  cudaStream_t rs;
+  ZPIR_TRY(answer(h, k, w, qu, cko, t_ld, &rs));
+  if (!kin) return d2h_rows_staged(out, L, w->t.p, t_ld, h->groups, w->h_out, rs);
   const int l2 = k->l2;
-  ZPIR_TRY(h2d_rows(w->k.p, l2, kin, 2 * L, h->groups, h->main));
+  ZPIR_TRY(h2d_rows(w->k.p, l2, kin, 2 * L, h->groups, rs));
   ZPIR_TRY(zpir_combine(w->t.as<uint32_t>(), w->k.as<uint32_t>(), h->groups, l2,
                         k->m2.as<uint32_t>(), k->np_2, k->r2_2.as<uint32_t>(),
-                        k->mr.as<uint32_t>(), w->K.as<uint32_t>(), h->main));
-  return d2h_rows_staged(out, 2 * L, w->K.p, l2, h->groups, w->h_out, h->main);
+                        k->mr.as<uint32_t>(), w->K.as<uint32_t>(), rs));
+  return d2h_rows_staged(out, 2 * L, w->K.p, l2, h->groups, w->h_out, rs);
 }
 
 int zpir_db_answer(zpir_db* h, const uint32_t* qu, const uint32_t* ck_o, const uint32_t* m, int L,

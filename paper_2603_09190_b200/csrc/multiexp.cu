@@ -176,13 +176,15 @@ struct GammaExp {
   int nbits;
 };
 
-template <int LPL, bool UNR>
+template <int LPL>
 __global__ void __launch_bounds__(128)
 slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __restrict__ group_ids,
                     int64_t ngroups, const uint32_t* __restrict__ N, uint32_t np,
                     uint32_t* __restrict__ out, GammaExp gm) {
   constexpr int L = 32 * LPL;
-#define MM(...) (UNR ? mont_mul_unrolled<LPL>(__VA_ARGS__) : mont_mul<LPL>(__VA_ARGS__))
+// latency-bound (one warp per group, few groups): the 4x-unrolled CIOS is
+// 17.4 -> 15.1 ms for one client at 1 GiB (tools/slot_probe.py, bit-identical)
+#define MM(...) mont_mul<LPL, 4>(__VA_ARGS__)
   const int lane = threadIdx.x & 31;
   const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gi >= ngroups) return;
@@ -495,21 +497,9 @@ int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, in
   GammaExp gm{};
   for (int i = 0; i < (gamma_bits + 31) / 32; ++i) gm.w[i] = gamma[i];
   gm.nbits = gamma_bits;
-  // latency-bound (one warp per group, few groups): the unrolled CIOS is
-  // 17.4 -> 15.1 ms for one client at 1 GiB (tools/slot_probe.py, bit-identical);
-  // ZPIR_SLOT_UNROLL=0 selects the rolled loop
-  static int unr = -1;
-  if (unr < 0) {
-    const char* e = getenv("ZPIR_SLOT_UNROLL");
-    unr = e ? atoi(e) : 1;
-  }
   ZPIR_LPL_DISPATCH2(limbs / 32, {
-    if (unr)
-      slot_combine_kernel<LPL, true><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
-          W, cap, group_ids, ngroups, N, np, out, gm);
-    else
-      slot_combine_kernel<LPL, false><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
-          W, cap, group_ids, ngroups, N, np, out, gm);
+    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
+        W, cap, group_ids, ngroups, N, np, out, gm);
   });
   return check_launch("slot_combine");
 }

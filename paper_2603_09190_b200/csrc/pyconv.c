@@ -175,8 +175,8 @@ static PyObject* ints_from(PyObject* self, PyObject* args) {
 static PyObject* digits_into(PyObject* self, PyObject* args) {
   PyObject* seq;
   Py_buffer view;
-  Py_ssize_t ndig;
-  if (!PyArg_ParseTuple(args, "Ow*n", &seq, &view, &ndig)) return NULL;
+  Py_ssize_t ndig, maxbits = 0;   /* maxbits > 0: reject wider values (the limb width) */
+  if (!PyArg_ParseTuple(args, "Ow*n|n", &seq, &view, &ndig, &maxbits)) return NULL;
   PyObject* fast = PySequence_Fast(seq, "expected a sequence of ints");
   if (!fast) {
     PyBuffer_Release(&view);
@@ -205,6 +205,14 @@ static PyObject* digits_into(PyObject* self, PyObject* args) {
     if (nd > ndig) {
       PyErr_SetString(PyExc_ValueError, "integer wider than the limb width");
       goto fail;
+    }
+    if (maxbits > 0 && nd > 0) {
+      const uint32_t top = (uint32_t)L->long_value.ob_digit[nd - 1];
+      const Py_ssize_t bits = 30 * (nd - 1) + (32 - __builtin_clz(top));
+      if (bits > maxbits) {
+        PyErr_SetString(PyExc_ValueError, "integer wider than the limb width");
+        goto fail;
+      }
     }
     uint32_t* o = out + (size_t)i * ndig;
     if (nd) memcpy(o, L->long_value.ob_digit, (size_t)nd * 4);

@@ -23,12 +23,7 @@ import threading
 import numpy as np
 import torch
 
-# respond()'s host-input graphs read qu from and write t's digits to pinned,
-# device-mapped host buffers directly (no copy nodes); ZPIR_E2E_ZEROCOPY=0 copies
-ZERO_COPY = os.environ.get("ZPIR_E2E_ZEROCOPY", "1") != "0"
-ZERO_COPY_CK = os.environ.get("ZPIR_E2E_ZEROCOPY_CK", "1") != "0"
-
-from . import device
+from . import _lib, device
 
 USE_GRAPHS = os.environ.get("ZPIR_GRAPHS", "1") != "0"
 _capture_lock = threading.Lock()
@@ -97,6 +92,10 @@ class AnswerPlan:
         self.ev_gemv = torch.cuda.Event()
         self.ev_gemv.record(torch.cuda.current_stream(dev))
         self._exec = {}
+        # respond()'s host-input graphs read qu / ck_o's digits from and write
+        # t's digits to the pinned host buffers directly (no copy nodes) when
+        # the device address of each is its host address (UVA); else copies
+        self.zero_copy = all(_mapped_in_place(b) for b in (self.h_qu, self.h_ckd, self.h_td))
 
     # -- eager pieces (also what gets captured) -----------------------------
 
@@ -196,7 +195,7 @@ class AnswerPlan:
         elif which == "e2e_g1":
             # respond(), graph 1 (main stream): query planes read straight from
             # the pinned (device-mapped) host qu -- no copy node -- then the GEMV
-            if ZERO_COPY:
+            if self.zero_copy:
                 device.query_planes(self.h_qu.view(1, -1), 16, stream, planes=self.planes)
                 device.umma_gemv(self.state.dbt, self.planes, 1, out=self.b, stream=stream,
                                  ctas=self.sms - self.ctas_e2e)
@@ -210,7 +209,7 @@ class AnswerPlan:
             # converts t to digits and copies it out, the others leave t in HBM
             if which == "w_g2t":
                 device.h2d_async(self.cko, self.h_cko, stream)
-            elif ZERO_COPY and ZERO_COPY_CK:     # digits read from pinned host memory
+            elif self.zero_copy:     # digits read from pinned host memory
                 device.digits_to_limbs(self.h_ckd, self.kctx.lm, self.cko, stream)
             else:
                 device.h2d_async(self.d_ckd, self.h_ckd, stream)
@@ -222,7 +221,7 @@ class AnswerPlan:
                 # t's digits written by the kernel straight into the pinned
                 # (device-mapped) host buffer: no copy node at the tail
                 self._finish(stream)
-                if ZERO_COPY:
+                if self.zero_copy:
                     device.limbs_to_digits(self.t, self.kctx.lm, self.h_td, stream)
                 else:
                     device.limbs_to_digits(self.t, self.kctx.lm, self.d_td, stream)
@@ -281,3 +280,14 @@ class AnswerPlan:
             self.graphs[which] = g
         with torch.cuda.stream(stream):
             g.replay()
+
+
+def _mapped_in_place(t) -> bool:
+    """The pinned host tensor's device alias is its own address."""
+    import ctypes
+    dev = ctypes.c_void_p()
+    try:
+        _lib.call("zpir_host_device_pointer", ctypes.c_void_p(t.data_ptr()), ctypes.byref(dev))
+    except _lib.ZpirError:
+        return False
+    return dev.value == t.data_ptr()

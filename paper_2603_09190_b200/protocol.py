@@ -793,7 +793,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
                 side.wait_stream(stream)     # the new key constants were copied on `stream`
             plan.launch("e2e_g1", stream)
             device.event_record(plan.ev_gemv, stream)
-            conv.digits_into(qmsg.ck_o, plan.np_ckd, plan.ndig_m)
+            conv.digits_into(qmsg.ck_o, plan.np_ckd, plan.ndig_m, 32 * kctx.lm)
             if mode == SEPARATE:
                 plan.launch("e2e_g2", side)
                 side.synchronize()
@@ -824,7 +824,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
                 events[1].record(stream)
             # meanwhile: ck_o digits (memcpy) -> side stream graph (compression
             # + Montgomery group stage on COMPRESS_CTAS SMs, concurrent with the GEMV)
-            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m, 32 * kctx.lm)
             side = plan.side
             side.wait_event(plan.ev_in)
             device.h2d_async(plan.d_ckd, plan.h_ckd, side)
@@ -835,7 +835,7 @@ def respond(state: ServerGlobalState, reg, qmsg, mode: str = None, timings=None,
             plan.run("gemv", stream)
             if events:
                 events[1].record(stream)
-            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m)
+            conv.digits_into(qmsg.ck_o, plan.h_ckd.numpy(), plan.ndig_m, 32 * kctx.lm)
             device.h2d_async(plan.d_ckd, plan.h_ckd, stream)
             plan.run("compress_digits", stream)
         else:
@@ -1108,7 +1108,7 @@ def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
         hi = min(nq, lo + sub)
         m = hi - lo
         for i in range(lo, hi):
-            conv.digits_into(qs[i].ck_o, cbuf[i * n:(i + 1) * n], nd1)
+            conv.digits_into(qs[i].ck_o, cbuf[i * n:(i + 1) * n], nd1, 32 * lm)
         dd = torch.empty((m * n, nd1), dtype=torch.int32, device=dev)
         device.h2d_async(dd, torch.from_numpy(cbuf[lo * n:hi * n]), stream)
         cd = torch.empty((m, n, lm), dtype=torch.int32, device=dev)

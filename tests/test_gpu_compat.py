@@ -95,3 +95,23 @@ def test_hint_counts_reference_group_mults(z, golden, name):
     assert [c.c for c in h.entries] == g.ints("k")
     assert mm.delta.group_mult == g.meta["hint_group_mults"]
     assert mm.delta.modexp == 0
+
+
+def test_cko_width_checked(z, golden):
+    """ck_o entries at or above 2^(32 lm) raise ValueError on every input path
+    (ADVICE r01); entries in [m, 2^(32 lm)) give the exact (H ck_o) mod m."""
+    g = golden("desk_reduced")
+    st = z.ServerGlobalState(g.params(z), g.db)
+    pk = z.PaillierPublicKey(g.m, g.m.bit_length())
+    reg = z.ClientRegistration(pk, g.seed, z.client_id_of(pk))
+    reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(1)] * g.groups)
+    ck = g.ints("ck_o")
+    lm = -(-g.m.bit_length() // 1024) * 32
+    wide = list(ck)
+    wide[3] = 1 << (32 * lm)
+    with pytest.raises(ValueError):
+        z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, wide, g.arr["qu0"]))
+    big = list(ck)
+    big[5] += g.m
+    r = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, big, g.arr["qu0"]))
+    assert r.t == g.ints("t")
