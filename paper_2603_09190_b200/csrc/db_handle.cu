@@ -678,7 +678,10 @@ int answer(zpir_db* h, Key* k, Work* w, const uint32_t* qu, const uint32_t* cko,
   ZPIR_TRY(rows_fit(cko, L, lm, n));
   const int nb = umma_nb(lm);
   if (h->prm.engine == 0 && nb && n % 4 == 0 && use_umma_gemv(h)) {
-    const bool split = h->stride && h->stride * h->prm.cap < lm && k->nchunks <= 3;
+    // the finish adds B_g < 2^(32 stride cap) with one conditional subtraction:
+    // exact when that bound is below m (always for keys of the params' size)
+    const bool split = h->stride && h->stride * h->prm.cap < lm && k->nchunks <= 3 &&
+                       32 * h->stride * h->prm.cap < k->bits;
     const int ctas = kCompressCtasE2E;
     std::memcpy(w->m_qu.p, qu, (size_t)h->prm.d0 * 4);
     ZPIR_TRY(cu(cudaEventRecord(h->ev_in, s), "event"));

@@ -441,8 +441,12 @@ class ServerGlobalState:
 
     def answer_plan(self, kctx, t_ld):
         """Per-thread captured plan for the tcgen05 path, or None."""
-        if not (self.engine == "umma" and kctx.lm in device.UMMA_NB and self.layout.n % 4 == 0
-                and self.layout.qmask == 0xFFFFFFFF and self.layout.stride == 1):
+        lay = self.layout
+        # the plan's finish adds B_g < 2^(32 cap) to tz mod m with one conditional
+        # subtraction: exact when 2^(32 cap) <= m (keys of the params' size)
+        if not (self.engine == "umma" and kctx.lm in device.UMMA_NB and lay.n % 4 == 0
+                and lay.qmask == 0xFFFFFFFF and lay.stride == 1
+                and 32 * lay.cap < kctx.m.bit_length()):
             return None
         plans = getattr(self._tls, "plans", None)
         if plans is None:

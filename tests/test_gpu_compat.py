@@ -115,3 +115,25 @@ def test_cko_width_checked(z, golden):
     big[5] += g.m
     r = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, big, g.arr["qu0"]))
     assert r.t == g.ints("t")
+
+
+def test_undersized_modulus_exact(z, golden):
+    """A modulus narrower than 32 * cap bits (respond() called directly, without
+    the server's key-size check): the capacity bound B_g < m no longer holds, the
+    answer must still equal the oracle (the captured plan's one-subtraction
+    finish is bypassed)."""
+    g = golden("desk_reduced")
+    st = z.ServerGlobalState(g.params(z), g.db)
+    rng = random.Random(5)
+    lw = g.lwe
+    A = ref.public_matrix(b"\x00" * 16, g.d0, lw["n"], lw["q"])
+    H = ref.global_hint(g.db, A, lw["q"])
+    for bits in (700, 950):
+        m = rng.getrandbits(bits) | (1 << (bits - 1)) | 1
+        pk = z.PaillierPublicKey(m, bits)
+        reg = z.ClientRegistration(pk, b"\x01" * 16, z.client_id_of(pk))
+        reg.hints[0] = z.ClientHint(0, 0, [z.PaillierCiphertext(1)] * g.groups)
+        ck = [rng.randrange(m) for _ in range(lw["n"])]
+        want = ref.answer_t(H, g.arr["b"], ck, m, g.cap, g.gamma, g.d1)
+        r = z.respond(st, reg, z.QueryMessage(reg.client_id, 0, z.SEPARATE, ck, g.arr["qu0"]))
+        assert r.t == want, bits
