@@ -794,10 +794,33 @@ def run_extra(args):
             z.respond_batch(st, [reg] * nq, qms)
             te.append(time.perf_counter() - t1)
         e2e_s = statistics.mean(te)
-        out["e2e"] = {"value": nq * D0 * D1 / e2e_s / 1e9, "unit": "GB/s",
-                      "ms_per_step": e2e_s * 1e3, "api": "paper_2603_09190_b200.respond_batch()",
+        out["e2e_ints"] = {"value": nq * D0 * D1 / e2e_s / 1e9, "unit": "GB/s",
+                           "ms_per_step": e2e_s * 1e3,
+                           "api": "paper_2603_09190_b200.respond_batch() (Python-int ck_o in, "
+                                  "Python-int t out: CPython int conversion dominates)",
+                           "h2d_bytes_per_step": nq * (4 * D0 + 4 * kctx.lm * N_LWE),
+                           "d2h_bytes_per_step": nq * 4 * kctx.lm * params.d1_prime}
+        # the same batch on wire fields (what PirServer's frame path holds): ck_o
+        # as (n, 256) LE byte rows, qu0 as u32, t limb rows out -- no Python ints
+        ckw = [np.ascontiguousarray(ints_to_limbs(q.ck_o, kctx.lm).view(np.uint8)
+                                    .reshape(N_LWE, 4 * kctx.lm)) for q in qms]
+        quw = [np.ascontiguousarray(q32[i, :D0]) for i in range(nq)]
+        args_w = ([reg] * nq, [0] * nq, [z.SEPARATE] * nq, ckw, quw)
+        for _ in range(3):
+            z.respond_batch_wire(st, *args_w)
+        tw = []
+        for _ in range(max(5, args.steps // 10)):
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            z.respond_batch_wire(st, *args_w)
+            tw.append(time.perf_counter() - t1)
+        ew = statistics.mean(tw)
+        out["e2e"] = {"value": nq * D0 * D1 / ew / 1e9, "unit": "GB/s",
+                      "ms_per_step": ew * 1e3, "ratio_to_device": ew * 1e3 / ms,
+                      "api": "paper_2603_09190_b200.respond_batch_wire() (wire fields in, "
+                             "limb rows out)",
                       "h2d_bytes_per_step": nq * (4 * D0 + 4 * kctx.lm * N_LWE),
-                      "d2h_bytes_per_step": nq * 4 * kctx.lm * params.d1_prime}
+                      "d2h_bytes_per_step": nq * 4 * kctx.l2 * params.d1_prime}
         if not args.no_cpu_baseline:
             # the reference has no batch path: 64 sequential respond()s
             # (protocol.py:333-365), here on a row sample

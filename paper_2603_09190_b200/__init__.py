@@ -12,11 +12,13 @@ from .paillier import (PaillierPublicKey, PaillierCiphertext, InvalidCiphertext,
 from .protocol import (SEPARATE, COMBINED, ServerGlobalState, ClientHint,  # noqa: F401
                        ClientRegistration, QueryMessage, ResponseMessage, HintRequest,
                        client_id_of, derive_ck_r, hint, hints, respond, respond_batch,
+                       respond_wire, respond_batch_wire, answer_wire,
                        refresh_hint, refresh_hints)
 
 __all__ = [
     "LweParams", "ProtocolParams", "PaillierPublicKey", "PaillierCiphertext", "multiexp",
     "paillier_matmul", "sample_ciphertext", "ServerGlobalState", "ClientHint",
     "ClientRegistration", "QueryMessage", "ResponseMessage", "client_id_of", "derive_ck_r",
-    "hint", "hints", "respond", "respond_batch", "refresh_hint", "SEPARATE", "COMBINED",
+    "hint", "hints", "respond", "respond_batch", "respond_wire", "respond_batch_wire",
+    "answer_wire", "refresh_hint", "refresh_hints", "SEPARATE", "COMBINED",
 ]

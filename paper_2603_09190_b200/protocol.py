@@ -1142,6 +1142,148 @@ def _respond_chunk(state, qs, ks, modes, storeds, lm, conv, stream):
     return _batch_messages(state, qs, modes, storeds, res)
 
 
+class _WireBatchBufs(threading.local):
+    """Per-thread pinned buffers of respond_batch_wire (grown on demand)."""
+
+    def __init__(self):
+        self.key = None
+        self.bufs = None
+
+
+_wire_bufs = _WireBatchBufs()
+
+
+def _parallel(fn, count):
+    """fn(i) for i < count on the device module's host-copy thread pool
+    (numpy copies release the GIL)."""
+    pool = device.host_pool()
+    if pool is None or count < 2:
+        for i in range(count):
+            fn(i)
+        return
+    list(pool.map(fn, range(count)))
+
+
+def respond_batch_wire(state: ServerGlobalState, regs, query_indices, modes, ck_bytes, qus,
+                       stream=None) -> list:
+    """respond_batch() on fixed-width wire fields (BASELINE configs[3]), no
+    Python ints anywhere: query i is (regs[i], query_indices[i], modes[i],
+    ck_bytes[i] (n, w) u8 little-endian ck_o magnitudes as wire.decode_query
+    returns them, qus[i] (d0,) integers). Returns per query the (d1', L) u32
+    limb rows of t (SEPARATE, L = limbs of m) or K (COMBINED, L = limbs of
+    m^2) for wire.field_rows -- views into per-thread pinned memory, valid
+    until the next call on this thread. Same validation and exceptions as
+    respond(); the reference answers one query at a time
+    (protocol.py:333-365, wire.py:141-206).
+
+    Pipeline: every qu0 staged (pinned, parallel host copies) -> ONE N = 4 nq
+    tensor-core GEMV over the DB; then per sub-batch of BATCH_SUB queries: ck_o
+    bytes staged and copied in, the CTA-pair planar compression + group stage,
+    COMBINED's K, results copied out -- the host stages sub-batch s + 1 while
+    the device works on s."""
+    nq = len(qus)
+    if not (len(regs) == len(query_indices) == len(modes) == len(ck_bytes) == nq):
+        raise ValueError("batch fields must have the same length")
+    if nq == 0:
+        return []
+    lay = state.layout
+    dev = state.device
+    stream = stream or torch.cuda.current_stream(dev)
+    storeds, kctxs = [], []
+    for reg, qi, md, ck, qu in zip(regs, query_indices, modes, ck_bytes, qus):
+        ck = np.asarray(ck)
+        qu = np.asarray(qu)
+        if ck.ndim != 2 or ck.shape[0] != lay.n or qu.shape != (lay.d0,):
+            raise ValueError("query dimensions do not match the parameters")
+        st = reg.hints.get(qi)
+        if st is None or st.db_version != state.db_version:
+            raise KeyError("no hint for this query index and database version")
+        if md not in (SEPARATE, COMBINED):
+            raise ValueError("unknown response mode")
+        kc = key_ctx(reg.pk.m, dev)
+        if ck.shape[1] > 4 * kc.lm:
+            raise ValueError("ck_o field wider than the modulus")
+        storeds.append(st)
+        kctxs.append(kc)
+    lm = kctxs[0].lm
+    umma_ok = (state.engine == "umma" and lay.qmask == 0xFFFFFFFF and lay.stride > 0
+               and lay.n % 4 == 0 and lm in device.UMMA_NB
+               and all(k.lm == lm for k in kctxs))
+    if not umma_ok:
+        return [respond_wire(state, r, qi, md, ck, qu, stream=stream).copy()
+                for r, qi, md, ck, qu in zip(regs, query_indices, modes, ck_bytes, qus)]
+    out = []
+    for c0 in range(0, nq, MAX_BATCH):
+        c1 = min(nq, c0 + MAX_BATCH)
+        out += _wire_chunk(state, regs[c0:c1], modes[c0:c1], ck_bytes[c0:c1], qus[c0:c1],
+                           storeds[c0:c1], kctxs[c0:c1], lm, stream, c0 > 0)
+    return out
+
+
+def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep_prev):
+    lay = state.layout
+    dev = state.device
+    nq, n, G = len(qus), lay.n, lay.groups
+    l2 = ks[0].l2
+    key = (id(state), nq, lm)
+    tb = _wire_bufs
+    if tb.key != key or keep_prev:
+        # pinned: qu rows (ld u32, zero tail), ck_o byte rows, results; device copies
+        tb.bufs = {
+            "q": torch.zeros((nq, lay.ld), dtype=torch.int32).pin_memory(),
+            "c": torch.zeros((nq, n, 4 * lm), dtype=torch.uint8).pin_memory(),
+            "w": [0] * nq,
+            "o": torch.empty((nq, G, l2), dtype=torch.int32).pin_memory(),
+            "qd": torch.empty((nq, lay.ld), dtype=torch.int32, device=dev),
+            "cd": torch.empty((nq, n, lm), dtype=torch.int32, device=dev),
+            "ev": [torch.cuda.Event() for _ in range(-(-nq // max(1, BATCH_SUB)))],
+        }
+        tb.key = key
+    B = tb.bufs
+    qn = B["q"].numpy().view(np.uint32)
+    cn = B["c"].numpy()
+    on = B["o"].numpy().view(np.uint32)
+
+    def stage_qu(i):
+        np.copyto(qn[i, : lay.d0], np.asarray(qus[i]), casting="unsafe")
+
+    def stage_ck(i):
+        ck = np.asarray(ck_bytes[i], dtype=np.uint8)
+        w = ck.shape[1]
+        cn[i, :, :w] = ck
+        if B["w"][i] > w:                    # a wider field was staged here before
+            cn[i, :, w:] = 0
+        B["w"][i] = w
+
+    _parallel(stage_qu, nq)
+    device.h2d_async(B["qd"], B["q"], stream)
+    b = state.gemv_batch_device(B["qd"], stream)                    # (nq, rows)
+    sub = max(1, BATCH_SUB)
+    res = [None] * nq
+    for si, lo in enumerate(range(0, nq, sub)):
+        hi = min(nq, lo + sub)
+        _parallel(lambda j: stage_ck(lo + j), hi - lo)
+        device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], stream)
+        t = state.compress_groups_batch(B["cd"][lo:hi], b[lo:hi], ks[lo:hi], l2, stream)
+        for i in range(lo, hi):
+            if modes[i] == SEPARATE:
+                r = t[i - lo]
+                L = lm
+            else:
+                r = device.combine(t[i - lo], _stored_device(storeds[i], ks[i], dev, stream),
+                                   ks[i], stream=stream)
+                L = l2
+            device.d2h_async(B["o"][i], r, stream)
+            res[i] = on[i, :, :L]
+        B["ev"][si].record(stream)
+    B["ev"][-1].synchronize()
+    for md in modes:
+        if md == COMBINED:
+            counters.bump("add", lay.groups)
+            counters.bump("group_mult", lay.groups)
+    return res
+
+
 def _batch_messages(state, qs, modes, storeds, res):
     lay = state.layout
     out = []

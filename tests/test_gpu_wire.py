@@ -88,3 +88,44 @@ def test_tcp_loopback_round_trip(golden):
         srv.shutdown()
         srv.server_close()
         pir.close()
+
+
+@pytest.mark.parametrize("name", ["desk_reduced", "ragged", "uniform_key"])
+def test_respond_batch_wire_matches_single(golden, name):
+    """respond_batch_wire (configs[3]'s batch on wire fields, no Python ints):
+    every query's limb rows equal respond_wire's, in both modes, with ck_o
+    fields of mixed widths (the minimal-width encoding included), and the
+    golden t / K for the golden query."""
+    import random
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200.bigint import ints_to_limbs, limbs_to_ints
+    g = golden(name)
+    st = z.ServerGlobalState(g.params(z), g.db)
+    pk = z.PaillierPublicKey(g.m, g.m.bit_length())
+    reg = z.ClientRegistration(pk, g.seed, z.client_id_of(pk))
+    reg.hints[0] = z.hint(st, reg, 0)
+    lm = -(-g.m.bit_length() // 1024) * 32
+    r = random.Random(17)
+    rng = np.random.default_rng(17)
+    cks, qus, modes = [], [], []
+    for i in range(37):                       # > BATCH_SUB: several sub-batches
+        ck = g.ints("ck_o") if i == 0 else [r.randrange(g.m) for _ in range(g.lwe["n"])]
+        b = ints_to_limbs(ck, lm).view(np.uint8).reshape(len(ck), 4 * lm)
+        w = 4 * lm if i % 3 else (max(v.bit_length() for v in ck) + 7) // 8
+        cks.append(np.ascontiguousarray(b[:, :w]))
+        qus.append(g.arr["qu0"] if i == 0 else rng.integers(0, g.q, g.d0, dtype=np.uint64))
+        modes.append(z.COMBINED if i % 4 == 1 else z.SEPARATE)
+    modes[0] = z.SEPARATE
+    modes[1] = z.COMBINED
+    cks[1], qus[1] = cks[0], qus[0]
+    out = z.respond_batch_wire(st, [reg] * 37, [0] * 37, modes, cks, qus)
+    out = [o.copy() for o in out]
+    assert limbs_to_ints(out[0]) == g.ints("t")
+    assert limbs_to_ints(out[1]) == g.ints("K")
+    for i in range(37):
+        one = z.respond_wire(st, reg, 0, modes[i], cks[i], qus[i])
+        assert np.array_equal(out[i], one), i
+    with pytest.raises(KeyError):
+        z.respond_batch_wire(st, [reg], [5], [z.SEPARATE], cks[:1], qus[:1])
+    with pytest.raises(ValueError):
+        z.respond_batch_wire(st, [reg], [0], [z.SEPARATE], [cks[0][:-1]], qus[:1])
