@@ -820,7 +820,7 @@ def run_extra(args):
                       "api": "paper_2603_09190_b200.respond_batch_wire() (wire fields in, "
                              "limb rows out)",
                       "h2d_bytes_per_step": nq * (4 * D0 + 4 * kctx.lm * N_LWE),
-                      "d2h_bytes_per_step": nq * 4 * kctx.l2 * params.d1_prime}
+                      "d2h_bytes_per_step": nq * 4 * kctx.lm * params.d1_prime}
         if not args.no_cpu_baseline:
             # the reference has no batch path: 64 sequential respond()s
             # (protocol.py:333-365), here on a row sample

@@ -13,7 +13,9 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <pthread.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 /* CPython 3.12/3.13 store ints as 30-bit digits behind lv_tag (ndigits << 3 |
@@ -304,7 +306,141 @@ static PyObject* narrow_u32(PyObject* self, PyObject* args) {
   Py_RETURN_NONE;
 }
 
+/* stage_rows(items, buf, item_bytes, rows, row_bytes, nthreads, words):
+ * copies a batch of host arrays into one (pinned) staging buffer, item i at
+ * buf + i * item_bytes, on nthreads threads with the GIL released -- the
+ * host half of respond_batch_wire (64 queries: 8 MB of qu0 + 16 MB of ck_o).
+ *   words = 0: item i is a C-contiguous (rows, w_i) byte matrix (w_i <=
+ *              row_bytes); row r goes to buf + i item_bytes + r row_bytes,
+ *              zero-padded to row_bytes (the ck_o wire fields -> u32 limbs)
+ *   words = 1: item i is a 1-D buffer of 4- or 8-byte words (qu0), narrowed
+ *              to u32 at buf + i item_bytes, zero-padded to row_bytes. */
+typedef struct {
+  const char* src;
+  Py_ssize_t len, item, stride, w;
+} StageItem;
+
+typedef struct {
+  StageItem* items;
+  Py_ssize_t lo, hi, item_bytes, rows, row_bytes;
+  int words;
+  char* dst;
+} StageJob;
+
+static void* stage_worker(void* arg) {
+  StageJob* j = (StageJob*)arg;
+  for (Py_ssize_t i = j->lo; i < j->hi; ++i) {
+    const StageItem* it = &j->items[i];
+    char* out = j->dst + i * j->item_bytes;
+    if (j->words) {
+      uint32_t* o = (uint32_t*)out;
+      if (it->item == 4 && it->stride == 4) {
+        memcpy(o, it->src, (size_t)it->len * 4);
+      } else if (it->item == 8 && it->stride == 8) {
+        const uint64_t* q = (const uint64_t*)it->src;
+        for (Py_ssize_t k = 0; k < it->len; ++k) o[k] = (uint32_t)q[k];
+      } else {
+        for (Py_ssize_t k = 0; k < it->len; ++k)
+          o[k] = it->item == 8 ? (uint32_t) * (const uint64_t*)(it->src + k * it->stride)
+                               : *(const uint32_t*)(it->src + k * it->stride);
+      }
+      if (it->len * 4 < j->row_bytes) memset(out + it->len * 4, 0, (size_t)(j->row_bytes - it->len * 4));
+    } else if (it->w == j->row_bytes) {
+      memcpy(out, it->src, (size_t)j->rows * j->row_bytes);
+    } else {
+      for (Py_ssize_t r = 0; r < j->rows; ++r) {
+        memcpy(out + r * j->row_bytes, it->src + r * it->w, (size_t)it->w);
+        memset(out + r * j->row_bytes + it->w, 0, (size_t)(j->row_bytes - it->w));
+      }
+    }
+  }
+  return NULL;
+}
+
+static PyObject* stage_rows(PyObject* self, PyObject* args) {
+  PyObject* seq;
+  Py_buffer dst;
+  Py_ssize_t item_bytes, rows, row_bytes, nthreads;
+  int words;
+  if (!PyArg_ParseTuple(args, "Ow*nnnnp", &seq, &dst, &item_bytes, &rows, &row_bytes, &nthreads,
+                        &words))
+    return NULL;
+  PyObject* fast = PySequence_Fast(seq, "expected a sequence of arrays");
+  if (!fast) {
+    PyBuffer_Release(&dst);
+    return NULL;
+  }
+  const Py_ssize_t n = PySequence_Fast_GET_SIZE(fast);
+  Py_buffer* views = (Py_buffer*)calloc((size_t)(n ? n : 1), sizeof(Py_buffer));
+  StageItem* items = (StageItem*)calloc((size_t)(n ? n : 1), sizeof(StageItem));
+  Py_ssize_t got = 0;
+  PyObject* ret = NULL;
+  if (!views || !items) {
+    PyErr_NoMemory();
+    goto done;
+  }
+  if ((size_t)dst.len < (size_t)n * item_bytes || row_bytes * (words ? 1 : rows) > item_bytes) {
+    PyErr_SetString(PyExc_ValueError, "stage_rows: staging buffer too small");
+    goto done;
+  }
+  for (; got < n; ++got) {
+    PyObject* o = PySequence_Fast_GET_ITEM(fast, got);
+    Py_buffer* v = &views[got];
+    if (PyObject_GetBuffer(o, v, words ? (PyBUF_STRIDED_RO | PyBUF_FORMAT) : PyBUF_C_CONTIGUOUS) < 0)
+      goto done;
+    StageItem* it = &items[got];
+    it->src = (const char*)v->buf;
+    if (words) {
+      it->item = v->itemsize;
+      it->stride = (v->ndim == 1 && v->strides) ? v->strides[0] : v->itemsize;
+      it->len = (v->ndim == 1 && v->shape) ? v->shape[0] : v->len / v->itemsize;
+      if ((it->item != 4 && it->item != 8) || v->ndim > 1 || it->len * 4 > row_bytes) {
+        PyErr_SetString(PyExc_ValueError, "stage_rows: need 1-D arrays of 4/8-byte words");
+        ++got;
+        goto done;
+      }
+    } else {
+      if (rows <= 0 || v->len % rows || v->len / rows > row_bytes) {
+        PyErr_SetString(PyExc_ValueError, "stage_rows: field rows wider than the limb width");
+        ++got;
+        goto done;
+      }
+      it->w = v->len / rows;
+    }
+  }
+  {
+    Py_ssize_t T = nthreads < 1 ? 1 : (nthreads > 32 ? 32 : nthreads);
+    if (T > n) T = n ? n : 1;
+    StageJob jobs[32];
+    pthread_t th[32];
+    int started[32] = {0};
+    for (Py_ssize_t t = 0; t < T; ++t)
+      jobs[t] = (StageJob){items, n * t / T, n * (t + 1) / T, item_bytes, rows, row_bytes, words,
+                           (char*)dst.buf};
+    Py_BEGIN_ALLOW_THREADS
+    for (Py_ssize_t t = 1; t < T; ++t)
+      started[t] = pthread_create(&th[t], NULL, stage_worker, &jobs[t]) == 0;
+    stage_worker(&jobs[0]);
+    for (Py_ssize_t t = 1; t < T; ++t) {
+      if (started[t]) pthread_join(th[t], NULL);
+      else stage_worker(&jobs[t]);     /* thread creation failed: copy here */
+    }
+    Py_END_ALLOW_THREADS
+  }
+  Py_INCREF(Py_None);
+  ret = Py_None;
+done:
+  for (Py_ssize_t i = 0; i < got; ++i)
+    if (views[i].obj) PyBuffer_Release(&views[i]);
+  free(views);
+  free(items);
+  Py_DECREF(fast);
+  PyBuffer_Release(&dst);
+  return ret;
+}
+
 static PyMethodDef methods[] = {
+    {"stage_rows", stage_rows, METH_VARARGS, "batch of host arrays -> one staging buffer (threads)"},
     {"narrow_u32", narrow_u32, METH_VARARGS, "4/8-byte words -> u32 buffer (truncating)"},
 #ifdef ZPIR_FAST_DIGITS
     {"digits_into", digits_into, METH_VARARGS, "ints -> raw 30-bit digits written into a buffer"},

@@ -463,19 +463,9 @@ def _upload_threads() -> int:
     return int(v) if v is not None else max(1, min(8, os.cpu_count() or 1))
 
 
-def host_pool():
-    """The host-copy thread pool (numpy copies release the GIL), or None."""
-    global _UPLOAD_POOL
-    nthreads = _upload_threads()
-    if nthreads <= 1:
-        return None
-    with _UPLOAD_LOCK:
-        if _UPLOAD_POOL is None or _UPLOAD_POOL[0] != nthreads:
-            from concurrent.futures import ThreadPoolExecutor
-            if _UPLOAD_POOL is not None:
-                _UPLOAD_POOL[1].shutdown(wait=False)
-            _UPLOAD_POOL = (nthreads, ThreadPoolExecutor(nthreads, thread_name_prefix="zpir-upload"))
-        return _UPLOAD_POOL[1]
+def host_threads() -> int:
+    """Threads for host-side staging copies (ZPIR_UPLOAD_THREADS, else <= 8)."""
+    return _upload_threads()
 
 
 def upload_bytes(a: np.ndarray, dev, stream) -> torch.Tensor:

@@ -746,6 +746,11 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
     return res
 
 
+def _conv_module():
+    from .bigint import _conv
+    return _conv()
+
+
 def _digit_conv():
     """The C extension's raw-digit entry points (CPython 3.12/3.13), or None."""
     from .bigint import _conv
@@ -1153,17 +1158,6 @@ class _WireBatchBufs(threading.local):
 _wire_bufs = _WireBatchBufs()
 
 
-def _parallel(fn, count):
-    """fn(i) for i < count on the device module's host-copy thread pool
-    (numpy copies release the GIL)."""
-    pool = device.host_pool()
-    if pool is None or count < 2:
-        for i in range(count):
-            fn(i)
-        return
-    list(pool.map(fn, range(count)))
-
-
 def respond_batch_wire(state: ServerGlobalState, regs, query_indices, modes, ck_bytes, qus,
                        stream=None) -> list:
     """respond_batch() on fixed-width wire fields (BASELINE configs[3]), no
@@ -1232,7 +1226,6 @@ def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep
         tb.bufs = {
             "q": torch.zeros((nq, lay.ld), dtype=torch.int32).pin_memory(),
             "c": torch.zeros((nq, n, 4 * lm), dtype=torch.uint8).pin_memory(),
-            "w": [0] * nq,
             "o": torch.empty((nq, G, l2), dtype=torch.int32).pin_memory(),
             "qd": torch.empty((nq, lay.ld), dtype=torch.int32, device=dev),
             "cd": torch.empty((nq, n, lm), dtype=torch.int32, device=dev),
@@ -1244,31 +1237,43 @@ def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep
     cn = B["c"].numpy()
     on = B["o"].numpy().view(np.uint32)
 
-    def stage_qu(i):
-        np.copyto(qn[i, : lay.d0], np.asarray(qus[i]), casting="unsafe")
+    conv = _digit_conv() or _conv_module()
+    nthr = device.host_threads()
 
-    def stage_ck(i):
-        ck = np.asarray(ck_bytes[i], dtype=np.uint8)
-        w = ck.shape[1]
-        cn[i, :, :w] = ck
-        if B["w"][i] > w:                    # a wider field was staged here before
+    def stage_ck(lo, hi):
+        if conv is not None and hasattr(conv, "stage_rows"):
+            conv.stage_rows(ck_bytes[lo:hi], cn[lo:hi], n * 4 * lm, n, 4 * lm, nthr, False)
+            return
+        for i in range(lo, hi):
+            ck = np.asarray(ck_bytes[i], dtype=np.uint8)
+            w = ck.shape[1]
+            cn[i, :, :w] = ck
             cn[i, :, w:] = 0
-        B["w"][i] = w
 
-    _parallel(stage_qu, nq)
+    if conv is not None and hasattr(conv, "stage_rows"):
+        conv.stage_rows(qus, qn, lay.ld * 4, 1, lay.ld * 4, nthr, True)
+    else:
+        for i in range(nq):
+            np.copyto(qn[i, : lay.d0], np.asarray(qus[i]), casting="unsafe")
     device.h2d_async(B["qd"], B["q"], stream)
     b = state.gemv_batch_device(B["qd"], stream)                    # (nq, rows)
     sub = max(1, BATCH_SUB)
     res = [None] * nq
     for si, lo in enumerate(range(0, nq, sub)):
         hi = min(nq, lo + sub)
-        _parallel(lambda j: stage_ck(lo + j), hi - lo)
+        stage_ck(lo, hi)
         device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], stream)
-        t = state.compress_groups_batch(B["cd"][lo:hi], b[lo:hi], ks[lo:hi], l2, stream)
+        # t rows of lm limbs unless a COMBINED query needs them widened for combine
+        t_ld = l2 if any(modes[i] == COMBINED for i in range(lo, hi)) else lm
+        t = state.compress_groups_batch(B["cd"][lo:hi], b[lo:hi], ks[lo:hi], t_ld, stream)
         for i in range(lo, hi):
             if modes[i] == SEPARATE:
                 r = t[i - lo]
                 L = lm
+                if t_ld == lm:                  # compact rows: copy into the row block
+                    device.d2h_async(B["o"][i].view(-1)[: G * lm], r, stream)
+                    res[i] = on[i].reshape(-1)[: G * lm].reshape(G, lm)
+                    continue
             else:
                 r = device.combine(t[i - lo], _stored_device(storeds[i], ks[i], dev, stream),
                                    ks[i], stream=stream)

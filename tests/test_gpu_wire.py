@@ -113,7 +113,7 @@ def test_respond_batch_wire_matches_single(golden, name):
         b = ints_to_limbs(ck, lm).view(np.uint8).reshape(len(ck), 4 * lm)
         w = 4 * lm if i % 3 else (max(v.bit_length() for v in ck) + 7) // 8
         cks.append(np.ascontiguousarray(b[:, :w]))
-        qus.append(g.arr["qu0"] if i == 0 else rng.integers(0, g.q, g.d0, dtype=np.uint64))
+        qus.append(g.arr["qu0"] if i == 0 else rng.integers(0, g.lwe["q"], g.d0, dtype=np.uint64))
         modes.append(z.COMBINED if i % 4 == 1 else z.SEPARATE)
     modes[0] = z.SEPARATE
     modes[1] = z.COMBINED
