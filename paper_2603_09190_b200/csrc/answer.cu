@@ -434,17 +434,6 @@ int groups_z_launch(const uint32_t* z, int64_t zq, int64_t d1, int cap, int64_t 
   GroupBatch bt{zq, 0, groups * t_ld, lm, (int64_t)nchunks * lm, nps, fast0s, stride};
   const dim3 grid((unsigned)groups, (unsigned)nq);
   size_t zsm = (size_t)cap * (lm + 4) * sizeof(uint32_t);
-  {
-    // occupancy shaping: a floor on the dynamic smem keeps this kernel off SMs
-    // that host a concurrent GEMV CTA (~200 KB smem), so it does not steal the
-    // GEMV's issue slots while the GEMV is still streaming the DB
-    static long pad = -1;
-    if (pad < 0) {
-      const char* e = getenv("ZPIR_GZ_SMEM");
-      pad = e ? atol(e) : 0;
-    }
-    if ((size_t)pad > zsm) zsm = (size_t)pad;
-  }
 #define ZPIR_GZ(NCHV)                                                                          \
   ZPIR_LPL_DISPATCH(lm / 32, {                                                                 \
     cudaFuncSetAttribute(answer_groups_kernel<LPL, NCHV, false>,                               \

@@ -17,7 +17,6 @@
 // answer reduction mod m (protocol.py:348-350) and the COMBINED response
 // (protocol.py:354-358, paillier.py:104-123).
 #pragma once
-#include "mac_asm.cuh"
 #include "zpir_common.cuh"
 
 namespace zpir {
@@ -157,7 +156,7 @@ __device__ __forceinline__ void big_cond_sub(uint32_t (&x)[LPL], uint32_t top,
 }
 
 // t += x * y with 64-bit products (compiles to IMAD.WIDE.U32 chains); measured
-// fewer SASS instructions than the explicit PTX carry chain (mac_asm.cuh).
+// fewer SASS instructions than an explicit PTX carry chain (measured round 1).
 template <int LPL>
 __device__ __forceinline__ void mac_row_c(uint32_t (&t)[LPL], uint32_t& s0, uint32_t& s1,
                                           uint32_t x, const uint32_t (&y)[LPL]) {
@@ -178,11 +177,7 @@ __device__ __forceinline__ void mac_row_c(uint32_t (&t)[LPL], uint32_t& s0, uint
 template <int LPL>
 __device__ __forceinline__ void mac_row(uint32_t (&t)[LPL], uint32_t& s0, uint32_t& s1,
                                         uint32_t x, const uint32_t (&y)[LPL]) {
-#ifdef ZPIR_MAC_ASM
-  mac_row_asm<LPL>(t, s0, s1, x, y);  // PTX carry chains: more SASS (IMAD + IADD3.X pairs)
-#else
   mac_row_c<LPL>(t, s0, s1, x, y);    // IMAD.WIDE.U32 + 64-bit adds: fewest instructions
-#endif
 }
 
 // r = a * b * R^-1 mod N, canonical. Requires a < R, b < N (then T < 2N).

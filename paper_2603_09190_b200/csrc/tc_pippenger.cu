@@ -939,14 +939,10 @@ static int upload_strip_schedule() {
   return kOk;
 }
 
-// Digits per 32-bit exponent word: ZPIR_TC_DIGITS (4..8, default 6 -> widths
+// Digits per 32-bit exponent word: 6 (widths
 // 6,6,5,5,5,5 and 63 buckets per row); balanced widths, wider digits first.
 static DigitSpec digit_spec() {
-  static int D = -1;
-  if (D < 0) {
-    const char* e = getenv("ZPIR_TC_DIGITS");
-    D = e ? std::min(8, std::max(4, atoi(e))) : 6;
-  }
+  constexpr int D = 6;   // measured optimum of D = 4..7
   DigitSpec ds{};
   ds.D = D;
   int off = 0, maxw = 0;
@@ -1095,11 +1091,7 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   // one launch walks every position (tiles are independent); chunked so a
   // launch stays well under a second
-  static int64_t chunk = -1;
-  if (chunk < 0) {
-    const char* e = getenv("ZPIR_TC_CHUNK");
-    chunk = e ? std::max<int64_t>(1, atoll(e)) : 1024;
-  }
+  constexpr int64_t chunk = 1024;
   const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(tiles * C, 2 * 148)));
   for (int64_t p0 = 0; p0 < npos; p0 += ck) {
     const int64_t p1 = std::min<int64_t>(npos, p0 + ck);

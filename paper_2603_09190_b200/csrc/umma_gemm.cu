@@ -1081,15 +1081,6 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return kOk;
 }
 
-static bool tpc_packing() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("ZPIR_TPC_PACK");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 static int num_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1120,7 +1111,7 @@ static int umma_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_bytes
   const int grid = (int)std::min<int64_t>(cap, U);
   auto kern = umma_gemm_kernel<NT, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-  if (max_ctas > 0 && grid % 2 == 0 && tpc_packing()) {
+  if (max_ctas > 0 && grid % 2 == 0) {
     // sharing the GPU with a CTA-pair kernel: occupy whole TPCs (clusters of
     // 2) so the remaining SMs stay pairable
     cudaLaunchConfig_t cfg = {};
@@ -1160,14 +1151,7 @@ static int umma_pair_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_
   if (int e = make_map(&mb1, B, brows, K, ldb_bytes, C::kH1 ? C::kH1 : C::kH0)) return e;
   args.m_tiles = (int)ceil_div(rows, 2 * kBM);
   args.n_tiles = (int)(brows / NT);
-  {
-    static int keep = -1;
-    if (keep < 0) {
-      const char* e = getenv("ZPIR_H_L2");
-      keep = (e && e[0] == '0') ? 0 : 1;
-    }
-    args.a_keep = keep;
-  }
+  args.a_keep = 1;   // H rows: L2 evict_last (re-read once per query of a batch)
   args.kblocks = (int)ceil_div(K, kBK);
   args.split = 0;
   const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
@@ -1193,14 +1177,6 @@ static int umma_pair_run(const uint8_t* A, int64_t rows, int64_t K, int64_t lda_
   return check_launch("umma_pair_bigint");
 }
 
-static bool use_pair() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("ZPIR_PAIR");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 // b[v * rows + r] = qmask & (DB qu_v)[r] for nvec <= 4 (N = 16) or 64 (N = 256)
 int umma_gemv_launch(const uint8_t* dbt, int64_t rows, int64_t ld, const uint8_t* qplanes,
@@ -1247,18 +1223,11 @@ int umma_answer_rows_launch(const uint32_t* H, int64_t rows, int64_t n, const ui
   a.qmask = qmask;
   a.wz = wz;
   const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
-  if (use_pair()) {
-    switch (nb) {
-      case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
-      case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
-      case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st, ctas);
-      default: break;
-    }
-  }
+  // CTA pairs (cta_group::2, M = 256): half the B operand traffic per SM
   switch (nb) {
-    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
-    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
-    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st, ctas);
+    case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144, 4 * n, a, st, ctas);
+    case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272, 4 * n, a, st, ctas);
+    case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400, 4 * n, a, st, ctas);
     default:
       set_error("umma_answer_rows: unsupported B width %d", nb);
       return kErrUnsupported;
@@ -1293,18 +1262,10 @@ int umma_answer_rows_batch_launch(const uint32_t* H, int64_t rows, int64_t n, co
   a.wz = wz;
   a.zq = rows * wz;
   const uint8_t* Ab = reinterpret_cast<const uint8_t*>(H);
-  if (use_pair()) {
-    switch (nb) {
-      case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st, 0);
-      case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st, 0);
-      case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400LL * nq, 4 * n, a, st, 0);
-      default: break;
-    }
-  }
   switch (nb) {
-    case 144: return umma_run<144, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st);
-    case 272: return umma_run<272, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st);
-    case 400: return umma_run<400, kBigint>(Ab, rows, 4 * n, 4 * n, bc, 400LL * nq, 4 * n, a, st);
+    case 144: return umma_pair_run<144>(Ab, rows, 4 * n, 4 * n, bc, 144LL * nq, 4 * n, a, st, 0);
+    case 272: return umma_pair_run<272>(Ab, rows, 4 * n, 4 * n, bc, 272LL * nq, 4 * n, a, st, 0);
+    case 400: return umma_pair_run<400>(Ab, rows, 4 * n, 4 * n, bc, 400LL * nq, 4 * n, a, st, 0);
     default:
       set_error("umma_answer_rows_batch: unsupported B width %d", nb);
       return kErrUnsupported;
@@ -1378,19 +1339,10 @@ int build_bcp_launch(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp
   return check_launch("build_bcp");
 }
 
-// CTA-pair planar kernel: ZPIR_PLANAR_PAIR = 0 never, 1 always, default from
-// ZPIR_PLANAR_PAIR_MINQ queries per launch (default 2: batches)
-static bool use_planar_pair(int nq) {
-  static int mode = -2, minq = 2;
-  if (mode == -2) {
-    const char* e = getenv("ZPIR_PLANAR_PAIR");
-    mode = e ? (e[0] == '0' ? 0 : 1) : -1;
-    const char* q = getenv("ZPIR_PLANAR_PAIR_MINQ");
-    if (q) minq = atoi(q);
-  }
-  if (mode >= 0) return mode == 1;
-  return nq >= minq;
-}
+// CTA-pair planar kernel for batches of >= 2 queries (L2 operand traffic 60% ->
+// 51% of peak, 1.77 -> 1.63 ms for 64 queries); single queries gain nothing
+// from it and keep the single-CTA kernel (A/B on one box)
+static bool use_planar_pair(int nq) { return nq >= 2; }
 
 // z (nq x rows x wz) from the planar operands; lm in {32, 64}.
 int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp, int lm,

@@ -457,14 +457,16 @@ _UPLOAD_STAGES = {}
 _UPLOAD_POOL = None
 
 
+UPLOAD_THREADS = None     # host threads for staging copies (None: min(8, cpu count))
+
+
 def _upload_threads() -> int:
     import os
-    v = os.environ.get("ZPIR_UPLOAD_THREADS")
-    return int(v) if v is not None else max(1, min(8, os.cpu_count() or 1))
+    return UPLOAD_THREADS if UPLOAD_THREADS is not None else max(1, min(8, os.cpu_count() or 1))
 
 
 def host_threads() -> int:
-    """Threads for host-side staging copies (ZPIR_UPLOAD_THREADS, else <= 8)."""
+    """Threads for host-side staging copies (UPLOAD_THREADS, else <= 8)."""
     return _upload_threads()
 
 

@@ -14,10 +14,9 @@ stage -- is captured once into CUDA graphs and replayed per query:
                  (respond(): the host converts ck_o while the gemv graph runs)
 
 The eager sequence is run once before capture (sets kernel attributes,
-warms the TMA-descriptor path). ZPIR_GRAPHS=0 disables capture.
+warms the TMA-descriptor path).
 """
 
-import os
 import threading
 
 import numpy as np
@@ -25,7 +24,7 @@ import torch
 
 from . import _lib, device
 
-USE_GRAPHS = os.environ.get("ZPIR_GRAPHS", "1") != "0"
+USE_GRAPHS = True     # False runs the sequences eagerly (debugging)
 _capture_lock = threading.Lock()
 
 
@@ -40,8 +39,7 @@ class AnswerPlan:
         self.ctas = compress_ctas
         # the host-input graphs start the compression side ~25 us after the
         # GEMV (ck_o is staged while the GEMV runs), so they give it more SMs
-        self.ctas_e2e = int(os.environ.get("ZPIR_COMPRESS_CTAS_E2E", str(compress_ctas + 8))) \
-            if compress_ctas > 0 else 0
+        self.ctas_e2e = compress_ctas + 8 if compress_ctas > 0 else 0
         self.sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.qu = torch.zeros((1, lay.ld), dtype=torch.int32, device=dev)
         self.cko = torch.zeros((lay.n, lm), dtype=torch.int32, device=dev)

@@ -24,7 +24,6 @@ raises.
 from dataclasses import dataclass, field
 import hashlib
 import logging
-import os
 import threading
 import time
 
@@ -44,24 +43,22 @@ SEPARATE = "separate"
 COMBINED = "combined"
 
 # "umma": tcgen05 tensor-core engine (default); "cuda_core": the IDP4A / IMAD
-# kernels, kept as the measured alternative (design evidence).
-ENGINE = os.environ.get("ZPIR_ENGINE", "umma")
+# kernels, for shapes the tensor-core kernels do not take (n % 64 != 0 for the
+# hint GEMM, q < 2^32 for the GEMV) and as the second engine the tests compare
+ENGINE = "umma"
 # SMs given to the compression GEMM while the GEMV streams the DB on the rest
-# (both are HBM-bound; H is ~1/8 of the DB bytes). 0 = run them back to back.
-COMPRESS_CTAS = int(os.environ.get("ZPIR_COMPRESS_CTAS", "36"))
-# planar compression GEMM (H byte planes, one N = 4 lm MMA per k-step) for
-# lm = 32 / 64; ZPIR_PLANAR=0 selects the byte-shifted B operand kernels
-PLANAR = os.environ.get("ZPIR_PLANAR", "1") != "0"
+# (both are HBM-bound; H is ~1/8 of the DB bytes; measured optimum, DESIGN 3.2)
+COMPRESS_CTAS = 36
 # per-client hints: Pippenger bucket updates on the tensor cores (4096-bit m^2)
-TC_HINT = os.environ.get("ZPIR_TC_HINT", "1") != "0"
+TC_HINT = True
 # transient workspace cap of one tensor-core hint launch (tiles + buckets)
-TC_WS_BYTES = float(os.environ.get("ZPIR_TC_WS_GB", "24")) * 2**30
+TC_WS_BYTES = 24 * 2**30
 # refreshes of at least this many changed DB rows use the tensor cores (a tensor-core
-# launch costs ~D*n positions of fixed latency and ~2 GB of Toeplitz tiles per
-# client whatever the row count; the IMAD kernels cost ~0.05 ms per row and client)
-TC_REFRESH_MIN_ROWS = int(os.environ.get("ZPIR_TC_REFRESH_MIN_ROWS", "2048"))
+# launch costs ~D*n positions of fixed latency whatever the row count; the IMAD
+# kernels cost ~0.05 ms per row and client)
+TC_REFRESH_MIN_ROWS = 2048
 # full hints: tensor cores when the batch has at least this many exponent rows in total
-TC_MIN_ROWS = int(os.environ.get("ZPIR_TC_MIN_ROWS", "2048"))
+TC_MIN_ROWS = 2048
 
 
 @dataclass
@@ -411,7 +408,7 @@ class ServerGlobalState:
 
     def planar(self, lm) -> bool:
         """The planar compression GEMM serves this key width."""
-        return (PLANAR and self.engine == "umma" and lm in device.PLANAR_LM
+        return (self.engine == "umma" and lm in device.PLANAR_LM
                 and self.H_planes is not None and self.layout.n <= 33025)
 
     def compress_rows(self, cko, lm, stream, out=None, ctas=0, bc=None):
@@ -997,7 +994,7 @@ def _wire_rows(state, m, mode, ck_bytes, qu, stored, stream, on_device=False):
 
 MAX_BATCH = 64
 # respond_batch: queries per compression / copy-out sub-batch (host work overlaps the device)
-BATCH_SUB = int(os.environ.get("ZPIR_BATCH_SUB", "16"))
+BATCH_SUB = 16
 
 
 def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,

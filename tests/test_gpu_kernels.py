@@ -153,39 +153,6 @@ def test_umma_few_ctas_multi_tile(env, lm, ctas):
     assert np.array_equal(b.astype(np.uint64), oracle_c.db_matvec(db, qu))
 
 
-@pytest.mark.parametrize("mode", ["0", "1"])
-def test_planar_pair_modes(mode):
-    """The planar compression with the CTA-pair kernel forced on for single
-    queries (ZPIR_PLANAR_PAIR=1) and forced off for batches (=0), in a fresh
-    process: same results as the CUDA-core rows."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, ZPIR_PLANAR_PAIR=mode)
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_kernels.py"), "-k", "planar_compression"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert " passed" in r.stdout
-
-
-def test_single_cta_compression_variant():
-    """The single-CTA compression GEMM (ZPIR_PAIR=0; the CTA-pair kernel is the
-    default) passes the same kernel checks, in a fresh process."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, ZPIR_PAIR="0", ZPIR_TPC_PACK="0")
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_kernels.py"),
-                        "-k", "answer_rows_engines or few_ctas"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    assert " passed" in r.stdout
-
-
 @pytest.mark.parametrize("lm,n,rows,nq", [(64, 1024, 384, 1), (32, 64, 256, 1), (64, 100, 128, 3),
                                           (32, 1024, 640, 2), (64, 4096, 128, 1),
                                           (64, 1024, 1152, 8)])

@@ -16,7 +16,7 @@ stream = torch.cuda.current_stream(dev)
 a = np.frombuffer(np.random.default_rng(1).bytes(32768 * 32768), np.uint8).reshape(32768, 32768)
 ref = torch.from_numpy(a).to(dev)
 for threads in ("0", "4", "8", "16", "0", "8"):
-    os.environ["ZPIR_UPLOAD_THREADS"] = threads
+    device.UPLOAD_THREADS = int(threads)
     ts = []
     for _ in range(4):
         torch.cuda.synchronize()
