@@ -556,6 +556,24 @@ def derive_ck_r(pk, seed: bytes, query_index: int, n: int):
     return [sample_ciphertext(pk, seed, (query_index << 32) | i) for i in range(n)]
 
 
+class _StreamPool(threading.local):
+    """Side streams of hints() / refresh_hints(), created once per thread and
+    device and reused (a hint worker thread calls them for every batch)."""
+
+    def __init__(self):
+        self.pools = {}
+
+
+_stream_pool = _StreamPool()
+
+
+def _side_streams(dev, count):
+    pool = _stream_pool.pools.setdefault(str(dev), [])
+    while len(pool) < count:
+        pool.append(torch.cuda.Stream(dev))
+    return pool[:count]
+
+
 def _tc_eligible(state, kctx) -> bool:
     return TC_HINT and kctx.l2 == 128 and 4 * state.layout.n <= 65536
 
@@ -621,7 +639,7 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
     # the per-client group recombination (slot_combine: one warp per group, a
     # 32 * cap-deep Horner chain) is latency bound for one client; several
     # clients' run side by side on a small stream pool
-    side = [stream] if len(jobs) == 1 else [torch.cuda.Stream(dev) for _ in range(min(4, len(jobs)))]
+    side = [stream] if len(jobs) == 1 else _side_streams(dev, min(4, len(jobs)))
     ev = torch.cuda.Event()
     ev.record(stream)
     out = []
@@ -717,8 +735,7 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
         for (W, k), kctx in zip(outs, kctxs):
             device.slot_combine(W, lay.cap, gid, ng, kctx, k, lay.gamma, main)
     else:
-        streams = [main] if len(pairs) == 1 else [torch.cuda.Stream(dev)
-                                                  for _ in range(min(nstreams, len(pairs)))]
+        streams = [main] if len(pairs) == 1 else _side_streams(dev, min(nstreams, len(pairs)))
         ev = torch.cuda.Event()
         ev.record(main)
         outs = []

@@ -231,13 +231,54 @@ def gamma_cases():
                   64, 100, 1024, seed=23)
 
 
+def compress_cases():
+    """The reference's standalone compressor (compress.py:99-258) on seeded
+    inputs: lwe_compress, fast_lwe_compress (expanded key), batched_lwe_compress
+    and fast_batched_lwe_compress -> compress_kat.json."""
+    from zippir import compress
+    from zippir.lwe import LweCiphertext
+    out = []
+    for bits, n, q, key_dist, ncts, seed in ((768, 64, 1 << 32, "binary", 4, 31),
+                                             (1024, 32, 1 << 16, "binary", 3, 32),
+                                             (2048, 128, 1 << 32, "uniform", 2, 33)):
+        rng = random.Random(seed)
+        pk, sk = paillier.keygen(bits, rng)
+        lwe = LweParams(n=n, q=q, p=256 if q > 256 else 16, noise_sigma=0.0, key_dist=key_dist)
+        lwe_sk = [rng.randrange(2) if key_dist == "binary" else rng.randrange(q)
+                  for _ in range(n)]
+        ck = compress.make_compression_key(pk, lwe, lwe_sk, rng)
+        cts = [LweCiphertext(np.array([rng.randrange(q) for _ in range(n)], dtype=np.uint64),
+                             rng.randrange(q)) for _ in range(ncts)]
+        single = [compress.lwe_compress(ck, ct).x.c for ct in cts]
+        eck = compress.expand_compression_key(ck)
+        fast = [compress.fast_lwe_compress(eck, ct).x.c for ct in cts]
+        gamma = compress.select_scale(lwe)
+        ell = min(len(cts), compress.batch_capacity(pk, gamma))
+        batched = compress.batched_lwe_compress(ck, cts[:ell], gamma).x.c
+        fast_batched = compress.fast_batched_lwe_compress(ck, cts[:ell], gamma).x.c
+        out.append(dict(bits=bits, n=n, q=q, key_dist=key_dist, m=hex(pk.m),
+                        ck=[hex(c.c) for c in ck.ck],
+                        cts=[dict(a=[int(x) for x in ct.a], b=int(ct.b)) for ct in cts],
+                        lwe_compress=[hex(v) for v in single],
+                        fast_lwe_compress=[hex(v) for v in fast],
+                        gamma=str(gamma), ell=ell, batched=hex(batched),
+                        fast_batched=hex(fast_batched)))
+    with open(os.path.join(HERE, "compress_kat.json"), "w") as f:
+        json.dump(out, f, indent=0)
+    print("compress_kat:", len(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--skip-tiny", action="store_true")
     ap.add_argument("--wire-only", action="store_true", help="only the wire fixtures")
+    ap.add_argument("--compress-only", action="store_true", help="only compress_kat.json")
     ap.add_argument("--gamma-only", action="store_true",
                     help="only the batch-scale cases (gamma != 2^32)")
     args = ap.parse_args()
+    if args.compress_only:
+        compress_cases()
+        return
     if args.wire_only:
         wire_cases()
         dbfile_cases()
@@ -247,6 +288,7 @@ def main():
         return
     prg_cases()
     multiexp_cases()
+    compress_cases()
     # reference's toy fixture (tests/test_protocol.py:12-19): standard regime
     protocol_case("toy", dict(n=4, q=16, p=4, noise_sigma=0.0, key_dist="binary"),
                   4, 4, 64, seed=0xC0FFEE, scale_regime="standard")

@@ -68,3 +68,33 @@ def test_batched_compress_matches_reference_scalar_mul_path():
     assert compress.batched_lwe_compress(ck, cts, gamma).x.c == want
     with pytest.raises(compress.CapacityExceeded):
         compress.batched_lwe_compress(ck, cts + cts[:1], gamma)
+
+
+def test_compressor_matches_reference_kat():
+    """The GPU compressor against the unmodified reference's outputs
+    (tests/golden/compress_kat.json, made by tests/golden/make_golden.py:
+    compress.py:99-258 on seeded keys and ciphertexts, binary and uniform
+    LWE keys, q = 2^16 / 2^32)."""
+    import json
+    import os
+    import paper_2603_09190_b200 as z
+    from paper_2603_09190_b200 import compress
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "compress_kat.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        m = int(c["m"], 16)
+        pk = z.PaillierPublicKey(m, m.bit_length())
+        lwe = SimpleNamespace(n=c["n"], q=c["q"], p=256, key_dist=c["key_dist"])
+        ckl = [z.PaillierCiphertext(int(x, 16)) for x in c["ck"]]
+        ck = SimpleNamespace(pk=pk, lwe_params=lwe, ck=ckl, key_scaling=1)
+        eck = SimpleNamespace(pk=pk, lwe_params=lwe, eck=[ckl], key_scaling=1)
+        cts = [SimpleNamespace(a=ct["a"], b=ct["b"]) for ct in c["cts"]]
+        got = compress.lwe_compress_many(ck, cts)
+        assert [g.x.c for g in got] == [int(v, 16) for v in c["lwe_compress"]], c["bits"]
+        assert [compress.fast_lwe_compress(eck, ct).x.c for ct in cts] == \
+            [int(v, 16) for v in c["fast_lwe_compress"]], c["bits"]
+        gamma, ell = int(c["gamma"]), c["ell"]
+        assert compress.batched_lwe_compress(ck, cts[:ell], gamma).x.c == int(c["batched"], 16)
+        assert compress.fast_batched_lwe_compress(ck, cts[:ell], gamma).x.c == \
+            int(c["fast_batched"], 16)

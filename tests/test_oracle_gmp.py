@@ -71,3 +71,22 @@ def test_hint_rows_matches_hint_cols():
     A = rng.integers(0, 1 << 32, (300, 96), dtype=np.uint64)
     H = oc.hint_rows(db, A, 17, 150)
     assert np.array_equal(H.astype(np.uint64), oc.hint_cols(db, A, list(range(17, 150))))
+
+
+def test_oracle_compressor_matches_reference_kat():
+    """oracle/ref's compressor restatement (the checker of test_gpu_compress)
+    against the reference's own outputs (tests/golden/compress_kat.json,
+    compress.py:99-258: lwe_compress, fast_lwe_compress, batched and
+    fast_batched_lwe_compress)."""
+    with open(os.path.join(GOLDEN, "compress_kat.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        m = int(c["m"], 16)
+        ck = [int(x, 16) for x in c["ck"]]
+        q = c["q"]
+        for ct, want, want_fast in zip(c["cts"], c["lwe_compress"], c["fast_lwe_compress"]):
+            got = ref.lwe_compress(m, ck, ct["a"], ct["b"], q)
+            assert got == int(want, 16) == int(want_fast, 16), c["bits"]
+        cts = [(ct["a"], ct["b"]) for ct in c["cts"][: c["ell"]]]
+        got = ref.batched_lwe_compress(m, ck, cts, int(c["gamma"]), q)
+        assert got == int(c["batched"], 16) == int(c["fast_batched"], 16), c["bits"]
