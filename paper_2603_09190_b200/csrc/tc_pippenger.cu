@@ -68,30 +68,6 @@ struct Step {
 };
 __constant__ Step kSched[kNSteps];
 
-// Strip form (tc_step_kernel<true>): the Toeplitz tiles of one multiplier are
-// 128-row shifts of each other (tile t = strip rows 128 t .. 128 t + 255), so
-// per position only three strips of 128-row half-tiles cross L2 -> SM: Y' (5),
-// Y (6) and N (6), 272 KB instead of the 20 x 32 KB = 640 KB of separate
-// tiles. They stream through 6 half-tile slots in shared memory; the B
-// descriptor of tile t starts at slot t (slots t and t + 1 are adjacent), so a
-// tile costs 16 KB of new data. Three phases per position: U from the Y'
-// strip, H's X * Y from the Y strip, H's u * N from the N strip.
-constexpr int kHalf = 128 * kBK;           // one 128-row half-tile (16 KB)
-constexpr int kSlots = 6;
-constexpr int kSSmem = 2 * kABytes + kSlots * kHalf + 1024 + 1024;
-__host__ __device__ constexpr int halfs(int ph) { return ph == 0 ? kTYp + 1 : kTY + 1; }
-struct SStep {
-  int8_t phase, a, ka, t;
-  uint8_t acc;      // 0: overwrite the accumulator (the task's first MMA of the position)
-  uint8_t wait;     // before: 1/2 tempty[0/1] of the previous position (not at the first),
-                    // 16/32 tempty[0/1], 4 xfull, 8 uready
-  uint8_t commit;   // after: 1/2 tfull[0/1], 4 xfree
-  uint8_t need;     // slots whose full barrier is first waited for in this phase
-  uint8_t rel;      // slots released (last read in this phase)
-  uint8_t buf;      // TMEM buffer (task & 1)
-};
-__constant__ SStep kSSched[kNSteps];
-
 }  // namespace tcp
 
 // Per-client arguments of one batched launch (device copy).
@@ -163,38 +139,6 @@ toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __
       w[q] = v;
     }
     *reinterpret_cast<uint4*>(row + a0) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-
-// strips[((c * npos + p) * H * 128 + r)][a] = byte_{delta0 + r - a}(y_{c,p}),
-// zero outside [0, 512): the H half-tiles (128 rows each) of one multiplier's
-// Toeplitz strip; y = Y[c][p] (which = 1) or the client's N (which = 2, npos = 1).
-__global__ void __launch_bounds__(256)
-toep_strip_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __restrict__ Ybase,
-                  int64_t npos, int H, int delta0, uint8_t* __restrict__ strips) {
-  const int64_t p = blockIdx.x;
-  const int c = blockIdx.y;
-  const uint32_t* ysrc = which == 1 ? Ybase + ((int64_t)c * npos + p) * tcp::kL : cl[c].N;
-  const uint8_t* y = reinterpret_cast<const uint8_t*>(ysrc);
-  uint8_t* base = strips + ((int64_t)c * npos + p) * H * tcp::kHalf;
-  for (int r = threadIdx.x; r < 128 * H; r += blockDim.x) {
-    uint8_t* row = base + (int64_t)r * tcp::kBK;
-#pragma unroll 1
-    for (int a0 = 0; a0 < tcp::kBK; a0 += 16) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t v = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int idx = delta0 + r - (a0 + 4 * q + e);
-          const uint32_t byte = (idx >= 0 && idx < 512) ? y[idx] : 0u;
-          v |= byte << (8 * e);
-        }
-        w[q] = v;
-      }
-      *reinterpret_cast<uint4*>(row + a0) = make_uint4(w[0], w[1], w[2], w[3]);
-    }
   }
 }
 
@@ -322,7 +266,6 @@ __device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long&
 // Pippenger positions pos0..pos1-1 for one 128-row tile of one client per CTA
 // (tiles are independent: a row only touches its own buckets):
 //   B[r][d - 1] *= P[pos] for d = digit(r, pos) != 0.
-template <bool STRIP>
 __global__ void __launch_bounds__(tcp::kThreads, 1)
 tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant__ CUtensorMap mapY,
                const __grid_constant__ CUtensorMap mapN, const TcClient* __restrict__ cl,
@@ -336,12 +279,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
   uint8_t* XA = smem;                       // X (4 k-blocks of 128 x 128 B, SW128)
   uint8_t* UA = smem + kABytes;             // u, same layout
-  uint8_t* BS = smem + 2 * kABytes;         // B tile stages / strip half-tile slots (96 KB)
-  constexpr int NB = STRIP ? kSlots : kStages;
-  static_assert(kSlots * kHalf == kStages * kTile, "same B region in both forms");
+  uint8_t* BS = smem + 2 * kABytes;         // B tile stages
   uint64_t* full = reinterpret_cast<uint64_t*>(BS + kStages * kTile);
-  uint64_t* empty = full + NB;
-  uint64_t* xfull = empty + NB;
+  uint64_t* empty = full + kStages;
+  uint64_t* xfull = empty + kStages;
   uint64_t* uready = xfull + 1;             // all 512 bytes of u written
   uint64_t* tfull = uready + 1;             // [2] per TMEM buffer
   uint64_t* tempty = tfull + 2;             // [2]
@@ -355,7 +296,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     tma_prefetch(&mapYp);
     tma_prefetch(&mapY);
     tma_prefetch(&mapN);
-    for (int s = 0; s < NB; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -378,24 +319,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
   const int64_t row0 = (int64_t)blockIdx.x * kRows;
 
   if (warp == 0) {
-    if (lane == 0 && STRIP) {
-      // ---------------- TMA producer: three strips of half-tiles per position ----------------
-      const uint64_t pol = l2_evict_last();
-      const int64_t cpos = (int64_t)client * npos;
-      uint32_t eph[kSlots] = {0, 0, 0, 0, 0, 0};
-      for (int pos = pos0; pos < pos1; ++pos)
-        for (int ph = 0; ph < 3; ++ph) {
-          const int nh = halfs(ph);
-          const CUtensorMap* map = ph == 0 ? &mapYp : ph == 1 ? &mapY : &mapN;
-          const int64_t row0 = ph == 2 ? (int64_t)client * nh * 128 : ((cpos + pos) * nh) * 128;
-          for (int h = 0; h < nh; ++h) {
-            mbar_wait(&empty[h], eph[h] ^ 1);
-            eph[h] ^= 1;
-            mbar_expect_tx(&full[h], kHalf);
-            tma_load_2d_hint(BS + h * kHalf, map, &full[h], 0, (int)(row0 + 128 * h), pol);
-          }
-        }
-    } else if (lane == 0) {
+    if (lane == 0) {
       // ---------------- TMA producer: the 20 B tiles of every position ----------------
       const uint64_t pol = l2_evict_last();
       const int64_t cpos = (int64_t)client * npos;
@@ -422,45 +346,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         }
     }
   } else if (warp == 1) {
-    if (lane == 0 && STRIP) {
-      // ---------------- MMA issuer, strip form: the static step table ----------------
-      const uint32_t idesc = idesc_u8(kRows, 256);
-      uint32_t fph[kSlots] = {0, 0, 0, 0, 0, 0};
-      uint32_t teph[2] = {0, 0}, xph = 0;
-      for (int pos = pos0; pos < pos1; ++pos) {
-        const bool first_pos = pos == pos0;
-        for (int s = 0; s < kNSteps; ++s) {
-          const SStep st = kSSched[s];
-          if (((st.wait & 1) && !first_pos) || (st.wait & 16)) {
-            mbar_wait(&tempty[0], teph[0]);
-            teph[0] ^= 1;
-          }
-          if (((st.wait & 2) && !first_pos) || (st.wait & 32)) {
-            mbar_wait(&tempty[1], teph[1]);
-            teph[1] ^= 1;
-          }
-          if (st.wait & 4) mbar_wait(xfull, xph);
-          if (st.wait & 8) mbar_wait(uready, xph);
-          for (uint32_t nm = st.need; nm; nm &= nm - 1) {
-            const int h = __ffs(nm) - 1;
-            mbar_wait(&full[h], fph[h]);
-            fph[h] ^= 1;
-          }
-          tc_fence_after();
-          const uint64_t ad = desc_sw128(smem_u32((st.a ? UA : XA) + st.ka * (kRows * kBK)));
-          const uint64_t bd = desc_sw128(smem_u32(BS + st.t * kHalf));
-          const uint32_t d = tbase + (uint32_t)(st.buf * 256);
-#pragma unroll
-          for (int k = 0; k < kBK / 32; ++k)
-            umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (st.acc || k) ? 1u : 0u);
-          for (uint32_t rm = st.rel; rm; rm &= rm - 1) umma_commit(&empty[__ffs(rm) - 1]);
-          if (st.commit & 1) umma_commit(&tfull[0]);
-          if (st.commit & 2) umma_commit(&tfull[1]);
-          if (st.commit & 4) umma_commit(xfree);
-        }
-        xph ^= 1;
-      }
-    } else if (lane == 0) {
+    if (lane == 0) {
       // ---------------- MMA issuer: six segments per position, buffer = task & 1 ----------------
       const uint32_t idesc = idesc_u8(kRows, 256);
       int stage = 0;
@@ -792,7 +678,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tcp_encode() {
   return fn;
 }
 
-static int tile_map(CUtensorMap* map, const void* base, int64_t rows, int box_rows = 256) {
+static int tile_map(CUtensorMap* map, const void* base, int64_t rows) {
   auto fn = tcp_encode();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -800,7 +686,7 @@ static int tile_map(CUtensorMap* map, const void* base, int64_t rows, int box_ro
   }
   cuuint64_t dims[2] = {(cuuint64_t)tcp::kBK, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)tcp::kBK};
-  cuuint32_t box[2] = {(cuuint32_t)tcp::kBK, (cuuint32_t)box_rows};
+  cuuint32_t box[2] = {(cuuint32_t)tcp::kBK, 256};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -848,97 +734,6 @@ static int upload_schedule() {
   return kOk;
 }
 
-// The strip form's static step table (tcp::SStep): phase 0 = U0 then U1
-// (X * Y' from the Y' strip), phase 1 = H0 then H1 X * Y (Y strip), phase 2 =
-// H0 then H1 u * N (N strip); each task's k-blocks in ascending tile order, so
-// a tile's half-tile slots are waited for once and released after their last
-// reader. The tiles are those of upload_schedule().
-static int upload_strip_schedule() {
-  static bool done = false;
-  if (done) return kOk;
-  struct Raw {
-    int phase, task, a, ka, t;
-  };
-  std::vector<Raw> raw;
-  for (int gc = 0; gc < 2; ++gc) {
-    std::vector<std::pair<int, int>> kt;
-    for (int ka = 0; ka < 4; ++ka) {
-      const int delta = 256 * gc - 128 * ka;
-      const int t = (delta - tcp::kDeltaYp) / 128;
-      if (delta - 127 < 512 && delta + 255 >= 0 && t >= 0 && t < tcp::kTYp) kt.push_back({t, ka});
-    }
-    std::sort(kt.begin(), kt.end());
-    for (auto& x : kt) raw.push_back({0, gc, 0, x.second, x.first});
-  }
-  for (int a = 0; a < 2; ++a)
-    for (int hh = 0; hh < 2; ++hh) {
-      std::vector<std::pair<int, int>> kt;
-      const int c0 = 508 + 256 * hh;
-      for (int ka = 0; ka < 4; ++ka) {
-        const int delta = c0 - 128 * ka;
-        if (delta - 127 >= 512) continue;
-        kt.push_back({(delta - tcp::kDeltaY) / 128, ka});
-      }
-      std::sort(kt.begin(), kt.end());
-      for (auto& x : kt) raw.push_back({1 + a, 2 + hh, a, x.second, x.first});
-    }
-  if ((int)raw.size() != tcp::kNSteps) {
-    set_error("tc_pippenger: strip schedule has %d steps", (int)raw.size());
-    return kErrCuda;
-  }
-  tcp::SStep h[tcp::kNSteps] = {};
-  for (int i = 0; i < tcp::kNSteps; ++i) {
-    const Raw& r = raw[i];
-    tcp::SStep& st = h[i];
-    st.phase = (int8_t)r.phase;
-    st.a = (int8_t)r.a;
-    st.ka = (int8_t)r.ka;
-    st.t = (int8_t)r.t;
-    st.buf = (uint8_t)(r.task & 1);
-    bool first_task = true, last_task = true, last_phase = true;
-    for (int j = 0; j < tcp::kNSteps; ++j) {
-      if (raw[j].phase != r.phase) continue;
-      if (j < i && raw[j].task == r.task) first_task = false;
-      if (j > i && raw[j].task == r.task) last_task = false;
-      if (j > i) last_phase = false;
-    }
-    st.acc = (r.phase < 2 && first_task) ? 0 : 1;
-    if (first_task) {
-      if (r.phase == 0) st.wait = r.task == 0 ? (1 | 4) : 2;
-      else if (r.phase == 1) st.wait = r.task == 2 ? 16 : 32;
-    }
-    if (r.phase == 2 && i > 0 && raw[i - 1].phase != 2) st.wait |= 8;
-    if (last_task && r.phase != 1) st.commit |= (r.task & 1) ? 2 : 1;
-    if (r.phase == 1 && last_phase) st.commit |= 4;
-    for (int sl = r.t; sl <= r.t + 1; ++sl) {
-      bool first_use = true, last_use = true;
-      for (int j = 0; j < tcp::kNSteps; ++j) {
-        if (raw[j].phase != r.phase || (sl != raw[j].t && sl != raw[j].t + 1)) continue;
-        if (j < i) first_use = false;
-        if (j > i) last_use = false;
-      }
-      if (first_use) st.need |= (uint8_t)(1u << sl);
-      if (last_use) st.rel |= (uint8_t)(1u << sl);
-    }
-  }
-  for (int ph = 0; ph < 3; ++ph) {            // every loaded slot is read, and released once
-    unsigned need = 0, rel = 0;
-    for (auto& st : h)
-      if (st.phase == ph) {
-        need |= st.need;
-        rel |= st.rel;
-      }
-    if (need != (1u << tcp::halfs(ph)) - 1 || rel != need) {
-      set_error("tc_pippenger: strip phase %d uses slots %x", ph, need);
-      return kErrCuda;
-    }
-  }
-  if (cudaMemcpyToSymbol(tcp::kSSched, h, sizeof(h)) != cudaSuccess)
-    return check_launch("strip schedule");
-  done = true;
-  return kOk;
-}
-
 // Digits per 32-bit exponent word: 6 (widths
 // 6,6,5,5,5,5 and 63 buckets per row); balanced widths, wider digits first.
 static DigitSpec digit_spec() {
@@ -957,25 +752,13 @@ static DigitSpec digit_spec() {
   return ds;
 }
 
-// Toeplitz strips (default) or separate tiles (ZPIR_TC_STRIP=0, the round-1 form).
-static bool strip_mode() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("ZPIR_TC_STRIP");
-    v = e ? atoi(e) != 0 : 1;
-  }
-  return v != 0;
-}
-
 int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
   using namespace tcp;
   const DigitSpec ds = digit_spec();
   const int64_t npos = ds.D * n;
   const int64_t rows_p = ceil_div(rows, kRows) * kRows;
-  const int64_t toep = strip_mode()
-                           ? npos * (halfs(0) + halfs(1)) * kHalf + halfs(2) * kHalf
-                           : npos * (kTY + kTYp) * kTile + kTY * kTile;
-  return (int64_t)clients * (2 * npos * kL * 4 + toep + rows_p * ds.nb * (kL * 4 + 1));
+  return (int64_t)clients * (2 * npos * kL * 4 + npos * (kTY + kTYp) * kTile + kTY * kTile +
+                             rows_p * ds.nb * (kL * 4 + 1));
 }
 
 // W_c[rid[r] or r] (Montgomery form, 4096-bit N_c) for rows r < rows of 32-bit
@@ -993,13 +776,12 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   const int nb = ds.nb;
   const int64_t npos = ds.D * n;
   if (clients <= 0 || clients > 65535 || n <= 0 || rows <= 0 || npos > 65536 ||
-      (int64_t)clients * npos * (kTY + 1) * 256 >= (1ll << 31)) {
+      (int64_t)clients * npos * kTY * 256 >= (1ll << 31)) {
     set_error("tc_slot_fixed: bad shapes (clients=%d n=%lld rows=%lld)", clients, (long long)n,
               (long long)rows);
     return kErrInput;
   }
-  const bool strip = strip_mode();
-  if (int e = strip ? upload_strip_schedule() : upload_schedule()) return e;
+  if (int e = upload_schedule()) return e;
   {
     // keep the multi-GB workspace in the stream-ordered pool between calls
     static bool pool_set = false;
@@ -1041,15 +823,9 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   if (cudaMallocAsync(reinterpret_cast<void**>(&dcl), sizeof(TcClient) * C, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Pd), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Yp), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tY),
-                      strip ? (size_t)C * npos * halfs(1) * kHalf : (size_t)C * npos * kTY * kTile,
-                      st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tYp),
-                      strip ? (size_t)C * npos * halfs(0) * kHalf : (size_t)C * npos * kTYp * kTile,
-                      st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tN),
-                      strip ? (size_t)C * halfs(2) * kHalf : (size_t)C * kTY * kTile,
-                      st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tY), (size_t)C * npos * kTY * kTile, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tYp), (size_t)C * npos * kTYp * kTile, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&tN), (size_t)C * kTY * kTile, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * nb * kL * 4, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)C * rows_p * nb, st) != cudaSuccess)
     return fail("workspace allocation");
@@ -1059,43 +835,28 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
     return fail("client table / flags");
   powtab_kernel<<<dim3((unsigned)ceil_div(n, 4), C), 128, 0, st>>>(dcl, n, ds, Pd);
   mul_lo_kernel<<<dim3((unsigned)ceil_div(npos, 128), C), 128, 0, st>>>(dcl, Pd, npos, Yp);
-  if (strip) {
-    toep_strip_kernel<<<dim3((unsigned)npos, C), 256, 0, st>>>(dcl, 1, Pd, npos, halfs(1), kDeltaY,
-                                                               tY);
-    toep_strip_kernel<<<dim3((unsigned)npos, C), 256, 0, st>>>(dcl, 1, Yp, npos, halfs(0),
-                                                               kDeltaYp, tYp);
-    toep_strip_kernel<<<dim3(1u, C), 256, 0, st>>>(dcl, 2, nullptr, 1, halfs(2), kDeltaY, tN);
-  } else {
-    toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 1, Pd, npos, kTY,
-                                                                       kDeltaY, tY);
-    toep_tiles_kernel<<<dim3((unsigned)(npos * kTYp), C), 256, 0, st>>>(dcl, 1, Yp, npos, kTYp,
-                                                                        kDeltaYp, tYp);
-    toep_tiles_kernel<<<dim3((unsigned)kTY, C), 256, 0, st>>>(dcl, 2, nullptr, 1, kTY, kDeltaY,
-                                                              tN);
-  }
+  toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 1, Pd, npos, kTY,
+                                                                     kDeltaY, tY);
+  toep_tiles_kernel<<<dim3((unsigned)(npos * kTYp), C), 256, 0, st>>>(dcl, 1, Yp, npos, kTYp,
+                                                                      kDeltaYp, tYp);
+  toep_tiles_kernel<<<dim3((unsigned)kTY, C), 256, 0, st>>>(dcl, 2, nullptr, 1, kTY, kDeltaY, tN);
   {
     const int64_t cnt = rows_p * nb;
     bucket_fill_kernel<<<dim3((unsigned)ceil_div(cnt * kL, 256), C), 256, 0, st>>>(dcl, Bk, cnt);
   }
   if (check_launch("tc_slot_fixed setup")) return fail("setup kernels");
   CUtensorMap mYp, mY, mN;
-  if (strip ? (tile_map(&mYp, tYp, C * npos * halfs(0) * 128, 128) ||
-               tile_map(&mY, tY, C * npos * halfs(1) * 128, 128) ||
-               tile_map(&mN, tN, (int64_t)C * halfs(2) * 128, 128))
-            : (tile_map(&mYp, tYp, C * npos * kTYp * 256) ||
-               tile_map(&mY, tY, C * npos * kTY * 256) ||
-               tile_map(&mN, tN, (int64_t)C * kTY * 256)))
+  if (tile_map(&mYp, tYp, C * npos * kTYp * 256) || tile_map(&mY, tY, C * npos * kTY * 256) ||
+      tile_map(&mN, tN, (int64_t)C * kTY * 256))
     return fail("tensor maps");
-  const int smem = strip ? kSSmem : kSmem;
-  auto kern = strip ? tc_step_kernel<true> : tc_step_kernel<false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(tc_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   // one launch walks every position (tiles are independent); chunked so a
   // launch stays well under a second
   constexpr int64_t chunk = 1024;
   const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(tiles * C, 2 * 148)));
   for (int64_t p0 = 0; p0 < npos; p0 += ck) {
     const int64_t p1 = std::min<int64_t>(npos, p0 + ck);
-    kern<<<dim3((unsigned)tiles, C), kThreads, smem, st>>>(
+    tc_step_kernel<<<dim3((unsigned)tiles, C), kThreads, kSmem, st>>>(
         mYp, mY, mN, dcl, Pd, ds, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk, Fk);
   }
   if (check_launch("tc_step")) return fail("tc_step launch");
