@@ -1012,6 +1012,9 @@ def _wire_rows(state, m, mode, ck_bytes, qu, stored, stream, on_device=False):
 MAX_BATCH = 64
 # respond_batch: queries per compression / copy-out sub-batch (host work overlaps the device)
 BATCH_SUB = 16
+# respond_batch_wire: every input is staged up front, so sub-batches only overlap
+# the copy-out with the next compression (fewer, larger compression launches)
+WIRE_BATCH_SUB = 32
 
 
 def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
@@ -1243,59 +1246,74 @@ def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep
             "o": torch.empty((nq, G, l2), dtype=torch.int32).pin_memory(),
             "qd": torch.empty((nq, lay.ld), dtype=torch.int32, device=dev),
             "cd": torch.empty((nq, n, lm), dtype=torch.int32, device=dev),
-            "ev": [torch.cuda.Event() for _ in range(-(-nq // max(1, BATCH_SUB)))],
+            "cs": torch.cuda.Stream(dev),      # host -> device copies
+            "ds": torch.cuda.Stream(dev),      # device -> host copies
         }
         tb.key = key
     B = tb.bufs
     qn = B["q"].numpy().view(np.uint32)
     cn = B["c"].numpy()
     on = B["o"].numpy().view(np.uint32)
-
-    conv = _digit_conv() or _conv_module()
+    cs, ds = B["cs"], B["ds"]
+    conv = _conv_module()
     nthr = device.host_threads()
-
-    def stage_ck(lo, hi):
-        if conv is not None and hasattr(conv, "stage_rows"):
-            conv.stage_rows(ck_bytes[lo:hi], cn[lo:hi], n * 4 * lm, n, 4 * lm, nthr, False)
-            return
-        for i in range(lo, hi):
-            ck = np.asarray(ck_bytes[i], dtype=np.uint8)
-            w = ck.shape[1]
-            cn[i, :, :w] = ck
-            cn[i, :, w:] = 0
-
-    if conv is not None and hasattr(conv, "stage_rows"):
+    fast = hasattr(conv, "stage_rows")
+    # qu0 rows -> pinned (C threads, GIL released) -> device, then ONE GEMV
+    if fast:
         conv.stage_rows(qus, qn, lay.ld * 4, 1, lay.ld * 4, nthr, True)
     else:
         for i in range(nq):
             np.copyto(qn[i, : lay.d0], np.asarray(qus[i]), casting="unsafe")
-    device.h2d_async(B["qd"], B["q"], stream)
+    cs.wait_stream(stream)
+    device.h2d_async(B["qd"], B["q"], cs)
+    ev = torch.cuda.Event()
+    ev.record(cs)
+    stream.wait_event(ev)
     b = state.gemv_batch_device(B["qd"], stream)                    # (nq, rows)
-    sub = max(1, BATCH_SUB)
+    # meanwhile every ck_o field -> pinned, then per sub-batch to the device on
+    # the copy stream (overlapping the previous sub-batch's compression)
+    if fast:
+        conv.stage_rows(ck_bytes, cn, n * 4 * lm, n, 4 * lm, nthr, False)
+    else:
+        for i in range(nq):
+            ck = np.asarray(ck_bytes[i], dtype=np.uint8)
+            cn[i, :, : ck.shape[1]] = ck
+            cn[i, :, ck.shape[1]:] = 0
+    sub = max(1, WIRE_BATCH_SUB)
+    ranges = [(lo, min(nq, lo + sub)) for lo in range(0, nq, sub)]
+    ev_c = []
+    for lo, hi in ranges:
+        device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], cs)
+        e = torch.cuda.Event()
+        e.record(cs)
+        ev_c.append(e)
     res = [None] * nq
-    for si, lo in enumerate(range(0, nq, sub)):
-        hi = min(nq, lo + sub)
-        stage_ck(lo, hi)
-        device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], stream)
+    for (lo, hi), e in zip(ranges, ev_c):
+        stream.wait_event(e)
         # t rows of lm limbs unless a COMBINED query needs them widened for combine
         t_ld = l2 if any(modes[i] == COMBINED for i in range(lo, hi)) else lm
         t = state.compress_groups_batch(B["cd"][lo:hi], b[lo:hi], ks[lo:hi], t_ld, stream)
+        outs = []
         for i in range(lo, hi):
             if modes[i] == SEPARATE:
-                r = t[i - lo]
-                L = lm
-                if t_ld == lm:                  # compact rows: copy into the row block
-                    device.d2h_async(B["o"][i].view(-1)[: G * lm], r, stream)
-                    res[i] = on[i].reshape(-1)[: G * lm].reshape(G, lm)
-                    continue
+                outs.append((i, t[i - lo], lm, t_ld == lm))
             else:
-                r = device.combine(t[i - lo], _stored_device(storeds[i], ks[i], dev, stream),
+                K = device.combine(t[i - lo], _stored_device(storeds[i], ks[i], dev, stream),
                                    ks[i], stream=stream)
-                L = l2
-            device.d2h_async(B["o"][i], r, stream)
-            res[i] = on[i, :, :L]
-        B["ev"][si].record(stream)
-    B["ev"][-1].synchronize()
+                outs.append((i, K, l2, False))
+        e = torch.cuda.Event()
+        e.record(stream)
+        ds.wait_event(e)                        # results out on the copy-back stream
+        t.record_stream(ds)
+        for i, r, L, compact in outs:
+            r.record_stream(ds)
+            if compact:                         # lm-limb rows: packed into the row block
+                device.d2h_async(B["o"][i].view(-1)[: G * lm], r, ds)
+                res[i] = on[i].reshape(-1)[: G * lm].reshape(G, lm)
+            else:
+                device.d2h_async(B["o"][i], r, ds)
+                res[i] = on[i, :, :L]
+    ds.synchronize()
     for md in modes:
         if md == COMBINED:
             counters.bump("add", lay.groups)

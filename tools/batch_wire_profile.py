@@ -31,22 +31,26 @@ cks = [np.ascontiguousarray(ints_to_limbs([r.randrange(m) for _ in range(1024)],
                             .view(np.uint8).reshape(1024, 256)) for _ in range(nq)]
 qus = [rng.integers(0, 1 << 32, bench.D0, dtype=np.uint64).astype(np.uint32) for _ in range(nq)]
 args = ([reg] * nq, [0] * nq, [z.SEPARATE] * nq, cks, qus)
-for _ in range(3):
-    z.respond_batch_wire(st, *args)
-torch.cuda.synchronize()
-ts = []
-for _ in range(10):
-    t = time.perf_counter()
-    z.respond_batch_wire(st, *args)
-    ts.append(time.perf_counter() - t)
-print(f"respond_batch_wire(64): {1e3 * min(ts):.2f} ms best, {1e3 * np.median(ts):.2f} median")
+for sub in (16, 32, 64, 32):
+    protocol.WIRE_BATCH_SUB = sub
+    for _ in range(3):
+        z.respond_batch_wire(st, *args)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(10):
+        t = time.perf_counter()
+        z.respond_batch_wire(st, *args)
+        ts.append(time.perf_counter() - t)
+    print(f"respond_batch_wire(64), sub-batches of {sub}: {1e3 * min(ts):.2f} ms best, "
+          f"{1e3 * np.median(ts):.2f} median")
 B = protocol._wire_bufs.bufs
 qn = B["q"].numpy().view(np.uint32)
 cn = B["c"].numpy()
+conv = protocol._conv_module()
 t = time.perf_counter()
-protocol._parallel(lambda i: np.copyto(qn[i, :bench.D0], qus[i], casting="unsafe"), nq)
+conv.stage_rows(qus, qn, qn.shape[1] * 4, 1, qn.shape[1] * 4, 8, True)
 t1 = time.perf_counter()
-protocol._parallel(lambda i: np.copyto(cn[i], cks[i]), nq)
+conv.stage_rows(cks, cn, 1024 * 256, 1024, 256, 8, False)
 t2 = time.perf_counter()
 print(f"staging qu {1e3 * (t1 - t):.2f} ms, ck {1e3 * (t2 - t1):.2f} ms")
 # device only
