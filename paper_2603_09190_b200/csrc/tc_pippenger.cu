@@ -44,6 +44,20 @@ namespace zpir {
 
 using namespace sm100;
 
+#ifdef ZPIR_TC_TRACE
+// debug timeline of CTA (0, 0): per position, 16 clock64 stamps (tools/tc_trace.py)
+__device__ unsigned long long g_tc_trace[64 * 16];
+#define TC_STAMP(pos, k)                                                                      \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (pos) - pos0 < 64)                              \
+      g_tc_trace[((pos) - pos0) * 16 + (k)] = clock64();                                      \
+  } while (0)
+#else
+#define TC_STAMP(pos, k) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace tcp {
 
 constexpr int kL = 128;            // limbs of N = m^2 (2048-bit m)
@@ -388,6 +402,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             }
             tc_fence_after();
             cur = st.seg;
+            if (cur < 5) TC_STAMP(pos, 11 + cur);
             first = cur <= 3;                              // u * N accumulates onto X * Y
           }
           mbar_wait(&full[stage], phase);
@@ -490,6 +505,8 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
 
     for (int pos = pos0; pos < pos1; ++pos) {
       const bool last = pos + 1 >= pos1;
+      const bool tr = threadIdx.x == 64;
+      if (tr) TC_STAMP(pos, 0);
       const int64_t bidx = (r * nb) + (dg ? dg - 1 : 0);
       uint32_t* brow = Bc + bidx * kL;
       const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
@@ -505,6 +522,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       for (int task = 0; task < 2; ++task) {
         mbar_wait(&tfull[task], fph[task]);
         fph[task] ^= 1;
+        if (tr) TC_STAMP(pos, 1 + 2 * task);
         tc_fence_after();
         const uint32_t taddr = lanebase + (uint32_t)(task * 256);
         drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
@@ -520,6 +538,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             utop = l[3];
           }
         });
+        if (tr) TC_STAMP(pos, 2 + 2 * task);
         if (task == 1) {
           fence_async_smem();
           mbar_arrive(uready);
@@ -532,23 +551,33 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       if (!last) {
         mbar_wait(xfree, xfph);
         xfph ^= 1;
+        if (tr) TC_STAMP(pos, 5);
         gather_issue(dg_n, conflict);
       }
       // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
-      uint32_t pend[4] = {0u, 0u, 0u, 0u};      // Z limbs awaiting a 16-byte store
-      auto emit = [&](int li) {               // limbs li-3..li complete
+      // Z limbs awaiting a 32-byte store (one 256-bit STG per 8 limbs: whole
+      // sectors, half the store instructions of 16-byte stores)
+      uint32_t pend[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      auto emit = [&](int li) {               // limbs li-7..li complete
         if (dg)
-          *reinterpret_cast<uint4*>(brow + li - 3) = make_uint4(pend[0], pend[1], pend[2], pend[3]);
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + li - 7),
+                       "r"(pend[0]), "r"(pend[1]), "r"(pend[2]), "r"(pend[3]), "r"(pend[4]),
+                       "r"(pend[5]), "r"(pend[6]), "r"(pend[7])
+                       : "memory");
         if (conflict) {
-          const int cc = (li - 3) >> 2, kb = cc >> 3, ch = cc & 7;
-          *reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
-              make_uint4(pend[0], pend[1], pend[2], pend[3]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = ((li - 7) >> 2) + h, kb = cc >> 3, ch = cc & 7;
+            *reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
+                make_uint4(pend[4 * h], pend[4 * h + 1], pend[4 * h + 2], pend[4 * h + 3]);
+          }
         }
       };
       carry = 0;
       {
         mbar_wait(&tfull[0], fph[0]);
         fph[0] ^= 1;
+        if (tr) TC_STAMP(pos, 6);
         tc_fence_after();
         const uint32_t taddr = lanebase;
         drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
@@ -564,26 +593,29 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
               continue;
             }
             const int li = slot - 1;           // Z limb
-            pend[li & 3] = limb4(v + 4 * k, carry);
-            if ((li & 3) == 3) emit(li);
+            pend[li & 7] = limb4(v + 4 * k, carry);
+            if ((li & 7) == 7) emit(li);
           }
         });
+        if (tr) TC_STAMP(pos, 7);
         tc_fence_before();
         mbar_arrive(&tempty[0]);
       }
       {
         mbar_wait(&tfull[1], fph[1]);
         fph[1] ^= 1;
+        if (tr) TC_STAMP(pos, 8);
         tc_fence_after();
         const uint32_t taddr = lanebase + 256u;
         drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             const int li = 63 + 8 * g + k;     // columns 764 + 4 (li - 63) ..
-            pend[li & 3] = limb4(v + 4 * k, carry);
-            if ((li & 3) == 3) emit(li);
+            pend[li & 7] = limb4(v + 4 * k, carry);
+            if ((li & 7) == 7) emit(li);
           }
         });
+        if (tr) TC_STAMP(pos, 9);
         tc_fence_before();
         mbar_arrive(&tempty[1]);
       }
@@ -600,7 +632,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
                                      ((unsigned long long)c2 << 16) + carry;
         const uint32_t z = (uint32_t)s;
         const uint32_t top = (uint32_t)(s >> 32);
-        pend[3] = z;
+        pend[7] = z;
         emit(kL - 1);
         // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or z >= N,
         // decided by the top two limbs unless both equal N's (then by all of
@@ -609,8 +641,8 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         uint32_t f;
         if (top) {
           f = 1u;
-        } else if (pend[3] != ntop || pend[2] != n126) {
-          f = (pend[3] > ntop || (pend[3] == ntop && pend[2] > n126)) ? 1u : 0u;
+        } else if (pend[7] != ntop || pend[6] != n126) {
+          f = (pend[7] > ntop || (pend[7] == ntop && pend[6] > n126)) ? 1u : 0u;
         } else {
           f = 1u;                                // z == N so far: equal counts as >=
           const uint32_t* zs = conflict ? nullptr : brow;
@@ -650,6 +682,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       }
       if (!last) {
         gather_finish(lazy_n);                  // + xfull for the next position
+        if (tr) TC_STAMP(pos, 10);
         xtop = *xtop_p;
         dg = dg_n;
         dg_n = pos + 2 < pos1 ? digit_at(pos + 2) : 0u;
@@ -866,6 +899,12 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   release();
   return check_launch("tc_slot_fixed");
 }
+
+#ifdef ZPIR_TC_TRACE
+extern "C" int zpir_tc_trace(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tc_trace, sizeof(g_tc_trace)) == cudaSuccess ? 0 : 2;
+}
+#endif
 
 // Single-client form (the original entry point).
 int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
