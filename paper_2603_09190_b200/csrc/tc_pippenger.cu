@@ -468,7 +468,9 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     };
     // copies landed; lazily reduced buckets: a set flag means the stored value
     // is Z with Z - N still to be taken (mod R)
-    auto gather_finish = [&](uint32_t lz) {
+    // gather_land: the copies landed, lazily reduced buckets reduced in place;
+    // gather_publish: X complete (conflict rows forwarded) -> the MMA warp
+    auto gather_land = [&](uint32_t lz) {
       asm volatile("cp.async.wait_all;" ::: "memory");
       __syncwarp();
       uint32_t lzm = __ballot_sync(0xffffffffu, lz != 0);
@@ -481,9 +483,15 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         big_cond_sub<4>(v, 1u, nl, lane);       // x - N mod R (warp-uniform)
         *reinterpret_cast<uint4*>(q) = make_uint4(v[0], v[1], v[2], v[3]);
       }
+    };
+    auto gather_publish = [&]() {
       fence_async_smem();
       mbar_arrive(xfull);
       __syncwarp();
+    };
+    auto gather_finish = [&](uint32_t lz) {
+      gather_land(lz);
+      gather_publish();
     };
     // bytes 508..511 of this row's X (k-block 3, chunk 7)
     const uint32_t* xtop_p =
@@ -553,6 +561,9 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         xfph ^= 1;
         if (tr) TC_STAMP(pos, 5);
         gather_issue(dg_n, conflict);
+        // land + reduce the gathered rows now: the epilogue would otherwise
+        // idle until H0 is computed, and this work leaves the critical path
+        gather_land(lazy_n);
       }
       // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
       // Z limbs awaiting a 32-byte store (one 256-bit STG per 8 limbs: whole
@@ -681,7 +692,7 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
         }
       }
       if (!last) {
-        gather_finish(lazy_n);                  // + xfull for the next position
+        gather_publish();                       // xfull for the next position
         if (tr) TC_STAMP(pos, 10);
         xtop = *xtop_p;
         dg = dg_n;
