@@ -212,6 +212,13 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
                       int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
                       int gamma_bits, uint32_t* out, void* stream);
+/* zpir_slot_combine for `clients` keys of the same width in one launch (host
+ * arrays of device pointers W / N / out and of n' values; shared group ids):
+ * the hint worker's batch (protocol.hints). */
+int zpir_slot_combine_many(int clients, const uint32_t* const* W, const uint32_t* const* N,
+                           const uint32_t* np, uint32_t* const* out, int cap,
+                           const int32_t* group_ids, int64_t ngroups, int limbs,
+                           const uint32_t* gamma, int gamma_bits, void* stream);
 /* Group stage for a general batch scale gamma (not 2^32 / 2^64):
  * t[g] = sum_j (gamma^j mod m) ((b[c] & qmask) + z[c]) mod m, with
  * ctab[j] = {gamma^j R mod m, gamma^j R^2 mod m} (lm limbs each) and w a

@@ -76,6 +76,8 @@ _SIGS = {
     "zpir_multiexp_rows": ([_p, _c_i64, _p, _p, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int,
                             _p, _c_u32, _p, _p, _c_int, _p, _p, _c_i64, _p], _c_int),
     "zpir_slot_combine": ([_p, _c_int, _p, _c_i64, _c_int, _p, _c_u32, _p, _c_int, _p, _p], _c_int),
+    "zpir_slot_combine_many": ([_c_int, _p, _p, _p, _p, _c_int, _p, _c_i64, _c_int, _p, _c_int, _p],
+                               _c_int),
     "zpir_answer_general": ([_p, _p, _c_u32, _c_i64, _c_int, _c_i64, _c_int, _p, _c_u32, _p, _p, _p,
                              _c_i64, _p], _c_int),
     "zpir_pow8_table": ([_p, _c_i64, _c_int, _p, _c_u32, _p, _p, _p], _c_int),

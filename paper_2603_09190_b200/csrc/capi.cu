@@ -67,6 +67,9 @@ int umma_probe(int, int, int, float*);
 int multiexp_rows_launch(const uint32_t*, int64_t, const uint32_t*, const int32_t*, int64_t, int64_t,
                          int64_t, int64_t, int, int, const uint32_t*, uint32_t, const uint32_t*,
                          const uint32_t*, int, uint32_t*, void*, int64_t, cudaStream_t);
+int slot_combine_many_launch(int, const uint32_t* const*, const uint32_t* const*, const uint32_t*,
+                             uint32_t* const*, int, const int32_t*, int64_t, int, const uint32_t*,
+                             int, cudaStream_t);
 int slot_combine_launch(const uint32_t*, int, const int32_t*, int64_t, int, const uint32_t*,
                         uint32_t, const uint32_t*, int, uint32_t*, cudaStream_t);
 int answer_general_launch(const uint32_t*, const uint32_t*, uint32_t, int64_t, int, int64_t, int,
@@ -279,6 +282,14 @@ int zpir_multiexp_rows(const uint32_t* bases, int64_t n, const uint32_t* exps,
   ZPIR_GUARD(multiexp_rows_launch(bases, n, exps, row_ids, rows, row_stride, base_stride,
                                   limb_stride, elimbs, limbs, N, np, r2, one_m, keep_mont, out,
                                   workspace, ws_bytes, S(stream)));
+}
+
+int zpir_slot_combine_many(int clients, const uint32_t* const* W, const uint32_t* const* N,
+                           const uint32_t* np, uint32_t* const* out, int cap,
+                           const int32_t* group_ids, int64_t ngroups, int limbs,
+                           const uint32_t* gamma, int gamma_bits, void* stream) {
+  ZPIR_GUARD(slot_combine_many_launch(clients, W, N, np, out, cap, group_ids, ngroups, limbs,
+                                      gamma, gamma_bits, S(stream)));
 }
 
 int zpir_slot_combine(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,

@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <vector>
+
 #include "bignum.cuh"
 
 namespace zpir {
@@ -176,11 +178,18 @@ struct GammaExp {
   int nbits;
 };
 
+// One client's slot-combine operands (the batched launch reads them per blockIdx.y).
+struct SlotClient {
+  const uint32_t* W;
+  const uint32_t* N;
+  uint32_t* out;
+  uint32_t np;
+};
+
 template <int LPL>
 __global__ void __launch_bounds__(128)
-slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __restrict__ group_ids,
-                    int64_t ngroups, const uint32_t* __restrict__ N, uint32_t np,
-                    uint32_t* __restrict__ out, GammaExp gm) {
+slot_combine_kernel(const SlotClient* __restrict__ cls, SlotClient one, int cap,
+                    const int32_t* __restrict__ group_ids, int64_t ngroups, GammaExp gm) {
   constexpr int L = 32 * LPL;
 // latency-bound (one warp per group, few groups): the 4x-unrolled CIOS is
 // 17.4 -> 15.1 ms for one client at 1 GiB (tools/slot_probe.py, bit-identical)
@@ -188,10 +197,12 @@ slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __re
   const int lane = threadIdx.x & 31;
   const int64_t gi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gi >= ngroups) return;
+  const SlotClient c = cls ? cls[blockIdx.y] : one;
+  const uint32_t np = c.np;
   const int64_t g = group_ids ? (int64_t)group_ids[gi] : gi;
   uint32_t n_[LPL], acc[LPL], x[LPL];
-  big_load<LPL>(n_, N, lane);
-  const uint32_t* Wg = W + (size_t)g * cap * L;
+  big_load<LPL>(n_, c.N, lane);
+  const uint32_t* Wg = c.W + (size_t)g * cap * L;
   big_load<LPL>(acc, Wg + (size_t)(cap - 1) * L, lane);
   uint32_t base[LPL];
   for (int j = cap - 2; j >= 0; --j) {
@@ -206,7 +217,7 @@ slot_combine_kernel(const uint32_t* __restrict__ W, int cap, const int32_t* __re
   }
   big_set_small<LPL>(x, 1, lane);
   MM(acc, acc, x, n_, np, lane);  // leave Montgomery form
-  big_store<LPL>(out + g * L, acc, lane);
+  big_store<LPL>(c.out + g * L, acc, lane);
 }
 #undef MM
 
@@ -487,21 +498,55 @@ int slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t r
   return check_launch("slot_fixed");
 }
 
-int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
-                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
-                        int gamma_bits, uint32_t* out, cudaStream_t st) {
-  if (limbs % 32 || cap <= 0 || ngroups <= 0 || gamma_bits < 1 || gamma_bits > 256) {
-    set_error("slot_combine: bad shapes (gamma_bits=%d)", gamma_bits);
+static int slot_combine_run(const SlotClient* cls, SlotClient one, int clients, int cap,
+                            const int32_t* group_ids, int64_t ngroups, int limbs,
+                            const uint32_t* gamma, int gamma_bits, cudaStream_t st) {
+  if (limbs % 32 || cap <= 0 || ngroups <= 0 || gamma_bits < 1 || gamma_bits > 256 ||
+      clients <= 0 || clients > 65535) {
+    set_error("slot_combine: bad shapes (gamma_bits=%d clients=%d)", gamma_bits, clients);
     return kErrInput;
   }
   GammaExp gm{};
   for (int i = 0; i < (gamma_bits + 31) / 32; ++i) gm.w[i] = gamma[i];
   gm.nbits = gamma_bits;
+  const dim3 grid((unsigned)ceil_div(ngroups, 4), (unsigned)clients);
   ZPIR_LPL_DISPATCH2(limbs / 32, {
-    slot_combine_kernel<LPL><<<(unsigned)ceil_div(ngroups, 4), 128, 0, st>>>(
-        W, cap, group_ids, ngroups, N, np, out, gm);
+    slot_combine_kernel<LPL><<<grid, 128, 0, st>>>(cls, one, cap, group_ids, ngroups, gm);
   });
   return check_launch("slot_combine");
+}
+
+int slot_combine_launch(const uint32_t* W, int cap, const int32_t* group_ids, int64_t ngroups,
+                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* gamma,
+                        int gamma_bits, uint32_t* out, cudaStream_t st) {
+  const SlotClient one{W, N, out, np};
+  return slot_combine_run(nullptr, one, 1, cap, group_ids, ngroups, limbs, gamma, gamma_bits, st);
+}
+
+// Several clients (same key width, same groups) in one launch, blockIdx.y =
+// client: the latency-bound Horner chains of all clients fill the GPU together.
+int slot_combine_many_launch(int clients, const uint32_t* const* W, const uint32_t* const* N,
+                             const uint32_t* np, uint32_t* const* out, int cap,
+                             const int32_t* group_ids, int64_t ngroups, int limbs,
+                             const uint32_t* gamma, int gamma_bits, cudaStream_t st) {
+  if (clients <= 0) {
+    set_error("slot_combine_many: no clients");
+    return kErrInput;
+  }
+  std::vector<SlotClient> h(clients);
+  for (int c = 0; c < clients; ++c) h[c] = {W[c], N[c], out[c], np[c]};
+  SlotClient* d = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&d), sizeof(SlotClient) * clients, st) !=
+          cudaSuccess ||
+      cudaMemcpyAsync(d, h.data(), sizeof(SlotClient) * clients, cudaMemcpyHostToDevice, st) !=
+          cudaSuccess) {
+    if (d) cudaFreeAsync(d, st);
+    return check_launch("slot_combine_many setup");
+  }
+  const int rc = slot_combine_run(d, h[0], clients, cap, group_ids, ngroups, limbs, gamma,
+                                  gamma_bits, st);
+  cudaFreeAsync(d, st);
+  return rc;
 }
 
 }  // namespace zpir

@@ -282,6 +282,23 @@ def slot_combine(W, cap, group_ids, ngroups, kctx, out, gamma=1 << 32, stream=No
     return out
 
 
+def slot_combine_many(jobs, cap, group_ids, ngroups, gamma=1 << 32, stream=None):
+    """slot_combine for several clients of one key width in one launch.
+    jobs: [(W, kctx, out)]."""
+    import ctypes
+    c = len(jobs)
+    arr = lambda vals: (ctypes.c_uint64 * c)(*vals)  # noqa: E731
+    W = arr([w.data_ptr() for w, _, _ in jobs])
+    N = arr([k.d_m2.data_ptr() for _, k, _ in jobs])
+    out = arr([o.data_ptr() for _, _, o in jobs])
+    np_ = (ctypes.c_uint32 * c)(*[k.c2.np for _, k, _ in jobs])
+    gw = np.frombuffer(int(gamma).to_bytes(32, "little"), dtype="<u4").copy()
+    _lib.call("zpir_slot_combine_many", c, W, N, np_, out, cap,
+              _lib.ptr(group_ids) if group_ids is not None else None, ngroups, jobs[0][1].l2,
+              gw.ctypes.data_as(ctypes.c_void_p), int(gamma).bit_length(), _s(stream))
+    return [o for _, _, o in jobs]
+
+
 def answer_general(z, b, qmask, d1, cap, groups, kctx, gamma, t_ld, stream=None):
     """Group stage for a general batch scale gamma (per-row weights)."""
     lm = kctx.lm

@@ -637,24 +637,35 @@ def hints(state: ServerGlobalState, jobs, stream=None, keep_slots: bool = False)
             continue
         tc_ids.update(id(j[2]) for j in batch)
     # the per-client group recombination (slot_combine: one warp per group, a
-    # 32 * cap-deep Horner chain) is latency bound for one client; several
-    # clients' run side by side on a small stream pool
-    side = [stream] if len(jobs) == 1 else _side_streams(dev, min(4, len(jobs)))
+    # 32 * cap-deep Horner chain) is latency bound for one client: the clients
+    # of the tensor-core batch run in one launch (blockIdx.y = client, grouped by
+    # key width); the IMAD-path clients (slot_fixed + slot_combine each) side by
+    # side on a small stream pool
+    out = {}
+    by_width = {}
+    for (P, kctx, W) in prep:
+        if id(W) in tc_ids:
+            k = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
+            out[id(W)] = k
+            by_width.setdefault(kctx.l2, []).append((W, kctx, k))
+    for group in by_width.values():
+        device.slot_combine_many(group, lay.cap, None, lay.groups, lay.gamma, stream)
+    rest = [j for j in prep if id(j[2]) not in tc_ids]
+    side = [stream] if len(rest) <= 1 else _side_streams(dev, min(4, len(rest)))
     ev = torch.cuda.Event()
     ev.record(stream)
-    out = []
-    for i, ((reg, qi), (P, kctx, W)) in enumerate(zip(jobs, prep)):
+    for i, (P, kctx, W) in enumerate(rest):
         st = side[i % len(side)]
         if st is not stream:
             st.wait_event(ev)
-        if id(W) not in tc_ids:
-            device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, st)
+        device.slot_fixed(P, lay.n, state.H_dev, lay.n, None, nslot, kctx, W, st)
         k = torch.empty((lay.groups, kctx.l2), dtype=torch.int32, device=dev)
         device.slot_combine(W, lay.cap, None, lay.groups, kctx, k, lay.gamma, st)
-        out.append(k)
+        out[id(W)] = k
     for st in side:
         if st is not stream:
             stream.wait_stream(st)
+    out = [out[id(W)] for _, _, W in prep]
     res = []
     for (reg, qi), (P, kctx, W), k in zip(jobs, prep, out):
         entries = limbs_to_ints(_d2h_u32(k, "hint", stream))
@@ -732,8 +743,11 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
                 log.warning("tensor-core refresh of %d fell back to IMAD: %s", len(batch), e)
                 for P, kctx, W in batch:
                     device.slot_fixed(P, lay.n, state.H_dev, lay.n, rid, rows, kctx, W, main)
+        by_width = {}
         for (W, k), kctx in zip(outs, kctxs):
-            device.slot_combine(W, lay.cap, gid, ng, kctx, k, lay.gamma, main)
+            by_width.setdefault(kctx.l2, []).append((W, kctx, k))
+        for group in by_width.values():
+            device.slot_combine_many(group, lay.cap, gid, ng, lay.gamma, main)
     else:
         streams = [main] if len(pairs) == 1 else _side_streams(dev, min(nstreams, len(pairs)))
         ev = torch.cuda.Event()
