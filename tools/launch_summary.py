@@ -16,7 +16,8 @@ if a.tail:
 agg = collections.OrderedDict()
 for r in rows:
     k = r["Kernel Name"].split("(")[0][:60]
-    v = float(r["Metric Value"]) / (1000.0 if r["Metric Unit"] == "nsecond" else 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
+    v = float(r["Metric Value"].replace(",", "")) * scale.get(r["Metric Unit"], 1e-3)
     c, t = agg.get(k, (0, 0.0))
     agg[k] = (c + 1, t + v)
 tot = sum(t for c, t in agg.values())
