@@ -46,6 +46,8 @@ for n in ("chacha_below", "pow8_table", "slot_fixed_tc_many", "slot_combine_many
 wrap(protocol, "_d2h_u32")
 wrap(protocol, "key_ctx")
 torch.cuda.synchronize()
+start = torch.cuda.Event(enable_timing=True)
+start.record(torch.cuda.current_stream())
 t0 = time.perf_counter()
 z.hints(st, [(r, 0) for r in regs])
 torch.cuda.synchronize()
@@ -54,4 +56,7 @@ print(f"hints(16): {wall:.3f} s wall, {wall / 16:.4f} s per client")
 for name, v in rec.items():
     dev = sum(e0.elapsed_time(e1) for e0, e1, _ in v)
     host = sum(h for _, _, h in v)
-    print(f"{name:22s} calls {len(v):3d} device(stream) {dev:9.1f} ms  host {1e3 * host:9.1f} ms")
+    first = start.elapsed_time(v[0][0])
+    last = start.elapsed_time(v[-1][1])
+    print(f"{name:22s} calls {len(v):3d} device(stream) {dev:9.1f} ms  host {1e3 * host:9.1f} ms"
+          f"  span {first:8.1f} .. {last:8.1f} ms after start")
