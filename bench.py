@@ -872,11 +872,6 @@ def run_extra(args):
         torch.cuda.synchronize()
         single = time.perf_counter() - t1
         ref_mulmods = 361620 * params.d1_prime
-        imad = None
-        try:
-            imad = json.load(open(os.path.join(ROOT, "profiles", "imad_peak.json")))["imad_per_s"]
-        except Exception:
-            pass
         per = t_all / nclients
         out = {"workload": "BASELINE configs[4]: global H = DB A (1 GiB, n=1024) + compressed hints "
                            "(521 entries, 2048-bit) for 256 client keys"
@@ -889,9 +884,7 @@ def run_extra(args):
                "hint_single_client_s": single,
                "schedule": f"protocol.hints in batches of {batch} clients (the hint worker's batch), "
                            "tensor-core Pippenger",
-               "reference_equivalent_mulmods_per_s": ref_mulmods / per,
-               "imad_peak_per_s": imad,
-               "imad_util_reference_equivalent": (ref_mulmods / per * 65792 / imad) if imad else None}
+               "reference_equivalent_mulmods_per_s": ref_mulmods / per}
         if keep:
             rng = np.random.default_rng(77)
             rows = np.sort(rng.choice(D1, size=D1 // 100, replace=False))
