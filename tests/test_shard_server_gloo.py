@@ -149,7 +149,7 @@ def _run(rank, out, cfg):
         return
     checks = {}
     try:
-        assert params.d1_prime >= 3 and srv.world == 2
+        assert params.d1_prime >= 3 and srv.world == dist.get_world_size()
         r = random.Random(11)
         sk, seed = client.setup(BITS, r)
         pk = z.PaillierPublicKey(sk.m, sk.m.bit_length())
@@ -192,7 +192,7 @@ def _run(rank, out, cfg):
         # errors map as the reference's (ValueError on dimensions)
         with pytest.raises(ValueError):
             srv.answer(cid, z.QueryMessage(cid, 0, z.SEPARATE, [1] * (N - 1), np.zeros(D0)))
-        checks["world"] = srv.world == 2 and srv.gmax >= 1
+        checks["world"] = srv.world == dist.get_world_size() and srv.gmax >= 1
     finally:
         srv.close()
     out.put(("ok", checks))
@@ -203,11 +203,11 @@ def _A(params):
     return ref.public_matrix(params.a_seed, params.d0, params.lwe.n, params.lwe.q)
 
 
-def run_two_ranks(cfg, timeout=300):
+def run_two_ranks(cfg, timeout=300, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, cfg)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, cfg)) for r in range(world)]
     for p in procs:
         p.start()
     res = q.get(timeout=timeout)
@@ -221,3 +221,9 @@ def run_two_ranks(cfg, timeout=300):
 
 def test_sharded_pirserver_full_api_gloo():
     run_two_ranks(CPU_CFG)
+
+
+def test_sharded_pirserver_three_ranks_uneven_groups():
+    """Three ranks over 6 groups of 7 rows minus a partial last group (d1 = 40):
+    uneven row counts per shard, the same bit-exact API run."""
+    run_two_ranks(CPU_CFG, world=3)
