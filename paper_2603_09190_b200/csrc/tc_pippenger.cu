@@ -367,6 +367,9 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       uint32_t phase = 0, xph = 0;
       uint32_t eph[2] = {0, 0};
       bool used0 = false, used1 = false;
+#ifdef ZPIR_TC_TRACE
+      unsigned long long fwait = 0;   // cycles the MMA thread waited for B tiles this position
+#endif
       for (int pos = pos0; pos < pos1; ++pos) {
         int cur = -1;
         bool first = true;
@@ -402,10 +405,16 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
             }
             tc_fence_after();
             cur = st.seg;
-            if (cur < 5) TC_STAMP(pos, 11 + cur);
+            if (cur < 4) TC_STAMP(pos, 11 + cur);
             first = cur <= 3;                              // u * N accumulates onto X * Y
           }
+#ifdef ZPIR_TC_TRACE
+          const unsigned long long tw0 = clock64();
           mbar_wait(&full[stage], phase);
+          fwait += clock64() - tw0;
+#else
+          mbar_wait(&full[stage], phase);
+#endif
           tc_fence_after();
           const uint32_t a0 = smem_u32((st.a ? UA : XA) + st.ka * (kRows * kBK));
           const uint64_t ad = desc_sw128(a0);
@@ -422,6 +431,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
           }
         }
         umma_commit(&tfull[1]);                            // H1
+#ifdef ZPIR_TC_TRACE
+        if (blockIdx.x == 0 && blockIdx.y == 0 && pos - pos0 < 64) g_tc_trace[(pos - pos0) * 16 + 15] = fwait;
+        fwait = 0;
+#endif
         xph ^= 1;
       }
     }

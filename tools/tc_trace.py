@@ -30,11 +30,17 @@ rc = _lib.lib().zpir_tc_trace(buf)
 assert rc == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
 names = ["start", "U0rdy", "U0drn", "U1rdy", "U1drn", "xfree", "H0rdy", "H0drn", "H1rdy", "H1drn",
-         "gathr", "m:U0", "m:U1", "m:H0xy", "m:H1xy", "m:H0uN"]
+         "gathr", "m:U0", "m:U1", "m:H0xy", "m:H1xy", "Bwait"]
 print("pos " + " ".join(f"{n:>7s}" for n in names) + "  period")
 for p in range(1, 40):
     rel = t[p] - t[p, 0]
+    rel[15] = t[p, 15]          # cumulative B-tile wait of the MMA thread (cycles)
     per = t[p + 1, 0] - t[p, 0] if p + 1 < 64 else 0
     print(f"{p:3d} " + " ".join(f"{int(x):7d}" for x in rel) + f"  {int(per):7d}")
-med = np.median(np.stack([t[p] - t[p, 0] for p in range(2, 60)]), axis=0)
+rows = []
+for p in range(2, 60):
+    rr = t[p] - t[p, 0]
+    rr[15] = t[p, 15]
+    rows.append(rr)
+med = np.median(np.stack(rows), axis=0)
 print("med " + " ".join(f"{int(x):7d}" for x in med) + f"  {int(np.median(np.diff(t[2:60, 0]))):7d}")
