@@ -239,27 +239,28 @@ int zpir_slot_fixed(const uint32_t* P, int64_t n, const uint32_t* exps, int64_t 
                     uint32_t np, const uint32_t* one_m, uint32_t* W, void* stream);
 /* zpir_slot_fixed for rows 0..rows-1 with the Pippenger bucket updates on the
  * tensor cores (position-major: each position multiplies one bucket per row by
- * the same P[pos]; Montgomery by a fixed multiplier = three byte-Toeplitz int8
- * GEMMs); 4096-bit N only (limbs = 128). Nprime = -N^-1 mod 2^4096 (128 limbs).
+ * the same y = P[pos]; X y mod N = sum_i x_i (y 256^i mod N) over the bytes x_i
+ * of X is one int8 GEMM against the table of reduced byte shifts of y, left
+ * unreduced in 515 bytes); 4096-bit N only (limbs = 128).
  * P is the pow8 table of zpir_pow8_table (only its first n entries, the
  * Montgomery bases, are read). Transient workspace:
- * zpir_slot_fixed_tc_workspace(n, rows, 1) bytes (~32 KB per row + ~1.8 GB per
+ * zpir_slot_fixed_tc_workspace(n, rows, 1) bytes (~34 KB per row + ~1.7 GB per
  * client at n = 1024). */
 int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
-                       const uint32_t* Nprime, uint32_t* W, void* stream);
+                       uint32_t* W, void* stream);
 /* zpir_slot_fixed_tc for `clients` independent keys in one launch (the hint
  * worker's batch; also the incremental refresh): client c's table P[c]
- * (4n x 128 limbs), N[c] / one_m[c] / Nprime[c] (128 limbs each) and output
+ * (4n x 128 limbs), N[c] / one_m[c] (128 limbs each) and output
  * rows W[c] are device addresses passed in HOST arrays; np is a host array.
  * Rows r < rows read exponent row e = row_ids ? row_ids[r] : r and write
  * W[c][e]. Replaces paillier.multiexp (paillier.py:134-193) as called by
  * protocol.hint (protocol.py:291-296) for each client of a batch.
  * Transient workspace: zpir_slot_fixed_tc_workspace(n, rows, clients) bytes. */
 int zpir_slot_fixed_tc_many(int clients, const uint64_t* P, const uint64_t* N, const uint32_t* np,
-                            const uint64_t* one_m, const uint64_t* Nprime, const uint64_t* W,
-                            int64_t n, const uint32_t* E, int64_t rs, const int32_t* row_ids,
-                            int64_t rows, void* stream);
+                            const uint64_t* one_m, const uint64_t* W, int64_t n,
+                            const uint32_t* E, int64_t rs, const int32_t* row_ids, int64_t rows,
+                            void* stream);
 int64_t zpir_slot_fixed_tc_workspace(int64_t n, int64_t rows, int clients);
 /* flags[r] = (row r of a != row r of b), rows of ld bytes. */
 int zpir_rows_differ(const uint8_t* a, const uint8_t* b, int64_t rows, int64_t ld, uint32_t* flags,

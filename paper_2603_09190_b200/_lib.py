@@ -98,10 +98,10 @@ _SIGS = {
     "zpir_memcpy_async": ([_p, _p, _c_i64, _c_int, _p], _c_int),
     "zpir_probe_imad": ([_c_int, _c_int, ctypes.POINTER(ctypes.c_float)], _c_int),
     "zpir_h_planes": ([_p, _c_i64, _c_i64, _p, _p], _c_int),
-    "zpir_slot_fixed_tc": ([_p, _c_i64, _p, _c_i64, _c_i64, _c_int, _p, _c_u32, _p, _p, _p, _p],
+    "zpir_slot_fixed_tc": ([_p, _c_i64, _p, _c_i64, _c_i64, _c_int, _p, _c_u32, _p, _p, _p],
                            _c_int),
-    "zpir_slot_fixed_tc_many": ([_c_int, _p, _p, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _c_i64,
-                                 _p], _c_int),
+    "zpir_slot_fixed_tc_many": ([_c_int, _p, _p, _p, _p, _p, _c_i64, _p, _c_i64, _p, _c_i64, _p],
+                                _c_int),
     "zpir_slot_fixed_tc_workspace": ([_c_i64, _c_i64, _c_int], _c_i64),
     "zpir_build_bcp": ([_p, _c_i64, _c_int, _c_int, _p, _p], _c_int),
     "zpir_umma_answer_rows_planar": ([_p, _c_i64, _c_i64, _p, _c_int, _c_int, _c_int, _p, _c_int,

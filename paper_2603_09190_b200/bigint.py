@@ -96,17 +96,6 @@ class KeyCtx:
         self._dev = dev
         self._lock = threading.Lock()
 
-    def d_nprime_full(self):
-        """-m^-2 mod R2 (R2 = 2^(32 l2)) as l2 limbs: the full Montgomery inverse
-        used by the tensor-core fixed-multiplier Montgomery product."""
-        with self._lock:
-            t = self._rpow.get("np2full")
-            if t is None:
-                R = 1 << (32 * self.l2)
-                t = self._rpow["np2full"] = self._dev(
-                    ints_to_limbs([(-pow(self.m2, -1, R)) % R], self.l2)[0])
-            return t
-
     def d_gamma_table(self, gamma: int, cap: int):
         """{gamma^j R mod m, gamma^j R^2 mod m} for j < cap (general-gamma answers)."""
         key = ("g", gamma, cap)

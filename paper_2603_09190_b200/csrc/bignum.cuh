@@ -155,6 +155,50 @@ __device__ __forceinline__ void big_cond_sub(uint32_t (&x)[LPL], uint32_t top,
   for (int i = 0; i < LPL; ++i) x[i] = ge ? d[i] : x[i];
 }
 
+// V = x + h * R (h small) to V mod N in place, given a quotient estimate q with
+// q <= floor(V / N) <= q + 1 (callers divide the top bits of V by the top bits
+// of N plus one): V - q N < 2N, then one conditional subtraction.
+template <int LPL>
+__device__ __forceinline__ void big_reduce_top(uint32_t (&x)[LPL], uint32_t h, uint32_t q,
+                                               const uint32_t (&n)[LPL], int lane) {
+  // M = q * N: lane-local limbs, the lane's high word owed to the next lane
+  uint32_t m[LPL];
+  uint64_t c = 0;
+#pragma unroll
+  for (int k = 0; k < LPL; ++k) {
+    c += (uint64_t)q * n[k];
+    m[k] = (uint32_t)c;
+    c >>= 32;
+  }
+  const uint32_t hi = (uint32_t)c;
+  uint32_t lo = __shfl_up_sync(ZPIR_FULL, hi, 1);
+  lo = lane == 0 ? 0u : lo;
+  c = lo;
+#pragma unroll
+  for (int k = 0; k < LPL; ++k) {
+    c += m[k];
+    m[k] = (uint32_t)c;
+    c >>= 32;
+  }
+  uint32_t cout;
+  const uint32_t cin = lane_carry_in(c != 0, lane_all(m, 0xffffffffu), lane, &cout);
+  lane_inc(m, cin);
+  const uint32_t mtop = __shfl_sync(ZPIR_FULL, hi, 31) + cout;   // limb L of M
+  // x <- x - M, borrow out of the top limb into h
+  uint32_t br = 0;
+#pragma unroll
+  for (int k = 0; k < LPL; ++k) {
+    const uint64_t v = (uint64_t)x[k] - m[k] - br;
+    x[k] = (uint32_t)v;
+    br = (uint32_t)(v >> 63);
+  }
+  const bool g = br != 0;
+  uint32_t bout;
+  const uint32_t bin = lane_carry_in(g, lane_all(x, 0u) && !g, lane, &bout);
+  lane_dec(x, bin);
+  big_cond_sub(x, h - mtop - bout, n, lane);
+}
+
 // t += x * y with 64-bit products (compiles to IMAD.WIDE.U32 chains); measured
 // fewer SASS instructions than an explicit PTX carry chain (measured round 1).
 template <int LPL>

@@ -52,12 +52,10 @@ int rns_residues_launch(const uint32_t*, int64_t, int64_t, int, int, const uint3
 int multiexp_opcount_launch(const uint32_t*, int64_t, int64_t, int, int, int64_t, long long*,
                             cudaStream_t);
 int tc_slot_fixed_launch(const uint32_t*, int64_t, const uint32_t*, int64_t, int64_t,
-                         const uint32_t*, uint32_t, const uint32_t*, const uint32_t*, uint32_t*,
-                         cudaStream_t);
+                         const uint32_t*, uint32_t, const uint32_t*, uint32_t*, cudaStream_t);
 int tc_slot_fixed_many_launch(int, const uint32_t* const*, const uint32_t* const*, const uint32_t*,
-                              const uint32_t* const*, const uint32_t* const*, uint32_t* const*,
-                              int64_t, const uint32_t*, int64_t, const int32_t*, int64_t,
-                              cudaStream_t);
+                              const uint32_t* const*, uint32_t* const*, int64_t, const uint32_t*,
+                              int64_t, const int32_t*, int64_t, cudaStream_t);
 int64_t tc_slot_fixed_workspace(int64_t, int64_t, int);
 int h_planes_launch(const uint32_t*, int64_t, int64_t, uint8_t*, cudaStream_t);
 int build_bcp_launch(const uint32_t*, int64_t, int, int, uint8_t*, cudaStream_t);
@@ -210,27 +208,26 @@ int zpir_probe_imad(int blocks, int iters, float* ms) { ZPIR_GUARD(imad_probe(bl
 
 int zpir_slot_fixed_tc(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
                        int limbs, const uint32_t* N, uint32_t np, const uint32_t* one_m,
-                       const uint32_t* Nprime, uint32_t* W, void* stream) {
+                       uint32_t* W, void* stream) {
   if (limbs != 128) {
     set_error("slot_fixed_tc: the tensor-core path is built for 4096-bit N (limbs=%d)", limbs);
     return kErrUnsupported;
   }
-  ZPIR_GUARD(tc_slot_fixed_launch(P, n, E, rs, rows, N, np, one_m, Nprime, W, S(stream)));
+  ZPIR_GUARD(tc_slot_fixed_launch(P, n, E, rs, rows, N, np, one_m, W, S(stream)));
 }
 
 int zpir_slot_fixed_tc_many(int clients, const uint64_t* P, const uint64_t* N, const uint32_t* np,
-                            const uint64_t* one_m, const uint64_t* Nprime, const uint64_t* W,
-                            int64_t n, const uint32_t* E, int64_t rs, const int32_t* row_ids,
-                            int64_t rows, void* stream) {
-  if (!P || !N || !np || !one_m || !Nprime || !W) {
+                            const uint64_t* one_m, const uint64_t* W, int64_t n,
+                            const uint32_t* E, int64_t rs, const int32_t* row_ids, int64_t rows,
+                            void* stream) {
+  if (!P || !N || !np || !one_m || !W) {
     set_error("slot_fixed_tc_many: null client array");
     return kErrInput;
   }
   ZPIR_GUARD(tc_slot_fixed_many_launch(
       clients, reinterpret_cast<const uint32_t* const*>(P), reinterpret_cast<const uint32_t* const*>(N),
-      np, reinterpret_cast<const uint32_t* const*>(one_m),
-      reinterpret_cast<const uint32_t* const*>(Nprime), reinterpret_cast<uint32_t* const*>(W), n, E,
-      rs, row_ids, rows, S(stream)));
+      np, reinterpret_cast<const uint32_t* const*>(one_m), reinterpret_cast<uint32_t* const*>(W), n,
+      E, rs, row_ids, rows, S(stream)));
 }
 
 int64_t zpir_slot_fixed_tc_workspace(int64_t n, int64_t rows, int clients) {

@@ -156,36 +156,6 @@ Vec mul_full(const uint32_t* a, int La, const uint32_t* b, int Lb) {
   return r;
 }
 
-// -N^-1 mod 2^(32 L) for odd N (L limbs): Newton x <- x (2 - N x), doubling
-// the number of correct limbs per step from the 32-bit inverse.
-Vec neg_inv_full(const uint32_t* N, int L) {
-  uint32_t inv = N[0];
-  for (int i = 0; i < 5; ++i) inv *= 2u - N[0] * inv;   // N^-1 mod 2^32
-  Vec x(1, inv);
-  for (int prec = 2; ; prec *= 2) {
-    const int p = prec < L ? prec : L;
-    x.resize(p, 0);
-    Vec t = mul_full(N, p, x.data(), p);                 // N x mod 2^(32p)
-    t.resize(p);
-    uint64_t c = 3;                                      // u = 2 - N x = ~t + 3 mod 2^(32p)
-    for (int i = 0; i < p; ++i) {
-      const uint64_t v = (uint64_t)(uint32_t)~t[i] + c;
-      t[i] = (uint32_t)v;
-      c = v >> 32;
-    }
-    x = mul_full(x.data(), p, t.data(), p);
-    x.resize(p);
-    if (p == L) break;
-  }
-  uint64_t c = 1;                                        // -x mod 2^(32L)
-  for (int i = 0; i < L; ++i) {
-    const uint64_t v = (uint64_t)(uint32_t)~x[i] + c;
-    x[i] = (uint32_t)v;
-    c = v >> 32;
-  }
-  return x;
-}
-
 uint32_t neg_inv32(uint32_t n0) {
   uint32_t inv = n0;  // Newton: correct to 3 bits for odd n0, doubles each step
   for (int i = 0; i < 5; ++i) inv *= 2u - n0 * inv;
@@ -263,7 +233,7 @@ struct DeviceGuard {
 struct Key {
   int bits = 0, L = 0, lm = 0, l2 = 0, nchunks = 0, fast0 = 0;
   uint32_t np_m = 0, np_2 = 0, np_m_dummy = 0;
-  DevBuf m, m2, rpow, npd, f0, one2, r2_2, mr, ctab, r2_m, nprime2;
+  DevBuf m, m2, rpow, npd, f0, one2, r2_2, mr, ctab, r2_m;
 };
 
 // Per key-width workspace of the online answer.
@@ -416,10 +386,6 @@ int get_key(zpir_db* h, const uint32_t* m, int L, Key** out) {
   ZPIR_TRY(up(k->r2_2, r22.data(), (size_t)l2 * 4, s));
   ZPIR_TRY(up(k->mr, mr.data(), (size_t)l2 * 4, s));
   ZPIR_TRY(up(k->r2_m, r2m.data(), (size_t)lm * 4, s));
-  if (l2 == 128) {   // the tensor-core Pippenger's full Montgomery inverse
-    Vec npf = neg_inv_full(M2.data(), l2);
-    ZPIR_TRY(up(k->nprime2, npf.data(), (size_t)l2 * 4, s));
-  }
   if (h->stride == 0) {
     // ctab[j] = {gamma^j R mod m, gamma^j R^2 mod m}
     const int cap = h->prm.cap;
@@ -923,8 +889,8 @@ int client_hint(zpir_db* h, const uint32_t* m, int L, const uint8_t* seed, int64
                            k->r2_2.as<uint32_t>(), P.as<uint32_t>(), s));
   if (l2 == 128 && nslot >= 2048)   // bucket updates on the tensor cores (tc_pippenger.cu)
     ZPIR_TRY(zpir_slot_fixed_tc(P.as<uint32_t>(), n, h->H.as<uint32_t>(), n, nslot, l2,
-                                k->m2.as<uint32_t>(), k->np_2, k->one2.as<uint32_t>(),
-                                k->nprime2.as<uint32_t>(), W.as<uint32_t>(), s));
+                                k->m2.as<uint32_t>(), k->np_2, k->one2.as<uint32_t>(), W.as<uint32_t>(),
+                                s));
   else
     ZPIR_TRY(zpir_slot_fixed(P.as<uint32_t>(), n, h->H.as<uint32_t>(), n, nullptr, nslot, l2,
                              k->m2.as<uint32_t>(), k->np_2, k->one2.as<uint32_t>(),

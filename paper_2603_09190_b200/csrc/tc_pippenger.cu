@@ -1,36 +1,33 @@
 // Per-client hint on the tensor cores: the Pippenger bucket updates of
-// slot_fixed (multiexp.cu) as Montgomery multiplications by a FIXED multiplier.
+// slot_fixed (multiexp.cu) as modular multiplications by a FIXED multiplier,
+// each one a plain int8 GEMM against a table of reduced shifts of the multiplier.
 //
 // W[r] = prod_{pos < D n} P[pos]^{digit(r, pos)}: every 32-bit exponent word
-// H[r][k] is cut into D digits (DigitSpec, default D = 6: widths 6,6,5,5,5,5),
-// pos = i n + k, digit(r, pos) = digit i of H[r][k] and P[pos] = ck_r[k]^(2^off_i)
-// (powtab_kernel, Montgomery form mod N = m^2). Position-major Pippenger: at
-// every position each row multiplies ONE of its 2^w - 1 buckets by the same
-// Y = P[pos], so a position is a batch "X (rows) times fixed Y mod N" --
-// Toeplitz int8 GEMMs:
-//   u = X * Y' mod R          (Y' = Y * N' mod R, N' = -N^-1 mod R, R = 2^4096)
-//   Z = (X * Y + u * N) / R   (< 2N; the conditional subtraction is deferred)
-// with a byte-Toeplitz B operand Toep(y)[j][a] = byte_{delta + j - a}(y).
+// H[r][k] is cut into D digits (DigitSpec), pos = i n + k, digit(r, pos) =
+// digit i of H[r][k] and P[pos] = ck_r[k]^(2^off_i). Position-major Pippenger:
+// at every position each row multiplies ONE of its 2^w - 1 buckets by the same
+// y = P[pos] (standard form), so a position is a batch "X (rows) times y mod N".
+// With X = sum_i x_i 256^i (bytes) and the table T_i = y 256^i mod N,
+//   X y = sum_i x_i T_i  (mod N)          -- one u8 x u8 -> s32 GEMM, K = bytes of X,
+// and the byte columns of the product (each < 515 * 255^2 < 2^25) carry-propagate
+// to V = sum_i x_i T_i < 515 * 255 * N < 2^4114: 515 bytes. V is NOT reduced; it
+// is the next X of its bucket as it stands (K = 515 bytes, padded to 544 = 17
+// MMA k-steps), and the bound is closed under the operation because every T_i
+// is < N whatever the size of X was. No Montgomery reduction, no quotient, no
+// dependency between the MMAs of one position: per position and 128-row tile
+//   task A: columns   0..255 (17 N = 256 MMAs) -> limbs 0..63
+//   task B: columns 256..511 (17 MMAs)          -> limbs 64..127 and the carry, limb 128
+// into two TMEM buffers, drained by the epilogue while the other one fills.
+// The bucket combine reduces each bucket once (quotient estimate from the top
+// limbs, bignum.cuh) before its IMAD running products.
 //
-// Only 1028 of the 1536 byte columns of u and X*Y + u*N are ever drained from
-// TMEM: S = X*Y + u*N is an exact multiple of R, every column sum is < 2^27,
-// so the carry out of the low half is ceil(low4 / 2^32) with low4 the 4 byte
-// columns 508..511 (the columns below add e < 2^20 to low4 / 2^32 and the total
-// is an integer). Per position and 128-row tile: four 256-column tasks
-//   U0, U1: columns 0..255 / 256..511 of X * Y'        -> u into shared memory
-//   H0:     columns 508..763 of X * Y + u * N           -> carry, Z limbs 0..62
-//   H1:     columns 764..1019                           -> Z limbs 63..126
-// and the three top columns 1020..1022 (12 byte products) on the CUDA cores.
-// 20 k-blocks (80 N = 256 MMAs) per position; the tasks ping-pong two TMEM
-// buffers so the epilogue drains one while the MMA warp fills the other. The
-// X * Y parts of H0 and H1 are issued before the u * N parts, so the next
-// position's bucket gather (cp.async) overlaps the H drains; a row whose digit
-// repeats gets its next X forwarded from Z by its own thread.
+// Buckets hold Montgomery-form values and y is in standard form, so products
+// stay in Montgomery form. A row whose digit repeats at the next position gets
+// its next X forwarded from this position's output by its own thread.
 //
 // Several clients (independent keys) run in one launch: blockIdx.y = client,
-// every client with its own Toeplitz tiles, buckets and output rows; rows may be
-// a subset of the exponent rows (row ids), which is the incremental refresh.
-// The bucket combine (prod_d B_d^d, running sums) stays on the IMAD warp path.
+// every client with its own tables, buckets and output rows; rows may be a
+// subset of the exponent rows (row ids), which is the incremental refresh.
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -61,26 +58,22 @@ __device__ unsigned long long g_tc_trace[64 * 16];
 namespace tcp {
 
 constexpr int kL = 128;            // limbs of N = m^2 (2048-bit m)
+constexpr int kXL = 136;           // limbs per stored bucket (129 used; 544 B = 17 sectors)
 constexpr int kRows = 128;         // rows per tile (TMEM lanes)
-constexpr int kBK = 128;           // K bytes per k-block
-constexpr int kTile = 256 * kBK;   // one Toeplitz tile: 256 columns x 128 K bytes
-constexpr int kTYp = 4;            // Y' tiles: delta = -128 + 128 t (U0, U1)
-constexpr int kDeltaYp = -128;
-constexpr int kTY = 5;             // Y / N tiles: delta = 124 + 128 t (H0, H1)
-constexpr int kDeltaY = 124;
-constexpr int kStages = 3;
+constexpr int kBK = 128;           // K bytes per full k-block
+constexpr int kKB = 4;             // full k-blocks: bytes 0..511 of X
+constexpr int kKT = 32;            // tail k-step: bytes 512..543 (512..514 used)
+constexpr int kTK = kKB * kBK + kKT;   // table row pitch = K bytes per position (544)
+constexpr int kUsedK = 515;        // bytes of X that can be non-zero
+constexpr int kCols = 512;         // byte columns of the product = table rows per position
+constexpr int kTile = 256 * kBK;   // B stage: 256 columns x 128 K bytes (SW128)
+constexpr int kTail = 256 * kKT;   // B tail stage: 256 columns x 32 K bytes (SW32)
+constexpr int kStages = 4;
+constexpr int kTStages = 3;
 constexpr int kThreads = 192;
-constexpr int kABytes = kRows * 512;     // one 128 x 512-byte A operand (4 k-blocks)
-constexpr int kSmem = 2 * kABytes + kStages * kTile + 1024 + 1024;
-constexpr int kNSteps = 20;
-
-// The static MMA schedule: task (0 U0, 1 U1, 2 H0, 3 H1; TMEM buffer = task & 1),
-// A operand (0 = X, 1 = u), k-block, B source (0 = Y', 1 = Y, 2 = N), tile t,
-// issue segment: 0 U0, 1 U1, 2 H0 X*Y, 3 H1 X*Y (then X is free), 4 H0 u*N, 5 H1 u*N.
-struct Step {
-  int8_t task, a, ka, src, t, seg;
-};
-__constant__ Step kSched[kNSteps];
+constexpr int kABytes = kRows * kKB * kBK;   // X bytes 0..511: 4 k-blocks of 128 x 128 B (SW128)
+constexpr int kATail = kRows * kKT;          // X bytes 512..543 (SW32)
+constexpr int kSmem = kABytes + kATail + kStages * kTile + kTStages * kTail + 1024 + 1024;
 
 }  // namespace tcp
 
@@ -89,15 +82,14 @@ struct TcClient {
   const uint32_t* P;        // (npos, 128) Montgomery multipliers
   const uint32_t* N;        // 128 limbs of N = m^2
   const uint32_t* one;      // R mod N
-  const uint32_t* Nprime;   // -N^-1 mod R
   uint32_t* W;              // output rows (Montgomery form), indexed by exponent row
   uint32_t np;              // -N^-1 mod 2^32
 };
 
 // Radix of the exponent digits: D digits per 32-bit exponent word, digit i
 // = bits off[i] .. off[i] + width[i] - 1; nb = 2^max(width) - 1 buckets per row.
-// Fewer, wider digits mean fewer positions (tensor-core work, 4n at D = 4) but
-// more buckets to combine on the IMAD path (2 nb Montgomery products per row).
+// Fewer, wider digits mean fewer positions (tensor-core work) but more buckets
+// to combine on the IMAD path (2 nb Montgomery products per row).
 struct DigitSpec {
   int D, nb;
   int off[8], width[8];
@@ -124,75 +116,77 @@ powtab_kernel(const TcClient* __restrict__ cl, int64_t n, DigitSpec ds, uint32_t
   }
 }
 
-// tiles[((c * npos + p) * T + t) * 256 + j][a] = byte_{delta0 + 128 t + j - a}(y_{c,p}),
-// zero outside [0, 512); y = Y[c][p] (which = 1, fixed stride) or the client's N.
-__global__ void __launch_bounds__(256)
-toep_tiles_kernel(const TcClient* __restrict__ cl, int which, const uint32_t* __restrict__ Ybase,
-                  int64_t npos, int T, int delta0, uint8_t* __restrict__ tiles) {
-  const int64_t pt = blockIdx.x;                 // p * T + t
-  const int c = blockIdx.y;
-  const int64_t p = pt / T;
-  const int t = (int)(pt - p * T);
-  const int j = threadIdx.x;
-  const uint32_t* ysrc = which == 1 ? Ybase + ((int64_t)c * npos + p) * tcp::kL : cl[c].N;
-  const uint8_t* y = reinterpret_cast<const uint8_t*>(ysrc);
-  const int delta = delta0 + 128 * t;
-  uint8_t* row = tiles + (((int64_t)c * npos * T + pt) * 256 + j) * tcp::kBK;
-#pragma unroll 1
-  for (int a0 = 0; a0 < tcp::kBK; a0 += 16) {
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int idx = delta + j - (a0 + 4 * q + e);
-        const uint32_t byte = (idx >= 0 && idx < 512) ? y[idx] : 0u;
-        v |= byte << (8 * e);
-      }
-      w[q] = v;
-    }
-    *reinterpret_cast<uint4*>(row + a0) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-
-// out[c][p] = Pd_c[p] * Nprime_c mod 2^4096, one thread per value (product scanning).
+// The multiplier tables: T[((c * npos + p) * 512 + j) * 544 + i] = byte j of
+// (y_{c,p} 256^i mod N_c), y = Pd[c][p] taken out of Montgomery form; zero for
+// i >= 515. One warp per position walks i upwards, t <- 256 t mod N (a byte
+// shift and one quotient-estimate reduction); every lane keeps the last 16 i's
+// of its 16 byte rows in registers and writes them as 16-byte row segments.
 __global__ void __launch_bounds__(128)
-mul_lo_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Pd, int64_t npos,
-              uint32_t* __restrict__ out) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+table_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Pd, int64_t npos,
+             uint8_t* __restrict__ T) {
+  constexpr int LPL = tcp::kL / 32;
+  static_assert(LPL == 4, "16 bytes per lane");
+  const int lane = threadIdx.x & 31;
   const int c = blockIdx.y;
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (p >= npos) return;
-  const uint32_t* y = Pd + ((int64_t)c * npos + p) * tcp::kL;
-  const uint32_t* Np = cl[c].Nprime;
-  uint32_t* o = out + ((int64_t)c * npos + p) * tcp::kL;
-  unsigned long long lo = 0, hi = 0;  // 128-bit column accumulator (lo, hi)
-  for (int k = 0; k < tcp::kL; ++k) {
-    for (int i = 0; i <= k; ++i) {
-      const unsigned long long pr = (unsigned long long)y[i] * Np[k - i];
-      const unsigned long long s = lo + pr;
-      hi += (s < lo);
-      lo = s;
+  uint32_t n_[LPL], t[LPL], e1[LPL];
+  big_load<LPL>(n_, cl[c].N, lane);
+  big_load<LPL>(t, Pd + ((int64_t)c * npos + p) * tcp::kL, lane);
+  big_set_small<LPL>(e1, 1u, lane);
+  mont_mul<LPL>(t, t, e1, n_, cl[c].np, lane);        // y in standard form, < N
+  const uint32_t nt8 = (__shfl_sync(ZPIR_FULL, n_[LPL - 1], 31) >> 8) + 1u;
+  uint8_t* out = T + (((int64_t)c * npos + p) * tcp::kCols + 16 * lane) * tcp::kTK;
+#pragma unroll 1
+  for (int blk = 0; blk < tcp::kTK / 16; ++blk) {
+    uint32_t acc[16][4];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const bool live = 16 * blk + s < tcp::kUsedK;
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        // byte b of this lane's 16 bytes into byte s of the row segment
+        const uint32_t src = live ? t[b >> 2] : 0u;
+        const uint32_t byte = (src >> (8 * (b & 3))) & 0xffu;
+        if ((s & 3) == 0) acc[b][s >> 2] = byte;
+        else acc[b][s >> 2] |= byte << (8 * (s & 3));
+      }
+      // t <- 256 t mod N
+      uint32_t prev = __shfl_up_sync(ZPIR_FULL, t[LPL - 1], 1);
+      prev = lane == 0 ? 0u : prev;
+      const uint32_t top = __shfl_sync(ZPIR_FULL, t[LPL - 1], 31);
+      const uint32_t tb = top >> 24;
+#pragma unroll
+      for (int k = LPL - 1; k >= 1; --k) t[k] = (t[k] << 8) | (t[k - 1] >> 24);
+      t[0] = (t[0] << 8) | (prev >> 24);
+      // quotient estimate from the top 40 bits over the top 24 bits of N (+1):
+      // never too large, at most one too small
+      const uint32_t xt8 = (tb << 24) | ((top << 8) >> 8);   // (tb 2^32 + new top limb) >> 8
+      big_reduce_top<LPL>(t, tb, xt8 / nt8, n_, lane);
     }
-    o[k] = (uint32_t)lo;
-    lo = (lo >> 32) | (hi << 32);
-    hi >>= 32;
+#pragma unroll
+    for (int b = 0; b < 16; ++b)
+      *reinterpret_cast<uint4*>(out + (int64_t)b * tcp::kTK + 16 * blk) =
+          make_uint4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
   }
 }
 
+// Buckets start at 1 (Montgomery form): limbs 0..127 = R mod N, 128..135 = 0.
 __global__ void bucket_fill_kernel(const TcClient* __restrict__ cl, uint32_t* __restrict__ B,
                                    int64_t count) {
   const int c = blockIdx.y;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;   // u32 index
-  if (i < count * tcp::kL) B[(int64_t)c * count * tcp::kL + i] = cl[c].one[i % tcp::kL];
+  if (i < count * tcp::kXL) {
+    const int l = (int)(i % tcp::kXL);
+    B[(int64_t)c * count * tcp::kXL + i] = l < tcp::kL ? cl[c].one[l] : 0u;
+  }
 }
 
 // W[row] = prod_d B[r][d]^d (running sums from d = nb down), Montgomery form.
-// Buckets are stored lazily reduced: flag F[r][d] set means "subtract N (mod R)".
+// Buckets are stored unreduced (129 limbs, < 2^4114): reduced mod N on load.
 __global__ void __launch_bounds__(128)
-bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Ball,
-                      const uint8_t* __restrict__ Fall, int nb, int64_t rows, int64_t rows_p,
-                      const int32_t* __restrict__ rid) {
+bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restrict__ Ball, int nb,
+                      int64_t rows, int64_t rows_p, const int32_t* __restrict__ rid) {
   constexpr int LPL = tcp::kL / 32;
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.y;
@@ -201,14 +195,19 @@ bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restric
   const uint32_t np = cl[c].np;
   uint32_t n_[LPL], run[LPL], tot[LPL], x[LPL];
   big_load<LPL>(n_, cl[c].N, lane);
-  const uint32_t* br = Ball + ((int64_t)c * rows_p + r) * nb * tcp::kL;
-  const uint8_t* fr = Fall + ((int64_t)c * rows_p + r) * nb;
-  big_load<LPL>(run, br + (nb - 1) * tcp::kL, lane);
-  if (fr[nb - 1]) big_cond_sub<LPL>(run, 1u, n_, lane);
+  const uint64_t nt1 = (uint64_t)__shfl_sync(ZPIR_FULL, n_[LPL - 1], 31) + 1u;
+  const uint32_t* br = Ball + ((int64_t)c * rows_p + r) * nb * tcp::kXL;
+  auto load = [&](uint32_t (&v)[LPL], int d) {
+    const uint32_t* q = br + (int64_t)d * tcp::kXL;
+    big_load<LPL>(v, q, lane);
+    const uint32_t h = q[tcp::kL];
+    const uint64_t xt = ((uint64_t)h << 32) | __shfl_sync(ZPIR_FULL, v[LPL - 1], 31);
+    big_reduce_top<LPL>(v, h, (uint32_t)(xt / nt1), n_, lane);
+  };
+  load(run, nb - 1);
   big_copy<LPL>(tot, run);
   for (int d = nb - 1; d >= 1; --d) {
-    big_load<LPL>(x, br + (d - 1) * tcp::kL, lane);
-    if (fr[d - 1]) big_cond_sub<LPL>(x, 1u, n_, lane);
+    load(x, d - 1);
     mont_mul<LPL>(run, run, x, n_, np, lane);
     mont_mul<LPL>(tot, tot, run, n_, np, lane);
   }
@@ -277,54 +276,67 @@ __device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long&
   return (uint32_t)s;
 }
 
+// K-major operand tile with SWIZZLE_32B: rows of 32 bytes, 8-row (256 B) atoms.
+__device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(256 >> 4) << 32;            // SBO = 256 B
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)6 << 61;                     // SWIZZLE_32B
+  return d;
+}
+
 // Pippenger positions pos0..pos1-1 for one 128-row tile of one client per CTA
 // (tiles are independent: a row only touches its own buckets):
-//   B[r][d - 1] *= P[pos] for d = digit(r, pos) != 0.
+//   B[r][d - 1] <- B[r][d - 1] * y[pos] for d = digit(r, pos) != 0.
 __global__ void __launch_bounds__(tcp::kThreads, 1)
-tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant__ CUtensorMap mapY,
-               const __grid_constant__ CUtensorMap mapN, const TcClient* __restrict__ cl,
-               const uint32_t* __restrict__ Pd, const __grid_constant__ DigitSpec ds,
-               const uint32_t* __restrict__ E, int64_t rs, const int32_t* __restrict__ rid,
-               int64_t n, int64_t npos, int pos0, int pos1, int64_t rows, int64_t rows_p,
-               uint32_t* __restrict__ Ball, uint8_t* __restrict__ Fall) {
+tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__ CUtensorMap mapTail,
+               const __grid_constant__ DigitSpec ds, const uint32_t* __restrict__ E, int64_t rs,
+               const int32_t* __restrict__ rid, int64_t n, int64_t npos, int pos0, int pos1,
+               int64_t rows, int64_t rows_p, uint32_t* __restrict__ Ball) {
   using namespace tcp;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* XA = smem;                       // X (4 k-blocks of 128 x 128 B, SW128)
-  uint8_t* UA = smem + kABytes;             // u, same layout
-  uint8_t* BS = smem + 2 * kABytes;         // B tile stages
-  uint64_t* full = reinterpret_cast<uint64_t*>(BS + kStages * kTile);
+  uint8_t* XA = smem;                       // X bytes 0..511: 4 k-blocks of 128 x 128 B, SW128
+  uint8_t* XT = smem + kABytes;             // X bytes 512..543: 128 x 32 B, SW32
+  uint8_t* BS = XT + kATail;                // table stages (256 x 128 B)
+  uint8_t* BT = BS + kStages * kTile;       // table tail stages (256 x 32 B)
+  uint64_t* full = reinterpret_cast<uint64_t*>(BT + kTStages * kTail);
   uint64_t* empty = full + kStages;
-  uint64_t* xfull = empty + kStages;
-  uint64_t* uready = xfull + 1;             // all 512 bytes of u written
-  uint64_t* tfull = uready + 1;             // [2] per TMEM buffer
+  uint64_t* tlfull = empty + kStages;       // tail ring
+  uint64_t* tlempty = tlfull + kTStages;
+  uint64_t* xfull = tlempty + kTStages;     // X of the position complete in shared memory
+  uint64_t* xfree = xfull + 1;              // every MMA reading X of the position done
+  uint64_t* tfull = xfree + 1;              // [2] per TMEM buffer
   uint64_t* tempty = tfull + 2;             // [2]
-  uint64_t* xfree = tempty + 2;             // every MMA reading X of this position done
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(xfree + 2);
-  uint32_t* sN = tslot + 4;                 // N limbs (512 B)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int client = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
-    tma_prefetch(&mapYp);
-    tma_prefetch(&mapY);
-    tma_prefetch(&mapN);
+    tma_prefetch(&mapT);
+    tma_prefetch(&mapTail);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(&tlfull[s], 1);
+      mbar_init(&tlempty[s], 1);
+    }
     mbar_init(xfull, 128);
-    mbar_init(uready, 128);
+    mbar_init(xfree, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 128);
     }
-    mbar_init(xfree, 1);
     fence_mbar_init();
   }
-  const uint32_t* Ncl = cl[client].N;
-  for (int i = threadIdx.x; i < kL; i += blockDim.x) sN[i] = Ncl[i];
+  // bytes 516..543 of every X stay zero
+  for (int i = threadIdx.x; i < kATail / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(XT)[i] = make_uint4(0u, 0u, 0u, 0u);
   if (warp == 1) tmem_alloc(tslot, 512);
   tc_fence_before();
   __syncthreads();
@@ -334,108 +346,92 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer: the 20 B tiles of every position ----------------
+      // ---------------- TMA producer: the table of every position, by column half ----------------
       const uint64_t pol = l2_evict_last();
       const int64_t cpos = (int64_t)client * npos;
-      int stage = 0;
-      uint32_t phase = 0;
+      int stage = 0, ts = 0;
+      uint32_t phase = 0, tph = 0;
       for (int pos = pos0; pos < pos1; ++pos)
-        for (int s = 0; s < kNSteps; ++s) {
-          const Step st = kSched[s];
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kTile);
-          uint8_t* dst = BS + stage * kTile;
-          if (st.src == 0)
-            tma_load_2d_hint(dst, &mapYp, &full[stage], 0, (int)(((cpos + pos) * kTYp + st.t) * 256),
-                             pol);
-          else if (st.src == 1)
-            tma_load_2d_hint(dst, &mapY, &full[stage], 0, (int)(((cpos + pos) * kTY + st.t) * 256),
-                             pol);
-          else
-            tma_load_2d_hint(dst, &mapN, &full[stage], 0, (client * kTY + st.t) * 256, pol);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+        for (int task = 0; task < 2; ++task) {
+          const int trow = (int)(((cpos + pos) * 2 + task) * 256);
+          for (int kb = 0; kb < kKB; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], kTile);
+            tma_load_2d_hint(BS + stage * kTile, &mapT, &full[stage], kb * kBK, trow, pol);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mbar_wait(&tlempty[ts], tph ^ 1);
+          mbar_expect_tx(&tlfull[ts], kTail);
+          tma_load_2d_hint(BT + ts * kTail, &mapTail, &tlfull[ts], kKB * kBK, trow, pol);
+          if (++ts == kTStages) {
+            ts = 0;
+            tph ^= 1;
           }
         }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer: six segments per position, buffer = task & 1 ----------------
+      // ---------------- MMA issuer: task A -> TMEM buffer 0, task B -> buffer 1 ----------------
       const uint32_t idesc = idesc_u8(kRows, 256);
-      int stage = 0;
-      uint32_t phase = 0, xph = 0;
+      const uint64_t xtd = desc_sw32(smem_u32(XT));
+      int stage = 0, ts = 0;
+      uint32_t phase = 0, tph = 0, xph = 0;
       uint32_t eph[2] = {0, 0};
-      bool used0 = false, used1 = false;
 #ifdef ZPIR_TC_TRACE
-      unsigned long long fwait = 0;   // cycles the MMA thread waited for B tiles this position
+      unsigned long long fwait = 0;   // cycles the MMA thread waited for table tiles this position
 #endif
       for (int pos = pos0; pos < pos1; ++pos) {
-        int cur = -1;
-        bool first = true;
-        for (int s = 0; s < kNSteps; ++s) {
-          const Step st = kSched[s];
-          const int buf = st.task & 1;
-          if (st.seg != cur) {
-            if (cur == 0) umma_commit(&tfull[0]);          // U0 -> epilogue
-            else if (cur == 1) umma_commit(&tfull[1]);     // U1
-            else if (cur == 3) umma_commit(xfree);         // X no longer read
-            else if (cur == 4) umma_commit(&tfull[0]);     // H0
-            switch (st.seg) {
-              case 0:                                      // buffer 0 after H0(pos-1) drained
-                if (used0) { mbar_wait(&tempty[0], eph[0]); eph[0] ^= 1; }
-                used0 = true;
-                mbar_wait(xfull, xph);
-                break;
-              case 1:                                      // buffer 1 after H1(pos-1) drained
-                if (used1) { mbar_wait(&tempty[1], eph[1]); eph[1] ^= 1; }
-                used1 = true;
-                break;
-              case 2:                                      // U0 drained
-                mbar_wait(&tempty[0], eph[0]); eph[0] ^= 1;
-                break;
-              case 3:                                      // U1 drained
-                mbar_wait(&tempty[1], eph[1]); eph[1] ^= 1;
-                break;
-              case 4:                                      // all of u written
-                mbar_wait(uready, xph);
-                break;
-              default:
-                break;
-            }
-            tc_fence_after();
-            cur = st.seg;
-            if (cur < 4) TC_STAMP(pos, 11 + cur);
-            first = cur <= 3;                              // u * N accumulates onto X * Y
+        for (int task = 0; task < 2; ++task) {
+          if (task == 0) {
+            mbar_wait(xfull, xph);
+            xph ^= 1;
           }
-#ifdef ZPIR_TC_TRACE
-          const unsigned long long tw0 = clock64();
-          mbar_wait(&full[stage], phase);
-          fwait += clock64() - tw0;
-#else
-          mbar_wait(&full[stage], phase);
-#endif
+          if (pos > pos0) {                              // the buffer's previous drain
+            mbar_wait(&tempty[task], eph[task]);
+            eph[task] ^= 1;
+          }
           tc_fence_after();
-          const uint32_t a0 = smem_u32((st.a ? UA : XA) + st.ka * (kRows * kBK));
-          const uint64_t ad = desc_sw128(a0);
-          const uint64_t bd = desc_sw128(smem_u32(BS + stage * kTile));
-          const uint32_t d = tbase + (uint32_t)(buf * 256);
+          TC_STAMP(pos, 11 + task);
+          const uint32_t d = tbase + (uint32_t)(task * 256);
+          for (int kb = 0; kb < kKB; ++kb) {
+#ifdef ZPIR_TC_TRACE
+            const unsigned long long tw0 = clock64();
+            mbar_wait(&full[stage], phase);
+            fwait += clock64() - tw0;
+#else
+            mbar_wait(&full[stage], phase);
+#endif
+            tc_fence_after();
+            const uint64_t ad = desc_sw128(smem_u32(XA + kb * (kRows * kBK)));
+            const uint64_t bd = desc_sw128(smem_u32(BS + stage * kTile));
 #pragma unroll
-          for (int k = 0; k < kBK / 32; ++k)
-            umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (first && k == 0) ? 0u : 1u);
-          first = false;
-          umma_commit(&empty[stage]);
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
+            for (int k = 0; k < kBK / 32; ++k)
+              umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (kb == 0 && k == 0) ? 0u : 1u);
+            umma_commit(&empty[stage]);
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
+          mbar_wait(&tlfull[ts], tph);
+          tc_fence_after();
+          umma_i8(d, xtd, desc_sw32(smem_u32(BT + ts * kTail)), idesc, 1u);
+          umma_commit(&tlempty[ts]);
+          if (++ts == kTStages) {
+            ts = 0;
+            tph ^= 1;
+          }
+          if (task == 1) umma_commit(xfree);             // X no longer read
+          umma_commit(&tfull[task]);
         }
-        umma_commit(&tfull[1]);                            // H1
+        TC_STAMP(pos, 13);
 #ifdef ZPIR_TC_TRACE
         if (blockIdx.x == 0 && blockIdx.y == 0 && pos - pos0 < 64) g_tc_trace[(pos - pos0) * 16 + 15] = fwait;
         fwait = 0;
 #endif
-        xph ^= 1;
       }
     }
   } else {
@@ -445,17 +441,15 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     const int64_t r = row0 + t;
     const int64_t er = r < rows ? (rid ? (int64_t)rid[r] : r) : 0;
     const int nb = ds.nb;
-    uint32_t* Bc = Ball + (int64_t)client * rows_p * nb * kL;
-    uint8_t* Fc = Fall + (int64_t)client * rows_p * nb;
-    const uint32_t* Pc = Pd + (int64_t)client * npos * kL;
+    uint32_t* Bc = Ball + (int64_t)client * rows_p * nb * kXL;
     const uint32_t lanebase = tbase + ((uint32_t)(quarter * 32) << 16);
-    uint32_t nl[4];                             // N limbs 4 lane .. 4 lane + 3 (gather)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) nl[i] = sN[4 * lane + i];
-    const uint32_t ntop = sN[kL - 1], n126 = sN[kL - 2];
     uint32_t fph[2] = {0, 0}, xfph = 0;
-    const int kbl = lane >> 3, chl = lane & 7;  // this lane's 16-byte chunk of a row
+    const int kbl = lane >> 3, chl = lane & 7;  // this lane's 16-byte chunk of bytes 0..511
     const uint32_t xa_l = smem_u32(XA) + kbl * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
+    const uint32_t xa_t = smem_u32(XA) + t * kBK;                        // + k-block, chunk
+    const uint32_t xt_t = smem_u32(XT) + t * kKT + (((t >> 2) & 1) << 4);  // chunk 0 of the tail row
+    uint8_t* xa_row = XA + t * kBK;
+    uint8_t* xt_row = XT + t * kKT + (((t >> 2) & 1) << 4);
     const int64_t rbase = row0 + quarter * 32;
     auto digit_at = [&](int p) -> uint32_t {
       if (r >= rows) return 0u;
@@ -464,63 +458,52 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
     };
     // X rows of the warp from their buckets, warp-cooperative async copies: lane
     // c moves bytes 16c..16c+15 of each of the warp's 32 rows into the SW128 A
-    // layout (zero fill for digit 0); rows with `skip` set are written by their
-    // own thread instead (bucket updated at this very position).
-    auto gather_issue = [&](uint32_t dgv, uint32_t skip) {
-      const uint32_t sk = __ballot_sync(0xffffffffu, skip != 0);
+    // layout (zero fill for digit 0), and the tail chunk of its own row. A row
+    // with `fwd` set (digit repeats) is copied by its own thread instead: the low
+    // half from the bucket it has just stored, the high half straight from the
+    // drain of task B.
+    auto gather_issue = [&](uint32_t dgv, uint32_t fwd) {
+      const uint32_t sk = __ballot_sync(0xffffffffu, fwd != 0);
 #pragma unroll 8
       for (int i = 0; i < 32; ++i) {
         const uint32_t d_i = __shfl_sync(0xffffffffu, dgv, i);
         if ((sk >> i) & 1u) continue;
-        const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kL + 4 * lane;
+        const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kXL + 4 * lane;
         const uint32_t dst = xa_l + i * kBK + ((chl ^ (i & 7)) << 4);
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                      "r"(d_i ? 16u : 0u)
                      : "memory");
       }
-    };
-    // copies landed; lazily reduced buckets: a set flag means the stored value
-    // is Z with Z - N still to be taken (mod R)
-    // gather_land: the copies landed, lazily reduced buckets reduced in place;
-    // gather_publish: X complete (conflict rows forwarded) -> the MMA warp
-    auto gather_land = [&](uint32_t lz) {
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncwarp();
-      uint32_t lzm = __ballot_sync(0xffffffffu, lz != 0);
-      while (lzm) {
-        const int i = __ffs(lzm) - 1;
-        lzm &= lzm - 1;
-        uint8_t* q = XA + kbl * (kRows * kBK) + (quarter * 32 + i) * kBK + ((chl ^ (i & 7)) << 4);
-        uint4 w = *reinterpret_cast<const uint4*>(q);
-        uint32_t v[4] = {w.x, w.y, w.z, w.w};
-        big_cond_sub<4>(v, 1u, nl, lane);       // x - N mod R (warp-uniform)
-        *reinterpret_cast<uint4*>(q) = make_uint4(v[0], v[1], v[2], v[3]);
+      const uint32_t* own = Bc + (r * nb + (dgv ? dgv - 1 : 0)) * kXL;
+      if (!fwd) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xt_t), "l"(own + kL),
+                     "r"(dgv ? 16u : 0u)
+                     : "memory");
+      } else {
+#pragma unroll 4
+        for (int cc = 0; cc < 16; ++cc)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           xa_t + (cc >> 3) * (kRows * kBK) + (((cc & 7) ^ (t & 7)) << 4)),
+                       "l"(own + 4 * cc)
+                       : "memory");
       }
     };
     auto gather_publish = [&]() {
+      asm volatile("cp.async.wait_all;" ::: "memory");
       fence_async_smem();
       mbar_arrive(xfull);
-      __syncwarp();
     };
-    auto gather_finish = [&](uint32_t lz) {
-      gather_land(lz);
-      gather_publish();
-    };
-    // bytes 508..511 of this row's X (k-block 3, chunk 7)
-    const uint32_t* xtop_p =
-        reinterpret_cast<const uint32_t*>(XA + 3 * (kRows * kBK) + t * kBK + ((7 ^ (t & 7)) << 4) + 12);
     auto prefetch_bucket = [&](uint32_t d) {
       if (!d) return;
-      const uint32_t* pb = Bc + (r * nb + d - 1) * kL;
+      const uint32_t* pb = Bc + (r * nb + d - 1) * kXL;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
+      for (int j = 0; j < 5; ++j) asm volatile("prefetch.global.L2 [%0];" ::"l"(pb + 32 * j));
     };
 
     // prologue: X of the first position
     uint32_t dg = digit_at(pos0);
     gather_issue(dg, 0u);
-    gather_finish((dg && Fc[r * nb + dg - 1]) ? 1u : 0u);
-    uint32_t xtop = *xtop_p;
+    gather_publish();
     uint32_t dg_n = pos0 + 1 < pos1 ? digit_at(pos0 + 1) : 0u;
     prefetch_bucket(dg_n);
 
@@ -528,186 +511,72 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapYp, const __grid_constant_
       const bool last = pos + 1 >= pos1;
       const bool tr = threadIdx.x == 64;
       if (tr) TC_STAMP(pos, 0);
-      const int64_t bidx = (r * nb) + (dg ? dg - 1 : 0);
-      uint32_t* brow = Bc + bidx * kL;
-      const uint32_t ytop = Pc[(int64_t)pos * kL + kL - 1];
+      uint32_t* brow = Bc + ((r * nb) + (dg ? dg - 1 : 0)) * kXL;
       // the next position's bucket is this position's (digit repeats): its X is
-      // this position's Z, written into the A layout by this thread below
-      const uint32_t conflict = (!last && dg && dg_n == dg) ? 1u : 0u;
-      const uint32_t lazy_n = (!last && dg_n && !conflict && Fc[r * nb + dg_n - 1]) ? 1u : 0u;
-
-      unsigned long long carry = 0;
-      uint32_t utop = 0;
-      // ---- U0, U1: u = X * Y' mod R, limbs into the SW128 A layout of u
-#pragma unroll 1
-      for (int task = 0; task < 2; ++task) {
-        mbar_wait(&tfull[task], fph[task]);
-        fph[task] ^= 1;
-        if (tr) TC_STAMP(pos, 1 + 2 * task);
-        tc_fence_after();
-        const uint32_t taddr = lanebase + (uint32_t)(task * 256);
-        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {        // 16-byte chunk of u: 4 limbs
-            uint32_t l[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) l[i] = limb4(v + 16 * j + 4 * i, carry);
-            const int cc = task * 16 + 2 * g + j;
-            const int kb = cc >> 3, ch = cc & 7;
-            *reinterpret_cast<uint4*>(UA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
-                make_uint4(l[0], l[1], l[2], l[3]);
-            utop = l[3];
-          }
-        });
-        if (tr) TC_STAMP(pos, 2 + 2 * task);
-        if (task == 1) {
-          fence_async_smem();
-          mbar_arrive(uready);
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[task]);
-      }
-      // ---- the next position's gather, once no MMA reads X any more; it lands
-      // while H0 / H1 are computed and drained
-      if (!last) {
-        mbar_wait(xfree, xfph);
-        xfph ^= 1;
-        if (tr) TC_STAMP(pos, 5);
-        gather_issue(dg_n, conflict);
-        // land + reduce the gathered rows now: the epilogue would otherwise
-        // idle until H0 is computed, and this work leaves the critical path
-        gather_land(lazy_n);
-      }
-      // ---- H0, H1: Z = (X * Y + u * N) / R from columns 508..1019 (+ 1020..1022)
-      // Z limbs awaiting a 32-byte store (one 256-bit STG per 8 limbs: whole
-      // sectors, half the store instructions of 16-byte stores)
+      // this position's output
+      const uint32_t fwd = (!last && dg && dg_n == dg) ? 1u : 0u;
+      // limbs awaiting a 32-byte store (one 256-bit STG per 8 limbs: whole sectors)
       uint32_t pend[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      auto emit = [&](int li) {               // limbs li-7..li complete
+      unsigned long long carry = 0;
+      // ---- task A: limbs 0..63
+      mbar_wait(&tfull[0], fph[0]);
+      fph[0] ^= 1;
+      if (tr) TC_STAMP(pos, 1);
+      tc_fence_after();
+      drain256(lanebase, carry, [&](int g, const uint32_t (&v)[32]) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pend[k] = limb4(v + 4 * k, carry);
         if (dg)
-          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + li - 7),
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + 8 * g),
                        "r"(pend[0]), "r"(pend[1]), "r"(pend[2]), "r"(pend[3]), "r"(pend[4]),
                        "r"(pend[5]), "r"(pend[6]), "r"(pend[7])
                        : "memory");
-        if (conflict) {
+      });
+      if (tr) TC_STAMP(pos, 2);
+      tc_fence_before();
+      mbar_arrive(&tempty[0]);
+      // ---- the next position's gather, once no MMA reads X any more; it lands
+      // while task B is drained
+      if (!last) {
+        mbar_wait(xfree, xfph);
+        xfph ^= 1;
+        if (tr) TC_STAMP(pos, 3);
+        gather_issue(dg_n, fwd);
+        if (tr) TC_STAMP(pos, 4);
+      }
+      // ---- task B: limbs 64..127 and the carry out (limb 128)
+      mbar_wait(&tfull[1], fph[1]);
+      fph[1] ^= 1;
+      if (tr) TC_STAMP(pos, 5);
+      tc_fence_after();
+      drain256(lanebase + 256u, carry, [&](int g, const uint32_t (&v)[32]) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pend[k] = limb4(v + 4 * k, carry);
+        if (dg)
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + 64 + 8 * g),
+                       "r"(pend[0]), "r"(pend[1]), "r"(pend[2]), "r"(pend[3]), "r"(pend[4]),
+                       "r"(pend[5]), "r"(pend[6]), "r"(pend[7])
+                       : "memory");
+        if (fwd) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int cc = ((li - 7) >> 2) + h, kb = cc >> 3, ch = cc & 7;
-            *reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4)) =
+            const int cc = 16 + 2 * g + h, kb = cc >> 3, ch = cc & 7;
+            *reinterpret_cast<uint4*>(xa_row + kb * (kRows * kBK) + ((ch ^ (t & 7)) << 4)) =
                 make_uint4(pend[4 * h], pend[4 * h + 1], pend[4 * h + 2], pend[4 * h + 3]);
           }
         }
-      };
-      carry = 0;
+      });
       {
-        mbar_wait(&tfull[0], fph[0]);
-        fph[0] ^= 1;
-        if (tr) TC_STAMP(pos, 6);
-        tc_fence_after();
-        const uint32_t taddr = lanebase;
-        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int slot = 8 * g + k;        // columns 508 + 4 slot ..
-            if (slot == 0) {
-              // low4 = columns 508..511 as one number (< 2^54)
-              const unsigned long long low4 =
-                  (unsigned long long)v[0] + ((unsigned long long)v[1] << 8) +
-                  ((unsigned long long)v[2] << 16) + ((unsigned long long)v[3] << 24);
-              carry = (low4 + 0xffffffffull) >> 32;
-              continue;
-            }
-            const int li = slot - 1;           // Z limb
-            pend[li & 7] = limb4(v + 4 * k, carry);
-            if ((li & 7) == 7) emit(li);
-          }
-        });
-        if (tr) TC_STAMP(pos, 7);
-        tc_fence_before();
-        mbar_arrive(&tempty[0]);
+        const uint4 top = make_uint4((uint32_t)carry, 0u, 0u, 0u);
+        if (dg) *reinterpret_cast<uint4*>(brow + kL) = top;
+        if (fwd) *reinterpret_cast<uint4*>(xt_row) = top;
       }
-      {
-        mbar_wait(&tfull[1], fph[1]);
-        fph[1] ^= 1;
-        if (tr) TC_STAMP(pos, 8);
-        tc_fence_after();
-        const uint32_t taddr = lanebase + 256u;
-        drain256(taddr, carry, [&](int g, const uint32_t (&v)[32]) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const int li = 63 + 8 * g + k;     // columns 764 + 4 (li - 63) ..
-            pend[li & 7] = limb4(v + 4 * k, carry);
-            if ((li & 7) == 7) emit(li);
-          }
-        });
-        if (tr) TC_STAMP(pos, 9);
-        tc_fence_before();
-        mbar_arrive(&tempty[1]);
-      }
-      // columns 1020..1022 (1023 is empty): bytes 509..511 of X, Y, u, N
-      {
-        const uint32_t x9 = (xtop >> 8) & 0xffu, x10 = (xtop >> 16) & 0xffu, x11 = xtop >> 24;
-        const uint32_t y9 = (ytop >> 8) & 0xffu, y10 = (ytop >> 16) & 0xffu, y11 = ytop >> 24;
-        const uint32_t u9 = (utop >> 8) & 0xffu, u10 = (utop >> 16) & 0xffu, u11 = utop >> 24;
-        const uint32_t n9 = (ntop >> 8) & 0xffu, n10 = (ntop >> 16) & 0xffu, n11 = ntop >> 24;
-        const uint32_t c0 = x9 * y11 + x10 * y10 + x11 * y9 + u9 * n11 + u10 * n10 + u11 * n9;
-        const uint32_t c1 = x10 * y11 + x11 * y10 + u10 * n11 + u11 * n10;
-        const uint32_t c2 = x11 * y11 + u11 * n11;
-        const unsigned long long s = (unsigned long long)c0 + ((unsigned long long)c1 << 8) +
-                                     ((unsigned long long)c2 << 16) + carry;
-        const uint32_t z = (uint32_t)s;
-        const uint32_t top = (uint32_t)(s >> 32);
-        pend[7] = z;
-        emit(kL - 1);
-        // Z = z + 2^4096 * top < 2N: Z >= N iff the top carry is set or z >= N,
-        // decided by the top two limbs unless both equal N's (then by all of
-        // them, read back). The bucket keeps Z and a flag (the subtraction is
-        // deferred to its next reader); the forwarded X is reduced right here.
-        uint32_t f;
-        if (top) {
-          f = 1u;
-        } else if (pend[7] != ntop || pend[6] != n126) {
-          f = (pend[7] > ntop || (pend[7] == ntop && pend[6] > n126)) ? 1u : 0u;
-        } else {
-          f = 1u;                                // z == N so far: equal counts as >=
-          const uint32_t* zs = conflict ? nullptr : brow;
-          for (int li = kL - 3; li >= 0; --li) {
-            uint32_t zl;
-            if (zs) {
-              zl = zs[li];
-            } else {
-              const int cc = li >> 2, kb = cc >> 3, ch = cc & 7;
-              zl = reinterpret_cast<const uint32_t*>(
-                  XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4))[li & 3];
-            }
-            if (zl != sN[li]) {
-              f = zl > sN[li] ? 1u : 0u;
-              break;
-            }
-          }
-        }
-        if (dg) Fc[bidx] = (uint8_t)f;
-        if (conflict && f) {
-          uint32_t bw = 0;
-#pragma unroll 1
-          for (int cc = 0; cc < 32; ++cc) {
-            const int kb = cc >> 3, ch = cc & 7;
-            uint4* q = reinterpret_cast<uint4*>(XA + kb * (kRows * kBK) + t * kBK + ((ch ^ (t & 7)) << 4));
-            uint4 w = *q;
-            uint32_t v[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const unsigned long long d = (unsigned long long)v[i] - sN[4 * cc + i] - bw;
-              v[i] = (uint32_t)d;
-              bw = (uint32_t)(d >> 63);
-            }
-            *q = make_uint4(v[0], v[1], v[2], v[3]);
-          }
-        }
-      }
+      if (tr) TC_STAMP(pos, 6);
+      tc_fence_before();
+      mbar_arrive(&tempty[1]);
       if (!last) {
         gather_publish();                       // xfull for the next position
-        if (tr) TC_STAMP(pos, 10);
-        xtop = *xtop_p;
+        if (tr) TC_STAMP(pos, 7);
         dg = dg_n;
         dg_n = pos + 2 < pos1 ? digit_at(pos + 2) : 0u;
         prefetch_bucket(dg_n);
@@ -735,66 +604,31 @@ static PFN_cuTensorMapEncodeTiled_v12000 tcp_encode() {
   return fn;
 }
 
-static int tile_map(CUtensorMap* map, const void* base, int64_t rows) {
+// (rows x 544) u8 table matrix, boxes of 256 rows x box_k K bytes.
+static int table_map(CUtensorMap* map, const void* base, int64_t rows, int box_k,
+                     CUtensorMapSwizzle sw) {
   auto fn = tcp_encode();
   if (!fn) {
     set_error("cuTensorMapEncodeTiled unavailable");
     return kErrCuda;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)tcp::kBK, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)tcp::kBK};
-  cuuint32_t box[2] = {(cuuint32_t)tcp::kBK, 256};
+  cuuint64_t dims[2] = {(cuuint64_t)tcp::kTK, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)tcp::kTK};
+  cuuint32_t box[2] = {(cuuint32_t)box_k, 256};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    set_error("cuTensorMapEncodeTiled (tiles) failed (%d)", (int)r);
+    set_error("cuTensorMapEncodeTiled (tables) failed (%d)", (int)r);
     return kErrCuda;
   }
   return kOk;
 }
 
-static int upload_schedule() {
-  static bool done = false;
-  if (done) return kOk;
-  tcp::Step h[tcp::kNSteps];
-  int k = 0;
-  // U0, U1: output columns 256 gc .. of X * Y', tile delta = 256 gc - 128 ka
-  for (int gc = 0; gc < 2; ++gc)
-    for (int ka = 0; ka < 4; ++ka) {
-      const int delta = 256 * gc - 128 * ka;
-      const int t = (delta - tcp::kDeltaYp) / 128;
-      if (delta - 127 < 512 && delta + 255 >= 0 && t >= 0 && t < tcp::kTYp)
-        h[k++] = {(int8_t)gc, 0, (int8_t)ka, 0, (int8_t)t, (int8_t)gc};
-    }
-  // H0, H1 (output columns c0 = 508 / 764 of X * Y + u * N): both X * Y parts
-  // first (after them X is no longer read: the next position's gather may
-  // start), then both u * N parts (they wait for u)
-  for (int a = 0; a < 2; ++a)
-    for (int hh = 0; hh < 2; ++hh) {
-      const int c0 = 508 + 256 * hh;
-      for (int ka = 0; ka < 4; ++ka) {
-        const int delta = c0 - 128 * ka;
-        if (delta - 127 >= 512) continue;           // window entirely above byte 511
-        const int t = (delta - tcp::kDeltaY) / 128;
-        h[k++] = {(int8_t)(2 + hh), (int8_t)a, (int8_t)ka, (int8_t)(a ? 2 : 1), (int8_t)t,
-                  (int8_t)(2 + 2 * a + hh)};
-      }
-    }
-  if (k != tcp::kNSteps) {
-    set_error("tc_pippenger: schedule has %d steps", k);
-    return kErrCuda;
-  }
-  if (cudaMemcpyToSymbol(tcp::kSched, h, sizeof(h)) != cudaSuccess) return check_launch("schedule");
-  done = true;
-  return kOk;
-}
-
-// Digits per 32-bit exponent word: 6 (widths
-// 6,6,5,5,5,5 and 63 buckets per row); balanced widths, wider digits first.
+// Digits per 32-bit exponent word; balanced widths, wider digits first.
 static DigitSpec digit_spec() {
-  constexpr int D = 6;   // measured optimum of D = 4..7
+  constexpr int D = 6;
   DigitSpec ds{};
   ds.D = D;
   int off = 0, maxw = 0;
@@ -814,8 +648,7 @@ int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
   const DigitSpec ds = digit_spec();
   const int64_t npos = ds.D * n;
   const int64_t rows_p = ceil_div(rows, kRows) * kRows;
-  return (int64_t)clients * (2 * npos * kL * 4 + npos * (kTY + kTYp) * kTile + kTY * kTile +
-                             rows_p * ds.nb * (kL * 4 + 1));
+  return (int64_t)clients * (npos * kL * 4 + npos * kCols * kTK + rows_p * ds.nb * kXL * 4);
 }
 
 // W_c[rid[r] or r] (Montgomery form, 4096-bit N_c) for rows r < rows of 32-bit
@@ -825,20 +658,18 @@ int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
 // on tcgen05.
 int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint32_t* const* N,
                               const uint32_t* np, const uint32_t* const* one_m,
-                              const uint32_t* const* Nprime, uint32_t* const* W, int64_t n,
-                              const uint32_t* E, int64_t rs, const int32_t* rid, int64_t rows,
-                              cudaStream_t st) {
+                              uint32_t* const* W, int64_t n, const uint32_t* E, int64_t rs,
+                              const int32_t* rid, int64_t rows, cudaStream_t st) {
   using namespace tcp;
   const DigitSpec ds = digit_spec();
   const int nb = ds.nb;
   const int64_t npos = ds.D * n;
   if (clients <= 0 || clients > 65535 || n <= 0 || rows <= 0 || npos > 65536 ||
-      (int64_t)clients * npos * kTY * 256 >= (1ll << 31)) {
+      (int64_t)clients * npos * kCols >= (1ll << 31)) {
     set_error("tc_slot_fixed: bad shapes (clients=%d n=%lld rows=%lld)", clients, (long long)n,
               (long long)rows);
     return kErrInput;
   }
-  if (int e = upload_schedule()) return e;
   {
     // keep the multi-GB workspace in the stream-ordered pool between calls
     static bool pool_set = false;
@@ -857,19 +688,15 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   const int64_t tiles = ceil_div(rows, kRows);
   const int64_t rows_p = tiles * kRows;
   std::vector<TcClient> hc(C);
-  for (int c = 0; c < C; ++c) hc[c] = {P[c], N[c], one_m[c], Nprime[c], W[c], np[c]};
+  for (int c = 0; c < C; ++c) hc[c] = {P[c], N[c], one_m[c], W[c], np[c]};
   TcClient* dcl = nullptr;
-  uint32_t *Pd = nullptr, *Yp = nullptr, *Bk = nullptr;
-  uint8_t *tY = nullptr, *tYp = nullptr, *tN = nullptr, *Fk = nullptr;
+  uint32_t *Pd = nullptr, *Bk = nullptr;
+  uint8_t* T = nullptr;
   auto release = [&]() {
     if (dcl) cudaFreeAsync(dcl, st);
     if (Pd) cudaFreeAsync(Pd, st);
-    if (Yp) cudaFreeAsync(Yp, st);
+    if (T) cudaFreeAsync(T, st);
     if (Bk) cudaFreeAsync(Bk, st);
-    if (tY) cudaFreeAsync(tY, st);
-    if (tYp) cudaFreeAsync(tYp, st);
-    if (tN) cudaFreeAsync(tN, st);
-    if (Fk) cudaFreeAsync(Fk, st);
   };
   auto fail = [&](const char* what) {
     release();
@@ -879,45 +706,35 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   };
   if (cudaMallocAsync(reinterpret_cast<void**>(&dcl), sizeof(TcClient) * C, st) != cudaSuccess ||
       cudaMallocAsync(reinterpret_cast<void**>(&Pd), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Yp), (size_t)C * npos * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tY), (size_t)C * npos * kTY * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tYp), (size_t)C * npos * kTYp * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&tN), (size_t)C * kTY * kTile, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * nb * kL * 4, st) != cudaSuccess ||
-      cudaMallocAsync(reinterpret_cast<void**>(&Fk), (size_t)C * rows_p * nb, st) != cudaSuccess)
+      cudaMallocAsync(reinterpret_cast<void**>(&T), (size_t)C * npos * kCols * kTK, st) != cudaSuccess ||
+      cudaMallocAsync(reinterpret_cast<void**>(&Bk), (size_t)C * rows_p * nb * kXL * 4, st) != cudaSuccess)
     return fail("workspace allocation");
   // the host vector is read at enqueue time for pageable memory (synchronous copy)
-  if (cudaMemcpyAsync(dcl, hc.data(), sizeof(TcClient) * C, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-      cudaMemsetAsync(Fk, 0, (size_t)C * rows_p * nb, st) != cudaSuccess)
-    return fail("client table / flags");
+  if (cudaMemcpyAsync(dcl, hc.data(), sizeof(TcClient) * C, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return fail("client table");
   powtab_kernel<<<dim3((unsigned)ceil_div(n, 4), C), 128, 0, st>>>(dcl, n, ds, Pd);
-  mul_lo_kernel<<<dim3((unsigned)ceil_div(npos, 128), C), 128, 0, st>>>(dcl, Pd, npos, Yp);
-  toep_tiles_kernel<<<dim3((unsigned)(npos * kTY), C), 256, 0, st>>>(dcl, 1, Pd, npos, kTY,
-                                                                     kDeltaY, tY);
-  toep_tiles_kernel<<<dim3((unsigned)(npos * kTYp), C), 256, 0, st>>>(dcl, 1, Yp, npos, kTYp,
-                                                                      kDeltaYp, tYp);
-  toep_tiles_kernel<<<dim3((unsigned)kTY, C), 256, 0, st>>>(dcl, 2, nullptr, 1, kTY, kDeltaY, tN);
+  table_kernel<<<dim3((unsigned)ceil_div(npos, 4), C), 128, 0, st>>>(dcl, Pd, npos, T);
   {
     const int64_t cnt = rows_p * nb;
-    bucket_fill_kernel<<<dim3((unsigned)ceil_div(cnt * kL, 256), C), 256, 0, st>>>(dcl, Bk, cnt);
+    bucket_fill_kernel<<<dim3((unsigned)ceil_div(cnt * kXL, 256), C), 256, 0, st>>>(dcl, Bk, cnt);
   }
   if (check_launch("tc_slot_fixed setup")) return fail("setup kernels");
-  CUtensorMap mYp, mY, mN;
-  if (tile_map(&mYp, tYp, C * npos * kTYp * 256) || tile_map(&mY, tY, C * npos * kTY * 256) ||
-      tile_map(&mN, tN, (int64_t)C * kTY * 256))
+  CUtensorMap mT, mTail;
+  if (table_map(&mT, T, (int64_t)C * npos * kCols, kBK, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      table_map(&mTail, T, (int64_t)C * npos * kCols, kKT, CU_TENSOR_MAP_SWIZZLE_32B))
     return fail("tensor maps");
   cudaFuncSetAttribute(tc_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   // one launch walks every position (tiles are independent); chunked so a
   // launch stays well under a second
-  constexpr int64_t chunk = 1024;
+  constexpr int64_t chunk = 4096;
   const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(tiles * C, 2 * 148)));
   for (int64_t p0 = 0; p0 < npos; p0 += ck) {
     const int64_t p1 = std::min<int64_t>(npos, p0 + ck);
     tc_step_kernel<<<dim3((unsigned)tiles, C), kThreads, kSmem, st>>>(
-        mYp, mY, mN, dcl, Pd, ds, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk, Fk);
+        mT, mTail, ds, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk);
   }
   if (check_launch("tc_step")) return fail("tc_step launch");
-  bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, Fk, nb, rows,
+  bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, nb, rows,
                                                                              rows_p, rid);
   if (check_launch("bucket_combine")) return fail("bucket_combine");
   release();
@@ -932,9 +749,9 @@ extern "C" int zpir_tc_trace(unsigned long long* out) {
 
 // Single-client form (the original entry point).
 int tc_slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs, int64_t rows,
-                         const uint32_t* N, uint32_t np, const uint32_t* one_m,
-                         const uint32_t* Nprime, uint32_t* W, cudaStream_t st) {
-  return tc_slot_fixed_many_launch(1, &P, &N, &np, &one_m, &Nprime, &W, n, E, rs, nullptr, rows, st);
+                         const uint32_t* N, uint32_t np, const uint32_t* one_m, uint32_t* W,
+                         cudaStream_t st) {
+  return tc_slot_fixed_many_launch(1, &P, &N, &np, &one_m, &W, n, E, rs, nullptr, rows, st);
 }
 
 }  // namespace zpir

@@ -359,8 +359,7 @@ def slot_fixed(P, n, E, rs, row_ids, rows, kctx, W, stream=None):
 def slot_fixed_tc(P, n, E, rs, rows, kctx, W, stream=None):
     """slot_fixed (all rows) with the bucket updates on the tensor cores."""
     _lib.call("zpir_slot_fixed_tc", _lib.ptr(P), n, _lib.ptr(E), rs, rows, kctx.l2,
-              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_one2), _lib.ptr(kctx.d_nprime_full()),
-              _lib.ptr(W), _s(stream))
+              _lib.ptr(kctx.d_m2), kctx.c2.np, _lib.ptr(kctx.d_one2), _lib.ptr(W), _s(stream))
     return W
 
 
@@ -376,10 +375,9 @@ def slot_fixed_tc_many(jobs, n, E, rs, rows, rid=None, stream=None):
     P = arr([p.data_ptr() for p, _, _ in jobs])
     N = arr([k.d_m2.data_ptr() for _, k, _ in jobs])
     one = arr([k.d_one2.data_ptr() for _, k, _ in jobs])
-    npr = arr([k.d_nprime_full().data_ptr() for _, k, _ in jobs])
     W = arr([w.data_ptr() for _, _, w in jobs])
     np_ = (ctypes.c_uint32 * c)(*[k.c2.np for _, k, _ in jobs])
-    _lib.call("zpir_slot_fixed_tc_many", c, P, N, np_, one, npr, W, n, _lib.ptr(E), rs,
+    _lib.call("zpir_slot_fixed_tc_many", c, P, N, np_, one, W, n, _lib.ptr(E), rs,
               _lib.ptr(rid) if rid is not None else None, rows, _s(stream))
     return [w for _, _, w in jobs]
 
