@@ -17,7 +17,7 @@
 // dependency between the MMAs of one position: per position and 128-row tile
 //   task A: columns   0..255 (17 N = 256 MMAs) -> limbs 0..63
 //   task B: columns 256..511 (17 MMAs)          -> limbs 64..127 and the carry, limb 128
-// into two TMEM buffers, drained by the epilogue while the other one fills.
+// into two TMEM buffers, each drained by its own four epilogue warps.
 // The bucket combine reduces each bucket once (quotient estimate from the top
 // limbs, bignum.cuh) before its IMAD running products.
 //
@@ -66,14 +66,16 @@ constexpr int kKT = 32;            // tail k-step: bytes 512..543 (512..514 used
 constexpr int kTK = kKB * kBK + kKT;   // table row pitch = K bytes per position (544)
 constexpr int kUsedK = 515;        // bytes of X that can be non-zero
 constexpr int kCols = 512;         // byte columns of the product = table rows per position
-constexpr int kTile = 256 * kBK;   // B stage: 256 columns x 128 K bytes (SW128)
-constexpr int kTail = 256 * kKT;   // B tail stage: 256 columns x 32 K bytes (SW32)
+constexpr int kHalf = 128;         // table columns staged per CTA of a pair and task
+constexpr int kTile = kHalf * kBK; // table stage: 128 columns x 128 K bytes (SW128)
+constexpr int kTail = kHalf * kKT; // table tail stage: 128 columns x 32 K bytes (SW32)
 constexpr int kStages = 4;
-constexpr int kTStages = 3;
-constexpr int kThreads = 192;
+constexpr int kTStages = 4;
+constexpr int kThreads = 320;     // tile X warps 0-3, tile Y warps 4-7, TMA warp 8, MMA warp 9
 constexpr int kABytes = kRows * kKB * kBK;   // X bytes 0..511: 4 k-blocks of 128 x 128 B (SW128)
 constexpr int kATail = kRows * kKT;          // X bytes 512..543 (SW32)
-constexpr int kSmem = kABytes + kATail + kStages * kTile + kTStages * kTail + 1024 + 1024;
+constexpr int kXBytes = kABytes + kATail;    // X of one tile
+constexpr int kSmem = 2 * kXBytes + kStages * kTile + kTStages * kTail + 1024 + 1024;
 
 }  // namespace tcp
 
@@ -218,6 +220,15 @@ bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restric
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Arrive on a barrier of the leader CTA. Relaxed: what the arrival publishes is
+// this CTA's own shared memory (ordered by the proxy fence before it) or drained
+// TMEM (tcgen05.wait::ld); a release at cluster scope would also wait for every
+// global store of the drain to be acknowledged (MEMBAR.ALL.GPU, thousands of
+// cycles on the critical path).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 
 // 32 lanes x 32 bit, 32 consecutive columns -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
@@ -236,8 +247,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 // Wait for this thread's outstanding TMEM loads, ordered after `dep` (the
 // last value computed from the previous batch) so the compiler keeps that
 // work ahead of the wait.
-__device__ __forceinline__ void tmem_wait_after(unsigned long long dep) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::"l"(dep) : "memory");
+__device__ __forceinline__ void tmem_wait_after(uint32_t dep) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::"r"(dep) : "memory");
 }
 __device__ __forceinline__ void regs_ready(uint32_t (&v)[32]) {
 #pragma unroll
@@ -249,31 +260,59 @@ __device__ __forceinline__ void regs_ready(uint32_t (&v)[32]) {
 // f(g, v) consumes columns 32 g .. 32 g + 31; it updates `carry`, which also
 // orders the next wait after the processing.
 template <class F>
-__device__ __forceinline__ void drain256(uint32_t taddr, unsigned long long& carry, F&& f) {
+__device__ __forceinline__ void drain256(uint32_t taddr, uint32_t& carry, F&& f) {
   uint32_t va[32], vb[32];
   tmem_ld32(taddr, va);
   tmem_wait_after(carry);
   regs_ready(va);
-#pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    uint32_t (&cur)[32] = (g & 1) ? vb : va;
-    uint32_t (&nxt)[32] = (g & 1) ? va : vb;
-    if (g < 7) tmem_ld32(taddr + 32 * (g + 1), nxt);
-    f(g, cur);
-    if (g < 7) {
+#pragma unroll 1
+  for (int g = 0; g < 8; g += 2) {
+    tmem_ld32(taddr + 32 * (g + 1), vb);
+    f(g, va);
+    tmem_wait_after(carry);
+    regs_ready(vb);
+    if (g < 6) tmem_ld32(taddr + 32 * (g + 2), va);
+    f(g + 1, vb);
+    if (g < 6) {
       tmem_wait_after(carry);
-      regs_ready(nxt);
+      regs_ready(va);
     }
   }
 }
 
-// Four byte columns (s32 sums) + carry -> one 32-bit limb.
-__device__ __forceinline__ uint32_t limb4(const uint32_t* v, unsigned long long& carry) {
-  const unsigned long long s = (unsigned long long)v[0] + ((unsigned long long)v[1] << 8) +
-                               ((unsigned long long)v[2] << 16) +
-                               ((unsigned long long)v[3] << 24) + carry;
-  carry = s >> 32;
-  return (uint32_t)s;
+// 32 byte columns (s32 sums < 2^25) + carry in -> eight 32-bit limbs + carry
+// out (< 2^26). Per limb s = v0 + 2^8 v1 + 2^16 v2 + 2^24 v3 in 32-bit pieces:
+// lo = s mod 2^32 by wrapping shift-adds, hi = floor(s / 2^32) through the
+// exact floors w1 = (v0 >> 8) + v1, w2 = (w1 >> 8) + v2, w3 = (w2 >> 8) + v3,
+// hi = w3 >> 8 (64-bit multiply-adds run at a fraction of the 32-bit rate, and
+// the drains are issue-bound). The eight (lo, hi) pairs are independent; only
+// the final add-with-carry chain lo_k + hi_{k-1} is sequential.
+__device__ __forceinline__ void limbs8(const uint32_t* v, uint32_t& cin, uint32_t (&out)[8]) {
+  uint32_t lo[8], hi[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t v0 = v[4 * k], v1 = v[4 * k + 1], v2 = v[4 * k + 2], v3 = v[4 * k + 3];
+    lo[k] = v0 + (v1 << 8) + (v2 << 16) + (v3 << 24);
+    const uint32_t w1 = (v0 >> 8) + v1;
+    const uint32_t w2 = (w1 >> 8) + v2;
+    const uint32_t w3 = (w2 >> 8) + v3;
+    hi[k] = w3 >> 8;
+  }
+  asm volatile(
+      "add.cc.u32 %0, %9, %17;\n\t"
+      "addc.cc.u32 %1, %10, %18;\n\t"
+      "addc.cc.u32 %2, %11, %19;\n\t"
+      "addc.cc.u32 %3, %12, %20;\n\t"
+      "addc.cc.u32 %4, %13, %21;\n\t"
+      "addc.cc.u32 %5, %14, %22;\n\t"
+      "addc.cc.u32 %6, %15, %23;\n\t"
+      "addc.cc.u32 %7, %16, %24;\n\t"
+      "addc.u32 %8, %25, 0;"
+      : "=r"(out[0]), "=r"(out[1]), "=r"(out[2]), "=r"(out[3]), "=r"(out[4]), "=r"(out[5]),
+        "=r"(out[6]), "=r"(out[7]), "=r"(cin)
+      : "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]),
+        "r"(lo[7]), "r"(cin), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]),
+        "r"(hi[5]), "r"(hi[6]), "r"(hi[7]));
 }
 
 // K-major operand tile with SWIZZLE_32B: rows of 32 bytes, 8-row (256 B) atoms.
@@ -287,9 +326,25 @@ __device__ __forceinline__ uint64_t desc_sw32(uint32_t saddr) {
   return d;
 }
 
-// Pippenger positions pos0..pos1-1 for one 128-row tile of one client per CTA
+// Pippenger positions pos0..pos1-1 for TWO 128-row tiles of one client per CTA
 // (tiles are independent: a row only touches its own buckets):
 //   B[r][d - 1] <- B[r][d - 1] * y[pos] for d = digit(r, pos) != 0.
+//
+// CTA pairs (clusters of 2 on one TPC, tcgen05 cta_group::2): the leader issues
+// M = 256 MMAs over both CTAs' X tiles, every CTA stages its own HALF of the
+// table columns of a task (128 of 256: half the L2 -> SM and shared-memory
+// traffic per MMA) and drains its own 128 TMEM lanes. The two tiles X and Y of a
+// CTA alternate on the tensor pipe, position by position:
+//   X.A(p) -> TMEM 0, X.B(p) -> TMEM 1, Y.A(p) -> TMEM 0, Y.B(p) -> TMEM 1, X.A(p+1) ...
+// so everything a tile's next position depends on -- the drain of its task B
+// (forwarded rows), the gather of its next X from the buckets, the drain that
+// frees a TMEM buffer -- happens under the other tile's MMAs. Per CTA:
+//   warps 0-3  tile X, one row per thread: drains, gather (cp.async)
+//   warps 4-7  tile Y
+//   warp 8     TMA producer (its table halves; completion on the leader's barrier)
+//   warp 9     MMA issuer (leader only)
+// (a scheduler serves its highest warp id first: the two single-thread warps
+// must not wait behind the draining warps.)
 __global__ void __launch_bounds__(tcp::kThreads, 1)
 tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__ CUtensorMap mapTail,
                const __grid_constant__ DigitSpec ds, const uint32_t* __restrict__ E, int64_t rs,
@@ -299,23 +354,24 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* XA = smem;                       // X bytes 0..511: 4 k-blocks of 128 x 128 B, SW128
-  uint8_t* XT = smem + kABytes;             // X bytes 512..543: 128 x 32 B, SW32
-  uint8_t* BS = XT + kATail;                // table stages (256 x 128 B)
-  uint8_t* BT = BS + kStages * kTile;       // table tail stages (256 x 32 B)
-  uint64_t* full = reinterpret_cast<uint64_t*>(BT + kTStages * kTail);
+  uint8_t* XB = smem;                       // per tile: X bytes 0..511 (4 k-blocks of 128 x 128 B,
+                                            // SW128), X bytes 512..543 (128 x 32 B, SW32)
+  uint8_t* BS = XB + 2 * kXBytes;           // table stages (128 x 128 B)
+  uint8_t* BT = BS + kStages * kTile;       // table tail stages (128 x 32 B)
+  uint64_t* full = reinterpret_cast<uint64_t*>(BT + kTStages * kTail);   // leader
   uint64_t* empty = full + kStages;
-  uint64_t* tlfull = empty + kStages;       // tail ring
+  uint64_t* tlfull = empty + kStages;       // tail ring (leader)
   uint64_t* tlempty = tlfull + kTStages;
-  uint64_t* xfull = tlempty + kTStages;     // X of the position complete in shared memory
-  uint64_t* xfree = xfull + 1;              // every MMA reading X of the position done
-  uint64_t* tfull = xfree + 1;              // [2] per TMEM buffer
-  uint64_t* tempty = tfull + 2;             // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xfull = tlempty + kTStages;     // [tile] leader: X of the tile complete in both CTAs
+  uint64_t* tfull = xfull + 2;              // [tile][task] accumulator complete
+  uint64_t* tempty = tfull + 4;             // [tile][task] leader: accumulator drained in both CTAs
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 4);
 
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
   const int client = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0 && lane == 0) {
+  if (warp == 8 && lane == 0) {
     tma_prefetch(&mapT);
     tma_prefetch(&mapTail);
     for (int s = 0; s < kStages; ++s) {
@@ -326,108 +382,115 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
       mbar_init(&tlfull[s], 1);
       mbar_init(&tlempty[s], 1);
     }
-    mbar_init(xfull, 128);
-    mbar_init(xfree, 1);
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&xfull[b], 2 * 128);
+    }
+    for (int b = 0; b < 4; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 2 * 128);
     }
     fence_mbar_init();
   }
   // bytes 516..543 of every X stay zero
-  for (int i = threadIdx.x; i < kATail / 16; i += blockDim.x)
-    reinterpret_cast<uint4*>(XT)[i] = make_uint4(0u, 0u, 0u, 0u);
-  if (warp == 1) tmem_alloc(tslot, 512);
+  for (int i = threadIdx.x; i < 2 * kATail / 16; i += blockDim.x) {
+    const int b = i / (kATail / 16), j = i % (kATail / 16);
+    reinterpret_cast<uint4*>(XB + b * kXBytes + kABytes)[j] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (warp == 9) tmem_alloc_pair(tslot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();   // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  const int64_t row0 = (int64_t)blockIdx.x * kRows;
 
-  if (warp == 0) {
+  if (warp == 8) {
     if (lane == 0) {
-      // ---------------- TMA producer: the table of every position, by column half ----------------
+      // ---------------- TMA producer: this CTA's half of the table columns of each task ----------------
       const uint64_t pol = l2_evict_last();
       const int64_t cpos = (int64_t)client * npos;
       int stage = 0, ts = 0;
       uint32_t phase = 0, tph = 0;
       for (int pos = pos0; pos < pos1; ++pos)
-        for (int task = 0; task < 2; ++task) {
-          const int trow = (int)(((cpos + pos) * 2 + task) * 256);
+#pragma unroll 1
+        for (int tt = 0; tt < 4; ++tt) {                  // (tile X, Y) x (task A, B)
+          const int trow = (int)(((cpos + pos) * 2 + (tt & 1)) * 256) + (int)rank * kHalf;
+#pragma unroll 1
           for (int kb = 0; kb < kKB; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            mbar_expect_tx(&full[stage], kTile);
-            tma_load_2d_hint(BS + stage * kTile, &mapT, &full[stage], kb * kBK, trow, pol);
+            if (leader) mbar_expect_tx(&full[stage], 2 * kTile);
+            tma_load_2d_pair(BS + stage * kTile, &mapT, mapa_shared(smem_u32(&full[stage]), 0),
+                             kb * kBK, trow, pol);
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
           mbar_wait(&tlempty[ts], tph ^ 1);
-          mbar_expect_tx(&tlfull[ts], kTail);
-          tma_load_2d_hint(BT + ts * kTail, &mapTail, &tlfull[ts], kKB * kBK, trow, pol);
+          if (leader) mbar_expect_tx(&tlfull[ts], 2 * kTail);
+          tma_load_2d_pair(BT + ts * kTail, &mapTail, mapa_shared(smem_u32(&tlfull[ts]), 0),
+                           kKB * kBK, trow, pol);
           if (++ts == kTStages) {
             ts = 0;
             tph ^= 1;
           }
         }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer: task A -> TMEM buffer 0, task B -> buffer 1 ----------------
-      const uint32_t idesc = idesc_u8(kRows, 256);
-      const uint64_t xtd = desc_sw32(smem_u32(XT));
+  } else if (warp == 9) {
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer: task A -> TMEM buffer 0, task B -> buffer 1, tiles alternating ----------------
+      const uint32_t idesc = idesc_u8(2 * kRows, 256);
       int stage = 0, ts = 0;
-      uint32_t phase = 0, tph = 0, xph = 0;
-      uint32_t eph[2] = {0, 0};
+      uint32_t phase = 0, tph = 0, xph = 0, eph = 0;
 #ifdef ZPIR_TC_TRACE
       unsigned long long fwait = 0;   // cycles the MMA thread waited for table tiles this position
 #endif
       for (int pos = pos0; pos < pos1; ++pos) {
-        for (int task = 0; task < 2; ++task) {
-          if (task == 0) {
-            mbar_wait(xfull, xph);
-            xph ^= 1;
-          }
-          if (pos > pos0) {                              // the buffer's previous drain
-            mbar_wait(&tempty[task], eph[task]);
-            eph[task] ^= 1;
-          }
-          tc_fence_after();
-          TC_STAMP(pos, 11 + task);
-          const uint32_t d = tbase + (uint32_t)(task * 256);
-          for (int kb = 0; kb < kKB; ++kb) {
-#ifdef ZPIR_TC_TRACE
-            const unsigned long long tw0 = clock64();
-            mbar_wait(&full[stage], phase);
-            fwait += clock64() - tw0;
-#else
-            mbar_wait(&full[stage], phase);
-#endif
+        for (int tile = 0; tile < 2; ++tile) {
+          const uint8_t* XA = XB + tile * kXBytes;
+          const uint64_t xtd = desc_sw32(smem_u32(XA + kABytes));
+          for (int task = 0; task < 2; ++task) {
+            if (task == 0) mbar_wait(&xfull[tile], xph);
+            // the buffer's previous drain: the other tile's, of this position (tile Y) or
+            // the previous one (tile X)
+            if (pos > pos0 || tile == 1)
+              mbar_wait(&tempty[2 * (tile ^ 1) + task], tile ? eph : eph ^ 1);
             tc_fence_after();
-            const uint64_t ad = desc_sw128(smem_u32(XA + kb * (kRows * kBK)));
-            const uint64_t bd = desc_sw128(smem_u32(BS + stage * kTile));
+            if (tile == 0) TC_STAMP(pos, 11 + task);
+            const uint32_t d = tbase + (uint32_t)(task * 256);
+            for (int kb = 0; kb < kKB; ++kb) {
+#ifdef ZPIR_TC_TRACE
+              const unsigned long long tw0 = clock64();
+              mbar_wait(&full[stage], phase);
+              fwait += clock64() - tw0;
+#else
+              mbar_wait(&full[stage], phase);
+#endif
+              tc_fence_after();
+              const uint64_t ad = desc_sw128(smem_u32(XA + kb * (kRows * kBK)));
+              const uint64_t bd = desc_sw128(smem_u32(BS + stage * kTile));
 #pragma unroll
-            for (int k = 0; k < kBK / 32; ++k)
-              umma_i8(d, ad + 2 * k, bd + 2 * k, idesc, (kb == 0 && k == 0) ? 0u : 1u);
-            umma_commit(&empty[stage]);
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
+              for (int k = 0; k < kBK / 32; ++k)
+                umma_i8_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb == 0 && k == 0) ? 0u : 1u);
+              umma_commit_pair(&empty[stage], 0x3);
+              if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
+            mbar_wait(&tlfull[ts], tph);
+            tc_fence_after();
+            umma_i8_pair(d, xtd, desc_sw32(smem_u32(BT + ts * kTail)), idesc, 1u);
+            umma_commit_pair(&tlempty[ts], 0x3);
+            if (++ts == kTStages) {
+              ts = 0;
+              tph ^= 1;
+            }
+            umma_commit_pair(&tfull[2 * tile + task], 0x3);
           }
-          mbar_wait(&tlfull[ts], tph);
-          tc_fence_after();
-          umma_i8(d, xtd, desc_sw32(smem_u32(BT + ts * kTail)), idesc, 1u);
-          umma_commit(&tlempty[ts]);
-          if (++ts == kTStages) {
-            ts = 0;
-            tph ^= 1;
-          }
-          if (task == 1) umma_commit(xfree);             // X no longer read
-          umma_commit(&tfull[task]);
+          if (tile == 0) TC_STAMP(pos, 13);
         }
-        TC_STAMP(pos, 13);
+        xph ^= 1;
+        eph ^= 1;
+        TC_STAMP(pos, 14);
 #ifdef ZPIR_TC_TRACE
         if (blockIdx.x == 0 && blockIdx.y == 0 && pos - pos0 < 64) g_tc_trace[(pos - pos0) * 16 + 15] = fwait;
         fwait = 0;
@@ -435,63 +498,81 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
       }
     }
   } else {
-    // ---------------- epilogue: one row per thread (TMEM lane), 4 warps ----------------
+    // ---------------- epilogue: one row per thread (TMEM lane), warps 0-3 tile X, 4-7 tile Y ----------------
+    const int tile = warp >> 2;
     const int quarter = warp & 3;
     const int t = quarter * 32 + lane;          // row within the tile = TMEM lane
+    const int64_t row0 = ((int64_t)blockIdx.x * 2 + tile) * kRows;
     const int64_t r = row0 + t;
     const int64_t er = r < rows ? (rid ? (int64_t)rid[r] : r) : 0;
     const int nb = ds.nb;
     uint32_t* Bc = Ball + (int64_t)client * rows_p * nb * kXL;
     const uint32_t lanebase = tbase + ((uint32_t)(quarter * 32) << 16);
-    uint32_t fph[2] = {0, 0}, xfph = 0;
-    const int kbl = lane >> 3, chl = lane & 7;  // this lane's 16-byte chunk of bytes 0..511
-    const uint32_t xa_l = smem_u32(XA) + kbl * (kRows * kBK) + (uint32_t)(quarter * 32) * kBK;
-    const uint32_t xa_t = smem_u32(XA) + t * kBK;                        // + k-block, chunk
-    const uint32_t xt_t = smem_u32(XT) + t * kKT + (((t >> 2) & 1) << 4);  // chunk 0 of the tail row
+    uint8_t* XA = XB + tile * kXBytes;
     uint8_t* xa_row = XA + t * kBK;
-    uint8_t* xt_row = XT + t * kKT + (((t >> 2) & 1) << 4);
-    const int64_t rbase = row0 + quarter * 32;
+    uint8_t* xt_row = XA + kABytes + t * kKT + (((t >> 2) & 1) << 4);   // chunk 0 of the tail row
+    const uint32_t xfull_l = mapa_shared(smem_u32(&xfull[tile]), 0);
+    const uint32_t tempty_a = mapa_shared(smem_u32(&tempty[2 * tile]), 0);
+    const uint32_t tempty_b = mapa_shared(smem_u32(&tempty[2 * tile + 1]), 0);
+    uint64_t* tfull_a = &tfull[2 * tile];
+    uint64_t* tfull_b = &tfull[2 * tile + 1];
     auto digit_at = [&](int p) -> uint32_t {
-      if (r >= rows) return 0u;
+      if (r >= rows || p >= pos1) return 0u;
       const int di = p / (int)n;
       return (E[er * rs + (p - (int64_t)di * n)] >> ds.off[di]) & ((1u << ds.width[di]) - 1u);
     };
-    // X rows of the warp from their buckets, warp-cooperative async copies: lane
-    // c moves bytes 16c..16c+15 of each of the warp's 32 rows into the SW128 A
-    // layout (zero fill for digit 0), and the tail chunk of its own row. A row
-    // with `fwd` set (digit repeats) is copied by its own thread instead: the low
-    // half from the bucket it has just stored, the high half straight from the
-    // drain of task B.
-    auto gather_issue = [&](uint32_t dgv, uint32_t fwd) {
-      const uint32_t sk = __ballot_sync(0xffffffffu, fwd != 0);
-#pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t d_i = __shfl_sync(0xffffffffu, dgv, i);
-        if ((sk >> i) & 1u) continue;
-        const uint32_t* src = Bc + ((rbase + i) * nb + (d_i ? d_i - 1 : 0)) * kXL + 4 * lane;
-        const uint32_t dst = xa_l + i * kBK + ((chl ^ (i & 7)) << 4);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-                     "r"(d_i ? 16u : 0u)
-                     : "memory");
+    auto store8 = [&](uint32_t* dst, const uint32_t (&v)[8]) {
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(v[0]),
+                   "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                   : "memory");
+    };
+    // X rows of the warp from their buckets, warp-cooperative async copies: eight
+    // lanes per row, lane q of them moving the 16-byte chunk q of each of the
+    // row's four 128-byte k-block segments into the SW128 A layout (whole
+    // 128-byte lines in global memory, conflict-free in shared memory; zero fill
+    // for digit 0), and lane 0 the tail chunk. A row with `fwd` set (digit
+    // repeats) is copied by its own thread instead: the low half from the bucket
+    // it has just stored, the high half straight from the drain of task B.
+    const int gj = lane >> 3, gq = lane & 7;
+    const uint4* wsrc = reinterpret_cast<const uint4*>(Bc + (row0 + quarter * 32) * nb * kXL) + gq;
+    const uint32_t rstride = (uint32_t)nb * (kXL / 4);   // one row's buckets, in 16-byte units
+    const uint32_t xa_w = smem_u32(XA) + (uint32_t)(quarter * 32) * kBK;
+    const uint32_t xt_w = smem_u32(XA) + kABytes + (uint32_t)(quarter * 32) * kKT;
+    auto gather_issue = [&](uint32_t dgv, uint32_t fwd, const uint32_t* own) {
+      // bucket index | live (digit != 0) | forwarded, of this lane's row
+      const uint32_t pk = (dgv ? dgv - 1u : 0u) | (dgv ? 0x100u : 0u) | (fwd ? 0x200u : 0u);
+#pragma unroll 2
+      for (int it = 0; it < 8; ++it) {
+        const int i = 4 * it + gj;                         // row of the warp
+        const uint32_t p_i = __shfl_sync(0xffffffffu, pk, i);
+        if (p_i & 0x200u) continue;
+        const uint4* src = wsrc + ((uint32_t)i * rstride + (p_i & 0xffu) * (kXL / 4));
+        const uint32_t dst = xa_w + i * kBK + ((gq ^ (i & 7)) << 4);
+        const uint32_t sz = (p_i >> 4) & 16u;
+#pragma unroll
+        for (int kb = 0; kb < kKB; ++kb)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + kb * (kRows * kBK)),
+                       "l"(src + 8 * kb), "r"(sz)
+                       : "memory");
+        if (gq == 0)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                           xt_w + i * kKT + (((i >> 2) & 1) << 4)),
+                       "l"(src + 32), "r"(sz)
+                       : "memory");
       }
-      const uint32_t* own = Bc + (r * nb + (dgv ? dgv - 1 : 0)) * kXL;
-      if (!fwd) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(xt_t), "l"(own + kL),
-                     "r"(dgv ? 16u : 0u)
-                     : "memory");
-      } else {
+      if (fwd) {
 #pragma unroll 4
         for (int cc = 0; cc < 16; ++cc)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                           xa_t + (cc >> 3) * (kRows * kBK) + (((cc & 7) ^ (t & 7)) << 4)),
+                           smem_u32(xa_row) + (cc >> 3) * (kRows * kBK) + (((cc & 7) ^ (t & 7)) << 4)),
                        "l"(own + 4 * cc)
                        : "memory");
       }
     };
-    auto gather_publish = [&]() {
+    auto publish = [&]() {
       asm volatile("cp.async.wait_all;" ::: "memory");
       fence_async_smem();
-      mbar_arrive(xfull);
+      mbar_arrive_remote(xfull_l);
     };
     auto prefetch_bucket = [&](uint32_t d) {
       if (!d) return;
@@ -501,93 +582,76 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
     };
 
     // prologue: X of the first position
-    uint32_t dg = digit_at(pos0);
-    gather_issue(dg, 0u);
-    gather_publish();
-    uint32_t dg_n = pos0 + 1 < pos1 ? digit_at(pos0 + 1) : 0u;
+    uint32_t dg = digit_at(pos0), dg_n = digit_at(pos0 + 1);
+    gather_issue(dg, 0u, nullptr);
+    publish();
     prefetch_bucket(dg_n);
-
+    uint32_t fph = 0;
     for (int pos = pos0; pos < pos1; ++pos) {
       const bool last = pos + 1 >= pos1;
-      const bool tr = threadIdx.x == 64;
+      const bool tr = threadIdx.x == 0;
       if (tr) TC_STAMP(pos, 0);
       uint32_t* brow = Bc + ((r * nb) + (dg ? dg - 1 : 0)) * kXL;
       // the next position's bucket is this position's (digit repeats): its X is
       // this position's output
       const uint32_t fwd = (!last && dg && dg_n == dg) ? 1u : 0u;
-      // limbs awaiting a 32-byte store (one 256-bit STG per 8 limbs: whole sectors)
-      uint32_t pend[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      unsigned long long carry = 0;
+      uint32_t carry = 0;
       // ---- task A: limbs 0..63
-      mbar_wait(&tfull[0], fph[0]);
-      fph[0] ^= 1;
+      mbar_wait(tfull_a, fph);
       if (tr) TC_STAMP(pos, 1);
       tc_fence_after();
       drain256(lanebase, carry, [&](int g, const uint32_t (&v)[32]) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pend[k] = limb4(v + 4 * k, carry);
-        if (dg)
-          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + 8 * g),
-                       "r"(pend[0]), "r"(pend[1]), "r"(pend[2]), "r"(pend[3]), "r"(pend[4]),
-                       "r"(pend[5]), "r"(pend[6]), "r"(pend[7])
-                       : "memory");
+        uint32_t pend[8];
+        limbs8(v, carry, pend);
+        if (dg) store8(brow + 8 * g, pend);
       });
       if (tr) TC_STAMP(pos, 2);
       tc_fence_before();
-      mbar_arrive(&tempty[0]);
-      // ---- the next position's gather, once no MMA reads X any more; it lands
-      // while task B is drained
-      if (!last) {
-        mbar_wait(xfree, xfph);
-        xfph ^= 1;
-        if (tr) TC_STAMP(pos, 3);
-        gather_issue(dg_n, fwd);
-        if (tr) TC_STAMP(pos, 4);
-      }
-      // ---- task B: limbs 64..127 and the carry out (limb 128)
-      mbar_wait(&tfull[1], fph[1]);
-      fph[1] ^= 1;
+      mbar_arrive_remote(tempty_a);
+      // ---- task B: limbs 64..127 and the carry out (limb 128). Once it is complete
+      // no MMA reads X any more: forwarded rows go straight into X
+      mbar_wait(tfull_b, fph);
+      fph ^= 1;
       if (tr) TC_STAMP(pos, 5);
       tc_fence_after();
       drain256(lanebase + 256u, carry, [&](int g, const uint32_t (&v)[32]) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) pend[k] = limb4(v + 4 * k, carry);
-        if (dg)
-          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(brow + 64 + 8 * g),
-                       "r"(pend[0]), "r"(pend[1]), "r"(pend[2]), "r"(pend[3]), "r"(pend[4]),
-                       "r"(pend[5]), "r"(pend[6]), "r"(pend[7])
-                       : "memory");
+        uint32_t pend[8];
+        limbs8(v, carry, pend);
+        if (dg) store8(brow + 64 + 8 * g, pend);
         if (fwd) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cc = 16 + 2 * g + h, kb = cc >> 3, ch = cc & 7;
-            *reinterpret_cast<uint4*>(xa_row + kb * (kRows * kBK) + ((ch ^ (t & 7)) << 4)) =
-                make_uint4(pend[4 * h], pend[4 * h + 1], pend[4 * h + 2], pend[4 * h + 3]);
-          }
+          const int cc = 16 + 2 * g;
+          *reinterpret_cast<uint4*>(xa_row + (cc >> 3) * (kRows * kBK) + (((cc & 7) ^ (t & 7)) << 4)) =
+              make_uint4(pend[0], pend[1], pend[2], pend[3]);
+          *reinterpret_cast<uint4*>(xa_row + (cc >> 3) * (kRows * kBK) + ((((cc + 1) & 7) ^ (t & 7)) << 4)) =
+              make_uint4(pend[4], pend[5], pend[6], pend[7]);
         }
       });
       {
-        const uint4 top = make_uint4((uint32_t)carry, 0u, 0u, 0u);
+        const uint4 top = make_uint4(carry, 0u, 0u, 0u);
         if (dg) *reinterpret_cast<uint4*>(brow + kL) = top;
         if (fwd) *reinterpret_cast<uint4*>(xt_row) = top;
       }
       if (tr) TC_STAMP(pos, 6);
       tc_fence_before();
-      mbar_arrive(&tempty[1]);
+      mbar_arrive_remote(tempty_b);
       if (!last) {
-        gather_publish();                       // xfull for the next position
+        // ---- the next position's gather; it lands under the other tile's MMAs
+        __syncwarp();
+        gather_issue(dg_n, fwd, brow);
+        if (tr) TC_STAMP(pos, 4);
+        publish();                              // xfull for the tile's next position
         if (tr) TC_STAMP(pos, 7);
         dg = dg_n;
-        dg_n = pos + 2 < pos1 ? digit_at(pos + 2) : 0u;
+        dg_n = digit_at(pos + 2);
         prefetch_bucket(dg_n);
       }
     }
   }
   tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
+  cluster_sync();   // all MMAs consumed, all TMEM reads done in both CTAs
+  if (warp == 9) {
     tc_fence_after();
-    tmem_dealloc(tbase, 512);
+    tmem_dealloc_pair(tbase, 512);
   }
 }
 
@@ -604,7 +668,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 tcp_encode() {
   return fn;
 }
 
-// (rows x 544) u8 table matrix, boxes of 256 rows x box_k K bytes.
+// (rows x 544) u8 table matrix, boxes of 128 rows (one CTA's half of a task) x box_k K bytes.
 static int table_map(CUtensorMap* map, const void* base, int64_t rows, int box_k,
                      CUtensorMapSwizzle sw) {
   auto fn = tcp_encode();
@@ -614,7 +678,7 @@ static int table_map(CUtensorMap* map, const void* base, int64_t rows, int box_k
   }
   cuuint64_t dims[2] = {(cuuint64_t)tcp::kTK, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)tcp::kTK};
-  cuuint32_t box[2] = {(cuuint32_t)box_k, 256};
+  cuuint32_t box[2] = {(cuuint32_t)box_k, (cuuint32_t)tcp::kHalf};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -628,7 +692,9 @@ static int table_map(CUtensorMap* map, const void* base, int64_t rows, int box_k
 
 // Digits per 32-bit exponent word; balanced widths, wider digits first.
 static DigitSpec digit_spec() {
-  constexpr int D = 6;
+  // measured optimum of D = 5..8: more digits mean more positions
+  // (bucket traffic) but fewer buckets for the IMAD combine
+  constexpr int D = 7;
   DigitSpec ds{};
   ds.D = D;
   int off = 0, maxw = 0;
@@ -647,7 +713,7 @@ int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
   using namespace tcp;
   const DigitSpec ds = digit_spec();
   const int64_t npos = ds.D * n;
-  const int64_t rows_p = ceil_div(rows, kRows) * kRows;
+  const int64_t rows_p = ceil_div(rows, 4 * kRows) * 4 * kRows;
   return (int64_t)clients * (npos * kL * 4 + npos * kCols * kTK + rows_p * ds.nb * kXL * 4);
 }
 
@@ -685,7 +751,8 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
     }
   }
   const int C = clients;
-  const int64_t tiles = ceil_div(rows, kRows);
+  const int64_t ctas = 2 * ceil_div(rows, 4 * kRows);    // whole CTA pairs, two tiles per CTA
+  const int64_t tiles = 2 * ctas;
   const int64_t rows_p = tiles * kRows;
   std::vector<TcClient> hc(C);
   for (int c = 0; c < C; ++c) hc[c] = {P[c], N[c], one_m[c], W[c], np[c]};
@@ -727,11 +794,24 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
   // one launch walks every position (tiles are independent); chunked so a
   // launch stays well under a second
   constexpr int64_t chunk = 4096;
-  const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(tiles * C, 2 * 148)));
+  const int64_t ck = std::max<int64_t>(1, chunk / std::max<int64_t>(1, ceil_div(ctas * C, 148)));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ctas, C);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   for (int64_t p0 = 0; p0 < npos; p0 += ck) {
     const int64_t p1 = std::min<int64_t>(npos, p0 + ck);
-    tc_step_kernel<<<dim3((unsigned)tiles, C), kThreads, kSmem, st>>>(
-        mT, mTail, ds, E, rs, rid, n, npos, (int)p0, (int)p1, rows, rows_p, Bk);
+    if (cudaLaunchKernelEx(&cfg, tc_step_kernel, mT, mTail, ds, E, rs, rid, n, npos, (int)p0,
+                           (int)p1, rows, rows_p, Bk) != cudaSuccess)
+      return fail("tc_step launch");
   }
   if (check_launch("tc_step")) return fail("tc_step launch");
   bucket_combine_kernel<<<dim3((unsigned)ceil_div(rows, 4), C), 128, 0, st>>>(dcl, Bk, nb, rows,

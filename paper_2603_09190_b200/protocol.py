@@ -52,7 +52,7 @@ COMPRESS_CTAS = 36
 # per-client hints: Pippenger bucket updates on the tensor cores (4096-bit m^2)
 TC_HINT = True
 # transient workspace cap of one tensor-core hint launch (tiles + buckets)
-TC_WS_BYTES = 24 * 2**30
+TC_WS_BYTES = 48 * 2**30
 # refreshes of at least this many changed DB rows use the tensor cores (a tensor-core
 # launch costs ~D*n positions of fixed latency whatever the row count; the IMAD
 # kernels cost ~0.05 ms per row and client)
@@ -580,7 +580,7 @@ def _tc_eligible(state, kctx) -> bool:
 
 def _tc_batches(state, items, rows):
     """Split tensor-core jobs into launches whose transient workspace stays
-    under ZPIR_TC_WS_GB (default 24 GB; at least one client per launch)."""
+    under TC_WS_BYTES (48 GB: 16 clients at n = 1024; at least one client per launch)."""
     per = device.slot_fixed_tc_workspace(state.layout.n, rows, 1)
     k = max(1, int(TC_WS_BYTES // max(per, 1)))
     return [items[i:i + k] for i in range(0, len(items), k)]

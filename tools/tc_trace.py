@@ -29,8 +29,8 @@ buf = (ctypes.c_ulonglong * (64 * 16))()
 rc = _lib.lib().zpir_tc_trace(buf)
 assert rc == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
-names = ["start", "U0rdy", "U0drn", "U1rdy", "U1drn", "xfree", "H0rdy", "H0drn", "H1rdy", "H1drn",
-         "gathr", "m:U0", "m:U1", "m:H0xy", "m:H1xy", "Bwait"]
+names = ["start", "Ardy", "Adrn", "-", "-", "Brdy", "Bdrn", "publ", "-", "-",
+         "-", "m:XA", "m:XB", "m:Xend", "m:Yend", "Bwait"]
 print("pos " + " ".join(f"{n:>7s}" for n in names) + "  period")
 for p in range(1, 40):
     rel = t[p] - t[p, 0]
