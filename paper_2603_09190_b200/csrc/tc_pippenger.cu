@@ -17,13 +17,18 @@
 // dependency between the MMAs of one position: per position and 128-row tile
 //   task A: columns   0..255 (17 N = 256 MMAs) -> limbs 0..63
 //   task B: columns 256..511 (17 MMAs)          -> limbs 64..127 and the carry, limb 128
-// into two TMEM buffers, each drained by its own four epilogue warps.
-// The bucket combine reduces each bucket once (quotient estimate from the top
-// limbs, bignum.cuh) before its IMAD running products.
+// into two TMEM buffers (34 MMAs and 512 drained columns per position; the
+// Montgomery form of this step needed 80 MMAs in a three-product chain and 1028
+// drained columns). The bucket combine reduces each bucket once (quotient
+// estimate from the top limbs, bignum.cuh) before its IMAD running products.
 //
 // Buckets hold Montgomery-form values and y is in standard form, so products
 // stay in Montgomery form. A row whose digit repeats at the next position gets
 // its next X forwarded from this position's output by its own thread.
+//
+// What bounds the step is the bucket traffic, not the tensor pipe: every live
+// row reads and writes one 544-byte bucket per position, 2.5e11 bytes per client
+// at n = 1024, far beyond L2.
 //
 // Several clients (independent keys) run in one launch: blockIdx.y = client,
 // every client with its own tables, buckets and output rows; rows may be a
@@ -220,16 +225,6 @@ bucket_combine_kernel(const TcClient* __restrict__ cl, const uint32_t* __restric
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-// Arrive on a barrier of the leader CTA. Relaxed: what the arrival publishes is
-// this CTA's own shared memory (ordered by the proxy fence before it) or drained
-// TMEM (tcgen05.wait::ld); a release at cluster scope would also wait for every
-// global store of the drain to be acknowledged (MEMBAR.ALL.GPU, thousands of
-// cycles on the critical path).
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-
 // 32 lanes x 32 bit, 32 consecutive columns -> 32 registers per thread.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
   asm volatile(

@@ -140,8 +140,14 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+// Arrive on a barrier of another CTA of the cluster (the pair leader). Relaxed:
+// what the arrival publishes is drained TMEM (tcgen05.wait::ld, then
+// tcgen05.fence::before_thread_sync) or this CTA's own shared memory (ordered by
+// a proxy fence before it); a release at cluster scope compiles to
+// MEMBAR.ALL.GPU and waits for every earlier global store of the thread to be
+// acknowledged -- thousands of cycles behind an epilogue's result stores.
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {

@@ -522,7 +522,7 @@ umma_pair_bigint_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int q = 0; q < kOvChunks; ++q) tmem_ld16(taddr + first + 16 * q, ov[q]);
         tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive_cluster(oempty_l);
+        mbar_arrive_remote(oempty_l);
       }
       const bool live = row < rows;
       unsigned long long carry = 0;
@@ -568,7 +568,7 @@ umma_pair_bigint_kernel(const __grid_constant__ CUtensorMap mapA,
           carry >>= 32;
         }
       tc_fence_before();
-      mbar_arrive_cluster(acc ? tempty_l1 : tempty_l0);
+      mbar_arrive_remote(acc ? tempty_l1 : tempty_l0);
       if (++acc == C::kAcc) {
         acc = 0;
         aphase ^= 1;
@@ -777,33 +777,66 @@ umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
   }
 }
 
-// Planar BIGINT GEMM on CTA pairs (cta_group::2): the umma_planar_kernel
-// contract with M = 256 rows per pair tile (128 per CTA, each CTA's own TMEM
-// lanes) and the ck_o byte rows (B, N = 4 lm) split by N halves, so each SM
-// stages its own 16 KB of H planes and HALF of the B k-block per MMA group:
-// 32 KB instead of 48 KB per 4 MMAs of L2->SM traffic (the single-CTA kernel
-// is L2-throughput bound when many queries are compressed at once). Both
-// CTAs' TMA loads complete on the leader's full barrier; the leader's commits
+// Planar BIGINT GEMM on CTA pairs (cta_group::2) for batches of queries: the
+// umma_planar_kernel contract with M = 256 rows per pair tile (128 per CTA, each
+// CTA's own TMEM lanes) and the ck_o byte rows (B, N = 4 lm) split by N halves.
+//
+// The B operand of a query -- its half, (NT / 2) x np bytes, 128 KB at n = 1024
+// and 2048-bit m -- stays RESIDENT in shared memory while the pair sweeps row
+// tiles, so a unit (pair tile, query) streams only its four H plane tiles
+// through the ring: 512 KB per SM and 128 MMAs instead of 1 MB (the streaming
+// form was bound by L2 -> SM traffic at ~0.5 of the tensor rate). Units are
+// ordered (block of row tiles, query, tile in block): a pair's contiguous range
+// covers one or two queries per block (one or two B loads), and every block's H
+// planes (<= 48 MB) are read from HBM once and then from L2 by all queries.
+// Both CTAs' TMA loads complete on the leader's barriers; the leader's commits
 // multicast to both CTAs; both epilogues arrive on the leader's tempty.
+template <int NT>
+struct PlanarPairCfg {
+  static constexpr int kH = NT / 2;                       // B rows per CTA
+  static constexpr int kABytes = kBM * kBK;               // one H plane k-block (16 KB)
+  static constexpr int kBResMax = 128 * 1024;             // resident B half
+  static constexpr int kStages = 6;
+  static constexpr int kAcc = 2;
+  static constexpr int kTmemCols = 512;
+  static constexpr int kSmem = kBResMax + kStages * kABytes + 1024 + 256;
+};
+
+// unit u -> (pair tile m, query q) in (block, query, tile in block) order
+struct PlanarUnits {
+  int m_tiles, nq, tb;   // tb = row tiles per block
+  __device__ void at(int64_t u, int& m, int& q) const {
+    const int64_t per = (int64_t)tb * nq;
+    int blk = (int)(u / per);
+    const int nblk = (m_tiles + tb - 1) / tb;
+    if (blk >= nblk) blk = nblk - 1;
+    const int64_t r = u - (int64_t)blk * per;
+    const int t = min(tb, m_tiles - blk * tb);            // tiles in this block
+    q = (int)(r / t);
+    m = blk * tb + (int)(r - (int64_t)q * t);
+  }
+};
+
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
 umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
                         const __grid_constant__ CUtensorMap mapB, const UmmaArgs args,
-                        int64_t np, int64_t rows) {
-  using C = PairCfg<NT>;
-  static_assert(C::kP1 == 0 && C::kAcc == 2 && C::kOv == 0, "planar pair: N <= 256");
+                        int64_t np, int64_t rows, int tb) {
+  using C = PlanarPairCfg<NT>;
   constexpr int kLimbs = NT / 4;
   constexpr int kZ = kLimbs + 4;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::kStages * C::kBBytes);
+  uint8_t* sB = smem;                                     // resident: kbp k-blocks of kH x 128 B
+  uint8_t* sA = smem + C::kBResMax;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sA + C::kStages * C::kABytes);   // leader
   uint64_t* empty = full + C::kStages;
   uint64_t* tfull = empty + C::kStages;
-  uint64_t* tempty = tfull + C::kAcc;
-  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(tempty + C::kAcc + 1);
+  uint64_t* tempty = tfull + C::kAcc;                     // leader
+  uint64_t* bfull = tempty + C::kAcc;                     // leader: the query's B landed in both CTAs
+  uint64_t* bfree = bfull + 1;                            // every MMA reading the resident B done
+  uint32_t* tbase_smem = reinterpret_cast<uint32_t*>(bfree + 1);
 
   const uint32_t rank = cluster_ctarank();
   const bool leader = rank == 0;
@@ -819,6 +852,8 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 256);
     }
+    mbar_init(bfull, 1);
+    mbar_init(bfree, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc_pair(tbase_smem, C::kTmemCols);
@@ -828,39 +863,42 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
   const uint32_t tbase = *tbase_smem;
   const int kbp = (int)(np / kBK);        // k-blocks per plane pass
 
-  // pair work list: units = (pair tile of 256 rows, query)
+  // this pair's contiguous range of units
   const int npairs = (int)(gridDim.x >> 1), pid = (int)(blockIdx.x >> 1);
-  SegIter it;
-  {
-    const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
-    it.u = pid * T / npairs;
-    it.u1 = (pid + 1) * T / npairs;
-    it.kb = args.kblocks;
-    it.split = false;
-  }
+  const PlanarUnits units{args.m_tiles, args.n_tiles, tb};
+  const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
+  const int64_t u0 = pid * T / npairs, u1 = (pid + 1) * T / npairs;
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs) ----------------
-      // batches: every H tile is re-read once per query by the same CTA (pair),
-      // so H stays in L2 (the working set is ~1 MB per pair tile in flight)
       const uint64_t pol_a = args.a_keep ? l2_evict_last() : l2_evict_first();
       const uint64_t pol_b = l2_evict_last();
-      int64_t t;
-      int k0, k1, stage = 0;
-      uint32_t phase = 0;
-      while (it.next(t, k0, k1)) {
-        const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+      int stage = 0, qcur = -1;
+      uint32_t phase = 0, bph = 0;
+      for (int64_t u = u0; u < u1; ++u) {
+        int m, q;
+        units.at(u, m, q);
+        if (q != qcur) {
+          // the resident B changes: wait until no MMA reads the old one
+          if (qcur >= 0) {
+            mbar_wait(bfree, bph);
+            bph ^= 1;
+          }
+          qcur = q;
+          const uint32_t fb = mapa_shared(smem_u32(bfull), 0);
+          if (leader) mbar_expect_tx(bfull, 2u * (uint32_t)(kbp * C::kH * kBK));
+          for (int kb = 0; kb < kbp; ++kb)
+            tma_load_2d_pair(sB + kb * (C::kH * kBK), &mapB, fb, kb * kBK,
+                             q * NT + (int)rank * C::kH, pol_b);
+        }
         const int arow = m * 2 * kBM + (int)rank * kBM;
         for (int a = 0; a < 4; ++a)
           for (int kb = 0; kb < kbp; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
-            const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
-            if (leader) mbar_expect_tx(&full[stage], 2 * C::kStageBytes);
-            tma_load_2d_pair(sA + stage * C::kABytes, &mapA, fb, (int)(a * np) + kb * kBK, arow,
-                             pol_a);
-            tma_load_2d_pair(sB + stage * C::kBBytes, &mapB, fb, kb * kBK,
-                             n * NT + (int)rank * C::kH0, pol_b);
+            if (leader) mbar_expect_tx(&full[stage], 2 * C::kABytes);
+            tma_load_2d_pair(sA + stage * C::kABytes, &mapA, mapa_shared(smem_u32(&full[stage]), 0),
+                             (int)(a * np) + kb * kBK, arow, pol_a);
             if (++stage == C::kStages) {
               stage = 0;
               phase ^= 1;
@@ -870,21 +908,28 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      // ---------------- MMA issuer (leader): one group per (pair tile, plane) ----------------
-      int64_t t;
-      int k0, k1, stage = 0, acc = 0;
-      uint32_t phase = 0, aphase = 0;
+      // ---------------- MMA issuer (leader): one group per (unit, plane) ----------------
+      int stage = 0, acc = 0, qcur = -1;
+      uint32_t phase = 0, aphase = 0, bph = 0;
       const uint32_t idesc = idesc_u8(2 * kBM, NT);
-      while (it.next(t, k0, k1)) {
+      for (int64_t u = u0; u < u1; ++u) {
+        int m, q;
+        units.at(u, m, q);
+        if (q != qcur) {
+          qcur = q;
+          mbar_wait(bfull, bph);
+          bph ^= 1;
+          tc_fence_after();
+        }
         for (int a = 0; a < 4; ++a) {
           mbar_wait(&tempty[acc], aphase ^ 1);
           tc_fence_after();
-          const uint32_t d = tbase + (uint32_t)(acc * C::kAccOff1);
+          const uint32_t d = tbase + (uint32_t)(acc * 256);
           for (int kb = 0; kb < kbp; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint64_t ad = desc_sw128(smem_u32(sA + stage * C::kABytes));
-            const uint64_t bd = desc_sw128(smem_u32(sB + stage * C::kBBytes));
+            const uint64_t bd = desc_sw128(smem_u32(sB + kb * (C::kH * kBK)));
 #pragma unroll
             for (int k = 0; k < kBK / 32; ++k)
               umma_i8_pair(d, ad + 2 * k, bd + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
@@ -900,6 +945,12 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
             aphase ^= 1;
           }
         }
+        // last unit of this query in the range: the resident B may be replaced
+        if (u + 1 < u1) {
+          int m2, q2;
+          units.at(u + 1, m2, q2);
+          if (q2 != q) umma_commit_pair(bfree, 0x3);
+        }
       }
     }
   } else {
@@ -908,11 +959,11 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
     const int lrow = quarter * 32 + lane;
     const uint32_t tempty_l[2] = {mapa_shared(smem_u32(&tempty[0]), 0),
                                   mapa_shared(smem_u32(&tempty[1]), 0)};
-    int64_t t;
-    int k0, k1, acc = 0;
+    int acc = 0;
     uint32_t aphase = 0;
-    while (it.next(t, k0, k1)) {
-      const int m = (int)(t / args.n_tiles), n = (int)(t % args.n_tiles);
+    for (int64_t u = u0; u < u1; ++u) {
+      int m, n;
+      units.at(u, m, n);
       const int64_t row = (int64_t)m * 2 * kBM + (int64_t)rank * kBM + lrow;
       uint32_t z[kZ];
 #pragma unroll
@@ -921,8 +972,7 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
       for (int a = 0; a < 4; ++a) {
         mbar_wait(&tfull[acc], aphase);
         tc_fence_after();
-        const uint32_t taddr =
-            tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * C::kAccOff1);
+        const uint32_t taddr = tbase + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * 256);
         const uint32_t sh = 8u * (uint32_t)a;
         unsigned long long carry = 0;
         uint32_t prev = 0, c2 = 0;
@@ -947,7 +997,7 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
           }
         }
         tc_fence_before();
-        mbar_arrive_cluster(tempty_l[acc]);
+        mbar_arrive_remote(tempty_l[acc]);
         {
           const uint32_t v0 = (uint32_t)carry, v1 = (uint32_t)(carry >> 32);
           const uint32_t w[4] = {__funnelshift_l(prev, v0, sh), __funnelshift_l(v0, v1, sh),
@@ -1342,7 +1392,9 @@ int build_bcp_launch(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp
 // CTA-pair planar kernel for batches of >= 2 queries (L2 operand traffic 60% ->
 // 51% of peak, 1.77 -> 1.63 ms for 64 queries); single queries gain nothing
 // from it and keep the single-CTA kernel (A/B on one box)
-static bool use_planar_pair(int nq) { return nq >= 2; }
+static bool use_planar_pair(int nq, int NT, int64_t np) {
+  return nq >= 2 && (int64_t)(NT / 2) * np <= PlanarPairCfg<256>::kBResMax;
+}
 
 // z (nq x rows x wz) from the planar operands; lm in {32, 64}.
 int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t* bp, int lm,
@@ -1370,12 +1422,16 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
   const int sms = num_sms();
   const int cap = (ctas > 0 && ctas < sms) ? ctas : sms;
   const int grid = (int)std::min<int64_t>(cap, T);
-  if (use_planar_pair(nq) && cap >= 2) {
+  if (use_planar_pair(nq, NT, np) && cap >= 2) {
     CUtensorMap mbp;
     if (int e = make_map(&mbp, bp, (int64_t)NT * nq, np, np, NT / 2)) return e;
     a.m_tiles = (int)ceil_div(rows, 2 * kBM);
     const int64_t Tp = (int64_t)a.m_tiles * a.n_tiles;
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(cap / 2, Tp));
+    // blocks of row tiles whose H planes (2 kBM x 4 np bytes per pair tile) stay in L2
+    const int64_t tile_bytes = 2ll * kBM * 4 * np;
+    const int nblk = (int)ceil_div((int64_t)a.m_tiles * tile_bytes, 48ll << 20);
+    const int tb = (int)ceil_div(a.m_tiles, std::max(1, nblk));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);
@@ -1390,14 +1446,16 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
     cudaError_t e;
     if (NT == 256) {
       auto kern = umma_planar_pair_kernel<256>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<256>::kSmem);
-      cfg.dynamicSmemBytes = PairCfg<256>::kSmem;
-      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           PlanarPairCfg<256>::kSmem);
+      cfg.dynamicSmemBytes = PlanarPairCfg<256>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows, tb);
     } else {
       auto kern = umma_planar_pair_kernel<128>;
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<128>::kSmem);
-      cfg.dynamicSmemBytes = PairCfg<128>::kSmem;
-      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           PlanarPairCfg<128>::kSmem);
+      cfg.dynamicSmemBytes = PlanarPairCfg<128>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, kern, ma, mbp, a, np, rows, tb);
     }
     if (e != cudaSuccess) return check_launch("umma_planar_pair launch");
     return check_launch("umma_planar_pair");
