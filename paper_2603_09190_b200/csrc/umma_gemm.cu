@@ -786,9 +786,10 @@ umma_planar_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_consta
 // tiles, so a unit (pair tile, query) streams only its four H plane tiles
 // through the ring: 512 KB per SM and 128 MMAs instead of 1 MB (the streaming
 // form was bound by L2 -> SM traffic at ~0.5 of the tensor rate). Units are
-// ordered (block of row tiles, query, tile in block): a pair's contiguous range
-// covers one or two queries per block (one or two B loads), and every block's H
-// planes (<= 48 MB) are read from HBM once and then from L2 by all queries.
+// taken block of row tiles by block, each block's (query, tile) units split
+// evenly over the pairs: a pair sees one or two queries per block (one or two B
+// loads), and every block's H planes (<= 48 MB) are read from HBM once and then
+// from L2 by all queries.
 // Both CTAs' TMA loads complete on the leader's barriers; the leader's commits
 // multicast to both CTAs; both epilogues arrive on the leader's tempty.
 template <int NT>
@@ -802,18 +803,36 @@ struct PlanarPairCfg {
   static constexpr int kSmem = kBResMax + kStages * kABytes + 1024 + 256;
 };
 
-// unit u -> (pair tile m, query q) in (block, query, tile in block) order
+// The units (pair tile m, query q) of one pair, block of row tiles by block:
+// every block's units, in (query, tile) order, are split evenly over all pairs,
+// so the whole GPU works on one block's H planes at a time.
 struct PlanarUnits {
   int m_tiles, nq, tb;   // tb = row tiles per block
-  __device__ void at(int64_t u, int& m, int& q) const {
-    const int64_t per = (int64_t)tb * nq;
-    int blk = (int)(u / per);
-    const int nblk = (m_tiles + tb - 1) / tb;
-    if (blk >= nblk) blk = nblk - 1;
-    const int64_t r = u - (int64_t)blk * per;
-    const int t = min(tb, m_tiles - blk * tb);            // tiles in this block
+  int npairs, pid;
+  int blk = 0, t = 0;    // current block, its tile count
+  int64_t r = 0, r1 = 0; // position / end of this pair's range in the block
+  __device__ PlanarUnits(int m_tiles_, int nq_, int tb_, int npairs_, int pid_)
+      : m_tiles(m_tiles_), nq(nq_), tb(tb_), npairs(npairs_), pid(pid_) {
+    open();
+  }
+  __device__ void open() {
+    t = min(tb, m_tiles - blk * tb);
+    const int64_t U = t > 0 ? (int64_t)t * nq : 0;
+    r = pid * U / npairs;
+    r1 = (pid + 1) * U / npairs;
+  }
+  // next unit; `lastq` = the following unit (if any) belongs to another query
+  __device__ bool next(int& m, int& q, bool& lastq) {
+    while (t > 0 && r >= r1) {
+      ++blk;
+      open();
+    }
+    if (t <= 0) return false;
     q = (int)(r / t);
     m = blk * tb + (int)(r - (int64_t)q * t);
+    ++r;
+    lastq = r >= r1 || (int)(r / t) != q;
+    return true;
   }
 };
 
@@ -863,11 +882,9 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
   const uint32_t tbase = *tbase_smem;
   const int kbp = (int)(np / kBK);        // k-blocks per plane pass
 
-  // this pair's contiguous range of units
-  const int npairs = (int)(gridDim.x >> 1), pid = (int)(blockIdx.x >> 1);
-  const PlanarUnits units{args.m_tiles, args.n_tiles, tb};
-  const int64_t T = (int64_t)args.m_tiles * args.n_tiles;
-  const int64_t u0 = pid * T / npairs, u1 = (pid + 1) * T / npairs;
+  PlanarUnits units(args.m_tiles, args.n_tiles, tb, (int)(gridDim.x >> 1), (int)(blockIdx.x >> 1));
+  int m, q;
+  bool lastq;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -876,10 +893,9 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
       const uint64_t pol_b = l2_evict_last();
       int stage = 0, qcur = -1;
       uint32_t phase = 0, bph = 0;
-      for (int64_t u = u0; u < u1; ++u) {
-        int m, q;
-        units.at(u, m, q);
-        if (q != qcur) {
+      bool fresh = true;                   // the next unit starts a new resident B
+      while (units.next(m, q, lastq)) {
+        if (fresh) {
           // the resident B changes: wait until no MMA reads the old one
           if (qcur >= 0) {
             mbar_wait(bfree, bph);
@@ -904,19 +920,18 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
               phase ^= 1;
             }
           }
+        fresh = lastq;
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (leader): one group per (unit, plane) ----------------
-      int stage = 0, acc = 0, qcur = -1;
+      int stage = 0, acc = 0;
       uint32_t phase = 0, aphase = 0, bph = 0;
       const uint32_t idesc = idesc_u8(2 * kBM, NT);
-      for (int64_t u = u0; u < u1; ++u) {
-        int m, q;
-        units.at(u, m, q);
-        if (q != qcur) {
-          qcur = q;
+      bool fresh = true;
+      while (units.next(m, q, lastq)) {
+        if (fresh) {
           mbar_wait(bfull, bph);
           bph ^= 1;
           tc_fence_after();
@@ -945,12 +960,9 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
             aphase ^= 1;
           }
         }
-        // last unit of this query in the range: the resident B may be replaced
-        if (u + 1 < u1) {
-          int m2, q2;
-          units.at(u + 1, m2, q2);
-          if (q2 != q) umma_commit_pair(bfree, 0x3);
-        }
+        // last unit on this resident B: it may be replaced once these MMAs are done
+        if (lastq) umma_commit_pair(bfree, 0x3);
+        fresh = lastq;
       }
     }
   } else {
@@ -961,9 +973,8 @@ umma_planar_pair_kernel(const __grid_constant__ CUtensorMap mapA,
                                   mapa_shared(smem_u32(&tempty[1]), 0)};
     int acc = 0;
     uint32_t aphase = 0;
-    for (int64_t u = u0; u < u1; ++u) {
-      int m, n;
-      units.at(u, m, n);
+    int n;
+    while (units.next(m, n, lastq)) {
       const int64_t row = (int64_t)m * 2 * kBM + (int64_t)rank * kBM + lrow;
       uint32_t z[kZ];
 #pragma unroll
