@@ -302,8 +302,8 @@ struct zpir_db {
 namespace zpir {
 namespace {
 
-constexpr int kCompressCtas = 36;     // measured SM split
-constexpr int kCompressCtasE2E = 44;  // host-input answers: the compression starts later
+constexpr int kCompressCtas = 34;     // measured SM split
+constexpr int kCompressCtasE2E = 42;  // host-input answers: the compression starts later
 
 int umma_nb(int lm) { return lm == 32 ? 144 : lm == 64 ? 272 : lm == 96 ? 400 : 0; }
 

@@ -27,6 +27,7 @@
 // ("stream-K", split = 1; exact because the LIMB outputs are sums mod 2^32
 // and are combined with wrapping atomics) or of whole tiles (split = 0).
 #include <cudaTypedefs.h>
+#include <cstdlib>
 
 #include <algorithm>
 
@@ -1400,11 +1401,13 @@ int build_bcp_launch(const uint32_t* cko, int64_t n, int lm, int nq, uint8_t* bp
   return check_launch("build_bcp");
 }
 
-// CTA-pair planar kernel for batches of >= 2 queries (L2 operand traffic 60% ->
-// 51% of peak, 1.77 -> 1.63 ms for 64 queries); single queries gain nothing
-// from it and keep the single-CTA kernel (A/B on one box)
-static bool use_planar_pair(int nq, int NT, int64_t np) {
-  return nq >= 2 && (int64_t)(NT / 2) * np <= PlanarPairCfg<256>::kBResMax;
+// The CTA-pair planar kernel keeps a query's B half resident in shared memory:
+// whenever that fits (n <= 1024 at 2048-bit m). Single queries use it too (the
+// answer step on a 36 / 112 SM split: 194-195 us against 201-206 us with the
+// single-CTA kernel, A/B on one box); larger n falls back to the single-CTA
+// kernel below.
+static bool use_planar_pair(int NT, int64_t np) {
+  return (int64_t)(NT / 2) * np <= PlanarPairCfg<256>::kBResMax;
 }
 
 // z (nq x rows x wz) from the planar operands; lm in {32, 64}.
@@ -1433,7 +1436,7 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
   const int sms = num_sms();
   const int cap = (ctas > 0 && ctas < sms) ? ctas : sms;
   const int grid = (int)std::min<int64_t>(cap, T);
-  if (use_planar_pair(nq, NT, np) && cap >= 2) {
+  if (use_planar_pair(NT, np) && cap >= 2) {
     CUtensorMap mbp;
     if (int e = make_map(&mbp, bp, (int64_t)NT * nq, np, np, NT / 2)) return e;
     a.m_tiles = (int)ceil_div(rows, 2 * kBM);
@@ -1441,7 +1444,7 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(cap / 2, Tp));
     // blocks of row tiles whose H planes (2 kBM x 4 np bytes per pair tile) stay in L2
     const int64_t tile_bytes = 2ll * kBM * 4 * np;
-    const int nblk = (int)ceil_div((int64_t)a.m_tiles * tile_bytes, 48ll << 20);
+    const int nblk = nq > 1 ? (int)ceil_div((int64_t)a.m_tiles * tile_bytes, 48ll << 20) : 1;
     const int tb = (int)ceil_div(a.m_tiles, std::max(1, nblk));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);

@@ -48,7 +48,7 @@ COMBINED = "combined"
 ENGINE = "umma"
 # SMs given to the compression GEMM while the GEMV streams the DB on the rest
 # (both are HBM-bound; H is ~1/8 of the DB bytes; measured optimum, DESIGN 3.2)
-COMPRESS_CTAS = 36
+COMPRESS_CTAS = 34
 # per-client hints: Pippenger bucket updates on the tensor cores (4096-bit m^2)
 TC_HINT = True
 # transient workspace cap of one tensor-core hint launch (tiles + buckets)
