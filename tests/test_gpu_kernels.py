@@ -186,9 +186,10 @@ def test_planar_compression(env, lm, n, rows, nq, ctas):
 
 @pytest.mark.parametrize("n,rows", [(64, 300), (256, 129), (32, 128)])
 def test_slot_fixed_tensor_core(env, n, rows):
-    """Tensor-core Pippenger bucket updates (fixed-multiplier Montgomery as three
-    byte-Toeplitz int8 GEMMs) == the IMAD warp path, bit for bit (2048-bit m,
-    4096-bit m^2), incl. zero digits, all-255 rows and a partial last tile."""
+    """Tensor-core Pippenger bucket updates (X * y mod N as one int8 GEMM against
+    the table of reduced byte shifts of y, buckets left unreduced in 515 bytes)
+    == the IMAD warp path, bit for bit (2048-bit m, 4096-bit m^2), incl. zero
+    digits, all-255 rows and a partial last tile."""
     torch, device = env
     from oracle import client
     from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
@@ -216,10 +217,12 @@ def test_slot_fixed_tensor_core(env, n, rows):
 
 @pytest.mark.parametrize("m", [(1 << 2048) - 1 - 2 * 12345, (1 << 2047) + 1, None])
 def test_slot_fixed_tensor_core_moduli(env, m):
-    """The column-508 carry shortcut and the deferred subtraction hold for any
-    odd 2048-bit m: m^2 just below R = 2^4096 (Z < 2N exceeds R), m^2 just above
-    2^4094 (N < R/2), and a random keygen modulus; every digit value 1..255
-    appears, buckets are hit back to back (equal digits at consecutive positions)."""
+    """The unreduced 515-byte buckets (V < 515 * 255 * N) and the reduce-on-load
+    quotient estimate hold for any odd 2048-bit m: m^2 just below 2^4096 (the top
+    limb of V is largest), m^2 just above 2^4094 (the estimate's divisor is
+    smallest), and a random keygen modulus; bases next to m^2 - 1; every digit
+    value appears, buckets are hit back to back (equal digits at consecutive
+    positions: the forwarded rows)."""
     torch, device = env
     from oracle import client
     from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx

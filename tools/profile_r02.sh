@@ -3,7 +3,7 @@
 # bench line, the reference arm on the same config, every workload line, ncu
 # launch lists and full captures of the GEMV, the compression and tc_step.
 set -u
-OUT=gpurun_out/r02
+OUT=gpurun_out/r02b
 mkdir -p $OUT
 python -c "from paper_2603_09190_b200 import build; build.build(); from oracle import c; c.build()" > $OUT/build.log 2>&1 || exit 1
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
@@ -28,7 +28,13 @@ PYTHONPATH=. python tools/profile_answer.py --plan full --reps 3 > $OUT/pa.log 2
   ncu --set full --import-source on --clock-control none -k regex:umma_planar -s 1 -c 1 \
     -o $OUT/compress_planar -f python tools/profile_answer.py --plan full --reps 3 > $OUT/ncu_planar.log 2>&1
 }
+python tools/batch_once.py > $OUT/pb.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:umma_planar_pair -s 1 -c 1 \
+  -o $OUT/compress_pair_batch64 -f python tools/batch_once.py > $OUT/ncu_pair.log 2>&1
 PYTHONPATH=. python tools/profile_answer.py --hint --reps 0 > $OUT/ph.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:tc_step_kernel -s 2 -c 1 \
+ncu --set full --import-source on --clock-control none -k regex:tc_step_kernel -s 1 -c 1 \
   -o $OUT/tc_step -f python tools/profile_answer.py --hint --reps 0 > $OUT/ncu_tc.log 2>&1
+python tools/ncu_summary.py $OUT/*.ncu-rep > $OUT/ncu_summary_table.md
+python tools/launch_summary.py $OUT/hint16_launches.csv > $OUT/hint16_summary.txt
+python tools/launch_summary.py $OUT/launches.csv --tail 60 > $OUT/launches_summary.txt
 ls -la $OUT
