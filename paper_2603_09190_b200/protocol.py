@@ -1284,25 +1284,26 @@ def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep
     ev.record(cs)
     stream.wait_event(ev)
     b = state.gemv_batch_device(B["qd"], stream)                    # (nq, rows)
-    # meanwhile every ck_o field -> pinned, then per sub-batch to the device on
-    # the copy stream (overlapping the previous sub-batch's compression)
-    if fast:
-        conv.stage_rows(ck_bytes, cn, n * 4 * lm, n, 4 * lm, nthr, False)
-    else:
-        for i in range(nq):
-            ck = np.asarray(ck_bytes[i], dtype=np.uint8)
-            cn[i, :, : ck.shape[1]] = ck
-            cn[i, :, ck.shape[1]:] = 0
+    # meanwhile, per sub-batch: its ck_o fields -> pinned -> device in pieces of 8
+    # queries on the copy stream (the copy of a piece runs while the host stages the
+    # next one), then its compression is launched -- the host stages sub-batch s + 1
+    # while the device compresses s
     sub = max(1, WIRE_BATCH_SUB)
-    ranges = [(lo, min(nq, lo + sub)) for lo in range(0, nq, sub)]
-    ev_c = []
-    for lo, hi in ranges:
-        device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], cs)
+    res = [None] * nq
+    for lo in range(0, nq, sub):
+        hi = min(nq, lo + sub)
+        for p0 in range(lo, hi, 8):
+            p1 = min(hi, p0 + 8)
+            if fast:
+                conv.stage_rows(ck_bytes[p0:p1], cn[p0:p1], n * 4 * lm, n, 4 * lm, nthr, False)
+            else:
+                for i in range(p0, p1):
+                    ck = np.asarray(ck_bytes[i], dtype=np.uint8)
+                    cn[i, :, : ck.shape[1]] = ck
+                    cn[i, :, ck.shape[1]:] = 0
+            device.h2d_async(B["cd"][p0:p1], B["c"][p0:p1], cs)
         e = torch.cuda.Event()
         e.record(cs)
-        ev_c.append(e)
-    res = [None] * nq
-    for (lo, hi), e in zip(ranges, ev_c):
         stream.wait_event(e)
         # t rows of lm limbs unless a COMBINED query needs them widened for combine
         t_ld = l2 if any(modes[i] == COMBINED for i in range(lo, hi)) else lm
