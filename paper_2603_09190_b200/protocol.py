@@ -53,9 +53,8 @@ COMPRESS_CTAS = 34
 TC_HINT = True
 # transient workspace cap of one tensor-core hint launch (tiles + buckets)
 TC_WS_BYTES = 48 * 2**30
-# refreshes of at least this many changed DB rows use the tensor cores (a tensor-core
-# launch costs ~D*n positions of fixed latency whatever the row count; the IMAD
-# kernels cost ~0.05 ms per row and client)
+# refreshes of at least this many changed DB rows always use the tensor cores; smaller
+# ones when the cost model of _tc_refresh_pays says the batch of clients fills the launch
 TC_REFRESH_MIN_ROWS = 2048
 # full hints: tensor cores when the batch has at least this many exponent rows in total
 TC_MIN_ROWS = 2048
@@ -578,6 +577,24 @@ def _tc_eligible(state, kctx) -> bool:
     return TC_HINT and kctx.l2 == 128 and 4 * state.layout.n <= 65536
 
 
+def _tc_refresh_pays(state, nclients: int, rows: int) -> bool:
+    """Tensor cores or IMAD kernels for a refresh of `rows` changed DB rows of
+    `nclients` hints (measured on a B200). A tensor-core launch walks
+    all D n positions (D = 7, ~7.5 us each) whatever the row count, with one CTA
+    pair per 512 rows and client and 74 pairs per wave, plus ~0.6 us per position
+    and client for the multiplier tables; the IMAD kernels cost ~35 us per row and
+    client (the Horner recombination of the changed groups is common to both).
+    One client's 327 rows stay on the IMAD path (11 ms against 58 ms); the hint
+    worker's 16 clients go to the tensor cores (122 ms against 183 ms; measured
+    16.1 against 17.9 ms per client with the recombination)."""
+    if rows >= TC_REFRESH_MIN_ROWS:
+        return True
+    npos = 7 * state.layout.n
+    waves = -(-nclients * -(-rows // 512) // 74)
+    tc_ms = waves * npos * 7.5e-3 + nclients * (npos * 0.6e-3 + rows * 0.5e-3)
+    return tc_ms < nclients * rows * 35e-3
+
+
 def _tc_batches(state, items, rows):
     """Split tensor-core jobs into launches whose transient workspace stays
     under TC_WS_BYTES (48 GB: 16 clients at n = 1024; at least one client per launch)."""
@@ -714,9 +731,10 @@ def refresh_hint(state: ServerGlobalState, reg, old: ClientHint, changed_rows,
 def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
                   nstreams: int = 8) -> list:
     """refresh_hint for many (registration, hint) pairs at once. For large
-    updates (>= ZPIR_TC_REFRESH_MIN_ROWS changed rows, default 2048) and
-    4096-bit m^2 the changed rows' W of all clients are recomputed by one
-    tensor-core launch (row ids, one grid row per client); otherwise the IMAD
+    updates (>= TC_REFRESH_MIN_ROWS changed rows) or enough clients to fill a
+    launch (_tc_refresh_pays) and 4096-bit m^2 the changed rows' W of all
+    clients are recomputed by one tensor-core launch (row ids, one grid row
+    per client); otherwise the IMAD
     kernels of each client are spread over `nstreams` CUDA streams so that
     small refreshes fill the GPU together."""
     for _, old in pairs:
@@ -727,7 +745,8 @@ def refresh_hints(state: ServerGlobalState, pairs, changed_rows, stream=None,
     main = stream or torch.cuda.current_stream(dev)
     rows, rid, gid, ng = _changed_ids(state, changed_rows)
     kctxs = [key_ctx(reg.pk.m, dev) for reg, _ in pairs]
-    use_tc = rows >= TC_REFRESH_MIN_ROWS and all(_tc_eligible(state, k) for k in kctxs)
+    use_tc = (all(_tc_eligible(state, k) for k in kctxs)
+              and _tc_refresh_pays(state, len(pairs), rows))
     if use_tc:
         outs = []
         jobs = []
@@ -1284,26 +1303,25 @@ def _wire_chunk(state, regs, modes, ck_bytes, qus, storeds, ks, lm, stream, keep
     ev.record(cs)
     stream.wait_event(ev)
     b = state.gemv_batch_device(B["qd"], stream)                    # (nq, rows)
-    # meanwhile, per sub-batch: its ck_o fields -> pinned -> device in pieces of 8
-    # queries on the copy stream (the copy of a piece runs while the host stages the
-    # next one), then its compression is launched -- the host stages sub-batch s + 1
-    # while the device compresses s
+    # meanwhile every ck_o field -> pinned, then per sub-batch to the device on
+    # the copy stream (overlapping the previous sub-batch's compression)
+    if fast:
+        conv.stage_rows(ck_bytes, cn, n * 4 * lm, n, 4 * lm, nthr, False)
+    else:
+        for i in range(nq):
+            ck = np.asarray(ck_bytes[i], dtype=np.uint8)
+            cn[i, :, : ck.shape[1]] = ck
+            cn[i, :, ck.shape[1]:] = 0
     sub = max(1, WIRE_BATCH_SUB)
-    res = [None] * nq
-    for lo in range(0, nq, sub):
-        hi = min(nq, lo + sub)
-        for p0 in range(lo, hi, 8):
-            p1 = min(hi, p0 + 8)
-            if fast:
-                conv.stage_rows(ck_bytes[p0:p1], cn[p0:p1], n * 4 * lm, n, 4 * lm, nthr, False)
-            else:
-                for i in range(p0, p1):
-                    ck = np.asarray(ck_bytes[i], dtype=np.uint8)
-                    cn[i, :, : ck.shape[1]] = ck
-                    cn[i, :, ck.shape[1]:] = 0
-            device.h2d_async(B["cd"][p0:p1], B["c"][p0:p1], cs)
+    ranges = [(lo, min(nq, lo + sub)) for lo in range(0, nq, sub)]
+    ev_c = []
+    for lo, hi in ranges:
+        device.h2d_async(B["cd"][lo:hi], B["c"][lo:hi], cs)
         e = torch.cuda.Event()
         e.record(cs)
+        ev_c.append(e)
+    res = [None] * nq
+    for (lo, hi), e in zip(ranges, ev_c):
         stream.wait_event(e)
         # t rows of lm limbs unless a COMBINED query needs them widened for combine
         t_ld = l2 if any(modes[i] == COMBINED for i in range(lo, hi)) else lm

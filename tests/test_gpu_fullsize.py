@@ -246,8 +246,8 @@ def test_fullsize_update_and_refresh(full, client_a, oracle_A):
         rebuilt = z.ServerGlobalState(params, db2, db_version=st2.db_version)
         assert torch.equal(st2.H_dev, rebuilt.H_dev)
         assert torch.equal(st2.H_planes, rebuilt.H_planes)
-        use_tc = changed.size >= z.protocol.TC_REFRESH_MIN_ROWS
-        assert use_tc == (step == 1)
+        use_tc = z.protocol._tc_refresh_pays(st2, len(regs), int(changed.size))
+        assert use_tc == (step == 1)     # IMAD row path first, then the tensor-core row-id path
         ref_h = z.hints(rebuilt, [(r_, 0) for r_ in regs])
         new_h = z.refresh_hints(st2, list(zip(regs, cur_h)), changed)
         for a_, b_ in zip(new_h, ref_h):
