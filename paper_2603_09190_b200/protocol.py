@@ -1045,9 +1045,9 @@ def _wire_rows(state, m, mode, ck_bytes, qu, stored, stream, on_device=False):
 MAX_BATCH = 64
 # respond_batch: queries per compression / copy-out sub-batch (host work overlaps the device)
 BATCH_SUB = 16
-# respond_batch_wire: every input is staged up front, so sub-batches only overlap
-# the copy-out with the next compression (fewer, larger compression launches)
-WIRE_BATCH_SUB = 32
+# respond_batch_wire: every input is staged up front; the sub-batches overlap the
+# copies in and out with the compressions (measured 16 / 32 / 64: 3.19 / 3.28 / 4.32 ms)
+WIRE_BATCH_SUB = 16
 
 
 def respond_batch(state: ServerGlobalState, regs, qmsgs, mode: str = None,
