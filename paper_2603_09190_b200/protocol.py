@@ -574,7 +574,7 @@ def _side_streams(dev, count):
 
 
 def _tc_eligible(state, kctx) -> bool:
-    return TC_HINT and kctx.l2 == 128 and 4 * state.layout.n <= 65536
+    return TC_HINT and kctx.l2 == 128 and 7 * state.layout.n <= 65536   # D n positions
 
 
 def _tc_refresh_pays(state, nclients: int, rows: int) -> bool:
