@@ -614,8 +614,8 @@ def hint(state: ServerGlobalState, reg, query_index: int, stream=None,
     Each W[c] (32-bit exponents) is one fixed-base Pippenger over a table of
     powers of ck_r[k]: on the IMAD path (slot_fixed) 8-bit digits, 255
     buckets, P[i][k] = ck_r[k]^(2^(8i)); for 4096-bit m^2 and enough rows the
-    bucket updates run on the tensor cores instead (tc_pippenger.cu: D digits
-    per word, default 6 -> 63 buckets). The groups are then recombined by
+    bucket updates run on the tensor cores instead (tc_pippenger.cu: D = 7
+    digits per word, 31 buckets). The groups are then recombined by
     Horner in gamma (slot_combine). Same group element as the reference's
     windowed multiexp, canonical mod m^2. keep_slots=True keeps W and the
     8-bit table P on the device for refresh_hint."""

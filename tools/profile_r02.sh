@@ -3,7 +3,7 @@
 # bench line, the reference arm on the same config, every workload line, ncu
 # launch lists and full captures of the GEMV, the compression and tc_step.
 set -u
-OUT=gpurun_out/r02b
+OUT=gpurun_out/r02c
 mkdir -p $OUT
 python -c "from paper_2603_09190_b200 import build; build.build(); from oracle import c; c.build()" > $OUT/build.log 2>&1 || exit 1
 timeout 900 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?"
