@@ -270,7 +270,9 @@ __device__ __forceinline__ void regs_ready(uint32_t (&v)[32]) {
 // Drain 256 TMEM columns of this thread's lane in eight 32-column batches,
 // double-buffered: batch g + 1 is in flight while batch g is processed.
 // f(g, v) consumes columns 32 g .. 32 g + 31; it updates `carry`, which also
-// orders the next wait after the processing.
+// orders the next wait after the processing. (Three buffers with two loads in
+// flight shorten a drain by ~0.6k cycles and change nothing end to end: the
+// position is bound by the load-store unit.)
 template <class F>
 __device__ __forceinline__ void drain256(uint32_t taddr, uint32_t& carry, F&& f) {
   uint32_t va[32], vb[32];
@@ -639,9 +641,10 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
         }
       });
       {
-        const uint4 top = make_uint4(carry, 0u, 0u, 0u);
-        if (dg) *reinterpret_cast<uint4*>(brow + kL) = top;
-        if (fwd) *reinterpret_cast<uint4*>(xt_row) = top;
+        // limb 128 and the row's zero padding as one whole 32-byte sector
+        const uint32_t topv[8] = {carry, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+        if (dg) store8(brow + kL, topv);
+        if (fwd) *reinterpret_cast<uint4*>(xt_row) = make_uint4(carry, 0u, 0u, 0u);
       }
       if (tr) TC_STAMP(pos, 6);
       tc_fence_before();

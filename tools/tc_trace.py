@@ -29,7 +29,7 @@ buf = (ctypes.c_ulonglong * (64 * 16))()
 rc = _lib.lib().zpir_tc_trace(buf)
 assert rc == 0
 t = np.array(buf, dtype=np.int64).reshape(64, 16)
-names = ["start", "Ardy", "Adrn", "-", "-", "Brdy", "Bdrn", "publ", "-", "-",
+names = ["start", "Ardy", "Adrn", "-", "gissue", "Brdy", "Bdrn", "publ", "-", "-",
          "-", "m:XA", "m:XB", "m:Xend", "m:Yend", "Bwait"]
 print("pos " + " ".join(f"{n:>7s}" for n in names) + "  period")
 for p in range(1, 40):
