@@ -41,5 +41,4 @@ for _ in range(a.reps):
     torch.cuda.synchronize()
     tbs.append((time.perf_counter() - t) / a.batch)
     assert all([c.c for c in x.entries] == [c.c for c in y.entries] for x, y in zip(hs, ref))
-print(f"ZPIR_TC_STRIP={os.environ.get('ZPIR_TC_STRIP', 'default')} single {min(t1s):.4f} s, "
-      f"batched {a.batch}: {min(tbs):.4f} s per client")
+print(f"single {min(t1s):.4f} s, batched {a.batch}: {min(tbs):.4f} s per client")

@@ -1,5 +1,5 @@
-"""Answer-step time vs the compression / GEMV SM split (and the compression
-kernel form via ZPIR_EXP_PAIR1), 1 GiB config, device-resident plan replays."""
+"""Answer-step time vs the compression / GEMV SM split, 1 GiB config,
+device-resident plan replays:    python tools/split_sweep.py 30 34 36 38"""
 import os
 import random
 import sys
@@ -49,4 +49,4 @@ for ctas in [int(x) for x in sys.argv[1:]] or [20, 24, 28, 32, 36]:
     if ref is None:
         ref = t
     ok = torch.equal(ref, t)
-    print(f"pair1={os.environ.get('ZPIR_EXP_PAIR1', '0')} ctas={ctas}: {e0.elapsed_time(e1) / 200 * 1e3:.1f} us/step  same_t={ok}", flush=True)
+    print(f"ctas={ctas}: {e0.elapsed_time(e1) / 200 * 1e3:.1f} us/step  same_t={ok}", flush=True)
