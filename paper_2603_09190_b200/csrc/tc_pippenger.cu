@@ -708,8 +708,8 @@ static int table_map(CUtensorMap* map, const void* base, int64_t rows, int box_k
 
 // Digits per 32-bit exponent word; balanced widths, wider digits first.
 static DigitSpec digit_spec() {
-  // measured optimum of D = 5..8: more digits mean more positions
-  // (bucket traffic) but fewer buckets for the IMAD combine
+  // measured optimum of D = 5..11: more digits mean more positions
+  // but fewer buckets (IMAD combine; more of them found in L2)
   constexpr int D = 7;
   DigitSpec ds{};
   ds.D = D;
