@@ -26,6 +26,9 @@ from . import _lib, device
 
 USE_GRAPHS = True     # False runs the sequences eagerly (debugging)
 _capture_lock = threading.Lock()
+# SMs the host-input graphs add to the compression side (it starts ~25 us after
+# the GEMV: ck_o is staged while the GEMV runs)
+E2E_EXTRA_CTAS = 8
 
 
 class AnswerPlan:
@@ -39,7 +42,7 @@ class AnswerPlan:
         self.ctas = compress_ctas
         # the host-input graphs start the compression side ~25 us after the
         # GEMV (ck_o is staged while the GEMV runs), so they give it more SMs
-        self.ctas_e2e = compress_ctas + 8 if compress_ctas > 0 else 0
+        self.ctas_e2e = compress_ctas + E2E_EXTRA_CTAS if compress_ctas > 0 else 0
         self.sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.qu = torch.zeros((1, lay.ld), dtype=torch.int32, device=dev)
         self.cko = torch.zeros((lay.n, lm), dtype=torch.int32, device=dev)
