@@ -6,6 +6,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/bulk_probe tools/probes/bulk_gather_probe.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int ROWS = 128, ROWB = 544;
@@ -80,10 +81,11 @@ __global__ void __launch_bounds__(128, 1) probe(const uint8_t* __restrict__ src,
   if (t == 0) cyc[blockIdx.x] = t1 - t0;
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int64_t nrows = 4 << 20;   // 2.3 GB: far beyond L2
+  // rows of the source array: 4 M = 2.3 GB (far beyond L2) by default; e.g. 100000 = 54 MB stays in L2
+  const int64_t nrows = argc > 1 ? atoll(argv[1]) : (4 << 20);
   uint8_t* src;
   unsigned long long* cyc;
   cudaMalloc(&src, nrows * ROWB);
@@ -105,9 +107,9 @@ int main() {
     double avg = 0;
     for (int i = 0; i < sms; ++i) avg += (double)h[i];
     avg /= sms * (double)iters;
-    printf("%s: %.0f cycles per %d-row gather, %.1f B/clk/SM (DRAM-resident rows, %d SMs)\n",
+    printf("%s: %.0f cycles per %d-row gather, %.1f B/clk/SM (%.0f MB of rows, %d SMs)\n",
            mode == 0 ? "cp.async 16 B x 8 lanes per row" : "cp.async.bulk 4 x 128 B + 32 B per row",
-           avg, ROWS, ROWS * ROWB / avg, sms);
+           avg, ROWS, ROWS * ROWB / avg, nrows * ROWB / 1e6, sms);
   }
   return 0;
 }
