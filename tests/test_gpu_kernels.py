@@ -155,12 +155,15 @@ def test_umma_few_ctas_multi_tile(env, lm, ctas):
 
 @pytest.mark.parametrize("lm,n,rows,nq", [(64, 1024, 384, 1), (32, 64, 256, 1), (64, 100, 128, 3),
                                           (32, 1024, 640, 2), (64, 4096, 128, 1),
-                                          (64, 1024, 1152, 8)])
+                                          (64, 1024, 1152, 8), (64, 1024, 13184, 3)])
 @pytest.mark.parametrize("ctas", [0, 2])
 def test_planar_compression(env, lm, n, rows, nq, ctas):
     """Planar compression (H byte planes x ck_o byte rows, 4 plane passes per
     tile) == CUDA-core rows, incl. n not a multiple of 128 (zero-padded
-    planes), several queries, few persistent CTAs, all-ones extremes."""
+    planes), several queries, few persistent CTAs, all-ones extremes, a partial
+    pair tile, n = 4096 (ck_o operand too large to stay in shared memory: the
+    single-CTA kernel) and 13184 rows (two blocks of row tiles, the last one
+    short, in the CTA-pair kernel's unit order)."""
     torch, device = env
     rng = np.random.default_rng(lm * n + nq)
     H = rng.integers(0, 1 << 32, (rows, n), dtype=np.uint64).astype(np.uint32)
