@@ -671,6 +671,11 @@ tc_step_kernel(const __grid_constant__ CUtensorMap mapT, const __grid_constant__
   }
 }
 
+// the IMAD kernel of the same contract (multiexp.cu)
+int slot_fixed_launch(const uint32_t* P, int64_t n, const uint32_t* E, int64_t rs,
+                      const int32_t* row_ids, int64_t rows, int limbs, const uint32_t* N,
+                      uint32_t np, const uint32_t* one_m, uint32_t* W, cudaStream_t st);
+
 static PFN_cuTensorMapEncodeTiled_v12000 tcp_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -741,8 +746,15 @@ int64_t tc_slot_fixed_workspace(int64_t n, int64_t rows, int clients) {
 int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint32_t* const* N,
                               const uint32_t* np, const uint32_t* const* one_m,
                               uint32_t* const* W, int64_t n, const uint32_t* E, int64_t rs,
-                              const int32_t* rid, int64_t rows, cudaStream_t st) {
+                              const int32_t* rid, int64_t rows_all, cudaStream_t st) {
   using namespace tcp;
+  // A CTA pair takes 512 rows. A short remainder (at most a quarter of a pair, next
+  // to at least one full pair) goes to the IMAD kernel instead of a pair of its own:
+  // 32823 rows are 64 pairs + 55 rows, and 16 clients x 128 CTAs are 13.8 waves of
+  // 148 SMs where 16 x 130 are 14.05.
+  const int64_t rem = rows_all % (4 * kRows);
+  const bool tail = rows_all > 4 * kRows && rem > 0 && rem <= kRows && 4 * n <= 65536;
+  const int64_t rows = tail ? rows_all - rem : rows_all;
   const DigitSpec ds = digit_spec();
   const int nb = ds.nb;
   const int64_t npos = ds.D * n;
@@ -834,6 +846,15 @@ int tc_slot_fixed_many_launch(int clients, const uint32_t* const* P, const uint3
                                                                              rows_p, rid);
   if (check_launch("bucket_combine")) return fail("bucket_combine");
   release();
+  if (tail)
+    for (int c = 0; c < C; ++c) {
+      // rows [rows, rows_all): by position in the row-id list, or by row
+      const int e = rid ? slot_fixed_launch(P[c], n, E, rs, rid + rows, rem, kL, N[c], np[c],
+                                            one_m[c], W[c], st)
+                        : slot_fixed_launch(P[c], n, E + rows * rs, rs, nullptr, rem, kL, N[c], np[c],
+                                            one_m[c], W[c] + rows * kL, st);
+      if (e) return e;
+    }
   return check_launch("tc_slot_fixed");
 }
 

@@ -187,12 +187,13 @@ def test_planar_compression(env, lm, n, rows, nq, ctas):
         assert np.array_equal(z[q], zr), q
 
 
-@pytest.mark.parametrize("n,rows", [(64, 300), (256, 129), (32, 128)])
+@pytest.mark.parametrize("n,rows", [(64, 300), (256, 129), (32, 128), (32, 552)])
 def test_slot_fixed_tensor_core(env, n, rows):
     """Tensor-core Pippenger bucket updates (X * y mod N as one int8 GEMM against
     the table of reduced byte shifts of y, buckets left unreduced in 515 bytes)
     == the IMAD warp path, bit for bit (2048-bit m, 4096-bit m^2), incl. zero
-    digits, all-255 rows and a partial last tile."""
+    digits, all-255 rows, a partial last tile, and 552 rows = one CTA pair plus
+    a 40-row remainder that goes to the IMAD kernel."""
     torch, device = env
     from oracle import client
     from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
@@ -254,20 +255,22 @@ def test_slot_fixed_tensor_core_moduli(env, m):
     assert not bad, f"{len(bad)} rows differ, first {bad[:5]}"
 
 
-def test_slot_fixed_tensor_core_many_clients_row_ids(env):
+@pytest.mark.parametrize("nrow,nsel", [(400, 150), (700, 540)])
+def test_slot_fixed_tensor_core_many_clients_row_ids(env, nrow, nsel):
     """One tensor-core launch for three clients (different keys and tables),
     on a row-id subset of the exponent rows (the incremental refresh): every
     client's rows equal its own IMAD slot_fixed; rows outside the subset are
-    left untouched."""
+    left untouched. 540 selected rows = one CTA pair plus a 28-row remainder
+    on the IMAD kernel, by position in the row-id list."""
     torch, device = env
     from oracle import client
     from paper_2603_09190_b200.bigint import ints_to_limbs, key_ctx
     dev = torch.device("cuda", 0)
-    n, nrow = 64, 400
+    n = 64
     nrng = np.random.default_rng(31)
     E = nrng.integers(0, 1 << 32, (nrow, n), dtype=np.uint64).astype(np.uint32)
     Ed = device.u32_tensor(E, dev)
-    rid_h = np.sort(nrng.choice(nrow, size=150, replace=False)).astype(np.int32)
+    rid_h = np.sort(nrng.choice(nrow, size=nsel, replace=False)).astype(np.int32)
     rid = torch.from_numpy(rid_h).to(dev)
     jobs, refs = [], []
     for c in range(3):
