@@ -1443,9 +1443,23 @@ int umma_planar_launch(const uint8_t* hp, int64_t rows, int64_t n, const uint8_t
     const int64_t Tp = (int64_t)a.m_tiles * a.n_tiles;
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(cap / 2, Tp));
     // blocks of row tiles whose H planes (2 kBM x 4 np bytes per pair tile) stay in L2
+    // (<= 48 MB); among the block sizes of at least half that, the one whose
+    // (query, tile) units split most evenly over the pairs, block by block
     const int64_t tile_bytes = 2ll * kBM * 4 * np;
-    const int nblk = nq > 1 ? (int)ceil_div((int64_t)a.m_tiles * tile_bytes, 48ll << 20) : 1;
-    const int tb = (int)ceil_div(a.m_tiles, std::max(1, nblk));
+    int tb = a.m_tiles;
+    if (nq > 1) {
+      const int tmax = (int)std::max<int64_t>(1, std::min<int64_t>(a.m_tiles, (48ll << 20) / tile_bytes));
+      int64_t best = -1;
+      for (int t = tmax; t >= std::max(1, tmax / 2); --t) {
+        int64_t steps = 0;                 // units of the busiest pair, summed over the blocks
+        for (int left = a.m_tiles; left > 0; left -= t)
+          steps += ceil_div((int64_t)std::min(left, t) * nq, (int64_t)pairs);
+        if (best < 0 || steps < best) {
+          best = steps;
+          tb = t;
+        }
+      }
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * pairs);
     cfg.blockDim = dim3(kThreads);

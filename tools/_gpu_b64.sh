@@ -9,7 +9,3 @@ for i in 1 2; do
 timeout 600 python bench.py --workload batch64 > gpurun_out/b64/batch64_$i.json 2> gpurun_out/b64/batch64.err; echo "batch64 rc=$?"
 python -c "import json; d=json.load(open('gpurun_out/b64/batch64_$i.json')); print({k: d[k] for k in ('ms_per_step','gemv_ms','compress_ms')}, d['e2e']['ms_per_step'])"
 done
-python tools/batch_once.py > gpurun_out/b64/b.log 2>&1 && \
-ncu --set full --import-source on --clock-control none -k regex:umma_planar_pair -s 1 -c 1 \
-  -o gpurun_out/b64/compress_pair -f python tools/batch_once.py > gpurun_out/b64/ncu_pair.log 2>&1
-python tools/ncu_summary.py gpurun_out/b64/*.ncu-rep | tee gpurun_out/b64/summary.md
